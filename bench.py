@@ -1,0 +1,401 @@
+#!/usr/bin/env python
+"""bench.py — fp64 cell-RHS evaluations per second of the narrow-stencil
+operator (a U_x)_x + (a U_y)_y + (a U_z)_z, BASELINE.json configs[1]
+(256^3 per GPU, periodic; weak scaling over z-slabs with a 4-plane NCCL halo
+exchange overlapped with the interior for N > 1, configs[3]-style).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+One "step" = one evaluation of the operator over the whole job's box.
+value   = cells of all ranks / max-over-ranks device time of K steps.
+e2e     = the same metric through the public API with host (pinned) buffers:
+          H2D of U, the operator, D2H of the result, inside the timed region.
+roofline: dominant kernel (narrow_kernel), FP64-bound: 341 flop/cell
+           against a DFMA-loop FP64 peak measured here.
+cpu_baseline: the reference's own kernels (oracle/_ref, built from
+          /root/reference) composed in 3-D, all host threads, rank 0, N=1.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+FLOP_PER_CELL = 341          # 3 x 112 + 3 + 2
+BYTES_PER_CELL = 24          # read U, a; write out (compulsory)
+N_CELLS_SIDE = 256
+
+
+def parse():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=4000)
+    p.add_argument("--warmup", type=int, default=50)
+    p.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    p.add_argument("--n", type=int, default=N_CELLS_SIDE)
+    p.add_argument("--kc", type=int, default=0)
+    p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--e2e-steps", type=int, default=20)
+    return p.parse_args()
+
+
+# ------------------------------------------------------------------ clocks
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons during the timed region."""
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if not self.proc:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.15)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=2)
+        except Exception:
+            self.proc.kill()
+        sm, smax, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            f = [x.strip() for x in ln.split(",")]
+            if len(f) < 9:
+                continue
+            try:
+                sm.append(float(f[1]))
+                smax = float(f[2])
+            except ValueError:
+                continue
+            for name, v in zip(names, f[5:9]):
+                if v.lower() == "active":
+                    reasons.add(name)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": smax,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ------------------------------------------------------------ CPU baselines
+def cpu_reference_rate(n: int, budget_s: float = 12.0, max_reps: int = 5):
+    """The reference's own line kernels composed in 3-D (oracle/_ref), all
+    host threads; returns (cells/s, cores, kind, sample)."""
+    import numpy as np
+    from oracle import oracle as O
+    from paper_1309_7327_b200 import workloads as W
+    a, u = W.narrow3d_inputs(n)
+    m, s = O.build_narrow(8, (3557.0 / 44100.0, -2083.0 / 117600.0))
+    if O.have_ref(fast=True):
+        r = O.ref(fast=True)
+        r.ref_set_workers(0)
+        cores = int(r.ref_worker_limit())
+        fn = lambda: O.ref_narrow3d(m, s, a, u, 1 / n, 1 / n, 1 / n, fast=True)  # noqa: E731
+        kind = "reference"
+        sample = f"full {n}^3 box per rep, reference kernels narrow_interfaces<4>/_rows<4> " \
+                 f"composed as narrow_rhs_rows (oracle/ref_capi.cpp), parallel_for over z planes"
+    else:
+        n = min(n, 96)
+        a, u = W.narrow3d_inputs(n)
+        cores = 1
+        fn = lambda: O.narrow3d(m, s, a, u, 1 / n, 1 / n, 1 / n)  # noqa: E731
+        kind = "port"
+        sample = f"full {n}^3 box per rep, C restatement oracle/oracle.c, 1 thread"
+    fn()  # warm-up
+    best, spent, reps = math.inf, 0.0, 0
+    while reps < max_reps and (spent < budget_s or reps < 1):
+        t0 = time.perf_counter()
+        fn()
+        dt = time.perf_counter() - t0
+        best = min(best, dt)
+        spent += dt
+        reps += 1
+    return n ** 3 / best, cores, kind, sample + f", best of {reps}", best
+
+
+def run_reference(args):
+    """--impl reference: the reference CPU path on the same workload."""
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    n = args.n
+    import numpy as np
+    from oracle import oracle as O
+    from paper_1309_7327_b200 import workloads as W
+    if not O.have_ref(fast=True):
+        O.build_ref()
+    a, u = W.narrow3d_inputs(n)
+    m, s = O.build_narrow(8, (3557.0 / 44100.0, -2083.0 / 117600.0))
+    have = O.have_ref(fast=True)
+    if have:
+        r = O.ref(fast=True)
+        r.ref_set_workers(0)
+        cores = int(r.ref_worker_limit())
+        step = lambda: O.ref_narrow3d(m, s, a, u, 1 / n, 1 / n, 1 / n, fast=True)  # noqa: E731
+        kind = "reference"
+    else:
+        cores = 1
+        step = lambda: O.narrow3d(m, s, a, u, 1 / n, 1 / n, 1 / n)  # noqa: E731
+        kind = "port"
+    for _ in range(min(args.warmup, 1)):
+        step()
+    t_one = None
+    times = []
+    budget = 120.0
+    k = 0
+    t_start = time.perf_counter()
+    while k < args.steps:
+        t0 = time.perf_counter()
+        step()
+        times.append(time.perf_counter() - t0)
+        k += 1
+        if time.perf_counter() - t_start > budget:
+            break
+    total = sum(times)
+    value = n ** 3 * k / total
+    out = {
+        "metric": "fp64 cell-RHS evals/sec (narrow operator, configs[1])",
+        "value": value, "unit": "cell-RHS/s", "n_gpus": args.gpus, "steps": k,
+        "steps_requested": args.steps, "warmup": args.warmup,
+        "ms_per_step": 1e3 * total / k, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": f"configs[1] narrow operator {n}^3 periodic (CPU reference path)",
+                   "cells": n ** 3},
+        "impl": "reference",
+        "cpu_baseline": {"value": value, "unit": "cell-RHS/s", "cores": cores, "kind": kind,
+                         "sample": f"full {n}^3 box per step; {k} steps (time-capped at "
+                                   f"{budget:.0f} s)"},
+        "e2e": {"value": value, "unit": "cell-RHS/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(out), flush=True)
+
+
+# ------------------------------------------------------------------- ours
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+        return
+    import torch
+    import torch.distributed as dist
+    import paper_1309_7327_b200 as P
+    from paper_1309_7327_b200 import _capi, workloads as W
+    from paper_1309_7327_b200.distributed import DistributedNarrow3D, Slab
+    import ctypes as C
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    n = args.n
+    cells_rank = n ** 3
+    cells_total = cells_rank * world
+    stream = torch.cuda.current_stream()
+
+    # ---- inputs resident in HBM
+    if world == 1:
+        a, u = W.narrow3d_inputs(n, xp=torch, device=dev)
+        op = P.Narrow3DOperator(a, 1 / n, 1 / n, 1 / n)
+        op.set_stream(stream)
+        if args.kc:
+            op.set_kc(args.kc)
+        out = torch.empty_like(u)
+
+        def step():
+            op(0.0, u, out)
+    else:
+        slab = Slab(rank, world, n)
+        zg = torch.tensor(slab.global_planes(), dtype=torch.float64, device=dev) / n
+        x = torch.arange(n, dtype=torch.float64, device=dev) / n
+        tw = 2 * math.pi
+        a = (1.0 + 0.5 * torch.sin(tw * x).view(1, 1, n) * torch.cos(tw * x).view(1, n, 1)
+             * torch.sin(tw * zg).view(-1, 1, 1)).contiguous()
+        ks, amps, ph = W.modes()
+        u = torch.zeros_like(a)
+        for k, A, p in zip(ks, amps, ph):
+            u += A * torch.sin(tw * (k[0] * x.view(1, 1, n) + k[1] * x.view(1, n, 1)
+                                     + k[2] * zg.view(-1, 1, 1)) + p)
+        dop = DistributedNarrow3D(a, slab, 1 / n, 1 / n, 1 / n, dist, exchange_a=False)
+        if args.kc:
+            dop.op.set_kc(args.kc)
+        op = dop.op
+        out = torch.empty((n, n, n), dtype=torch.float64, device=dev)
+
+        def step():
+            dop.apply(u, out)
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    def max_over_ranks(v: float) -> float:
+        if world == 1:
+            return v
+        t = torch.tensor([v], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    # ---- FP64 peak of this device (roofline denominator)
+    peak = C.c_double()
+    _capi.check(_capi.lib().smc_measure_fp64_peak(20000, C.byref(peak)))
+    fp64_peak = max_over_ranks(peak.value)
+
+    # ---- warm-up + timed region (inputs 403 MB/step per rank > 126 MB L2)
+    for _ in range(max(args.warmup, 3)):
+        step()
+    barrier()
+    sampler = ClockSampler(local)
+    sampler.start()
+    time.sleep(0.3)
+    barrier()
+    launches0 = P.launch_count()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(args.steps):
+        step()
+    e1.record(stream)
+    barrier()
+    launches = P.launch_count() - launches0
+    clocks = sampler.stop()
+    ms = max_over_ranks(e0.elapsed_time(e1))
+    ms_step = ms / args.steps
+    value = cells_total * args.steps / (ms * 1e-3)
+
+    # ---- dominant kernel alone (for N > 1 the step also holds the exchange)
+    if world == 1:
+        k_ms = ms_step
+    else:
+        k0, k1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        barrier()
+        k0.record(stream)
+        kk = max(10, args.steps // 10)
+        for _ in range(kk):
+            op.apply_planes(u, out, 0, n)
+        k1.record(stream)
+        barrier()
+        k_ms = max_over_ranks(k0.elapsed_time(k1)) / kk
+    achieved_tf = FLOP_PER_CELL * cells_rank / (k_ms * 1e-3) / 1e12
+    achieved_gbs = BYTES_PER_CELL * cells_rank / (k_ms * 1e-3) / 1e9
+    peaks = {}
+    try:
+        peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+    except Exception:
+        pass
+    hbm_peak = peaks.get("hbm_gbs", 6650.0)
+    traffic = None
+    try:
+        prof = json.load(open(os.path.join(ROOT, "profiles", "ncu_narrow3d.json")))
+        traffic = prof.get("dram_bytes_per_launch")
+    except Exception:
+        pass
+
+    # ---- e2e through the public API with host buffers
+    e2e_steps = max(3, min(args.e2e_steps, args.steps))
+    if world == 1:
+        uh = torch.empty((n, n, n), dtype=torch.float64).pin_memory()
+        oh = torch.empty((n, n, n), dtype=torch.float64).pin_memory()
+        uh.copy_(u.cpu())
+
+        def e2e_step():
+            op(0.0, uh, oh)          # H2D, kernel, D2H, synchronize (smc_rhs_eval, SMC_HOST)
+    else:
+        uh = torch.empty((n, n, n), dtype=torch.float64).pin_memory()
+        oh = torch.empty((n, n, n), dtype=torch.float64).pin_memory()
+        uh.copy_(u[4:4 + n].cpu())
+
+        def e2e_step():
+            u[4:4 + n].copy_(uh, non_blocking=True)
+            dop.apply(u, out)
+            oh.copy_(out, non_blocking=True)
+            torch.cuda.current_stream().synchronize()
+    e2e_step()
+    barrier()
+    f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    f0.record(stream)
+    for _ in range(e2e_steps):
+        e2e_step()
+    f1.record(stream)
+    barrier()
+    e2e_ms = max_over_ranks(f0.elapsed_time(f1)) / e2e_steps
+    e2e_value = cells_total / (e2e_ms * 1e-3)
+
+    # ---- CPU baseline (rank 0, N = 1 only)
+    cpu = None
+    if world == 1 and rank == 0 and not args.no_cpu_baseline:
+        try:
+            v, cores, kind, sample, best = cpu_reference_rate(n)
+            cpu = {"value": v, "unit": "cell-RHS/s", "cores": cores, "kind": kind,
+                   "sample": sample}
+        except Exception as exc:  # noqa: BLE001
+            cpu = {"value": None, "unit": "cell-RHS/s", "cores": 0, "kind": "unavailable",
+                   "sample": f"failed: {exc}"}
+
+    if rank == 0:
+        line = {
+            "metric": "fp64 cell-RHS evals/sec (narrow operator, configs[1])",
+            "value": value, "unit": "cell-RHS/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {
+                "workload": f"configs[1] narrow 8th-order (a U_x)_x+(a U_y)_y+(a U_z)_z, "
+                            f"{n}^3 per GPU, periodic" +
+                            ("" if world == 1 else f", z-slabs of a {n}x{n}x{n * world} box, "
+                                                   "4-plane NCCL halo overlapped"),
+                "cells_per_gpu": cells_rank, "stencil": "SMC (m47=3557/44100, m48=-2083/117600)",
+                "l2": f"inputs larger than L2 ({(2 * 8 * cells_rank) / 1e6:.0f} MB read + "
+                      f"{8 * cells_rank / 1e6:.0f} MB written per step per GPU)",
+                "kc": args.kc or "heuristic",
+            },
+            "roofline": {
+                "bound": "fp64", "achieved": achieved_tf, "peak": fp64_peak,
+                "unit": "TFLOP/s", "frac": achieved_tf / fp64_peak, "traffic": traffic,
+                "peak_source": "DFMA-loop peak measured in this run (smc_measure_fp64_peak); "
+                               "MEASURED_PEAKS.json has no FP64 figure",
+                "flop_per_cell": FLOP_PER_CELL, "kernel_ms": k_ms,
+                "hbm": {"achieved": achieved_gbs, "peak": hbm_peak, "unit": "GB/s",
+                        "frac": achieved_gbs / hbm_peak, "bytes_per_cell": BYTES_PER_CELL},
+            },
+            "e2e": {"value": e2e_value, "unit": "cell-RHS/s",
+                    "h2d_bytes_per_step": 8 * cells_rank, "d2h_bytes_per_step": 8 * cells_rank,
+                    "ms_per_step": e2e_ms},
+            "gpu_launches": launches,
+            "clocks": clocks,
+            "cpu_baseline": cpu,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,185 @@
+/*
+ * smc_b200.h — C ABI of the B200-native RHS library (libsmc_b200.so).
+ *
+ * Drop-in boundary for the reference `nsdc` library's RHS hot path
+ * (/root/reference/proj/core).  Every entry point below names the reference
+ * interface it replaces (file:line, relative to /root/reference/proj).  The
+ * ABI is plain C: pointers, sizes, status codes; no C++ or torch types.
+ * The C++ mirror of the reference API (include/nsdc_b200/*.hpp) and the
+ * Python bindings (paper_1309_7327_b200/_capi.py) are thin layers over it.
+ *
+ * Conventions
+ *  - Fields are fp64, x fastest: v[(k*ny + j)*nx + i] (the reference Field2D
+ *    flattening, core/include/nsdc/pde.hpp:24-35, extended by one axis).
+ *  - `where` says where caller pointers live: SMC_HOST (staged through the
+ *    library's device buffers, synchronous) or SMC_DEVICE (stream-ordered on
+ *    the handle's stream, asynchronous).
+ *  - Status: SMC_OK, SMC_EINVAL (reference: std::invalid_argument),
+ *    SMC_EINTEGRATION (reference: nsdc::IntegrationError,
+ *    core/include/nsdc/errors.hpp:16-19), SMC_ECUDA.  smc_last_error() gives
+ *    the message of the last failure on the calling thread.
+ *  - Handles are not thread-safe; use one per host thread (the reference
+ *    steppers carry the same rule, core/include/nsdc/sdc.hpp:43-44).
+ */
+#ifndef SMC_B200_H
+#define SMC_B200_H
+
+#include <stddef.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define SMC_OK 0
+#define SMC_EINVAL 1
+#define SMC_EINTEGRATION 2
+#define SMC_ECUDA 3
+
+#define SMC_HOST 0
+#define SMC_DEVICE 1
+
+/* StencilChoice::Kind (core/include/nsdc/stencil.hpp:65-75) */
+#define SMC_NARROW8 0
+#define SMC_NARROW6 1
+#define SMC_WIDE8 2
+
+/* NodeKind families (core/include/nsdc/quadrature.hpp:9) */
+#define SMC_GAUSS_LOBATTO 0
+#define SMC_CLENSHAW_CURTIS 1
+
+typedef struct smc_rhs smc_rhs;     /* a right-hand side f(t, u) on the device */
+typedef struct smc_sdc smc_sdc;     /* device-resident single-rate SDC stepper */
+typedef struct smc_mrsdc smc_mrsdc; /* device-resident multirate SDC stepper */
+
+typedef void (*smc_rhs_fn)(double t, const double* u, double* out, long long n, void* ctx);
+typedef double (*smc_time_fn)(double t, void* ctx);
+typedef void (*smc_field_fn)(double t, double* field, void* ctx);
+typedef double (*smc_reduce_fn)(double local, void* ctx);
+
+/* Sweep diagnostics: SweepDiagnostics (core/include/nsdc/sdc.hpp:30-35) and
+ * MrsdcDiagnostics (core/include/nsdc/mrsdc.hpp:30-38).  `residuals` is a
+ * caller buffer of `residual_capacity` doubles; n_residuals is the full
+ * history length (entries past the capacity are dropped). */
+typedef struct {
+  int sweeps;
+  int fresh_evals;
+  int f1_evals;
+  int f2_evals;
+  int early_stop;
+  int nonfinite;
+  int n_residuals;
+  int residual_capacity;
+  double* residuals;
+} smc_diag;
+
+/* ------------------------------------------------------------- library */
+int smc_version(void);
+const char* smc_last_error(void);
+/* Number of kernel launches issued by this library since load (evidence
+ * counter for bench.py's gpu_launches). */
+long long smc_launch_count(void);
+int smc_synchronize(void);
+/* FP64 pipe peak of the current device (DFMA loop, TFLOP/s): the FP64
+ * roofline denominator (no reference counterpart). */
+int smc_measure_fp64_peak(int iters, double* tflops);
+
+/* ------------------------------------------------------------- stencil */
+/* nsdc::build_narrow — core/src/stencil.cpp:117-132.  m64: 8x8 row-major. */
+int smc_build_narrow(int order, const double* params, int nparams, double* m64, int* s);
+/* nsdc::apply_narrow — core/src/stencil.cpp:134-155 (periodic 1-D, on device). */
+int smc_apply_narrow(int order, const double* params, int nparams, const double* a,
+                     const double* u, int n, double dx, double* out, int where);
+/* nsdc::first_derivative8 — core/src/stencil.cpp:157-169. */
+int smc_first_derivative8(const double* u, int n, double dx, double* out, int where);
+/* nsdc::apply_wide — core/src/stencil.cpp:171-176. */
+int smc_apply_wide(const double* a, const double* u, int n, double dx, double* out, int where);
+
+/* --------------------------------------------------------- operators */
+/* HeatOperator(const HeatProblem&, const Grid2D&, const StencilChoice&) —
+ * core/include/nsdc/pde.hpp:69-84, core/src/pde.cpp:209-258.  a, b, g0 are
+ * the problem's a(x,y), b(x,y), g_space(x,y) sampled on the nodes (host
+ * arrays, nx*ny; g0 may be NULL).  params: {m47, m48} / {m36} / unused. */
+int smc_heat_create(int nx, int ny, int kind, const double* params, const double* a,
+                    const double* b, const double* g0, smc_rhs** out);
+/* separable source g0 * g_time(t) (pde.cpp:107-108, :121-123) */
+int smc_heat_set_time_source(smc_rhs* h, smc_time_fn g_time, void* ctx);
+/* non-separable source g(t, x, y) filled on the grid per call (pde.cpp:124-126) */
+int smc_heat_set_full_source(smc_rhs* h, smc_field_fn g_full, void* ctx);
+
+/* 3-D narrow operator (a U_x)_x + (a U_y)_y + (a U_z)_z on a periodic box —
+ * the composition of narrow_interfaces<S> / narrow_interfaces_rows<S>
+ * (core/src/stencil_kernel.hpp:13-44) used by narrow_rhs_rows<S>
+ * (core/src/pde.cpp:85-129), one axis up (BASELINE.json configs[1]). */
+int smc_narrow3d_create(int nx, int ny, int nz, double dx, double dy, double dz, int order,
+                        const double* params, int nparams, const double* a, int where,
+                        smc_rhs** out);
+/* The same operator on one z-slab of a block-decomposed periodic box
+ * (multi-GPU): `a` (and every u passed to apply_planes)
+ * holds nz + 2*zghost planes, zghost >= S ghost planes below and above the
+ * interior, filled by the caller's halo exchange; out holds the nz interior
+ * planes.  Device pointers; stream-ordered on the handle's stream. */
+int smc_narrow3d_create_slab(int nx, int ny, int nz, int zghost, double dx, double dy, double dz,
+                             int order, const double* params, int nparams, const double* a,
+                             int where, smc_rhs** out);
+/* Interior planes [kbeg, kend) only, so the interior can run while the halo
+ * is in flight and the boundary planes after it lands. */
+int smc_narrow3d_apply_planes(smc_rhs* op, const double* u, double* out, int kbeg, int kend);
+/* z planes per CTA of the narrow kernel (tuning knob; 0 = heuristic). */
+int smc_narrow3d_set_kc(smc_rhs* op, int kc);
+
+/* Any host callback as an operator (nsdc::Rhs, core/include/nsdc/field.hpp:14-16). */
+int smc_rhs_from_callback(long long dim, smc_rhs_fn f, void* ctx, smc_rhs** out);
+
+/* Rhs call: out = f(t, u) — HeatOperator::rhs / as_rhs (pde.cpp:266-284). */
+int smc_rhs_eval(smc_rhs* op, double t, const double* u, double* out, int where);
+long long smc_rhs_dim(const smc_rhs* op);
+/* cudaStream_t as void*; NULL = legacy default stream. */
+int smc_rhs_set_stream(smc_rhs* op, void* stream);
+int smc_rhs_destroy(smc_rhs* op);
+
+/* ------------------------------------------------------- quadrature */
+/* gauss_lobatto / clenshaw_curtis — core/src/quadrature.cpp:101-132 */
+int smc_nodes(int family, int n, double* t);
+/* integration_matrices — core/src/quadrature.cpp:134-158; q, s: (n-1) x n */
+int smc_integration_matrices(int family, int n, double* q, double* s);
+/* build_hierarchy(coarse, TypeB{inner}) (repeats 1) or TypeC{inner, repeats}
+ * — core/src/quadrature.cpp:178-248.  *m2p1 receives the fine node count;
+ * arrays may be NULL (query), else sized for m2p1 = 1 + (nc-1)*repeats*(ni-1). */
+int smc_build_hierarchy(int coarse_family, int coarse_nodes, int inner_family, int inner_nodes,
+                        int repeats, int* m2p1, double* fine, double* q21, double* s21,
+                        double* q22, double* s22, int* fine_of_coarse, int* p_map);
+
+/* ---------------------------------------------------------- steppers */
+/* SdcStepper(NodeSet, StepControls) — core/include/nsdc/sdc.hpp:45-69. */
+int smc_sdc_create(int family, int num_nodes, int iterations, double residual_ratio_cutoff,
+                   int reuse_first_eval, smc_sdc** out);
+/* SdcStepper::step — core/src/sdc.cpp:38-96.  f0 / f_end may be NULL. */
+int smc_sdc_step(smc_sdc* s, smc_rhs* f, const double* u0, double t_n, double dt,
+                 const double* f0, double* u_out, double* f_end, int where, smc_diag* diag);
+/* integrate_sdc — core/src/sdc.cpp:105-127 (state stays on the device). */
+int smc_sdc_integrate(smc_sdc* s, smc_rhs* f, const double* u0, double t0, double t1,
+                      int nsteps, double* u_out, int where, smc_diag* diag);
+/* Cross-rank max of the per-sweep residual (multi-GPU; identity if unset). */
+int smc_sdc_set_reducer(smc_sdc* s, smc_reduce_fn fn, void* ctx);
+int smc_sdc_destroy(smc_sdc* s);
+
+/* MrsdcStepper(MultirateHierarchy, StepControls) with the hierarchy
+ * build_hierarchy(coarse, TypeB/TypeC{inner}) — core/include/nsdc/mrsdc.hpp:51-82. */
+int smc_mrsdc_create(int coarse_family, int coarse_nodes, int inner_family, int inner_nodes,
+                     int repeats, int iterations, double residual_ratio_cutoff,
+                     int reuse_first_eval, smc_mrsdc** out);
+/* MrsdcStepper::step_mode1 — core/src/mrsdc.cpp:84-135. */
+int smc_mrsdc_step_mode1(smc_mrsdc* m, smc_rhs* f1, smc_rhs* f2, const double* u0, double t_n,
+                         double dt, const double* f0_1, const double* f0_2, double* u_out,
+                         double* f1_end, double* f2_end, int where, smc_diag* diag);
+/* integrate_mrsdc, mode 1 — core/src/mrsdc.cpp:227-259. */
+int smc_mrsdc_integrate_mode1(smc_mrsdc* m, smc_rhs* f1, smc_rhs* f2, const double* u0,
+                              double t0, double t1, int nsteps, double* u_out, int where,
+                              smc_diag* diag);
+int smc_mrsdc_set_reducer(smc_mrsdc* m, smc_reduce_fn fn, void* ctx);
+int smc_mrsdc_destroy(smc_mrsdc* m);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SMC_B200_H */

@@ -1,0 +1,420 @@
+/* TEST INFRASTRUCTURE ONLY — CPU restatement of the reference RHS hot path.
+ * See oracle.h for the usage rule and pinning status.  Every function cites
+ * the reference file:line (paths relative to /root/reference/proj) it
+ * restates.  Compiled with -ffp-contract=off so sums are evaluated exactly in
+ * the written order (the reference's own summation order). */
+#include "oracle.h"
+
+#include <math.h>
+#include <stdlib.h>
+#include <string.h>
+
+/* ------------------------------------------------------------------ M */
+/* Affine entries c + p*m47 + q*m48 of rows 1..s (PAPER.md:263-300 for order
+ * 8, PAPER.md:320-345 for order 6, same layout as core/src/stencil.cpp:19-73). */
+typedef struct {
+  double c, p, q;
+} affine_t;
+
+static const affine_t T8[4][8] = {
+    {{5.0 / 336, 0, 1}, {-83.0 / 3600, -1.0 / 5, -14.0 / 5}, {299.0 / 50400, 2.0 / 5, 13.0 / 5},
+     {17.0 / 12600, -1.0 / 5, -4.0 / 5}, {1.0 / 1120, 0, 0}, {0, 0, 0}, {0, 0, 0}, {0, 0, 0}},
+    {{-11.0 / 560, 0, -2}, {-31.0 / 360, 1, 3}, {41.0 / 200, -9.0 / 5, 4.0 / 5},
+     {-5927.0 / 50400, 4.0 / 5, -9.0 / 5}, {17.0 / 600, -1.0 / 5, -4.0 / 5},
+     {-503.0 / 50400, 1.0 / 5, 4.0 / 5}, {0, 0, 0}, {0, 0, 0}},
+    {{-1.0 / 280, 0, 0}, {1097.0 / 5040, -2, 6}, {-1349.0 / 10080, 3, -12},
+     {-887.0 / 5040, -1, 6}, {3613.0 / 50400, 4.0 / 5, -9.0 / 5},
+     {467.0 / 25200, -3.0 / 5, 18.0 / 5}, {139.0 / 25200, -1.0 / 5, -9.0 / 5}, {0, 0, 0}},
+    {{17.0 / 1680, 0, 2}, {-319.0 / 2520, 2, -8}, {-919.0 / 5040, -2, 6}, {-445.0 / 2016, 0, 0},
+     {583.0 / 720, -1, 6}, {-65.0 / 224, 0, -7}, {0, 1, 0}, {0, 0, 1}},
+};
+static const affine_t T6[3][6] = {
+    {{-11.0 / 180, 1, 0}, {1.0 / 9, -2, 0}, {-1.0 / 18, 1, 0}, {1.0 / 180, 0, 0}, {0, 0, 0},
+     {0, 0, 0}},
+    {{7.0 / 60, -3, 0}, {-1.0 / 120, 5, 0}, {-17.0 / 90, -2, 0}, {5.0 / 72, 1, 0},
+     {1.0 / 90, -1, 0}, {0, 0, 0}},
+    {{-1.0 / 15, 3, 0}, {-11.0 / 60, -3, 0}, {-101.0 / 360, 0, 0}, {137.0 / 180, -2, 0},
+     {-83.0 / 360, 1, 0}, {0, 1, 0}},
+};
+
+int or_build_narrow(int order, const double* params, int nparams, double* m64, int* s_out) {
+  if (!((order == 8 && nparams == 2) || (order == 6 && nparams == 1))) return 1;
+  const int s = order == 8 ? 4 : 3;
+  const double x = params[0];
+  const double y = order == 8 ? params[1] : 0.0;
+  memset(m64, 0, sizeof(double) * 64);
+  for (int i = 0; i < s; ++i)
+    for (int j = 0; j < 2 * s; ++j) {
+      const affine_t t = order == 8 ? T8[i][j] : T6[i][j];
+      const double v = t.c + t.p * x + t.q * y; /* stencil.cpp:85 eval() order */
+      m64[i * 8 + j] = v;
+      m64[(2 * s - 1 - i) * 8 + (2 * s - 1 - j)] = -v; /* central antisymmetry */
+    }
+  *s_out = s;
+  return 0;
+}
+
+/* ------------------------------------------------------- line kernels */
+void or_narrow_interfaces(int s, const double* a, const double* u, int n, const double* m64,
+                          double* h) {
+  /* stencil_kernel.hpp:13-25 */
+  for (int i = 0; i < n; ++i) {
+    double acc = 0.0;
+    for (int mm = -s + 1; mm <= s; ++mm) {
+      double v = 0.0;
+      for (int nn = -s + 1; nn <= s; ++nn) v += m64[(mm + s - 1) * 8 + nn + s - 1] * u[i + nn];
+      acc += a[i + mm] * v;
+    }
+    h[i] = acc;
+  }
+}
+
+/* periodic copy into a buffer valid on [-l, n + r) (stencil.cpp:105-113,
+ * pde.cpp:79-83) */
+static double* pad(const double* f, int n, int l, int r, double* buf) {
+  double* p = buf + l;
+  for (int i = 0; i < n; ++i) p[i] = f[i];
+  for (int i = 1; i <= l; ++i) p[-i] = f[((n - i) % n + n) % n];
+  for (int i = 0; i < r; ++i) p[n + i] = f[i % n];
+  return p;
+}
+
+int or_apply_narrow(const double* m64, int s, const double* a, const double* u, int n, double dx,
+                    double* out) {
+  /* stencil.cpp:134-155 */
+  if (n < 2 * s || !(dx > 0.0)) return 1;
+  double* ab = malloc(sizeof(double) * (n + 2 * s));
+  double* ub = malloc(sizeof(double) * (n + 2 * s));
+  double* h = malloc(sizeof(double) * n);
+  const double* ap = pad(a, n, s - 1, s, ab);
+  const double* up = pad(u, n, s - 1, s, ub);
+  or_narrow_interfaces(s, ap, up, n, m64, h);
+  const double inv = 1.0 / (dx * dx);
+  out[0] = (h[0] - h[n - 1]) * inv;
+  for (int i = 1; i < n; ++i) out[i] = (h[i] - h[i - 1]) * inv;
+  free(ab);
+  free(ub);
+  free(h);
+  return 0;
+}
+
+static const double C1 = 4.0 / 5.0, C2 = -1.0 / 5.0, C3 = 4.0 / 105.0, C4 = -1.0 / 280.0;
+
+int or_first_derivative8(const double* u, int n, double dx, double* out) {
+  /* stencil.cpp:157-169, stencil_kernel.hpp:48-54 */
+  if (n < 9 || !(dx > 0.0)) return 1;
+  double* b = malloc(sizeof(double) * (n + 8));
+  const double* p = pad(u, n, 4, 4, b);
+  const double inv = 1.0 / dx;
+  for (int i = 0; i < n; ++i)
+    out[i] = (C1 * (p[i + 1] - p[i - 1]) + C2 * (p[i + 2] - p[i - 2]) +
+              C3 * (p[i + 3] - p[i - 3]) + C4 * (p[i + 4] - p[i - 4])) *
+             inv;
+  free(b);
+  return 0;
+}
+
+int or_apply_wide(const double* a, const double* u, int n, double dx, double* out) {
+  /* stencil.cpp:171-176 */
+  double* du = malloc(sizeof(double) * n);
+  if (or_first_derivative8(u, n, dx, du)) {
+    free(du);
+    return 1;
+  }
+  for (int i = 0; i < n; ++i) du[i] *= a[i];
+  const int rc = or_first_derivative8(du, n, dx, out);
+  free(du);
+  return rc;
+}
+
+/* ------------------------------------------------------ 3-D operators */
+static inline long long lin(int i, int j, int k, int nx, int ny) {
+  return ((long long)k * ny + j) * nx + i;
+}
+
+void or_narrow_dir(const double* m64, int s, const double* c, const double* u, int nx, int ny,
+                   int nz, int dir, double inv_d2, int accumulate, double* out) {
+  /* One direction of narrow_rhs_rows<S> (pde.cpp:85-129): interfaces once per
+   * line, then differenced.  Lines along dir are gathered with periodic wrap. */
+  const int n = dir == 0 ? nx : dir == 1 ? ny : nz;
+  double* cl = malloc(sizeof(double) * n);
+  double* ul = malloc(sizeof(double) * n);
+  double* cb = malloc(sizeof(double) * (n + 2 * s));
+  double* ub = malloc(sizeof(double) * (n + 2 * s));
+  double* h = malloc(sizeof(double) * n);
+  const int n1 = dir == 0 ? ny : nx, n2 = dir == 2 ? ny : nz;
+  for (int b2 = 0; b2 < n2; ++b2)
+    for (int b1 = 0; b1 < n1; ++b1) {
+      long long idx[1];
+      (void)idx;
+      for (int q = 0; q < n; ++q) {
+        int i, j, k;
+        if (dir == 0) { i = q; j = b1; k = b2; }
+        else if (dir == 1) { i = b1; j = q; k = b2; }
+        else { i = b1; j = b2; k = q; }
+        const long long o = lin(i, j, k, nx, ny);
+        cl[q] = c[o];
+        ul[q] = u[o];
+      }
+      const double* cp = pad(cl, n, s - 1, s, cb);
+      const double* up = pad(ul, n, s - 1, s, ub);
+      or_narrow_interfaces(s, cp, up, n, m64, h);
+      for (int q = 0; q < n; ++q) {
+        int i, j, k;
+        if (dir == 0) { i = q; j = b1; k = b2; }
+        else if (dir == 1) { i = b1; j = q; k = b2; }
+        else { i = b1; j = b2; k = q; }
+        const long long o = lin(i, j, k, nx, ny);
+        const double v = (h[q] - h[(q - 1 + n) % n]) * inv_d2;
+        out[o] = accumulate ? out[o] + v : v;
+      }
+    }
+  free(cl);
+  free(ul);
+  free(cb);
+  free(ub);
+  free(h);
+}
+
+void or_deriv8_dir(const double* u, int nx, int ny, int nz, int dir, double inv_d, double* out) {
+  /* stencil_kernel.hpp:48-54 along dir with periodic wrap */
+  const long long st = dir == 0 ? 1 : dir == 1 ? nx : (long long)nx * ny;
+  const int n = dir == 0 ? nx : dir == 1 ? ny : nz;
+  for (int k = 0; k < nz; ++k)
+    for (int j = 0; j < ny; ++j)
+      for (int i = 0; i < nx; ++i) {
+        const int q = dir == 0 ? i : dir == 1 ? j : k;
+        const long long base = lin(i, j, k, nx, ny) - (long long)q * st;
+#define AT(d) u[base + (long long)(((q + (d)) % n + n) % n) * st]
+        out[lin(i, j, k, nx, ny)] =
+            (C1 * (AT(1) - AT(-1)) + C2 * (AT(2) - AT(-2)) + C3 * (AT(3) - AT(-3)) +
+             C4 * (AT(4) - AT(-4))) *
+            inv_d;
+#undef AT
+      }
+}
+
+int or_narrow3d(const double* m64, int s, const double* a, const double* u, int nx, int ny,
+                int nz, double dx, double dy, double dz, double* out) {
+  if (nx < 2 * s || ny < 2 * s || nz < 2 * s) return 1;
+  /* out = dHx/dx^2 + dHy/dy^2 + dHz/dz^2, added in that order (pde.cpp:118-120) */
+  or_narrow_dir(m64, s, a, u, nx, ny, nz, 0, 1.0 / (dx * dx), 0, out);
+  or_narrow_dir(m64, s, a, u, nx, ny, nz, 1, 1.0 / (dy * dy), 1, out);
+  or_narrow_dir(m64, s, a, u, nx, ny, nz, 2, 1.0 / (dz * dz), 1, out);
+  return 0;
+}
+
+int or_heat2d_rhs(int kind, const double* m64, int s, const double* a, const double* b,
+                  const double* g0, double gt, const double* u, int nx, int ny, double dx,
+                  double dy, double* out) {
+  const long long n = (long long)nx * ny;
+  if (kind == 0 || kind == 1) {
+    /* narrow_rhs_rows<S> (pde.cpp:85-129) */
+    if (nx < 2 * s + 1 || ny < 2 * s + 1) return 1;
+    or_narrow_dir(m64, s, a, u, nx, ny, 1, 0, 1.0 / (dx * dx), 0, out);
+    or_narrow_dir(m64, s, b, u, nx, ny, 1, 1, 1.0 / (dy * dy), 1, out);
+  } else {
+    /* wide_pass1 / wide_pass2 (pde.cpp:131-194) */
+    if (nx < 9 || ny < 9) return 1;
+    double* w1 = malloc(sizeof(double) * n);
+    double* w2 = malloc(sizeof(double) * n);
+    double* t = malloc(sizeof(double) * n);
+    or_deriv8_dir(u, nx, ny, 1, 0, 1.0 / dx, t);
+    for (long long q = 0; q < n; ++q) w1[q] = a[q] * t[q];
+    or_deriv8_dir(u, nx, ny, 1, 1, 1.0 / dy, t);
+    for (long long q = 0; q < n; ++q) w2[q] = b[q] * t[q];
+    or_deriv8_dir(w1, nx, ny, 1, 0, 1.0 / dx, out);
+    or_deriv8_dir(w2, nx, ny, 1, 1, 1.0 / dy, t);
+    for (long long q = 0; q < n; ++q) out[q] = out[q] + t[q];
+    free(w1);
+    free(w2);
+    free(t);
+  }
+  if (g0)
+    for (long long q = 0; q < n; ++q) out[q] += g0[q] * gt; /* pde.cpp:121-123 */
+  return 0;
+}
+
+/* ------------------------------------------------------------- SDC */
+static int stalled(const double* hist, int len, double cutoff) {
+  /* sdc.cpp:9-16 */
+  if (cutoff <= 0.0 || len < 2) return 0;
+  const double prev = hist[len - 2], cur = hist[len - 1];
+  if (cur == 0.0) return 1;
+  const double ratio = prev / cur;
+  return ratio >= 1.0 - cutoff && ratio <= 1.0 + cutoff;
+}
+
+int or_integrate_sdc(or_rhs_cb f, void* ctx, long long dim, const double* u0, double t0,
+                     double t1, int nsteps, int m, const double* tau, const double* q,
+                     const double* smat, int iterations, double cutoff, int reuse_first,
+                     double* u_out, double* residuals, int max_res, int* sweeps,
+                     int* fresh_evals, int* early_stop) {
+  if (nsteps < 0 || iterations < 1) return 1;
+  const size_t bytes = sizeof(double) * dim;
+  double* U = malloc(bytes * (m + 1));
+  double* F = malloc(bytes * (m + 1));
+  double* I = malloc(bytes * m);
+  double* fold = malloc(bytes);
+  double* u = malloc(bytes);
+  double* fcarry = malloc(bytes);
+  double* hist = malloc(sizeof(double) * (iterations + 1));
+  memcpy(u, u0, bytes);
+  *sweeps = 0;
+  *fresh_evals = 0;
+  *early_stop = 0;
+  int nres = 0;
+  const double dt = (t1 - t0) / (nsteps > 1 ? nsteps : 1);
+  for (int step = 0; step < nsteps; ++step) {
+    const double tn = t0 + step * dt;
+    /* SdcStepper::step, sdc.cpp:38-96 */
+    for (int k = 0; k <= m; ++k) memcpy(U + k * dim, u, bytes);
+    if (step > 0 && reuse_first) {
+      memcpy(F, fcarry, bytes);
+    } else {
+      f(tn, u, F, dim, ctx);
+      ++*fresh_evals;
+    }
+    for (int k = 1; k <= m; ++k) memcpy(F + k * dim, F, bytes);
+    int hl = 0;
+    for (int it = 1; it <= iterations; ++it) {
+      for (int r = 0; r < m; ++r)
+        for (long long i = 0; i < dim; ++i) {
+          double acc = 0.0;
+          for (int j = 0; j <= m; ++j) acc += smat[r * (m + 1) + j] * F[j * dim + i];
+          I[r * dim + i] = dt * acc;
+        }
+      for (int r = 0; r < m; ++r) {
+        const double dtm = (tau[r + 1] - tau[r]) * dt;
+        double* next = U + (r + 1) * dim;
+        const double* cur = U + r * dim;
+        if (r == 0) {
+          for (long long i = 0; i < dim; ++i) next[i] = cur[i] + I[i];
+        } else {
+          for (long long i = 0; i < dim; ++i)
+            next[i] = cur[i] + dtm * (F[r * dim + i] - fold[i]) + I[r * dim + i];
+        }
+        memcpy(fold, F + (r + 1) * dim, bytes);
+        f(tn + tau[r + 1] * dt, next, F + (r + 1) * dim, dim, ctx);
+        ++*fresh_evals;
+      }
+      /* sdc_residual, sdc.cpp:20-30 */
+      double res = 0.0;
+      for (long long i = 0; i < dim; ++i) {
+        double acc = 0.0;
+        for (int j = 0; j <= m; ++j) acc += q[(m - 1) * (m + 1) + j] * F[j * dim + i];
+        const double r = fabs(u[i] + dt * acc - U[m * dim + i]);
+        if (r > res) res = r;
+      }
+      hist[hl++] = res;
+      if (residuals && nres < max_res) residuals[nres] = res;
+      ++nres;
+      ++*sweeps;
+      if (stalled(hist, hl, cutoff)) {
+        *early_stop = 1;
+        break;
+      }
+    }
+    memcpy(u, U + m * dim, bytes);
+    memcpy(fcarry, F + m * dim, bytes);
+  }
+  memcpy(u_out, u, bytes);
+  free(U);
+  free(F);
+  free(I);
+  free(fold);
+  free(u);
+  free(fcarry);
+  free(hist);
+  return 0;
+}
+
+/* ------------------------------------------------------------ MRSDC */
+int or_integrate_mrsdc1(or_rhs_cb f1, void* c1, or_rhs_cb f2, void* c2, long long dim,
+                        const double* u0, double t0, double tend, int nsteps, int m1,
+                        const double* t1, int m2, const double* t2, const double* s21,
+                        const double* q21, const double* s22, const double* q22,
+                        const int* fine_of_coarse, const int* p_map, int iterations,
+                        double cutoff, double* u_out, double* residuals, int max_res,
+                        int* sweeps, int* f1_evals, int* f2_evals) {
+  if (nsteps < 0 || iterations < 1) return 1;
+  const size_t bytes = sizeof(double) * dim;
+  double* U = malloc(bytes * (m2 + 1));
+  double* F1 = malloc(bytes * (m1 + 1));
+  double* F2 = malloc(bytes * (m2 + 1));
+  double* OF1 = malloc(bytes * (m1 + 1));
+  double* SO = malloc(bytes * m2);
+  double* fold = malloc(bytes);
+  double* u = malloc(bytes);
+  double* c1s = malloc(bytes);
+  double* c2s = malloc(bytes);
+  double* hist = malloc(sizeof(double) * (iterations + 1));
+  int* coarse_at = malloc(sizeof(int) * (m2 + 1));
+  memcpy(u, u0, bytes);
+  *sweeps = *f1_evals = *f2_evals = 0;
+  int nres = 0;
+  const double dt = (tend - t0) / (nsteps > 1 ? nsteps : 1);
+  for (int q = 0; q <= m2; ++q) coarse_at[q] = -1;
+  for (int p = 0; p <= m1; ++p) coarse_at[fine_of_coarse[p]] = p;
+  for (int step = 0; step < nsteps; ++step) {
+    const double tn = t0 + step * dt;
+    /* provisional, mrsdc.cpp:43-66 (reuse_first_eval defaults to true) */
+    for (int q = 0; q <= m2; ++q) memcpy(U + q * dim, u, bytes);
+    if (step > 0) memcpy(F1, c1s, bytes); else { f1(tn, u, F1, dim, c1); ++*f1_evals; }
+    if (step > 0) memcpy(F2, c2s, bytes); else { f2(tn, u, F2, dim, c2); ++*f2_evals; }
+    for (int p = 1; p <= m1; ++p) memcpy(F1 + p * dim, F1, bytes);
+    for (int q = 1; q <= m2; ++q) memcpy(F2 + q * dim, F2, bytes);
+    int hl = 0;
+    for (int it = 1; it <= iterations; ++it) {
+      /* accumulate_node_terms, mrsdc.cpp:69-82 */
+      for (int q = 0; q < m2; ++q)
+        for (long long i = 0; i < dim; ++i) {
+          double acc = 0.0;
+          for (int j = 0; j <= m1; ++j) acc += s21[q * (m1 + 1) + j] * F1[j * dim + i];
+          for (int j = 0; j <= m2; ++j) acc += s22[q * (m2 + 1) + j] * F2[j * dim + i];
+          SO[q * dim + i] = dt * acc;
+        }
+      memcpy(OF1, F1, bytes * (m1 + 1));
+      memcpy(fold, F2, bytes);
+      /* step_mode1 fine sweep, mrsdc.cpp:105-120 */
+      for (int q = 0; q < m2; ++q) {
+        const double dtq = (t2[q + 1] - t2[q]) * dt;
+        const int p = p_map[q];
+        double* next = U + (q + 1) * dim;
+        const double* cur = U + q * dim;
+        for (long long i = 0; i < dim; ++i)
+          next[i] = cur[i] + dtq * (F1[p * dim + i] - OF1[p * dim + i]) +
+                    dtq * (F2[q * dim + i] - fold[i]) + SO[q * dim + i];
+        memcpy(fold, F2 + (q + 1) * dim, bytes);
+        f2(tn + t2[q + 1] * dt, next, F2 + (q + 1) * dim, dim, c2);
+        ++*f2_evals;
+        const int pc = coarse_at[q + 1];
+        if (pc > 0) {
+          f1(tn + t1[pc] * dt, next, F1 + pc * dim, dim, c1);
+          ++*f1_evals;
+        }
+      }
+      /* mrsdc_residual, mrsdc.cpp:23-35 */
+      double res = 0.0;
+      for (long long i = 0; i < dim; ++i) {
+        double acc = 0.0;
+        for (int j = 0; j <= m1; ++j) acc += q21[(m2 - 1) * (m1 + 1) + j] * F1[j * dim + i];
+        for (int j = 0; j <= m2; ++j) acc += q22[(m2 - 1) * (m2 + 1) + j] * F2[j * dim + i];
+        const double r = fabs(u[i] + dt * acc - U[m2 * dim + i]);
+        if (r > res) res = r;
+      }
+      hist[hl++] = res;
+      if (residuals && nres < max_res) residuals[nres] = res;
+      ++nres;
+      ++*sweeps;
+      if (stalled(hist, hl, cutoff)) break;
+    }
+    memcpy(u, U + m2 * dim, bytes);
+    memcpy(c1s, F1 + m1 * dim, bytes);
+    memcpy(c2s, F2 + m2 * dim, bytes);
+  }
+  memcpy(u_out, u, bytes);
+  free(U); free(F1); free(F2); free(OF1); free(SO); free(fold); free(u); free(c1s); free(c2s);
+  free(hist); free(coarse_at);
+  return 0;
+}

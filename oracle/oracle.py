@@ -1,0 +1,175 @@
+"""TEST INFRASTRUCTURE ONLY — ctypes access to the checkers.
+
+* ``lib()``  -> oracle/liboracle.so, the C restatement (oracle.c, ns_oracle.c)
+* ``ref()``  -> oracle/_ref/libnsdc_ref.so, the unmodified reference library
+  (built from /root/reference sources by oracle/Makefile) plus ref_capi.cpp
+* ``ref_fast()`` -> the same with the reference's Release flags (CPU baseline)
+
+Only tests/, __graft_entry__.smoke() and bench.py's cpu_baseline and
+``--impl reference`` legs may import this module.  The product package never does.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+import subprocess
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+REF_DIR = os.path.join(HERE, "_ref")
+_D = C.POINTER(C.c_double)
+_I = C.POINTER(C.c_int)
+
+RHS_CB = C.CFUNCTYPE(None, C.c_double, _D, _D, C.c_longlong, C.c_void_p)
+
+_lib = None
+_ref = {}
+
+
+def dp(a: np.ndarray):
+    assert a.dtype == np.float64 and a.flags.c_contiguous
+    return a.ctypes.data_as(_D)
+
+
+def ip(a: np.ndarray):
+    assert a.dtype == np.int32 and a.flags.c_contiguous
+    return a.ctypes.data_as(_I)
+
+
+def build_oracle() -> None:
+    """Compile the C restatement (gcc; present on the GPU box too)."""
+    subprocess.run(["make", "-s", "-C", HERE, "oracle"], check=True)
+
+
+def build_ref() -> bool:
+    """Compile oracle/_ref from /root/reference (only where it exists)."""
+    if not os.path.isdir("/root/reference/proj/core/src"):
+        return os.path.exists(os.path.join(REF_DIR, "libnsdc_ref.so"))
+    subprocess.run(["make", "-s", "-C", HERE, "ref"], check=True)
+    return True
+
+
+def lib():
+    global _lib
+    if _lib is None:
+        path = os.path.join(HERE, "liboracle.so")
+        if not os.path.exists(path):
+            build_oracle()
+        _lib = C.CDLL(path)
+        _lib.or_narrow_dir.restype = None
+        _lib.or_deriv8_dir.restype = None
+        _lib.or_narrow_interfaces.restype = None
+    return _lib
+
+
+def have_ref(fast: bool = False) -> bool:
+    name = "libnsdc_ref_fast.so" if fast else "libnsdc_ref.so"
+    return os.path.exists(os.path.join(REF_DIR, name))
+
+
+def ref(fast: bool = False):
+    name = "libnsdc_ref_fast.so" if fast else "libnsdc_ref.so"
+    if name not in _ref:
+        r = C.CDLL(os.path.join(REF_DIR, name))
+        r.ref_last_error.restype = C.c_char_p
+        r.ref_truncation_bound.restype = C.c_double
+        r.ref_appendix_dt.restype = C.c_double
+        r.ref_set_workers.restype = None
+        _ref[name] = r
+    return _ref[name]
+
+
+# ----------------------------------------------------------------- helpers
+def build_narrow(order: int, params) -> tuple[np.ndarray, int]:
+    p = np.ascontiguousarray(params, dtype=np.float64)
+    m = np.zeros(64)
+    s = C.c_int()
+    rc = lib().or_build_narrow(order, dp(p), len(p), dp(m), C.byref(s))
+    if rc:
+        raise ValueError("or_build_narrow: bad order/params")
+    return m, s.value
+
+
+def narrow3d(m64, s, a, u, dx, dy, dz) -> np.ndarray:
+    nz, ny, nx = u.shape
+    out = np.empty_like(u)
+    rc = lib().or_narrow3d(dp(m64), s, dp(a), dp(u), nx, ny, nz, C.c_double(dx), C.c_double(dy),
+                           C.c_double(dz), dp(out))
+    assert rc == 0
+    return out
+
+
+def ref_narrow3d(m64, s, a, u, dx, dy, dz, fast: bool = False) -> np.ndarray:
+    nz, ny, nx = u.shape
+    out = np.empty_like(u)
+    r = ref(fast)
+    rc = r.ref_narrow3d(dp(m64), s, dp(a), dp(u), nx, ny, nz, C.c_double(dx), C.c_double(dy),
+                        C.c_double(dz), dp(out))
+    if rc:
+        raise ValueError(r.ref_last_error().decode())
+    return out
+
+
+def heat2d_rhs(kind, m64, s, a, b, g0, gt, u, dx, dy) -> np.ndarray:
+    ny, nx = u.shape
+    out = np.empty_like(u)
+    g0p = dp(g0) if g0 is not None else None
+    rc = lib().or_heat2d_rhs(kind, dp(m64), s, dp(a), dp(b), g0p, C.c_double(gt), dp(u), nx, ny,
+                             C.c_double(dx), C.c_double(dy), dp(out))
+    if rc:
+        raise ValueError("or_heat2d_rhs: bad args")
+    return out
+
+
+def ref_heat2d_fields(pid: int, nx: int, ny: int):
+    a, b, g0, u0 = (np.zeros((ny, nx)) for _ in range(4))
+    rc = ref().ref_heat2d_fields(pid, nx, ny, dp(a), dp(b), dp(g0), dp(u0))
+    assert rc == 0
+    return a, b, g0, u0
+
+
+def ref_heat2d_rhs(pid, kind, params, t, u, a=None, b=None, g0=None, fast=False) -> np.ndarray:
+    ny, nx = u.shape
+    p = np.ascontiguousarray(list(params) + [0.0] * (2 - len(params)), dtype=np.float64)
+    out = np.empty_like(u)
+    r = ref(fast)
+    rc = r.ref_heat2d_rhs(pid, nx, ny, kind, dp(p), dp(a) if a is not None else None,
+                          dp(b) if b is not None else None, dp(g0) if g0 is not None else None,
+                          C.c_double(t), dp(u), dp(out))
+    if rc:
+        raise ValueError(r.ref_last_error().decode())
+    return out
+
+
+def ref_integration_matrices(family: int, n: int):
+    q = np.zeros((n - 1, n))
+    s = np.zeros((n - 1, n))
+    nodes = np.zeros(n)
+    assert ref().ref_nodes(family, n, dp(nodes)) == 0
+    assert ref().ref_integration_matrices(family, n, dp(q), dp(s)) == 0
+    return nodes, q, s
+
+
+def ref_hierarchy(coarse_family, coarse_n, fine_type, fine_family, fine_n, repeats=1):
+    m2p1 = C.c_int()
+    big = 1 + (coarse_n - 1) * repeats * (fine_n - 1)
+    fine = np.zeros(big)
+    m1 = coarse_n - 1
+    q21 = np.zeros((big - 1, m1 + 1))
+    s21 = np.zeros((big - 1, m1 + 1))
+    q22 = np.zeros((big - 1, big))
+    s22 = np.zeros((big - 1, big))
+    foc = np.zeros(coarse_n, dtype=np.int32)
+    pm = np.zeros(big, dtype=np.int32)
+    r = ref()
+    rc = r.ref_build_hierarchy(coarse_family, coarse_n, fine_type, fine_family, fine_n, repeats,
+                               C.byref(m2p1), dp(fine), dp(q21), dp(s21), dp(q22), dp(s22), ip(foc),
+                               ip(pm))
+    assert rc == 0, r.ref_last_error()
+    n2 = m2p1.value
+    assert n2 == big
+    coarse = np.zeros(coarse_n)
+    r.ref_nodes(coarse_family, coarse_n, dp(coarse))
+    return dict(coarse=coarse, fine=fine, q21=q21, s21=s21, q22=q22, s22=s22,
+                fine_of_coarse=foc, p_map=pm)

@@ -1,0 +1,408 @@
+"""B200-native RHS hot path of the SMC method (arXiv 1309.7327).
+
+Python view of the C ABI (include/smc_b200.h) for tests and bench.py.  The
+names mirror the reference `nsdc` C++ API (/root/reference/proj/core/include/nsdc):
+build_narrow / apply_narrow / apply_wide / first_derivative8 (stencil.hpp),
+HeatOperator (pde.hpp), SdcStepper / integrate_sdc (sdc.hpp), MrsdcStepper /
+integrate_mrsdc (mrsdc.hpp), gauss_lobatto / integration_matrices /
+build_hierarchy (quadrature.hpp).  The C++ drop-in with the reference's exact
+signatures is include/nsdc_b200/.
+
+Arrays: numpy float64 (host, synchronous) or torch.float64 CUDA tensors
+(device, stream-ordered on the operator's stream).  There is no CPU fallback:
+without libsmc_b200.so (built by __graft_entry__.build()) every call raises.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import math
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import _capi
+from ._capi import (CLENSHAW_CURTIS, DEVICE, GAUSS_LOBATTO, HOST, NARROW6, NARROW8, WIDE8,
+                    SmcError, SmcIntegrationError, SmcInvalidArgument, check, dptr, where_of)
+
+__all__ = [
+    "SmcError", "SmcInvalidArgument", "SmcIntegrationError", "StencilChoice", "stencil_preset",
+    "build_narrow", "apply_narrow", "apply_wide", "first_derivative8", "HeatOperator",
+    "Narrow3DOperator", "Narrow3DSlab", "CallbackRhs", "SdcStepper", "MrsdcStepper", "StepControls", "nodes",
+    "integration_matrices", "build_hierarchy", "SMC_M47", "SMC_M48", "OPTIMAL_M47",
+    "OPTIMAL_M48", "DEFAULT_M36", "launch_count",
+]
+
+# stencil.hpp:29-35
+SMC_M47 = 3557.0 / 44100.0
+SMC_M48 = -2083.0 / 117600.0
+OPTIMAL_M47 = 1059283.0 / 13608000.0
+OPTIMAL_M48 = -856481.0 / 40824000.0
+DEFAULT_M36 = 281.0 / 3600.0
+
+
+def launch_count() -> int:
+    return int(_capi.lib().smc_launch_count())
+
+
+@dataclass
+class StencilChoice:
+    """StencilChoice (stencil.hpp:65-75)."""
+    kind: int = NARROW8
+    params: tuple = (SMC_M47, SMC_M48)
+
+    @staticmethod
+    def narrow8(m47, m48):
+        return StencilChoice(NARROW8, (m47, m48))
+
+    @staticmethod
+    def narrow6(m36):
+        return StencilChoice(NARROW6, (m36,))
+
+    @staticmethod
+    def wide8():
+        return StencilChoice(WIDE8, ())
+
+    @property
+    def order(self) -> int:
+        return 8 if self.kind == NARROW8 else 6
+
+
+def stencil_preset(name: str) -> StencilChoice:
+    """stencil_preset (stencil.cpp:235-242)."""
+    table = {"SMC": StencilChoice.narrow8(SMC_M47, SMC_M48),
+             "ZERO": StencilChoice.narrow8(0.0, 0.0),
+             "OPTIMAL": StencilChoice.narrow8(OPTIMAL_M47, OPTIMAL_M48),
+             "NARROW6": StencilChoice.narrow6(DEFAULT_M36),
+             "WIDE": StencilChoice.wide8()}
+    if name not in table:
+        raise SmcInvalidArgument(f"unknown stencil preset: {name}")
+    return table[name]
+
+
+def _params(params):
+    p = (C.c_double * 2)(*(list(params) + [0.0, 0.0])[:2])
+    return C.cast(p, C.POINTER(C.c_double)), p
+
+
+def build_narrow(order: int, params) -> tuple[np.ndarray, int]:
+    m = np.zeros(64)
+    s = C.c_int()
+    pp, keep = _params(params)
+    check(_capi.lib().smc_build_narrow(order, pp, len(params), m.ctypes.data_as(
+        C.POINTER(C.c_double)), C.byref(s)))
+    return m.reshape(8, 8), s.value
+
+
+def _out_like(u):
+    if hasattr(u, "is_cuda"):
+        import torch
+        return torch.empty_like(u)
+    return np.empty_like(u)
+
+
+def apply_narrow(order: int, params, a, u, dx: float):
+    out = _out_like(u)
+    pp, keep = _params(params)
+    check(_capi.lib().smc_apply_narrow(order, pp, len(params), dptr(a), dptr(u), len(u), dx,
+                                       dptr(out), where_of(u)))
+    return out
+
+
+def first_derivative8(u, dx: float):
+    out = _out_like(u)
+    check(_capi.lib().smc_first_derivative8(dptr(u), len(u), dx, dptr(out), where_of(u)))
+    return out
+
+
+def apply_wide(a, u, dx: float):
+    out = _out_like(u)
+    check(_capi.lib().smc_apply_wide(dptr(a), dptr(u), len(u), dx, dptr(out), where_of(u)))
+    return out
+
+
+class _Rhs:
+    """Owner of an smc_rhs handle."""
+
+    def __init__(self, handle):
+        self._h = handle
+        self._keep = []
+
+    @property
+    def handle(self):
+        return self._h
+
+    @property
+    def dim(self) -> int:
+        return int(_capi.lib().smc_rhs_dim(self._h))
+
+    def set_stream(self, stream) -> None:
+        """stream: torch.cuda.Stream, raw cudaStream_t int, or None."""
+        raw = getattr(stream, "cuda_stream", stream)
+        check(_capi.lib().smc_rhs_set_stream(self._h, C.c_void_p(raw or 0)))
+
+    def __call__(self, t: float, u, out=None):
+        """Rhs contract (field.hpp:14-16): out = f(t, u)."""
+        if out is None:
+            out = _out_like(u)
+        check(_capi.lib().smc_rhs_eval(self._h, t, dptr(u), dptr(out), where_of(u)))
+        return out
+
+    def close(self):
+        if self._h:
+            _capi.lib().smc_rhs_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+class HeatOperator(_Rhs):
+    """HeatOperator (pde.hpp:69-84) on the periodic [0, 2pi)^2 node grid.
+
+    a, b, g_space: arrays (ny, nx) sampled on the nodes, or callables f(x, y);
+    g_time: callable of t (separable source, pde.cpp:107-108) or None."""
+
+    def __init__(self, nx: int, ny: int, choice: StencilChoice, a, b, g_space=None,
+                 g_time=None):
+        self.nx, self.ny = nx, ny
+        xs = np.arange(nx) * (2 * math.pi / nx)
+        ys = np.arange(ny) * (2 * math.pi / ny)
+
+        def grid(f):
+            if f is None:
+                return None
+            if callable(f):
+                return np.ascontiguousarray(
+                    np.array([[f(x, y) for x in xs] for y in ys], dtype=np.float64))
+            return np.ascontiguousarray(f, dtype=np.float64)
+
+        A, B, G = grid(a), grid(b), grid(g_space)
+        h = C.c_void_p()
+        pp, keep = _params(choice.params)
+        D = C.POINTER(C.c_double)
+        check(_capi.lib().smc_heat_create(nx, ny, choice.kind, pp, A.ctypes.data_as(D),
+                                          B.ctypes.data_as(D),
+                                          G.ctypes.data_as(D) if G is not None else None,
+                                          C.byref(h)))
+        super().__init__(h)
+        if G is not None and g_time is not None:
+            cb = _capi.TIME_FN(lambda t, ctx: float(g_time(t)))
+            self._keep.append(cb)
+            check(_capi.lib().smc_heat_set_time_source(self._h, cb, None))
+
+
+class Narrow3DOperator(_Rhs):
+    """(a U_x)_x + (a U_y)_y + (a U_z)_z on a periodic nz x ny x nx box."""
+
+    def __init__(self, a, dx: float, dy: float, dz: float, choice: StencilChoice = None):
+        choice = choice or StencilChoice()
+        nz, ny, nx = a.shape
+        self.shape = (nz, ny, nx)
+        h = C.c_void_p()
+        pp, keep = _params(choice.params)
+        check(_capi.lib().smc_narrow3d_create(nx, ny, nz, dx, dy, dz, choice.order, pp,
+                                              len(choice.params), dptr(a), where_of(a),
+                                              C.byref(h)))
+        super().__init__(h)
+
+    def set_kc(self, kc: int) -> None:
+        check(_capi.lib().smc_narrow3d_set_kc(self._h, kc))
+
+
+class Narrow3DSlab(_Rhs):
+    """The narrow operator on one z-slab of a block-decomposed periodic box:
+    a (device tensor) has nz + 2*zghost planes; u passed to apply_planes too."""
+
+    def __init__(self, a, nz: int, zghost: int, dx: float, dy: float, dz: float,
+                 choice: StencilChoice = None):
+        choice = choice or StencilChoice()
+        nzg, ny, nx = a.shape
+        assert nzg == nz + 2 * zghost
+        self.nz, self.zghost = nz, zghost
+        h = C.c_void_p()
+        pp, keep = _params(choice.params)
+        check(_capi.lib().smc_narrow3d_create_slab(nx, ny, nz, zghost, dx, dy, dz, choice.order,
+                                                   pp, len(choice.params), dptr(a), where_of(a),
+                                                   C.byref(h)))
+        super().__init__(h)
+
+    def apply_planes(self, u, out, kbeg: int, kend: int) -> None:
+        check(_capi.lib().smc_narrow3d_apply_planes(self._h, dptr(u), dptr(out), kbeg, kend))
+
+    def set_kc(self, kc: int) -> None:
+        check(_capi.lib().smc_narrow3d_set_kc(self._h, kc))
+
+
+class CallbackRhs(_Rhs):
+    """A Python callable f(t, u: np.ndarray) -> np.ndarray as an operator."""
+
+    def __init__(self, dim: int, fn):
+        def tramp(t, u, out, n, ctx):
+            uu = np.ctypeslib.as_array(u, shape=(n,))
+            oo = np.ctypeslib.as_array(out, shape=(n,))
+            oo[:] = fn(t, uu)
+
+        cb = _capi.RHS_FN(tramp)
+        h = C.c_void_p()
+        check(_capi.lib().smc_rhs_from_callback(dim, cb, None, C.byref(h)))
+        super().__init__(h)
+        self._keep.append(cb)
+
+
+@dataclass
+class StepControls:
+    """StepControls (sdc.hpp:12-20)."""
+    num_iterations: int = 4
+    residual_ratio_cutoff: float = 0.05
+    reuse_first_eval: bool = True
+
+
+@dataclass
+class SweepDiagnostics:
+    residual_history: list = field(default_factory=list)
+    sweeps: int = 0
+    fresh_evals: int = 0
+    f1_evals: int = 0
+    f2_evals: int = 0
+    early_stop: bool = False
+    nonfinite: bool = False
+
+
+def _diag(cap=4096):
+    buf = (C.c_double * cap)()
+    d = _capi.Diag()
+    d.residual_capacity = cap
+    d.residuals = C.cast(buf, C.POINTER(C.c_double))
+    return d, buf
+
+
+def _from_diag(d, buf) -> SweepDiagnostics:
+    n = min(d.n_residuals, d.residual_capacity)
+    return SweepDiagnostics(list(buf[:n]), d.sweeps, d.fresh_evals, d.f1_evals, d.f2_evals,
+                            bool(d.early_stop), bool(d.nonfinite))
+
+
+def _reducer(fn):
+    return _capi.REDUCE_FN(lambda v, ctx: float(fn(v)))
+
+
+class SdcStepper:
+    """Device-resident SdcStepper (sdc.hpp:45-69)."""
+
+    def __init__(self, num_nodes: int = 3, controls: StepControls = None,
+                 family: int = GAUSS_LOBATTO):
+        c = controls or StepControls()
+        h = C.c_void_p()
+        check(_capi.lib().smc_sdc_create(family, num_nodes, c.num_iterations,
+                                         c.residual_ratio_cutoff, int(c.reuse_first_eval),
+                                         C.byref(h)))
+        self._h = h
+        self._keep = []
+
+    def set_reducer(self, fn) -> None:
+        """fn(local_max) -> global max over ranks (multi-GPU)."""
+        cb = _reducer(fn)
+        self._keep.append(cb)
+        check(_capi.lib().smc_sdc_set_reducer(self._h, cb, None))
+
+    def step(self, f: _Rhs, u0, t_n: float, dt: float, f0=None):
+        u = _out_like(u0)
+        fe = _out_like(u0)
+        d, buf = _diag()
+        check(_capi.lib().smc_sdc_step(self._h, f.handle, dptr(u0), t_n, dt, dptr(f0), dptr(u),
+                                       dptr(fe), where_of(u0), C.byref(d)))
+        return u, fe, _from_diag(d, buf)
+
+    def integrate(self, f: _Rhs, u0, t0: float, t1: float, nsteps: int, out=None):
+        u = out if out is not None else _out_like(u0)
+        d, buf = _diag()
+        check(_capi.lib().smc_sdc_integrate(self._h, f.handle, dptr(u0), t0, t1, nsteps, dptr(u),
+                                            where_of(u0), C.byref(d)))
+        return u, _from_diag(d, buf)
+
+    def __del__(self):
+        try:
+            _capi.lib().smc_sdc_destroy(self._h)
+        except Exception:
+            pass
+
+
+class MrsdcStepper:
+    """Device-resident MrsdcStepper, mode 1 (mrsdc.hpp:51-82), hierarchy
+    build_hierarchy(coarse, TypeB{inner}) (repeats=1) or TypeC{inner, repeats}."""
+
+    def __init__(self, coarse_nodes=3, inner_nodes=5, controls: StepControls = None, repeats=1,
+                 coarse_family=GAUSS_LOBATTO, inner_family=GAUSS_LOBATTO):
+        c = controls or StepControls()
+        h = C.c_void_p()
+        check(_capi.lib().smc_mrsdc_create(coarse_family, coarse_nodes, inner_family, inner_nodes,
+                                           repeats, c.num_iterations, c.residual_ratio_cutoff,
+                                           int(c.reuse_first_eval), C.byref(h)))
+        self._h = h
+        self._keep = []
+
+    def set_reducer(self, fn) -> None:
+        cb = _reducer(fn)
+        self._keep.append(cb)
+        check(_capi.lib().smc_mrsdc_set_reducer(self._h, cb, None))
+
+    def step_mode1(self, f1: _Rhs, f2: _Rhs, u0, t_n, dt, f0_1=None, f0_2=None):
+        u, e1, e2 = _out_like(u0), _out_like(u0), _out_like(u0)
+        d, buf = _diag()
+        check(_capi.lib().smc_mrsdc_step_mode1(self._h, f1.handle, f2.handle, dptr(u0), t_n, dt,
+                                               dptr(f0_1), dptr(f0_2), dptr(u), dptr(e1),
+                                               dptr(e2), where_of(u0), C.byref(d)))
+        return u, e1, e2, _from_diag(d, buf)
+
+    def integrate_mode1(self, f1: _Rhs, f2: _Rhs, u0, t0, t1, nsteps, out=None):
+        u = out if out is not None else _out_like(u0)
+        d, buf = _diag()
+        check(_capi.lib().smc_mrsdc_integrate_mode1(self._h, f1.handle, f2.handle, dptr(u0), t0,
+                                                    t1, nsteps, dptr(u), where_of(u0),
+                                                    C.byref(d)))
+        return u, _from_diag(d, buf)
+
+    def __del__(self):
+        try:
+            _capi.lib().smc_mrsdc_destroy(self._h)
+        except Exception:
+            pass
+
+
+# ---------------------------------------------------------------- quadrature
+def nodes(family: int, n: int) -> np.ndarray:
+    t = np.zeros(n)
+    check(_capi.lib().smc_nodes(family, n, t.ctypes.data_as(C.POINTER(C.c_double))))
+    return t
+
+
+def integration_matrices(family: int, n: int):
+    q = np.zeros((n - 1, n))
+    s = np.zeros((n - 1, n))
+    D = C.POINTER(C.c_double)
+    check(_capi.lib().smc_integration_matrices(family, n, q.ctypes.data_as(D),
+                                               s.ctypes.data_as(D)))
+    return q, s
+
+
+def build_hierarchy(coarse_n, inner_n, repeats=1, coarse_family=GAUSS_LOBATTO,
+                    inner_family=GAUSS_LOBATTO) -> dict:
+    D, I = C.POINTER(C.c_double), C.POINTER(C.c_int)
+    L = _capi.lib()
+    m2p1 = C.c_int()
+    check(L.smc_build_hierarchy(coarse_family, coarse_n, inner_family, inner_n, repeats,
+                                C.byref(m2p1), None, None, None, None, None, None, None))
+    n2, m1 = m2p1.value, coarse_n - 1
+    fine = np.zeros(n2)
+    q21, s21 = np.zeros((n2 - 1, m1 + 1)), np.zeros((n2 - 1, m1 + 1))
+    q22, s22 = np.zeros((n2 - 1, n2)), np.zeros((n2 - 1, n2))
+    foc, pm = np.zeros(coarse_n, dtype=np.int32), np.zeros(n2, dtype=np.int32)
+    check(L.smc_build_hierarchy(coarse_family, coarse_n, inner_family, inner_n, repeats,
+                                C.byref(m2p1), fine.ctypes.data_as(D), q21.ctypes.data_as(D),
+                                s21.ctypes.data_as(D), q22.ctypes.data_as(D),
+                                s22.ctypes.data_as(D), foc.ctypes.data_as(I),
+                                pm.ctypes.data_as(I)))
+    return dict(fine=fine, q21=q21, s21=s21, q22=q22, s22=s22, fine_of_coarse=foc, p_map=pm)

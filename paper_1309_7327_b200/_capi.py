@@ -1,0 +1,150 @@
+"""ctypes bindings of the C ABI (include/smc_b200.h) for Python callers
+(tests, bench.py).  No fallback: if libsmc_b200.so is missing or cannot be
+loaded, every entry point raises."""
+from __future__ import annotations
+
+import ctypes as C
+import os
+import re
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "libsmc_b200.so")
+HEADER = os.path.join(HERE, "..", "include", "smc_b200.h")
+
+OK, EINVAL, EINTEGRATION, ECUDA = 0, 1, 2, 3
+HOST, DEVICE = 0, 1
+NARROW8, NARROW6, WIDE8 = 0, 1, 2
+GAUSS_LOBATTO, CLENSHAW_CURTIS = 0, 1
+
+_D = C.POINTER(C.c_double)
+_I = C.POINTER(C.c_int)
+_VP = C.c_void_p
+
+RHS_FN = C.CFUNCTYPE(None, C.c_double, _D, _D, C.c_longlong, C.c_void_p)
+TIME_FN = C.CFUNCTYPE(C.c_double, C.c_double, C.c_void_p)
+FIELD_FN = C.CFUNCTYPE(None, C.c_double, _D, C.c_void_p)
+REDUCE_FN = C.CFUNCTYPE(C.c_double, C.c_double, C.c_void_p)
+
+
+class SmcError(RuntimeError):
+    pass
+
+
+class SmcInvalidArgument(SmcError, ValueError):
+    pass
+
+
+class SmcIntegrationError(SmcError):
+    pass
+
+
+class Diag(C.Structure):
+    _fields_ = [("sweeps", C.c_int), ("fresh_evals", C.c_int), ("f1_evals", C.c_int),
+                ("f2_evals", C.c_int), ("early_stop", C.c_int), ("nonfinite", C.c_int),
+                ("n_residuals", C.c_int), ("residual_capacity", C.c_int), ("residuals", _D)]
+
+
+_lib = None
+
+# name -> (restype, argtypes)
+_SIG = {
+    "smc_version": (C.c_int, []),
+    "smc_last_error": (C.c_char_p, []),
+    "smc_launch_count": (C.c_longlong, []),
+    "smc_synchronize": (C.c_int, []),
+    "smc_measure_fp64_peak": (C.c_int, [C.c_int, _D]),
+    "smc_build_narrow": (C.c_int, [C.c_int, _D, C.c_int, _D, _I]),
+    "smc_apply_narrow": (C.c_int, [C.c_int, _D, C.c_int, _VP, _VP, C.c_int, C.c_double, _VP,
+                                   C.c_int]),
+    "smc_first_derivative8": (C.c_int, [_VP, C.c_int, C.c_double, _VP, C.c_int]),
+    "smc_apply_wide": (C.c_int, [_VP, _VP, C.c_int, C.c_double, _VP, C.c_int]),
+    "smc_heat_create": (C.c_int, [C.c_int, C.c_int, C.c_int, _D, _D, _D, _D, C.POINTER(_VP)]),
+    "smc_heat_set_time_source": (C.c_int, [_VP, TIME_FN, _VP]),
+    "smc_heat_set_full_source": (C.c_int, [_VP, FIELD_FN, _VP]),
+    "smc_narrow3d_create": (C.c_int, [C.c_int, C.c_int, C.c_int, C.c_double, C.c_double,
+                                      C.c_double, C.c_int, _D, C.c_int, _VP, C.c_int,
+                                      C.POINTER(_VP)]),
+    "smc_narrow3d_set_kc": (C.c_int, [_VP, C.c_int]),
+    "smc_narrow3d_create_slab": (C.c_int, [C.c_int, C.c_int, C.c_int, C.c_int, C.c_double,
+                                           C.c_double, C.c_double, C.c_int, _D, C.c_int, _VP,
+                                           C.c_int, C.POINTER(_VP)]),
+    "smc_narrow3d_apply_planes": (C.c_int, [_VP, _VP, _VP, C.c_int, C.c_int]),
+    "smc_rhs_from_callback": (C.c_int, [C.c_longlong, RHS_FN, _VP, C.POINTER(_VP)]),
+    "smc_rhs_eval": (C.c_int, [_VP, C.c_double, _VP, _VP, C.c_int]),
+    "smc_rhs_dim": (C.c_longlong, [_VP]),
+    "smc_rhs_set_stream": (C.c_int, [_VP, _VP]),
+    "smc_rhs_destroy": (C.c_int, [_VP]),
+    "smc_nodes": (C.c_int, [C.c_int, C.c_int, _D]),
+    "smc_integration_matrices": (C.c_int, [C.c_int, C.c_int, _D, _D]),
+    "smc_build_hierarchy": (C.c_int, [C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, _I, _D, _D,
+                                      _D, _D, _D, _I, _I]),
+    "smc_sdc_create": (C.c_int, [C.c_int, C.c_int, C.c_int, C.c_double, C.c_int,
+                                 C.POINTER(_VP)]),
+    "smc_sdc_step": (C.c_int, [_VP, _VP, _VP, C.c_double, C.c_double, _VP, _VP, _VP, C.c_int,
+                               C.POINTER(Diag)]),
+    "smc_sdc_integrate": (C.c_int, [_VP, _VP, _VP, C.c_double, C.c_double, C.c_int, _VP,
+                                    C.c_int, C.POINTER(Diag)]),
+    "smc_sdc_set_reducer": (C.c_int, [_VP, REDUCE_FN, _VP]),
+    "smc_sdc_destroy": (C.c_int, [_VP]),
+    "smc_mrsdc_create": (C.c_int, [C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int,
+                                   C.c_double, C.c_int, C.POINTER(_VP)]),
+    "smc_mrsdc_step_mode1": (C.c_int, [_VP, _VP, _VP, _VP, C.c_double, C.c_double, _VP, _VP,
+                                       _VP, _VP, _VP, C.c_int, C.POINTER(Diag)]),
+    "smc_mrsdc_integrate_mode1": (C.c_int, [_VP, _VP, _VP, _VP, C.c_double, C.c_double, C.c_int,
+                                            _VP, C.c_int, C.POINTER(Diag)]),
+    "smc_mrsdc_set_reducer": (C.c_int, [_VP, REDUCE_FN, _VP]),
+    "smc_mrsdc_destroy": (C.c_int, [_VP]),
+}
+
+
+def header_symbols() -> list[str]:
+    """Every function declared in include/smc_b200.h."""
+    text = open(HEADER).read()
+    return sorted(set(re.findall(r"^\s*(?:const\s+)?[A-Za-z_][\w\s\*]*?\b(smc_\w+)\s*\(", text,
+                                 flags=re.M)))
+
+
+def lib():
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise SmcError(f"{LIB_PATH} is missing: run __graft_entry__.build() "
+                           "(there is no CPU fallback)")
+        L = C.CDLL(LIB_PATH)
+        for name, (res, args) in _SIG.items():
+            f = getattr(L, name)
+            f.restype = res
+            f.argtypes = args
+        _lib = L
+    return _lib
+
+
+def check(rc: int) -> None:
+    if rc == OK:
+        return
+    msg = lib().smc_last_error().decode()
+    if rc == EINVAL:
+        raise SmcInvalidArgument(msg)
+    if rc == EINTEGRATION:
+        raise SmcIntegrationError(msg)
+    raise SmcError(msg)
+
+
+def dptr(a) -> C.c_void_p:
+    """Raw pointer of a C-contiguous float64 numpy array or torch tensor."""
+    if a is None:
+        return None
+    if hasattr(a, "data_ptr"):
+        assert a.is_contiguous() and str(a.dtype) == "torch.float64"
+        return C.c_void_p(a.data_ptr())
+    assert a.dtype.name == "float64" and a.flags.c_contiguous
+    return C.c_void_p(a.ctypes.data)
+
+
+def where_of(a) -> int:
+    return DEVICE if hasattr(a, "is_cuda") and a.is_cuda else HOST
+
+
+def cdouble_array(vals):
+    arr = (C.c_double * max(1, len(vals)))(*vals)
+    return C.cast(arr, _D), arr

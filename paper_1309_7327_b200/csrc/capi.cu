@@ -1,0 +1,449 @@
+// extern "C" entry points (include/smc_b200.h).  Exceptions never cross the
+// boundary: they become status codes plus a thread-local message.
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/smc_b200.h"
+#include "narrow.cuh"
+#include "ops.hpp"
+#include "quadrature.hpp"
+#include "sweeps.hpp"
+
+struct smc_rhs {
+  std::unique_ptr<smc::RhsOp> op;
+};
+struct smc_sdc {
+  std::unique_ptr<smc::DeviceSdc> s;
+  smc_reduce_fn reduce = nullptr;
+  void* reduce_ctx = nullptr;
+};
+struct smc_mrsdc {
+  std::unique_ptr<smc::DeviceMrsdc> m;
+  smc_reduce_fn reduce = nullptr;
+  void* reduce_ctx = nullptr;
+};
+
+namespace {
+
+thread_local std::string g_error;
+
+template <class F>
+int guarded(F&& f) {
+  try {
+    f();
+    return SMC_OK;
+  } catch (const std::invalid_argument& e) {
+    g_error = e.what();
+    return SMC_EINVAL;
+  } catch (const smc::IntegrationFailure& e) {
+    g_error = e.what();
+    return SMC_EINTEGRATION;
+  } catch (const smc::CudaFailure& e) {
+    g_error = e.what();
+    return SMC_ECUDA;
+  } catch (const std::exception& e) {
+    g_error = e.what();
+    return SMC_ECUDA;
+  }
+}
+
+void need(const void* p, const char* what) {
+  if (!p) throw smc::InvalidArgument(std::string(what) + ": null pointer");
+}
+
+// Stage caller arrays to the device when they live on the host.
+struct Staged {
+  smc::DevBuf buf;
+  const double* dev = nullptr;
+  Staged(const double* p, long long n, int where, cudaStream_t st) {
+    if (!p) return;
+    if (where == SMC_DEVICE) {
+      dev = p;
+      return;
+    }
+    buf.resize(static_cast<std::size_t>(n));
+    SMC_CUDA(cudaMemcpyAsync(buf.get(), p, n * sizeof(double), cudaMemcpyHostToDevice, st));
+    dev = buf.get();
+  }
+};
+struct StagedOut {
+  smc::DevBuf buf;
+  double* dev = nullptr;
+  double* host = nullptr;
+  long long n = 0;
+  StagedOut(double* p, long long n_, int where) : n(n_) {
+    if (!p) return;
+    if (where == SMC_DEVICE) {
+      dev = p;
+      return;
+    }
+    buf.resize(static_cast<std::size_t>(n));
+    dev = buf.get();
+    host = p;
+  }
+  void finish(cudaStream_t st) {
+    if (host)
+      SMC_CUDA(cudaMemcpyAsync(host, dev, n * sizeof(double), cudaMemcpyDeviceToHost, st));
+  }
+};
+
+void fill_diag(const smc::SweepDiag& d, smc_diag* out) {
+  if (!out) return;
+  out->sweeps = d.sweeps;
+  out->fresh_evals = d.fresh_evals;
+  out->f1_evals = d.f1_evals;
+  out->f2_evals = d.f2_evals;
+  out->early_stop = d.early_stop ? 1 : 0;
+  out->nonfinite = d.nonfinite ? 1 : 0;
+  out->n_residuals = static_cast<int>(d.residuals.size());
+  if (out->residuals)
+    for (int i = 0; i < out->residual_capacity && i < out->n_residuals; ++i)
+      out->residuals[i] = d.residuals[i];
+}
+
+smc::RhsOp& op_of(smc_rhs* h) {
+  need(h, "rhs handle");
+  return *h->op;
+}
+
+}  // namespace
+
+extern "C" {
+
+int smc_version(void) { return 100; }
+const char* smc_last_error(void) { return g_error.c_str(); }
+long long smc_launch_count(void) { return smc::launch_counter().load(); }
+int smc_synchronize(void) {
+  return guarded([] { SMC_CUDA(cudaDeviceSynchronize()); });
+}
+
+// ------------------------------------------------------------- stencil
+int smc_build_narrow(int order, const double* params, int nparams, double* m64, int* s) {
+  return guarded([&] {
+    need(params, "params");
+    need(m64, "m64");
+    smc::StencilM M = smc::make_stencil(order, params, nparams, s);
+    std::memcpy(m64, &M.m[0][0], sizeof(double) * 64);
+  });
+}
+
+int smc_apply_narrow(int order, const double* params, int nparams, const double* a,
+                     const double* u, int n, double dx, double* out, int where) {
+  return guarded([&] {
+    need(a, "a"), need(u, "u"), need(out, "out");
+    int s = 0;
+    smc::StencilM M = smc::make_stencil(order, params, nparams, &s);
+    smc::require(n >= 2 * s, "apply_narrow: grid too small for stencil");
+    smc::require(dx > 0.0, "apply_narrow: dx must be positive");
+    Staged da(a, n, where, nullptr), du(u, n, where, nullptr);
+    StagedOut o(out, n, where);
+    smc::NarrowArgs p;
+    p.u = du.dev, p.cx = p.cy = p.cz = da.dev, p.out = o.dev;
+    p.nx = n, p.ny = 1, p.nz = 1, p.dims = 1, p.kc = 1;
+    p.idx2 = 1.0 / (dx * dx);
+    smc::launch_narrow(p, s, M, nullptr);
+    o.finish(nullptr);
+    SMC_CUDA(cudaStreamSynchronize(nullptr));
+  });
+}
+
+int smc_first_derivative8(const double* u, int n, double dx, double* out, int where) {
+  return guarded([&] {
+    need(u, "u"), need(out, "out");
+    smc::require(n >= 9, "first_derivative8: need at least 9 points");
+    smc::require(dx > 0.0, "first_derivative8: dx must be positive");
+    Staged du(u, n, where, nullptr);
+    StagedOut o(out, n, where);
+    smc::launch_deriv8(du.dev, o.dev, n, 1, 1, 0, dx, nullptr);
+    o.finish(nullptr);
+    SMC_CUDA(cudaStreamSynchronize(nullptr));
+  });
+}
+
+int smc_apply_wide(const double* a, const double* u, int n, double dx, double* out, int where) {
+  return guarded([&] {
+    need(a, "a"), need(u, "u"), need(out, "out");
+    smc::require(n >= 9, "first_derivative8: need at least 9 points");
+    smc::require(dx > 0.0, "first_derivative8: dx must be positive");
+    Staged da(a, n, where, nullptr), du(u, n, where, nullptr);
+    StagedOut o(out, n, where);
+    smc::DevBuf w1(n);
+    smc::launch_wide2d(du.dev, da.dev, nullptr, nullptr, 0.0, w1.get(), nullptr, o.dev, n, 1, dx,
+                       1.0, nullptr);
+    o.finish(nullptr);
+    SMC_CUDA(cudaStreamSynchronize(nullptr));
+  });
+}
+
+// ----------------------------------------------------------- operators
+int smc_heat_create(int nx, int ny, int kind, const double* params, const double* a,
+                    const double* b, const double* g0, smc_rhs** out) {
+  return guarded([&] {
+    need(out, "out");
+    *out = nullptr;
+    static const double zero[2] = {0.0, 0.0};
+    auto h = std::make_unique<smc_rhs>();
+    h->op = std::make_unique<smc::HeatOp>(nx, ny, kind, params ? params : zero, a, b, g0);
+    *out = h.release();
+  });
+}
+
+int smc_heat_set_time_source(smc_rhs* h, smc_time_fn g_time, void* ctx) {
+  return guarded([&] {
+    auto* op = dynamic_cast<smc::HeatOp*>(&op_of(h));
+    smc::require(op != nullptr, "not a heat operator");
+    op->set_time_source(g_time, ctx);
+  });
+}
+
+int smc_heat_set_full_source(smc_rhs* h, smc_field_fn g_full, void* ctx) {
+  return guarded([&] {
+    auto* op = dynamic_cast<smc::HeatOp*>(&op_of(h));
+    smc::require(op != nullptr, "not a heat operator");
+    op->set_full_source(g_full, ctx);
+  });
+}
+
+int smc_narrow3d_create(int nx, int ny, int nz, double dx, double dy, double dz, int order,
+                        const double* params, int nparams, const double* a, int where,
+                        smc_rhs** out) {
+  return guarded([&] {
+    need(out, "out");
+    need(params, "params");
+    *out = nullptr;
+    auto h = std::make_unique<smc_rhs>();
+    h->op = std::make_unique<smc::Narrow3DOp>(nx, ny, nz, dx, dy, dz, order, params, nparams, a,
+                                              where);
+    *out = h.release();
+  });
+}
+
+int smc_narrow3d_create_slab(int nx, int ny, int nz, int zghost, double dx, double dy, double dz,
+                             int order, const double* params, int nparams, const double* a,
+                             int where, smc_rhs** out) {
+  return guarded([&] {
+    need(out, "out");
+    need(params, "params");
+    *out = nullptr;
+    smc::require(zghost >= 1, "narrow3d slab: zghost must be positive");
+    auto h = std::make_unique<smc_rhs>();
+    h->op = std::make_unique<smc::Narrow3DOp>(nx, ny, nz, dx, dy, dz, order, params, nparams, a,
+                                              where, zghost);
+    *out = h.release();
+  });
+}
+
+int smc_narrow3d_apply_planes(smc_rhs* h, const double* u, double* out, int kbeg, int kend) {
+  return guarded([&] {
+    auto* op = dynamic_cast<smc::Narrow3DOp*>(&op_of(h));
+    smc::require(op != nullptr, "not a narrow3d operator");
+    need(u, "u"), need(out, "out");
+    op->eval_planes(u, out, kbeg, kend);
+  });
+}
+
+int smc_narrow3d_set_kc(smc_rhs* h, int kc) {
+  return guarded([&] {
+    auto* op = dynamic_cast<smc::Narrow3DOp*>(&op_of(h));
+    smc::require(op != nullptr, "not a narrow3d operator");
+    smc::require(kc >= 0, "kc must be >= 0");
+    if (kc > 0) op->set_kc(kc);
+  });
+}
+
+int smc_rhs_from_callback(long long dim, smc_rhs_fn f, void* ctx, smc_rhs** out) {
+  return guarded([&] {
+    need(out, "out");
+    *out = nullptr;
+    auto h = std::make_unique<smc_rhs>();
+    h->op = std::make_unique<smc::HostCallbackOp>(dim, f, ctx);
+    *out = h.release();
+  });
+}
+
+int smc_rhs_eval(smc_rhs* h, double t, const double* u, double* out, int where) {
+  return guarded([&] {
+    need(u, "u"), need(out, "out");
+    op_of(h).eval(t, u, out, where);
+  });
+}
+
+long long smc_rhs_dim(const smc_rhs* h) { return h ? h->op->dim() : -1; }
+
+int smc_rhs_set_stream(smc_rhs* h, void* stream) {
+  return guarded([&] { op_of(h).set_stream(static_cast<cudaStream_t>(stream)); });
+}
+
+int smc_rhs_destroy(smc_rhs* h) {
+  delete h;
+  return SMC_OK;
+}
+
+// ---------------------------------------------------------- quadrature
+int smc_nodes(int family, int n, double* t) {
+  return guarded([&] {
+    need(t, "t");
+    smc::Nodes s = smc::make_nodes(family, n);
+    std::memcpy(t, s.t.data(), sizeof(double) * s.t.size());
+  });
+}
+
+int smc_integration_matrices(int family, int n, double* q, double* s) {
+  return guarded([&] {
+    smc::SweepTables m = smc::integration_matrices(smc::make_nodes(family, n));
+    if (q) std::memcpy(q, m.q.a.data(), sizeof(double) * m.q.a.size());
+    if (s) std::memcpy(s, m.s.a.data(), sizeof(double) * m.s.a.size());
+  });
+}
+
+int smc_build_hierarchy(int coarse_family, int coarse_nodes, int inner_family, int inner_nodes,
+                        int repeats, int* m2p1, double* fine, double* q21, double* s21,
+                        double* q22, double* s22, int* fine_of_coarse, int* p_map) {
+  return guarded([&] {
+    smc::Hierarchy h = smc::build_hierarchy(smc::make_nodes(coarse_family, coarse_nodes),
+                                            smc::make_nodes(inner_family, inner_nodes), repeats);
+    if (m2p1) *m2p1 = h.fine.count();
+    auto put = [](const smc::Table& t, double* d) {
+      if (d) std::memcpy(d, t.a.data(), sizeof(double) * t.a.size());
+    };
+    if (fine) std::memcpy(fine, h.fine.t.data(), sizeof(double) * h.fine.t.size());
+    put(h.q21, q21), put(h.s21, s21), put(h.q22, q22), put(h.s22, s22);
+    if (fine_of_coarse)
+      std::memcpy(fine_of_coarse, h.fine_of_coarse.data(), sizeof(int) * h.fine_of_coarse.size());
+    if (p_map) std::memcpy(p_map, h.p_map.data(), sizeof(int) * h.p_map.size());
+  });
+}
+
+// ------------------------------------------------------------ steppers
+int smc_sdc_create(int family, int num_nodes, int iterations, double cutoff, int reuse_first,
+                   smc_sdc** out) {
+  return guarded([&] {
+    need(out, "out");
+    *out = nullptr;
+    auto s = std::make_unique<smc_sdc>();
+    s->s = std::make_unique<smc::DeviceSdc>(smc::make_nodes(family, num_nodes), iterations, cutoff,
+                                            reuse_first != 0);
+    *out = s.release();
+  });
+}
+
+int smc_sdc_set_reducer(smc_sdc* s, smc_reduce_fn fn, void* ctx) {
+  return guarded([&] {
+    need(s, "sdc handle");
+    if (fn)
+      s->s->set_reducer([fn, ctx](double v) { return fn(v, ctx); });
+    else
+      s->s->set_reducer(nullptr);
+  });
+}
+
+int smc_sdc_step(smc_sdc* s, smc_rhs* f, const double* u0, double t_n, double dt,
+                 const double* f0, double* u_out, double* f_end, int where, smc_diag* diag) {
+  return guarded([&] {
+    need(s, "sdc handle"), need(u0, "u0"), need(u_out, "u_out");
+    smc::RhsOp& op = op_of(f);
+    const long long n = op.dim();
+    cudaStream_t st = op.stream();
+    Staged du(u0, n, where, st), df0(f0, n, where, st);
+    StagedOut ou(u_out, n, where), of(f_end, n, where);
+    smc::SweepDiag d;
+    s->s->step(op, du.dev, t_n, dt, df0.dev, ou.dev, of.dev, d);
+    ou.finish(st);
+    of.finish(st);
+    if (where == SMC_HOST) SMC_CUDA(cudaStreamSynchronize(st));
+    fill_diag(d, diag);
+  });
+}
+
+int smc_sdc_integrate(smc_sdc* s, smc_rhs* f, const double* u0, double t0, double t1,
+                      int nsteps, double* u_out, int where, smc_diag* diag) {
+  return guarded([&] {
+    need(s, "sdc handle"), need(u0, "u0"), need(u_out, "u_out");
+    smc::RhsOp& op = op_of(f);
+    const long long n = op.dim();
+    cudaStream_t st = op.stream();
+    Staged du(u0, n, where, st);
+    StagedOut ou(u_out, n, where);
+    smc::SweepDiag d;
+    s->s->integrate(op, du.dev, t0, t1, nsteps, ou.dev, d);
+    ou.finish(st);
+    if (where == SMC_HOST) SMC_CUDA(cudaStreamSynchronize(st));
+    fill_diag(d, diag);
+  });
+}
+
+int smc_sdc_destroy(smc_sdc* s) {
+  delete s;
+  return SMC_OK;
+}
+
+int smc_mrsdc_create(int coarse_family, int coarse_nodes, int inner_family, int inner_nodes,
+                     int repeats, int iterations, double cutoff, int reuse_first,
+                     smc_mrsdc** out) {
+  return guarded([&] {
+    need(out, "out");
+    *out = nullptr;
+    auto m = std::make_unique<smc_mrsdc>();
+    m->m = std::make_unique<smc::DeviceMrsdc>(
+        smc::build_hierarchy(smc::make_nodes(coarse_family, coarse_nodes),
+                             smc::make_nodes(inner_family, inner_nodes), repeats),
+        iterations, cutoff, reuse_first != 0);
+    *out = m.release();
+  });
+}
+
+int smc_mrsdc_set_reducer(smc_mrsdc* m, smc_reduce_fn fn, void* ctx) {
+  return guarded([&] {
+    need(m, "mrsdc handle");
+    if (fn)
+      m->m->set_reducer([fn, ctx](double v) { return fn(v, ctx); });
+    else
+      m->m->set_reducer(nullptr);
+  });
+}
+
+int smc_mrsdc_step_mode1(smc_mrsdc* m, smc_rhs* f1, smc_rhs* f2, const double* u0, double t_n,
+                         double dt, const double* f0_1, const double* f0_2, double* u_out,
+                         double* f1_end, double* f2_end, int where, smc_diag* diag) {
+  return guarded([&] {
+    need(m, "mrsdc handle"), need(u0, "u0"), need(u_out, "u_out");
+    smc::RhsOp& a = op_of(f1);
+    smc::RhsOp& b = op_of(f2);
+    const long long n = a.dim();
+    cudaStream_t st = b.stream();
+    Staged du(u0, n, where, st), d1(f0_1, n, where, st), d2(f0_2, n, where, st);
+    StagedOut ou(u_out, n, where), o1(f1_end, n, where), o2(f2_end, n, where);
+    smc::SweepDiag d;
+    m->m->step_mode1(a, b, du.dev, t_n, dt, d1.dev, d2.dev, ou.dev, o1.dev, o2.dev, d);
+    ou.finish(st), o1.finish(st), o2.finish(st);
+    if (where == SMC_HOST) SMC_CUDA(cudaStreamSynchronize(st));
+    fill_diag(d, diag);
+  });
+}
+
+int smc_mrsdc_integrate_mode1(smc_mrsdc* m, smc_rhs* f1, smc_rhs* f2, const double* u0,
+                              double t0, double t1, int nsteps, double* u_out, int where,
+                              smc_diag* diag) {
+  return guarded([&] {
+    need(m, "mrsdc handle"), need(u0, "u0"), need(u_out, "u_out");
+    smc::RhsOp& a = op_of(f1);
+    smc::RhsOp& b = op_of(f2);
+    const long long n = a.dim();
+    cudaStream_t st = b.stream();
+    Staged du(u0, n, where, st);
+    StagedOut ou(u_out, n, where);
+    smc::SweepDiag d;
+    m->m->integrate_mode1(a, b, du.dev, t0, t1, nsteps, ou.dev, d);
+    ou.finish(st);
+    if (where == SMC_HOST) SMC_CUDA(cudaStreamSynchronize(st));
+    fill_diag(d, diag);
+  });
+}
+
+int smc_mrsdc_destroy(smc_mrsdc* m) {
+  delete m;
+  return SMC_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,107 @@
+// Shared device/host helpers for the sm_100a RHS library.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <atomic>
+#include <cstdint>
+#include <stdexcept>
+#include <string>
+
+namespace smc {
+
+// Status codes of the C ABI (include/smc_b200.h).
+enum Status : int { kOk = 0, kInvalid = 1, kIntegration = 2, kCuda = 3 };
+
+struct InvalidArgument : std::invalid_argument {
+  using std::invalid_argument::invalid_argument;
+};
+struct IntegrationFailure : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+struct CudaFailure : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+
+#define SMC_CUDA(expr)                                                                    \
+  do {                                                                                    \
+    cudaError_t _e = (expr);                                                              \
+    if (_e != cudaSuccess)                                                                \
+      throw ::smc::CudaFailure(std::string(#expr) + ": " + cudaGetErrorString(_e) + " (" + \
+                               __FILE__ + ":" + std::to_string(__LINE__) + ")");          \
+  } while (0)
+
+// Kernel launches issued by the library (exported as smc_launch_count()).
+inline std::atomic<long long>& launch_counter() {
+  static std::atomic<long long> c{0};
+  return c;
+}
+
+#define SMC_CHECK_LAUNCH()                 \
+  do {                                     \
+    ::smc::launch_counter().fetch_add(1);  \
+    SMC_CUDA(cudaGetLastError());          \
+  } while (0)
+
+inline void require(bool ok, const std::string& what) {
+  if (!ok) throw InvalidArgument(what);
+}
+
+// The 8x8 coupling matrix of the narrow operator (stencil.hpp:20-27), laid
+// out [mm + S - 1][nn + S - 1].  Passed by value as a kernel parameter so
+// every launch carries its own copy (kernel parameters live in the constant
+// bank; DFMA reads them as c[0x0][...] operands at no issue cost).
+struct StencilM {
+  double m[8][8];
+};
+
+// Structural nonzeros of row r (PAPER.md:263-300 / :320-345): rows of the
+// upper half start at column 0 and end at S + r; the lower half mirrors.
+template <int S>
+__host__ __device__ constexpr int row_lo(int r) {
+  return r < S ? 0 : r - S + 1;
+}
+template <int S>
+__host__ __device__ constexpr int row_hi(int r) {
+  return r < S ? S + r : 2 * S - 1;
+}
+
+__host__ __device__ inline int wrap(int i, int n) {
+  i %= n;
+  return i < 0 ? i + n : i;
+}
+
+#ifdef __CUDACC__
+// H_{i+1/2} = sum_mm a_{i+mm} (sum_nn M[mm][nn] u_{i+nn}) for one interface.
+// a[w], u[w] hold offsets w - (S - 1), w = 0 .. 2S-1.  Order fixed as in
+// stencil_kernel.hpp:13-25 (mm ascending outer, nn ascending inner); explicit
+// fma so the instruction sequence (and hence the bits) is the same no matter
+// which thread or tiling computes the interface.
+template <int S>
+__device__ __forceinline__ double narrow_iface(const double* a, const double* u,
+                                               const StencilM& M) {
+  double acc;
+#pragma unroll
+  for (int r = 0; r < 2 * S; ++r) {
+    double v = M.m[r][row_lo<S>(r)] * u[row_lo<S>(r)];
+#pragma unroll
+    for (int c = row_lo<S>(r) + 1; c <= row_hi<S>(r); ++c) v = __fma_rn(M.m[r][c], u[c], v);
+    acc = (r == 0) ? a[0] * v : __fma_rn(a[r], v, acc);
+  }
+  return acc;
+}
+
+// 8th-order centred first derivative (stencil_kernel.hpp:48-54) from a
+// 9-point window w[0..8] centred at w[4].
+__device__ __forceinline__ double deriv8_w(const double* w, double inv_d) {
+  const double c1 = 4.0 / 5.0, c2 = -1.0 / 5.0, c3 = 4.0 / 105.0, c4 = -1.0 / 280.0;
+  double r = c1 * (w[5] - w[3]);
+  r = __fma_rn(c2, w[6] - w[2], r);
+  r = __fma_rn(c3, w[7] - w[1], r);
+  r = __fma_rn(c4, w[8] - w[0], r);
+  return r * inv_d;
+}
+
+#endif  // __CUDACC__
+
+}  // namespace smc

@@ -1,0 +1,370 @@
+// Narrow-stencil variable-coefficient diffusion  sum_d (c_d U_d)_d  on sm_100a.
+//
+// Reference: the interface sums of nsdc::detail::narrow_interfaces<S> /
+// narrow_interfaces_rows<S> (proj/core/src/stencil_kernel.hpp:13-44) composed
+// as narrow_rhs_rows<S> composes them (proj/core/src/pde.cpp:85-129): every
+// interface H_{i+1/2} is computed once and differenced, the y (and z)
+// interface is carried from one row (plane) to the next.
+//
+// B200 mapping ("2.5-D" z-march, SURVEY.md §7 "Carried interface"):
+//   * a CTA owns a TX x TY (x, y) tile and marches along z over KC planes;
+//   * the z window (2S planes of U and c_z for the CTA's own columns) lives
+//     in registers, so every z interface is computed once and carried;
+//   * the current plane, with a 4-cell halo in x and y, is staged in shared
+//     memory by cp.async (LDGSTS), double-buffered so plane k+1 lands while
+//     plane k is being differenced;
+//   * x and y interfaces of plane k are computed once each into shared
+//     memory (TX+1 resp. TY+1 per line, the extra one by an idle lane group),
+//     then differenced; the periodic wrap is folded into the load addresses,
+//     so the product keeps the reference's ghost-free Field layout.
+// The work is FP64-bound (341 flop / 24 B per cell); there
+// is nothing GEMM-shaped here, so no tensor cores.
+#include "common.cuh"
+#include "narrow.cuh"
+
+namespace smc {
+
+namespace {
+
+constexpr int TX = 32;            // x extent of a tile (one warp row)
+constexpr int TYW = 8;            // warps per CTA
+constexpr int RPT = 2;            // rows per thread
+constexpr int TY = TYW * RPT;     // y extent of a tile
+constexpr int NTHREADS = TX * TYW;
+
+__device__ __forceinline__ void cp_async8(double* dst, const double* src) {
+  const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(dst));
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(s), "l"(src));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+__device__ __forceinline__ void cp_async_wait_all() {
+  asm volatile("cp.async.wait_group 0;\n" ::: "memory");
+}
+
+template <int S, bool HAS_Y, bool SAME>
+struct Smem {
+  static constexpr int W = TX + 2 * S;                 // tile columns incl. halo
+  static constexpr int H = HAS_Y ? TY + 2 * S : TY;    // tile rows incl. halo
+  static constexpr int CELLS = W * H;
+  static constexpr int FIELDS = SAME ? 2 : 3;          // u, c_x(, c_y)
+  double tile[2][FIELDS][CELLS];
+  double hx[TY][TX + 1];
+  double hy[HAS_Y ? TY + 1 : 1][TX];
+};
+
+// Global index of tile cell (row, col) of plane pointer `plane`.
+template <int S, bool HAS_Y>
+__device__ __forceinline__ long long tile_src(int row, int col, int x0, int y0, int nx, int ny) {
+  const int gx = wrap(x0 - S + col, nx);
+  const int gy = HAS_Y ? wrap(y0 - S + row, ny) : wrap(y0 + row, ny);
+  return static_cast<long long>(gy) * nx + gx;
+}
+
+template <int S, bool HAS_Y, bool SAME>
+__device__ __forceinline__ void stage_plane(Smem<S, HAS_Y, SAME>& sm, int buf, const NarrowArgs& p,
+                                            long long plane_off, int x0, int y0) {
+  using SM = Smem<S, HAS_Y, SAME>;
+  const double* u = p.u + plane_off;
+  const double* cx = p.cx + plane_off;
+  const double* cy = p.cy + plane_off;
+  for (int e = threadIdx.x; e < SM::CELLS; e += NTHREADS) {
+    const int row = e / SM::W, col = e - row * SM::W;
+    const long long g = tile_src<S, HAS_Y>(row, col, x0, y0, p.nx, p.ny);
+    cp_async8(&sm.tile[buf][0][e], u + g);
+    cp_async8(&sm.tile[buf][1][e], cx + g);
+    if constexpr (!SAME) cp_async8(&sm.tile[buf][SM::FIELDS - 1][e], cy + g);
+  }
+  cp_async_commit();
+}
+
+template <int S, bool HAS_Y, bool HAS_Z, bool SAME, bool HAS_SRC>
+__global__ void __launch_bounds__(NTHREADS, 2)
+    narrow_kernel(const NarrowArgs p, const StencilM M) {
+  using SM = Smem<S, HAS_Y, SAME>;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  SM& sm = *reinterpret_cast<SM*>(smem_raw);
+
+  const int tiles_x = (p.nx + TX - 1) / TX;
+  const int x0 = (blockIdx.x % tiles_x) * TX;
+  const int y0 = (blockIdx.x / tiles_x) * TY;
+  const int tx = threadIdx.x % TX;
+  const int ty = threadIdx.x / TX;
+  const int kend = p.kend < 0 ? p.nz : p.kend;
+  const int k0 = p.kbeg + blockIdx.y * p.kc;
+  const int k1 = min(k0 + p.kc, kend);
+  const long long plane = static_cast<long long>(p.nx) * p.ny;
+
+  // Own columns (wrapped so partial tiles stay in bounds; stores predicated).
+  long long col_off[RPT];
+  bool col_ok[RPT];
+#pragma unroll
+  for (int j = 0; j < RPT; ++j) {
+    const int gx = x0 + tx, gy = y0 + ty + TYW * j;
+    col_ok[j] = gx < p.nx && gy < p.ny;
+    col_off[j] = static_cast<long long>(wrap(gy, p.ny)) * p.nx + wrap(gx, p.nx);
+  }
+  auto zplane = [&](int k) -> long long {
+    return static_cast<long long>(p.zwrap ? wrap(k, p.nz) : k) * plane;
+  };
+
+  // z window: offsets k-(S-1) .. k+S of U and c_z for the own columns.
+  double wu[RPT][2 * S], wc[RPT][2 * S], hz_prev[RPT], pf_u[RPT], pf_c[RPT];
+  if constexpr (HAS_Z) {
+#pragma unroll
+    for (int j = 0; j < RPT; ++j) {
+#pragma unroll
+      for (int w = 0; w < 2 * S; ++w) {  // planes k0-S .. k0+S-1 (window of k0-1)
+        const long long o = zplane(k0 - S + w) + col_off[j];
+        wu[j][w] = __ldg(p.u + o);
+        wc[j][w] = __ldg(p.cz + o);
+      }
+      hz_prev[j] = narrow_iface<S>(wc[j], wu[j], M);  // interface k0 - 1/2
+      const long long o = zplane(k0 + S) + col_off[j];
+      pf_u[j] = __ldg(p.u + o);
+      pf_c[j] = __ldg(p.cz + o);
+    }
+  }
+
+  int buf = 0;
+  stage_plane<S, HAS_Y, SAME>(sm, 0, p, zplane(k0), x0, y0);
+
+  for (int k = k0; k < k1; ++k) {
+    cp_async_wait_all();
+    __syncthreads();  // tile[buf] complete; hx/hy of the previous plane consumed
+    if (k + 1 < k1) stage_plane<S, HAS_Y, SAME>(sm, buf ^ 1, p, zplane(k + 1), x0, y0);
+
+    double hz[RPT];
+    if constexpr (HAS_Z) {
+#pragma unroll
+      for (int j = 0; j < RPT; ++j) {
+#pragma unroll
+        for (int w = 0; w < 2 * S - 1; ++w) {
+          wu[j][w] = wu[j][w + 1];
+          wc[j][w] = wc[j][w + 1];
+        }
+        wu[j][2 * S - 1] = pf_u[j];
+        wc[j][2 * S - 1] = pf_c[j];
+        if (k + 1 < k1) {
+          const long long o = zplane(k + 1 + S) + col_off[j];
+          pf_u[j] = __ldg(p.u + o);
+          pf_c[j] = __ldg(p.cz + o);
+        }
+      }
+    }
+
+    const double* tu = sm.tile[buf][0];
+    const double* tcx = sm.tile[buf][1];
+    const double* tcy = sm.tile[buf][SM::FIELDS - 1];
+    constexpr int RY = HAS_Y ? S : 0;  // row offset of the tile interior
+
+    // x interfaces x0+tx+1/2 of rows ty + 8j
+#pragma unroll
+    for (int j = 0; j < RPT; ++j) {
+      const int r = ty + TYW * j;
+      double a[2 * S], u[2 * S];
+#pragma unroll
+      for (int w = 0; w < 2 * S; ++w) {
+        a[w] = tcx[(r + RY) * SM::W + tx + 1 + w];
+        u[w] = tu[(r + RY) * SM::W + tx + 1 + w];
+      }
+      sm.hx[r][tx + 1] = narrow_iface<S>(a, u, M);
+    }
+    // the extra interface x0-1/2 of every row (one half-warp)
+    if (ty == 0 && tx < TY) {
+      const int r = tx;
+      double a[2 * S], u[2 * S];
+#pragma unroll
+      for (int w = 0; w < 2 * S; ++w) {
+        a[w] = tcx[(r + RY) * SM::W + w];
+        u[w] = tu[(r + RY) * SM::W + w];
+      }
+      sm.hx[r][0] = narrow_iface<S>(a, u, M);
+    }
+    if constexpr (HAS_Y) {
+      // y interfaces y0+r+1/2 of column tx
+#pragma unroll
+      for (int j = 0; j < RPT; ++j) {
+        const int r = ty + TYW * j;
+        double a[2 * S], u[2 * S];
+#pragma unroll
+        for (int w = 0; w < 2 * S; ++w) {
+          a[w] = tcy[(r + 1 + w) * SM::W + tx + S];
+          u[w] = tu[(r + 1 + w) * SM::W + tx + S];
+        }
+        sm.hy[r + 1][tx] = narrow_iface<S>(a, u, M);
+      }
+      if (ty == 1) {  // the extra interface y0-1/2 of every column
+        double a[2 * S], u[2 * S];
+#pragma unroll
+        for (int w = 0; w < 2 * S; ++w) {
+          a[w] = tcy[w * SM::W + tx + S];
+          u[w] = tu[w * SM::W + tx + S];
+        }
+        sm.hy[0][tx] = narrow_iface<S>(a, u, M);
+      }
+    }
+    if constexpr (HAS_Z) {
+#pragma unroll
+      for (int j = 0; j < RPT; ++j) hz[j] = narrow_iface<S>(wc[j], wu[j], M);
+    }
+    __syncthreads();
+
+    const long long po = zplane(k);
+#pragma unroll
+    for (int j = 0; j < RPT; ++j) {
+      const int r = ty + TYW * j;
+      // (dHx)/dx^2 + (dHy)/dy^2 + (dHz)/dz^2 [+ g0 g(t)], pde.cpp:118-126 order
+      double o = __dmul_rn(__dsub_rn(sm.hx[r][tx + 1], sm.hx[r][tx]), p.idx2);
+      if constexpr (HAS_Y)
+        o = __dadd_rn(o, __dmul_rn(__dsub_rn(sm.hy[r + 1][tx], sm.hy[r][tx]), p.idy2));
+      if constexpr (HAS_Z) {
+        o = __dadd_rn(o, __dmul_rn(__dsub_rn(hz[j], hz_prev[j]), p.idz2));
+        hz_prev[j] = hz[j];
+      }
+      if (col_ok[j]) {
+        if constexpr (HAS_SRC) o = __dadd_rn(o, __dmul_rn(p.g0[po + col_off[j]], p.gt));
+        p.out[po + col_off[j]] = o;
+      }
+    }
+    buf ^= 1;
+  }
+}
+
+template <int S, bool HAS_Y, bool HAS_Z, bool SAME, bool HAS_SRC>
+void launch_t(const NarrowArgs& p, const StencilM& M, cudaStream_t st) {
+  using SM = Smem<S, HAS_Y, SAME>;
+  auto kern = narrow_kernel<S, HAS_Y, HAS_Z, SAME, HAS_SRC>;
+  static bool configured = false;
+  if (!configured) {
+    SMC_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  static_cast<int>(sizeof(SM))));
+    configured = true;
+  }
+  const int tiles = ((p.nx + TX - 1) / TX) * ((p.ny + TY - 1) / TY);
+  const int kend = p.kend < 0 ? p.nz : p.kend;
+  if (kend <= p.kbeg) return;
+  const dim3 grid(tiles, (kend - p.kbeg + p.kc - 1) / p.kc);
+  kern<<<grid, NTHREADS, sizeof(SM), st>>>(p, M);
+  SMC_CHECK_LAUNCH();
+}
+
+template <int S>
+void launch_s(const NarrowArgs& p, const StencilM& M, cudaStream_t st) {
+  const bool same = p.cx == p.cy && p.cy == p.cz;
+  if (p.dims == 3) {
+    require(same, "narrow3d: one coefficient field shared by all directions");
+    require(p.g0 == nullptr, "narrow3d: no source term");
+    launch_t<S, true, true, true, false>(p, M, st);
+  } else if (p.dims == 2) {
+    if (p.g0)
+      launch_t<S, true, false, false, true>(p, M, st);
+    else
+      launch_t<S, true, false, false, false>(p, M, st);
+  } else {
+    launch_t<S, false, false, true, false>(p, M, st);
+  }
+}
+
+}  // namespace
+
+int narrow_default_kc(int nx, int ny, int nz, int dims, int num_sms) {
+  if (dims < 3) return 1;
+  const long long tiles = static_cast<long long>((nx + TX - 1) / TX) * ((ny + TY - 1) / TY);
+  // ~8 CTAs per SM slot pair in flight over the run, but at least 8 planes
+  // per CTA so the 2S-plane window warm-up stays below ~50% extra z loads.
+  const long long target = 8LL * 2 * num_sms;
+  long long kc = (tiles * nz + target - 1) / target;
+  if (kc < 8) kc = 8;
+  if (kc > nz) kc = nz;
+  return static_cast<int>(kc);
+}
+
+void launch_narrow(const NarrowArgs& p, int s, const StencilM& M, cudaStream_t st) {
+  require(s == 3 || s == 4, "narrow: half width must be 3 or 4");
+  require(p.kc >= 1, "narrow: kc >= 1");
+  if (s == 4)
+    launch_s<4>(p, M, st);
+  else
+    launch_s<3>(p, M, st);
+}
+
+// ----------------------------------------------------------- wide route
+// D(a D u) as two passes of the 8th-order first derivative
+// (pde.cpp:131-194, stencil.cpp:171-176).  Memory-bound, one thread per cell.
+namespace {
+
+__device__ __forceinline__ double d8_line(const double* f, long long base, int q, int n,
+                                          long long stride, double inv_d) {
+  double w[9];
+#pragma unroll
+  for (int d = -4; d <= 4; ++d) w[d + 4] = __ldg(f + base + static_cast<long long>(wrap(q + d, n)) * stride);
+  return deriv8_w(w, inv_d);
+}
+
+__global__ void wide_pass1(const double* __restrict__ u, const double* __restrict__ a,
+                           const double* __restrict__ b, double* __restrict__ w1,
+                           double* __restrict__ w2, int nx, int ny, double inv_dx,
+                           double inv_dy) {
+  const long long n = static_cast<long long>(nx) * ny;
+  for (long long c = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; c < n;
+       c += static_cast<long long>(gridDim.x) * blockDim.x) {
+    const int i = static_cast<int>(c % nx), j = static_cast<int>(c / nx);
+    w1[c] = a[c] * d8_line(u, static_cast<long long>(j) * nx, i, nx, 1, inv_dx);
+    if (w2) w2[c] = b[c] * d8_line(u, i, j, ny, nx, inv_dy);
+  }
+}
+
+__global__ void wide_pass2(const double* __restrict__ w1, const double* __restrict__ w2,
+                           const double* __restrict__ g0, double gt, double* __restrict__ out,
+                           int nx, int ny, double inv_dx, double inv_dy) {
+  const long long n = static_cast<long long>(nx) * ny;
+  for (long long c = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; c < n;
+       c += static_cast<long long>(gridDim.x) * blockDim.x) {
+    const int i = static_cast<int>(c % nx), j = static_cast<int>(c / nx);
+    double o = d8_line(w1, static_cast<long long>(j) * nx, i, nx, 1, inv_dx);
+    if (w2) o = __dadd_rn(o, d8_line(w2, i, j, ny, nx, inv_dy));
+    if (g0) o = __dadd_rn(o, __dmul_rn(g0[c], gt));
+    out[c] = o;
+  }
+}
+
+__global__ void deriv8_kernel(const double* __restrict__ u, double* __restrict__ out, int nx,
+                              int ny, int nz, int dir, double inv_d) {
+  const long long n = static_cast<long long>(nx) * ny * nz;
+  for (long long c = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; c < n;
+       c += static_cast<long long>(gridDim.x) * blockDim.x) {
+    const int i = static_cast<int>(c % nx);
+    const long long jk = c / nx;
+    const int j = static_cast<int>(jk % ny), k = static_cast<int>(jk / ny);
+    const int q = dir == 0 ? i : dir == 1 ? j : k;
+    const int len = dir == 0 ? nx : dir == 1 ? ny : nz;
+    const long long stride = dir == 0 ? 1 : dir == 1 ? nx : static_cast<long long>(nx) * ny;
+    out[c] = d8_line(u, c - q * stride, q, len, stride, inv_d);
+  }
+}
+
+int grid_for(long long n) {
+  long long b = (n + 255) / 256;
+  return static_cast<int>(b > 148 * 64 ? 148 * 64 : (b < 1 ? 1 : b));
+}
+
+}  // namespace
+
+void launch_wide2d(const double* u, const double* a, const double* b, const double* g0, double gt,
+                   double* w1, double* w2, double* out, int nx, int ny, double dx, double dy,
+                   cudaStream_t st) {
+  const long long n = static_cast<long long>(nx) * ny;
+  wide_pass1<<<grid_for(n), 256, 0, st>>>(u, a, b, w1, w2, nx, ny, 1.0 / dx, 1.0 / dy);
+  SMC_CHECK_LAUNCH();
+  wide_pass2<<<grid_for(n), 256, 0, st>>>(w1, w2, g0, gt, out, nx, ny, 1.0 / dx, 1.0 / dy);
+  SMC_CHECK_LAUNCH();
+}
+
+void launch_deriv8(const double* u, double* out, int nx, int ny, int nz, int dir, double dx,
+                   cudaStream_t st) {
+  const long long n = static_cast<long long>(nx) * ny * nz;
+  deriv8_kernel<<<grid_for(n), 256, 0, st>>>(u, out, nx, ny, nz, dir, 1.0 / dx);
+  SMC_CHECK_LAUNCH();
+}
+
+}  // namespace smc

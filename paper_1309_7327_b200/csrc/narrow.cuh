@@ -1,0 +1,37 @@
+#pragma once
+#include "common.cuh"
+
+namespace smc {
+
+// Arguments of the narrow-operator kernel.  Fields are x-fastest,
+// v[(k*ny + j)*nx + i] (the reference Field / Field2D flattening,
+// proj/core/include/nsdc/pde.hpp:24-35 extended by one axis).  With zwrap the
+// z index wraps periodically over [0, nz); without it the pointers address
+// plane 0 of an array that carries S ghost planes on both sides (multi-GPU
+// slabs, filled by the halo exchange).
+struct NarrowArgs {
+  const double* u = nullptr;
+  const double* cx = nullptr;  // coefficient for the x sweep (a)
+  const double* cy = nullptr;  // ... y sweep (b in the 2-D heat operator)
+  const double* cz = nullptr;  // ... z sweep
+  const double* g0 = nullptr;  // separable source factor, may be null
+  double* out = nullptr;
+  int nx = 0, ny = 1, nz = 1;
+  int dims = 3;                // 1, 2 or 3 active directions
+  int kc = 1;                  // z planes per CTA
+  int kbeg = 0, kend = -1;     // plane range [kbeg, kend) to compute (kend < 0: nz)
+  bool zwrap = true;
+  double idx2 = 0, idy2 = 0, idz2 = 0, gt = 0;
+};
+
+void launch_narrow(const NarrowArgs& p, int s, const StencilM& M, cudaStream_t st);
+int narrow_default_kc(int nx, int ny, int nz, int dims, int num_sms);
+
+// Wide route D(a D u) (+ y term when w2/b given) + g0*gt; w1/w2 scratch.
+void launch_wide2d(const double* u, const double* a, const double* b, const double* g0, double gt,
+                   double* w1, double* w2, double* out, int nx, int ny, double dx, double dy,
+                   cudaStream_t st);
+void launch_deriv8(const double* u, double* out, int nx, int ny, int nz, int dir, double dx,
+                   cudaStream_t st);
+
+}  // namespace smc

@@ -1,0 +1,149 @@
+// Right-hand-side operators behind the C ABI.  Each one implements the
+// reference's `nsdc::Rhs` contract (proj/core/include/nsdc/field.hpp:14-16:
+// "writes f(t, u) into out ... out may alias nothing") on device buffers.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "common.cuh"
+
+namespace smc {
+
+// Owning device buffer of doubles.
+class DevBuf {
+ public:
+  DevBuf() = default;
+  explicit DevBuf(std::size_t n) { resize(n); }
+  ~DevBuf() { release(); }
+  DevBuf(const DevBuf&) = delete;
+  DevBuf& operator=(const DevBuf&) = delete;
+  DevBuf(DevBuf&& o) noexcept : p_(o.p_), n_(o.n_) { o.p_ = nullptr, o.n_ = 0; }
+  DevBuf& operator=(DevBuf&& o) noexcept {
+    if (this != &o) {
+      release();
+      p_ = o.p_, n_ = o.n_;
+      o.p_ = nullptr, o.n_ = 0;
+    }
+    return *this;
+  }
+  void resize(std::size_t n) {
+    if (n == n_) return;
+    release();
+    if (n) SMC_CUDA(cudaMalloc(&p_, n * sizeof(double)));
+    n_ = n;
+  }
+  double* get() const { return p_; }
+  std::size_t size() const { return n_; }
+
+ private:
+  void release() {
+    if (p_) cudaFree(p_);
+    p_ = nullptr;
+    n_ = 0;
+  }
+  double* p_ = nullptr;
+  std::size_t n_ = 0;
+};
+
+enum Where : int { kHost = 0, kDevice = 1 };
+
+class RhsOp {
+ public:
+  virtual ~RhsOp() = default;
+  virtual long long dim() const = 0;
+  // out = f(t, u) on device buffers, stream-ordered on stream().
+  virtual void eval_device(double t, const double* u, double* out) = 0;
+  virtual const char* name() const = 0;
+
+  // Host or device pointers; host calls stage through owned buffers and
+  // synchronize before returning.
+  void eval(double t, const double* u, double* out, int where);
+
+  cudaStream_t stream() const { return stream_; }
+  void set_stream(cudaStream_t s) { stream_ = s; }
+  long long evals() const { return evals_; }
+
+ protected:
+  cudaStream_t stream_ = nullptr;
+  long long evals_ = 0;
+  DevBuf stage_u_, stage_out_;
+};
+
+// configs[1]: (a U_x)_x + (a U_y)_y + (a U_z)_z on a periodic box.
+class Narrow3DOp final : public RhsOp {
+ public:
+  // zghost == 0: periodic box, arrays hold nz planes.  zghost >= S: a and u
+  // carry zghost ghost planes below and above the nz interior planes (a
+  // z-slab of a decomposed box, ghosts filled by the halo exchange); out
+  // holds the nz interior planes.
+  Narrow3DOp(int nx, int ny, int nz, double dx, double dy, double dz, int order,
+             const double* params, int nparams, const double* a, int where, int zghost = 0);
+  long long dim() const override { return static_cast<long long>(nx_) * ny_ * nz_; }
+  void eval_device(double t, const double* u, double* out) override;
+  const char* name() const override { return "narrow3d"; }
+  void set_kc(int kc) { kc_ = kc; }
+  int kc() const { return kc_; }
+  int s() const { return s_; }
+  int zghost() const { return zghost_; }
+  // interior planes [kb, ke) only (overlap of halo exchange and compute)
+  void eval_planes(const double* u, double* out, int kb, int ke);
+
+ private:
+  int nx_, ny_, nz_, s_ = 4, kc_ = 8, zghost_ = 0;
+  double dx_, dy_, dz_;
+  StencilM M_{};
+  DevBuf a_;
+};
+
+// HeatOperator (proj/core/include/nsdc/pde.hpp:69-84): u_t = (a u_x)_x +
+// (b u_y)_y + g on the periodic [0, 2pi)^2 grid, narrow8 / narrow6 / wide.
+class HeatOp final : public RhsOp {
+ public:
+  using GTime = double (*)(double t, void* ctx);
+  using GFull = void (*)(double t, double* field, void* ctx);
+
+  HeatOp(int nx, int ny, int kind, const double* params, const double* a, const double* b,
+         const double* g0);
+  long long dim() const override { return static_cast<long long>(nx_) * ny_; }
+  void eval_device(double t, const double* u, double* out) override;
+  const char* name() const override { return "heat2d"; }
+  void set_time_source(GTime f, void* ctx) { gtime_ = f, gtime_ctx_ = ctx; }
+  void set_full_source(GFull f, void* ctx) { gfull_ = f, gfull_ctx_ = ctx; }
+
+ private:
+  int nx_, ny_, kind_, s_ = 0;
+  StencilM M_{};
+  DevBuf a_, b_, g0_, w1_, w2_, gfull_dev_;
+  std::vector<double> gfull_host_;
+  bool has_g0_ = false;
+  GTime gtime_ = nullptr;
+  void* gtime_ctx_ = nullptr;
+  GFull gfull_ = nullptr;
+  void* gfull_ctx_ = nullptr;
+};
+
+// A host callback wrapped as an operator (for ODE-sized problems and for
+// driving the device steppers with any nsdc::Rhs, e.g. the reference's own).
+class HostCallbackOp final : public RhsOp {
+ public:
+  using Cb = void (*)(double t, const double* u, double* out, long long n, void* ctx);
+  HostCallbackOp(long long dim, Cb cb, void* ctx);
+  long long dim() const override { return dim_; }
+  void eval_device(double t, const double* u, double* out) override;
+  const char* name() const override { return "host_callback"; }
+
+ private:
+  long long dim_;
+  Cb cb_;
+  void* ctx_;
+  std::vector<double> hu_, ho_;
+};
+
+StencilM make_stencil(int order, const double* params, int nparams, int* s);
+int num_sms();
+
+}  // namespace smc

@@ -1,0 +1,63 @@
+// FP64 pipe peak on this device: a dependent-chain-free DFMA loop (8
+// independent accumulators per thread, 148 x 8 CTAs of 256 threads), timed
+// with CUDA events.  MEASURED_PEAKS.json carries HBM and bf16 only; this is
+// the denominator of the FP64 roofline (SURVEY.md §8(d) note).
+#include "../../include/smc_b200.h"
+#include "common.cuh"
+
+namespace smc {
+namespace {
+
+__global__ void __launch_bounds__(256) dfma_loop(double* out, int iters, double a, double b) {
+  double r0 = threadIdx.x, r1 = r0 + 1, r2 = r0 + 2, r3 = r0 + 3, r4 = r0 + 4, r5 = r0 + 5,
+         r6 = r0 + 6, r7 = r0 + 7;
+  for (int i = 0; i < iters; ++i) {
+#pragma unroll
+    for (int u = 0; u < 16; ++u) {
+      r0 = __fma_rn(r0, a, b);
+      r1 = __fma_rn(r1, a, b);
+      r2 = __fma_rn(r2, a, b);
+      r3 = __fma_rn(r3, a, b);
+      r4 = __fma_rn(r4, a, b);
+      r5 = __fma_rn(r5, a, b);
+      r6 = __fma_rn(r6, a, b);
+      r7 = __fma_rn(r7, a, b);
+    }
+  }
+  const double s = r0 + r1 + r2 + r3 + r4 + r5 + r6 + r7;
+  if (s == 1234.5678) out[0] = s;  // keep the chain alive
+}
+
+}  // namespace
+}  // namespace smc
+
+extern "C" int smc_measure_fp64_peak(int iters, double* tflops) {
+  try {
+    int dev = 0, sms = 0;
+    SMC_CUDA(cudaGetDevice(&dev));
+    SMC_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    double* d = nullptr;
+    SMC_CUDA(cudaMalloc(&d, sizeof(double)));
+    cudaEvent_t e0, e1;
+    SMC_CUDA(cudaEventCreate(&e0));
+    SMC_CUDA(cudaEventCreate(&e1));
+    const int blocks = sms * 8;
+    smc::dfma_loop<<<blocks, 256>>>(d, 16, 0.999999, 1e-7);  // warm-up
+    SMC_CHECK_LAUNCH();
+    SMC_CUDA(cudaEventRecord(e0));
+    smc::dfma_loop<<<blocks, 256>>>(d, iters, 0.999999, 1e-7);
+    SMC_CHECK_LAUNCH();
+    SMC_CUDA(cudaEventRecord(e1));
+    SMC_CUDA(cudaEventSynchronize(e1));
+    float ms = 0;
+    SMC_CUDA(cudaEventElapsedTime(&ms, e0, e1));
+    const double flops = 2.0 * 8 * 16 * static_cast<double>(iters) * blocks * 256;
+    *tflops = flops / (ms * 1e-3) / 1e12;
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    cudaFree(d);
+    return SMC_OK;
+  } catch (const std::exception&) {
+    return SMC_ECUDA;
+  }
+}

@@ -1,0 +1,506 @@
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <utility>
+
+#include "sweeps.hpp"
+
+namespace smc {
+
+// ---------------------------------------------------------------- kernels
+namespace {
+
+struct UpdateP {
+  double* next;
+  const double* cur;
+  const double* da[2];
+  const double* db[2];
+  double dc[2];
+  const double* g[kMaxTerms];
+  double w[kMaxTerms];
+  const double* pre;
+  double dt;
+  long long n;
+  int nd, ng;
+};
+
+// Grid-stride, HBM-bound.  Summation order per element follows
+// sdc.cpp:73-78 / mrsdc.cpp:110-112: cur + dtm (F_new - F_old) [+ ...] + I,
+// with I = dt * (sum_j w_j F_j) as sdc.cpp:61-68 / mrsdc.cpp:69-82.
+template <int ND, int NG>
+__global__ void __launch_bounds__(256) sweep_update_kernel(const UpdateP p) {
+  const long long stride = static_cast<long long>(gridDim.x) * blockDim.x;
+  for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < p.n;
+       i += stride) {
+    double integ;
+    if (NG == 0) {
+      integ = p.pre[i];
+    } else {
+      double acc = p.w[0] * p.g[0][i];
+#pragma unroll
+      for (int j = 1; j < NG; ++j) acc = __fma_rn(p.w[j], p.g[j][i], acc);
+      integ = __dmul_rn(p.dt, acc);
+    }
+    double v = p.cur[i];
+#pragma unroll
+    for (int d = 0; d < ND; ++d) v = __fma_rn(p.dc[d], __dsub_rn(p.da[d][i], p.db[d][i]), v);
+    p.next[i] = __dadd_rn(v, integ);
+  }
+}
+
+struct IntegralP {
+  double* out[kMaxRows];
+  const double* g[kMaxTerms];
+  double w[kMaxRows][kMaxTerms];
+  double dt;
+  long long n;
+  int rows, ng;
+};
+
+__global__ void __launch_bounds__(256) integrals_kernel(const IntegralP p) {
+  const long long stride = static_cast<long long>(gridDim.x) * blockDim.x;
+  for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < p.n;
+       i += stride) {
+    double gv[kMaxTerms];
+#pragma unroll
+    for (int j = 0; j < kMaxTerms; ++j)
+      if (j < p.ng) gv[j] = p.g[j][i];
+    for (int r = 0; r < p.rows; ++r) {
+      double acc = p.w[r][0] * gv[0];
+#pragma unroll
+      for (int j = 1; j < kMaxTerms; ++j)
+        if (j < p.ng) acc = __fma_rn(p.w[r][j], gv[j], acc);
+      p.out[r][i] = __dmul_rn(p.dt, acc);
+    }
+  }
+}
+
+struct ResidualP {
+  const double* u0;
+  const double* um;
+  const double* g[kMaxTerms];
+  double q[kMaxTerms];
+  double dt;
+  long long n;
+  int ng;
+  unsigned long long* slot;  // [0] max as bits, [1] non-finite flag
+};
+
+// sdc.cpp:20-30 / mrsdc.cpp:23-35.  Non-negative doubles order like their
+// bit patterns, so the block maxima combine with an integer atomicMax.  A
+// NaN is skipped by the max (as std::max(r, NaN) == r in the reference) but
+// raises the non-finite flag.
+__global__ void __launch_bounds__(256) residual_kernel(const ResidualP p) {
+  double r = 0.0;
+  unsigned long long bad = 0;
+  const long long stride = static_cast<long long>(gridDim.x) * blockDim.x;
+  for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < p.n;
+       i += stride) {
+    double acc = p.q[0] * p.g[0][i];
+    for (int j = 1; j < p.ng; ++j) acc = __fma_rn(p.q[j], p.g[j][i], acc);
+    const double v = fabs(__dsub_rn(__fma_rn(p.dt, acc, p.u0[i]), p.um[i]));
+    if (!isfinite(v)) bad = 1;
+    if (v > r) r = v;
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    r = fmax(r, __shfl_xor_sync(0xffffffffu, r, o));
+    bad |= __shfl_xor_sync(0xffffffffu, bad, o);
+  }
+  __shared__ double wr[8];
+  __shared__ unsigned long long wb[8];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  if (lane == 0) {
+    wr[warp] = r;
+    wb[warp] = bad;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int w = 1; w < static_cast<int>(blockDim.x >> 5); ++w) {
+      r = fmax(r, wr[w]);
+      bad |= wb[w];
+    }
+    if (isinf(r)) bad = 1;
+    atomicMax(p.slot, static_cast<unsigned long long>(__double_as_longlong(r)));
+    if (bad) atomicMax(p.slot + 1, 1ull);
+  }
+}
+
+int blocks_for(long long n) {
+  const long long want = (n + 255) / 256;
+  const long long cap = static_cast<long long>(num_sms()) * 8;
+  return static_cast<int>(std::max(1LL, std::min(want, cap)));
+}
+
+}  // namespace
+
+void launch_sweep_update(double* next, const double* cur, int nd, const double* const* da,
+                         const double* const* db, const double* dc, int ng,
+                         const double* const* g, const double* w, double dt, const double* pre,
+                         long long n, cudaStream_t st) {
+  require(nd >= 0 && nd <= 2 && ng >= 0 && ng <= kMaxTerms, "sweep update: too many terms");
+  require(ng > 0 || pre, "sweep update: no integral");
+  UpdateP p{};
+  p.next = next, p.cur = cur, p.pre = pre, p.dt = dt, p.n = n, p.nd = nd, p.ng = pre ? 0 : ng;
+  for (int d = 0; d < nd; ++d) p.da[d] = da[d], p.db[d] = db[d], p.dc[d] = dc[d];
+  for (int j = 0; j < p.ng; ++j) p.g[j] = g[j], p.w[j] = w[j];
+  const int blocks = blocks_for(n);
+#define SMC_UPD(ND, NG) \
+  sweep_update_kernel<ND, NG><<<blocks, 256, 0, st>>>(p)
+#define SMC_UPD_ND(NG)          \
+  do {                          \
+    if (nd == 0) SMC_UPD(0, NG); \
+    else if (nd == 1) SMC_UPD(1, NG); \
+    else SMC_UPD(2, NG);        \
+  } while (0)
+  switch (p.ng) {
+    case 0: SMC_UPD_ND(0); break;
+    case 1: SMC_UPD_ND(1); break;
+    case 2: SMC_UPD_ND(2); break;
+    case 3: SMC_UPD_ND(3); break;
+    case 4: SMC_UPD_ND(4); break;
+    case 5: SMC_UPD_ND(5); break;
+    case 6: SMC_UPD_ND(6); break;
+    case 7: SMC_UPD_ND(7); break;
+    case 8: SMC_UPD_ND(8); break;
+    case 9: SMC_UPD_ND(9); break;
+    default: throw InvalidArgument("sweep update: use precomputed integrals beyond 9 nodes");
+  }
+#undef SMC_UPD_ND
+#undef SMC_UPD
+  SMC_CHECK_LAUNCH();
+}
+
+void launch_integrals(int rows, double* const* out, int ng, const double* const* g,
+                      const double* w, double dt, long long n, cudaStream_t st) {
+  require(rows >= 1 && rows <= kMaxRows && ng >= 1 && ng <= kMaxTerms,
+          "integrals: table too large");
+  IntegralP p{};
+  p.rows = rows, p.ng = ng, p.dt = dt, p.n = n;
+  for (int r = 0; r < rows; ++r) {
+    p.out[r] = out[r];
+    for (int j = 0; j < ng; ++j) p.w[r][j] = w[r * ng + j];
+  }
+  for (int j = 0; j < ng; ++j) p.g[j] = g[j];
+  integrals_kernel<<<blocks_for(n), 256, 0, st>>>(p);
+  SMC_CHECK_LAUNCH();
+}
+
+void launch_residual(const double* u0, const double* um, int ng, const double* const* g,
+                     const double* q, double dt, long long n, double* slot, cudaStream_t st) {
+  require(ng >= 1 && ng <= kMaxTerms, "residual: too many terms");
+  ResidualP p{};
+  p.u0 = u0, p.um = um, p.dt = dt, p.n = n, p.ng = ng;
+  p.slot = reinterpret_cast<unsigned long long*>(slot);
+  for (int j = 0; j < ng; ++j) p.g[j] = g[j], p.q[j] = q[j];
+  residual_kernel<<<blocks_for(n), 256, 0, st>>>(p);
+  SMC_CHECK_LAUNCH();
+}
+
+void SweepDiag::add(const SweepDiag& o) {
+  residuals.insert(residuals.end(), o.residuals.begin(), o.residuals.end());
+  sweeps += o.sweeps;
+  fresh_evals += o.fresh_evals;
+  f1_evals += o.f1_evals;
+  f2_evals += o.f2_evals;
+  early_stop = early_stop || o.early_stop;
+  nonfinite = nonfinite || o.nonfinite;
+}
+
+namespace {
+
+// sdc.cpp:9-16 / mrsdc.cpp:9-16
+bool stalled(const std::vector<double>& h, double cutoff) {
+  if (cutoff <= 0.0 || h.size() < 2) return false;
+  const double prev = h[h.size() - 2], cur = h.back();
+  if (cur == 0.0) return true;
+  const double ratio = prev / cur;
+  return ratio >= 1.0 - cutoff && ratio <= 1.0 + cutoff;
+}
+
+void d2d(double* dst, const double* src, long long n, cudaStream_t st) {
+  if (dst != src)
+    SMC_CUDA(cudaMemcpyAsync(dst, src, n * sizeof(double), cudaMemcpyDeviceToDevice, st));
+}
+
+// Reads the residual slots of sweeps [first, first + count) and applies the
+// cross-rank reduction; slots are (max bits, flag) pairs.
+void collect(const DevBuf& res, int first, int count, cudaStream_t st, const Reducer& reduce,
+             SweepDiag& d) {
+  std::vector<double> h(2 * count);
+  SMC_CUDA(cudaMemcpyAsync(h.data(), res.get() + 2 * first, 2 * count * sizeof(double),
+                           cudaMemcpyDeviceToHost, st));
+  SMC_CUDA(cudaStreamSynchronize(st));
+  for (int i = 0; i < count; ++i) {
+    double r = h[2 * i];
+    unsigned long long flag;
+    std::memcpy(&flag, &h[2 * i + 1], sizeof(flag));
+    if (flag) d.nonfinite = true;
+    if (reduce) r = reduce(r);
+    d.residuals.push_back(r);
+  }
+}
+
+}  // namespace
+
+// ------------------------------------------------------------- DeviceSdc
+DeviceSdc::DeviceSdc(Nodes nodes, int iterations, double cutoff, bool reuse_first)
+    : nodes_(std::move(nodes)), iterations_(iterations), cutoff_(cutoff), reuse_first_(reuse_first) {
+  require(iterations >= 1, "SdcStepper: need at least one sweep");
+  tab_ = integration_matrices(nodes_);
+  require(nodes_.intervals() <= 8, "SdcStepper: at most 9 nodes on the device path");
+}
+
+void DeviceSdc::ensure(long long dim) {
+  if (dim == dim_) return;
+  const int m = nodes_.intervals();
+  U_.clear(), FA_.clear(), FB_.clear();
+  for (int i = 0; i <= m; ++i) U_.emplace_back(dim);
+  for (int i = 0; i < m; ++i) FA_.emplace_back(dim), FB_.emplace_back(dim);
+  F0_.resize(dim);
+  res_.resize(2 * static_cast<std::size_t>(iterations_));
+  u_.clear(), fa_.clear(), fb_.clear();
+  for (auto& b : U_) u_.push_back(b.get());
+  for (auto& b : FA_) fa_.push_back(b.get());
+  for (auto& b : FB_) fb_.push_back(b.get());
+  f0_ = F0_.get();
+  dim_ = dim;
+}
+
+// One SdcStepper::step (sdc.cpp:38-96) on the internal buffers: u_[0] holds
+// u0; F0 is valid when have_f0.  Leaves the end state in u_[M] and the final
+// node's F in f_last_.
+void DeviceSdc::run(RhsOp& f, double t_n, double dt, bool have_f0, SweepDiag& d) {
+  const int m = nodes_.intervals();
+  const long long n = dim_;
+  const auto& tau = nodes_.t;
+  cudaStream_t st = f.stream();
+  if (!have_f0) {
+    f.eval_device(t_n, u_[0], f0_);
+    ++d.fresh_evals;
+  }
+  std::vector<const double*> fold(m + 1, f0_), fnew(m + 1, f0_);
+  SMC_CUDA(cudaMemsetAsync(res_.get(), 0, res_.size() * sizeof(double), st));
+  std::vector<double> hist;
+  int collected = 0;
+  for (int k = 1; k <= iterations_; ++k) {
+    std::vector<double*>& set = (k % 2) ? fa_ : fb_;
+    for (int j = 1; j <= m; ++j) fnew[j] = set[j - 1];
+    for (int r = 0; r < m; ++r) {
+      const double dtm = (tau[r + 1] - tau[r]) * dt;
+      const double* da[1] = {fnew[r]};
+      const double* db[1] = {fold[r]};
+      const double dc[1] = {dtm};
+      const int nd = (r == 0 || fnew[r] == fold[r]) ? 0 : 1;  // m == 0 branch, sdc.cpp:74
+      launch_sweep_update(u_[r + 1], u_[r], nd, da, db, dc, m + 1, fold.data(),
+                          &tab_.s.a[static_cast<std::size_t>(r) * (m + 1)], dt, nullptr, n, st);
+      f.eval_device(t_n + tau[r + 1] * dt, u_[r + 1], set[r]);
+      ++d.fresh_evals;
+    }
+    launch_residual(u_[0], u_[m], m + 1, fnew.data(),
+                    &tab_.q.a[static_cast<std::size_t>(m - 1) * (m + 1)], dt, n, res_.get() + 2 * (k - 1),
+                    st);
+    d.sweeps = k;
+    fold = fnew;
+    if (cutoff_ > 0.0) {
+      collect(res_, k - 1, 1, st, reduce_, d);
+      collected = k;
+      if (stalled(d.residuals, cutoff_)) {
+        d.early_stop = true;
+        break;
+      }
+    }
+  }
+  if (collected < d.sweeps) collect(res_, collected, d.sweeps - collected, st, reduce_, d);
+  f_last_ = const_cast<double*>(fold[m]);
+}
+
+void DeviceSdc::step(RhsOp& f, const double* u0, double t_n, double dt, const double* f0,
+                     double* u_out, double* f_end, SweepDiag& d) {
+  ensure(f.dim());
+  const long long n = dim_;
+  cudaStream_t st = f.stream();
+  d2d(u_[0], u0, n, st);
+  const bool have = f0 && reuse_first_;
+  if (have) d2d(f0_, f0, n, st);
+  run(f, t_n, dt, have, d);
+  d2d(u_out, u_[nodes_.intervals()], n, st);
+  if (f_end) d2d(f_end, f_last_, n, st);
+}
+
+void DeviceSdc::integrate(RhsOp& f, const double* u0, double t0, double t1, int nsteps,
+                          double* u_out, SweepDiag& total) {
+  require(nsteps >= 0, "integrate_sdc: negative step count");
+  ensure(f.dim());
+  const long long n = dim_;
+  const int m = nodes_.intervals();
+  cudaStream_t st = f.stream();
+  d2d(u_[0], u0, n, st);
+  const double dt = (t1 - t0) / std::max(nsteps, 1);
+  for (int step = 0; step < nsteps; ++step) {
+    SweepDiag d;
+    run(f, t0 + step * dt, dt, step > 0 && reuse_first_, d);
+    // recycle: next u0 = U_M, next F0 = F at the last node (sdc.cpp:116-118)
+    std::swap(u_[0], u_[m]);
+    for (auto* set : {&fa_, &fb_})
+      for (auto& p : *set)
+        if (p == f_last_) std::swap(p, f0_);
+    total.add(d);
+  }
+  d2d(u_out, u_[0], n, st);
+}
+
+// ----------------------------------------------------------- DeviceMrsdc
+DeviceMrsdc::DeviceMrsdc(Hierarchy h, int iterations, double cutoff, bool reuse_first)
+    : h_(std::move(h)), iterations_(iterations), cutoff_(cutoff), reuse_first_(reuse_first) {
+  require(iterations >= 1, "MrsdcStepper: need at least one sweep");
+  require(h_.fine.intervals() <= kMaxRows, "MrsdcStepper: at most 16 fine intervals on device");
+  require(h_.coarse.count() + h_.fine.count() <= kMaxTerms,
+          "MrsdcStepper: hierarchy too large for the device path");
+}
+
+void DeviceMrsdc::ensure(long long dim) {
+  if (dim == dim_) return;
+  const int m1 = h_.coarse.intervals(), m2 = h_.fine.intervals();
+  U_.clear(), F1A_.clear(), F1B_.clear(), F2A_.clear(), F2B_.clear(), SO_.clear();
+  for (int i = 0; i <= m2; ++i) U_.emplace_back(dim);
+  for (int i = 0; i < m1; ++i) F1A_.emplace_back(dim), F1B_.emplace_back(dim);
+  for (int i = 0; i < m2; ++i) F2A_.emplace_back(dim), F2B_.emplace_back(dim), SO_.emplace_back(dim);
+  F10_.resize(dim);
+  F20_.resize(dim);
+  res_.resize(2 * static_cast<std::size_t>(iterations_));
+  auto ptrs = [](std::vector<DevBuf>& v) {
+    std::vector<double*> p;
+    for (auto& b : v) p.push_back(b.get());
+    return p;
+  };
+  u_ = ptrs(U_), f1a_ = ptrs(F1A_), f1b_ = ptrs(F1B_), f2a_ = ptrs(F2A_), f2b_ = ptrs(F2B_);
+  so_ = ptrs(SO_);
+  f10_ = F10_.get(), f20_ = F20_.get();
+  dim_ = dim;
+}
+
+// MrsdcStepper::step_mode1 (mrsdc.cpp:84-135) on the internal buffers.
+void DeviceMrsdc::run(RhsOp& f1, RhsOp& f2, double t_n, double dt, bool have1, bool have2,
+                      SweepDiag& d) {
+  const int m1 = h_.coarse.intervals(), m2 = h_.fine.intervals();
+  const long long n = dim_;
+  const auto& t1 = h_.coarse.t;
+  const auto& t2 = h_.fine.t;
+  cudaStream_t st = f2.stream();
+  require(f1.stream() == st, "mrsdc: f1 and f2 must share a stream");
+  if (!have1) {
+    f1.eval_device(t_n, u_[0], f10_);
+    ++d.f1_evals;
+  }
+  if (!have2) {
+    f2.eval_device(t_n, u_[0], f20_);
+    ++d.f2_evals;
+  }
+  std::vector<int> coarse_at(m2 + 1, -1);
+  for (int p = 0; p <= m1; ++p) coarse_at[h_.fine_of_coarse[p]] = p;
+  std::vector<const double*> o1(m1 + 1, f10_), n1(m1 + 1, f10_), o2(m2 + 1, f20_),
+      n2(m2 + 1, f20_);
+  // integral weights: row q = [s21(q, :), s22(q, :)] against [F1_old, F2_old]
+  const int ng = m1 + 1 + m2 + 1;
+  std::vector<double> w(static_cast<std::size_t>(m2) * ng);
+  for (int q = 0; q < m2; ++q) {
+    for (int j = 0; j <= m1; ++j) w[q * ng + j] = h_.s21(q, j);
+    for (int j = 0; j <= m2; ++j) w[q * ng + m1 + 1 + j] = h_.s22(q, j);
+  }
+  std::vector<double> qrow(ng);
+  for (int j = 0; j <= m1; ++j) qrow[j] = h_.q21(m2 - 1, j);
+  for (int j = 0; j <= m2; ++j) qrow[m1 + 1 + j] = h_.q22(m2 - 1, j);
+  SMC_CUDA(cudaMemsetAsync(res_.get(), 0, res_.size() * sizeof(double), st));
+  int collected = 0;
+  for (int k = 1; k <= iterations_; ++k) {
+    std::vector<double*>& s1 = (k % 2) ? f1a_ : f1b_;
+    std::vector<double*>& s2 = (k % 2) ? f2a_ : f2b_;
+    // accumulate_node_terms (mrsdc.cpp:69-82) from the previous sweep's values
+    std::vector<const double*> g(o1.begin(), o1.end());
+    g.insert(g.end(), o2.begin(), o2.end());
+    launch_integrals(m2, so_.data(), ng, g.data(), w.data(), dt, n, st);
+    for (int p = 1; p <= m1; ++p) n1[p] = o1[p];  // refreshed when the sweep reaches node p
+    for (int q = 0; q < m2; ++q) {
+      const double dtq = (t2[q + 1] - t2[q]) * dt;
+      const int p = h_.p_map[q];
+      const double* da[2];
+      const double* db[2];
+      double dc[2];
+      int nd = 0;
+      if (n1[p] != o1[p]) da[nd] = n1[p], db[nd] = o1[p], dc[nd] = dtq, ++nd;
+      if (n2[q] != o2[q]) da[nd] = n2[q], db[nd] = o2[q], dc[nd] = dtq, ++nd;
+      launch_sweep_update(u_[q + 1], u_[q], nd, da, db, dc, 0, nullptr, nullptr, dt, so_[q], n,
+                          st);
+      f2.eval_device(t_n + t2[q + 1] * dt, u_[q + 1], s2[q]);
+      n2[q + 1] = s2[q];
+      ++d.f2_evals;
+      if (const int pc = coarse_at[q + 1]; pc > 0) {
+        f1.eval_device(t_n + t1[pc] * dt, u_[q + 1], s1[pc - 1]);
+        n1[pc] = s1[pc - 1];
+        ++d.f1_evals;
+      }
+    }
+    std::vector<const double*> gn(n1.begin(), n1.end());
+    gn.insert(gn.end(), n2.begin(), n2.end());
+    launch_residual(u_[0], u_[m2], ng, gn.data(), qrow.data(), dt, n, res_.get() + 2 * (k - 1), st);
+    d.sweeps = k;
+    o1 = n1;
+    o2 = n2;
+    if (cutoff_ > 0.0) {
+      collect(res_, k - 1, 1, st, reduce_, d);
+      collected = k;
+      if (stalled(d.residuals, cutoff_)) {
+        d.early_stop = true;
+        break;
+      }
+    }
+  }
+  if (collected < d.sweeps) collect(res_, collected, d.sweeps - collected, st, reduce_, d);
+  f1_last_ = const_cast<double*>(o1[m1]);
+  f2_last_ = const_cast<double*>(o2[m2]);
+}
+
+void DeviceMrsdc::step_mode1(RhsOp& f1, RhsOp& f2, const double* u0, double t_n, double dt,
+                             const double* f01, const double* f02, double* u_out, double* f1_end,
+                             double* f2_end, SweepDiag& d) {
+  require(f1.dim() == f2.dim(), "mrsdc: f1/f2 dimension mismatch");
+  ensure(f1.dim());
+  const long long n = dim_;
+  cudaStream_t st = f2.stream();
+  d2d(u_[0], u0, n, st);
+  const bool h1 = f01 && reuse_first_, h2 = f02 && reuse_first_;
+  if (h1) d2d(f10_, f01, n, st);
+  if (h2) d2d(f20_, f02, n, st);
+  run(f1, f2, t_n, dt, h1, h2, d);
+  d2d(u_out, u_[h_.fine.intervals()], n, st);
+  if (f1_end) d2d(f1_end, f1_last_, n, st);
+  if (f2_end) d2d(f2_end, f2_last_, n, st);
+}
+
+void DeviceMrsdc::integrate_mode1(RhsOp& f1, RhsOp& f2, const double* u0, double t0, double t1,
+                                  int nsteps, double* u_out, SweepDiag& total) {
+  require(nsteps >= 0, "integrate_mrsdc: negative step count");
+  require(f1.dim() == f2.dim(), "mrsdc: f1/f2 dimension mismatch");
+  ensure(f1.dim());
+  const long long n = dim_;
+  const int m2 = h_.fine.intervals();
+  cudaStream_t st = f2.stream();
+  d2d(u_[0], u0, n, st);
+  const double dt = (t1 - t0) / std::max(nsteps, 1);
+  for (int step = 0; step < nsteps; ++step) {
+    SweepDiag d;
+    run(f1, f2, t0 + step * dt, dt, step > 0 && reuse_first_, step > 0 && reuse_first_, d);
+    std::swap(u_[0], u_[m2]);
+    for (auto* set : {&f1a_, &f1b_})
+      for (auto& p : *set)
+        if (p == f1_last_) std::swap(p, f10_);
+    for (auto* set : {&f2a_, &f2b_})
+      for (auto& p : *set)
+        if (p == f2_last_) std::swap(p, f20_);
+    total.add(d);
+  }
+  d2d(u_out, u_[0], n, st);
+}
+
+}  // namespace smc

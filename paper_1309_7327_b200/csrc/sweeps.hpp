@@ -1,0 +1,102 @@
+// Device-resident SDC / MRSDC (mode 1) sweeps, host-orchestrated.
+// Reference: SdcStepper::step / integrate_sdc (proj/core/src/sdc.cpp:38-127),
+// MrsdcStepper::step_mode1 / integrate_mrsdc (proj/core/src/mrsdc.cpp:43-135,
+// :227-259).  Node values never leave HBM; per sweep the host only reads the
+// residual (or, with early stop disabled, once per step).
+#pragma once
+
+#include <functional>
+#include <vector>
+
+#include "ops.hpp"
+#include "quadrature.hpp"
+
+namespace smc {
+
+struct SweepDiag {
+  std::vector<double> residuals;
+  int sweeps = 0;
+  int fresh_evals = 0;  // SDC
+  int f1_evals = 0, f2_evals = 0;  // MRSDC
+  bool early_stop = false;
+  bool nonfinite = false;  // a non-finite residual was seen
+  void add(const SweepDiag& o);
+};
+
+// global max over ranks of a per-rank residual (identity on one rank)
+using Reducer = std::function<double(double)>;
+
+class DeviceSdc {
+ public:
+  DeviceSdc(Nodes nodes, int iterations, double cutoff, bool reuse_first);
+  void step(RhsOp& f, const double* u0, double t_n, double dt, const double* f0, double* u_out,
+            double* f_end, SweepDiag& d);
+  void integrate(RhsOp& f, const double* u0, double t0, double t1, int nsteps, double* u_out,
+                 SweepDiag& d);
+  void set_reducer(Reducer r) { reduce_ = std::move(r); }
+  const Nodes& nodes() const { return nodes_; }
+  const SweepTables& tables() const { return tab_; }
+
+ private:
+  void ensure(long long dim);
+  void run(RhsOp& f, double t_n, double dt, bool have_f0, SweepDiag& d);
+  Nodes nodes_;
+  SweepTables tab_;
+  int iterations_;
+  double cutoff_;
+  bool reuse_first_;
+  long long dim_ = -1;
+  std::vector<DevBuf> U_, FA_, FB_;
+  DevBuf F0_, res_;
+  std::vector<double*> u_, fa_, fb_;
+  double* f0_ = nullptr;
+  double* f_last_ = nullptr;
+  Reducer reduce_;
+};
+
+class DeviceMrsdc {
+ public:
+  DeviceMrsdc(Hierarchy h, int iterations, double cutoff, bool reuse_first);
+  void step_mode1(RhsOp& f1, RhsOp& f2, const double* u0, double t_n, double dt,
+                  const double* f01, const double* f02, double* u_out, double* f1_end,
+                  double* f2_end, SweepDiag& d);
+  void integrate_mode1(RhsOp& f1, RhsOp& f2, const double* u0, double t0, double t1, int nsteps,
+                       double* u_out, SweepDiag& d);
+  void set_reducer(Reducer r) { reduce_ = std::move(r); }
+  const Hierarchy& hierarchy() const { return h_; }
+
+ private:
+  void ensure(long long dim);
+  void run(RhsOp& f1, RhsOp& f2, double t_n, double dt, bool have_f01, bool have_f02,
+           SweepDiag& d);
+  Hierarchy h_;
+  int iterations_;
+  double cutoff_;
+  bool reuse_first_;
+  long long dim_ = -1;
+  std::vector<DevBuf> U_, F1A_, F1B_, F2A_, F2B_, SO_;
+  DevBuf F10_, F20_, res_;
+  std::vector<double*> u_, f1a_, f1b_, f2a_, f2b_, so_;
+  double* f10_ = nullptr;
+  double* f20_ = nullptr;
+  double* f1_last_ = nullptr;
+  double* f2_last_ = nullptr;
+  Reducer reduce_;
+};
+
+// Pointwise sweep kernels (exposed for tests / the NS path).
+constexpr int kMaxTerms = 24;
+constexpr int kMaxRows = 16;
+// next = cur + sum_d c_d (a_d - b_d) + (pre ? pre : dt * sum_j w_j g_j)
+void launch_sweep_update(double* next, const double* cur, int nd, const double* const* da,
+                         const double* const* db, const double* dc, int ng,
+                         const double* const* g, const double* w, double dt, const double* pre,
+                         long long n, cudaStream_t st);
+// rows r: out_r = dt * sum_j w[r][j] g_j
+void launch_integrals(int rows, double* const* out, int ng, const double* const* g,
+                      const double* w /*rows x ng*/, double dt, long long n, cudaStream_t st);
+// *slot = max_i |u0 + dt sum_j q_j g_j - um|  (slot must be zeroed; NaN -> +inf)
+void launch_residual(const double* u0, const double* um, int ng, const double* const* g,
+                     const double* q, double dt, long long n, double* slot, cudaStream_t st);
+
+}  // namespace smc

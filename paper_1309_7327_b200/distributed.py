@@ -1,0 +1,122 @@
+"""Block decomposition of the periodic box into z-slabs, one per GPU, with a
+4-plane halo exchanged over NCCL (torch.distributed send/recv over NVLink /
+NVSwitch) and overlapped with the interior compute.
+
+Why z-slabs: with 256^3 cells per GPU a slab has 2 halo faces (vs 6 for a 3-D
+block), the ghost planes are contiguous in memory (no pack/unpack kernels:
+the 4 boundary planes are sent straight from the state array and received
+straight into the ghost planes), and x/y stay periodic inside the kernel.
+Weak scaling keeps 256^3 per GPU: the global box is nx x ny x (nz * N).
+
+The host logic here (neighbours, plane offsets, message order) is covered on
+CPU by tests/test_distributed_cpu.py with the gloo backend.
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+G = 4  # ghost planes (stencil half width S = 4)
+
+
+@dataclass(frozen=True)
+class Slab:
+    """Rank `rank` of `world` owns global z planes [z0, z0 + nz)."""
+    rank: int
+    world: int
+    nz: int
+    ghost: int = G
+
+    @property
+    def z0(self) -> int:
+        return self.rank * self.nz
+
+    @property
+    def prev(self) -> int:  # neighbour below (periodic)
+        return (self.rank - 1) % self.world
+
+    @property
+    def next(self) -> int:  # neighbour above (periodic)
+        return (self.rank + 1) % self.world
+
+    @property
+    def nz_global(self) -> int:
+        return self.nz * self.world
+
+    def global_planes(self):
+        """Global z index of every plane of the ghosted local array."""
+        return [(self.z0 + k - self.ghost) % self.nz_global for k in range(self.nz + 2 * self.ghost)]
+
+    # plane ranges inside the ghosted local array [0, nz + 2G)
+    def send_up(self):      # top interior planes -> next rank's bottom ghosts
+        return (self.nz, self.nz + self.ghost)
+
+    def recv_down(self):    # bottom ghosts <- prev rank's top interior planes
+        return (0, self.ghost)
+
+    def send_down(self):    # bottom interior planes -> prev rank's top ghosts
+        return (self.ghost, 2 * self.ghost)
+
+    def recv_up(self):      # top ghosts <- next rank's bottom interior planes
+        return (self.nz + self.ghost, self.nz + 2 * self.ghost)
+
+    def interior_planes(self, s: int = 4):
+        """Interior planes whose stencil needs no ghost plane."""
+        return (s, self.nz - s)
+
+
+def exchange_ops(u, slab: Slab, dist):
+    """P2P ops for one halo exchange of the ghosted array u (planes first).
+    Ordered so that, between any pair of ranks (also when prev == next at
+    world 2), the k-th send matches the k-th receive: first every rank sends
+    up / receives from below, then sends down / receives from above."""
+    a, b = slab.send_up()
+    c, d = slab.recv_down()
+    e, f = slab.send_down()
+    g, h = slab.recv_up()
+    return [dist.P2POp(dist.isend, u[a:b], slab.next),
+            dist.P2POp(dist.irecv, u[c:d], slab.prev),
+            dist.P2POp(dist.isend, u[e:f], slab.prev),
+            dist.P2POp(dist.irecv, u[g:h], slab.next)]
+
+
+def exchange_halo(u, slab: Slab, dist) -> list:
+    """Start the exchange; returns the requests.  With one rank the ghosts
+    are a periodic self-copy."""
+    if slab.world == 1:
+        a, b = slab.send_up()
+        c, d = slab.recv_down()
+        e, f = slab.send_down()
+        g, h = slab.recv_up()
+        u[c:d].copy_(u[a:b])
+        u[g:h].copy_(u[e:f])
+        return []
+    return dist.batch_isend_irecv(exchange_ops(u, slab, dist))
+
+
+class DistributedNarrow3D:
+    """configs[1]/[3]: the narrow operator on this rank's slab of a periodic
+    nx x ny x (nz * world) box.  `a_local` holds nz + 2G planes (coefficient
+    ghosts filled by the caller or by one exchange at construction)."""
+
+    def __init__(self, a_local, slab: Slab, dx, dy, dz, dist=None, choice=None, exchange_a=True):
+        import torch
+        from . import Narrow3DSlab
+        self.slab, self.dist = slab, dist
+        if exchange_a and slab.world > 1:
+            for r in exchange_halo(a_local, slab, dist):
+                r.wait()
+        elif exchange_a:
+            exchange_halo(a_local, slab, dist)
+        self.op = Narrow3DSlab(a_local, slab.nz, slab.ghost, dx, dy, dz, choice)
+        self.op.set_stream(torch.cuda.current_stream())
+
+    def apply(self, u_ghosted, out) -> None:
+        """out (nz planes) = operator(u); u's ghost planes are refreshed by an
+        exchange that overlaps the interior planes."""
+        lo, hi = self.slab.interior_planes()
+        reqs = exchange_halo(u_ghosted, self.slab, self.dist)
+        self.op.apply_planes(u_ghosted, out, lo, hi)     # needs no ghost
+        for r in reqs:
+            r.wait()                                     # current stream waits on NCCL
+        self.op.apply_planes(u_ghosted, out, 0, lo)
+        self.op.apply_planes(u_ghosted, out, hi, self.slab.nz)

@@ -1,0 +1,147 @@
+"""GPU parity of the device-resident SDC / MRSDC (mode 1) steppers against the
+reference (golden vectors from integrate_sdc / integrate_mrsdc) and the
+reference's stepper tests (proj/tests/sdc_test.cpp, mrsdc_test.cpp,
+acceptance_test.cpp c1).  Time-advance tolerance: 1e-9 of the field max
+after 10 steps (BASELINE.json north_star)."""
+import math
+
+import numpy as np
+import pytest
+
+import paper_1309_7327_b200 as P
+from conftest import rel_err
+
+pytestmark = pytest.mark.gpu
+SMC = (P.SMC_M47, P.SMC_M48)
+
+
+def _t2_op(n):
+    x = np.arange(n) * 2 * math.pi / n
+    X, Y = np.meshgrid(x, x)
+    a = 1 + 0.9 * np.cos(2 * X) * np.sin(2 * Y + math.pi / 3)
+    b = 1 + 0.9 * np.cos(2 * X + math.pi / 3) * np.sin(2 * Y)
+    return P.HeatOperator(n, n, P.StencilChoice.narrow8(*SMC), a, b)
+
+
+def test_sdc_heat_t2_ten_steps(golden, cuda):
+    nn, steps, t1, sweeps, fresh = golden["sdc_t2_meta"]
+    nn, steps = int(nn), int(steps)
+    op = _t2_op(nn)
+    st = P.SdcStepper(3, P.StepControls(4, 0.0))
+    u, d = st.integrate(op, golden["sdc_t2_u0"], 0.0, t1, steps)
+    assert rel_err(u, golden["sdc_t2_u"]) <= 1e-9
+    assert d.sweeps == int(sweeps) and d.fresh_evals == int(fresh)
+    np.testing.assert_allclose(d.residual_history, golden["sdc_t2_res"], rtol=1e-3, atol=1e-14)
+
+
+def test_sdc_device_pointers_match_host(golden, cuda):
+    import torch
+    nn, steps, t1, _, _ = golden["sdc_t2_meta"]
+    op = _t2_op(int(nn))
+    st = P.SdcStepper(3, P.StepControls(4, 0.0))
+    uh, _ = st.integrate(op, golden["sdc_t2_u0"], 0.0, t1, 3)
+    ud, _ = st.integrate(op, torch.from_numpy(golden["sdc_t2_u0"]).to(cuda), 0.0, t1, 3)
+    torch.cuda.synchronize()
+    assert np.array_equal(ud.cpu().numpy(), uh)
+
+
+def _decay(lam=-1.0):
+    calls = [0]
+
+    def f(t, u):
+        calls[0] += 1
+        return lam * u
+
+    return f, calls
+
+
+def test_collocation_fixed_point(cuda):
+    """sdc_test.cpp:48-67: 40 sweeps converge to U_end = 7/19."""
+    f, _ = _decay()
+    op = P.CallbackRhs(1, f)
+    st = P.SdcStepper(3, P.StepControls(40, 0.0))
+    u, fe, d = st.step(op, np.array([1.0]), 0.0, 1.0)
+    assert abs(u[0] - 7.0 / 19.0) < 1e-12
+    assert d.residual_history[-1] < 1e-13
+
+
+@pytest.mark.parametrize("case", ["unseeded", "seeded", "reuse_off", "integrate"])
+def test_eval_counts(cuda, case):
+    """sdc_test.cpp:101-140: K*M (+1) fresh evaluations."""
+    f, calls = _decay()
+    op = P.CallbackRhs(1, f)
+    c = P.StepControls(3, 0.0, case != "reuse_off")
+    st = P.SdcStepper(3, c)
+    if case == "unseeded":
+        _, _, d = st.step(op, np.array([1.0]), 0.0, 0.1)
+        assert d.fresh_evals == 7 and calls[0] == 7
+    elif case in ("seeded", "reuse_off"):
+        _, _, d = st.step(op, np.array([1.0]), 0.0, 0.1, f0=np.array([-1.0]))
+        assert d.fresh_evals == (6 if case == "seeded" else 7)
+    else:
+        u, d = st.integrate(op, np.array([1.0]), 0.0, 1.0, 4)
+        assert d.fresh_evals == 4 * 6 + 1 and calls[0] == d.fresh_evals
+        assert abs(u[0] - math.exp(-1.0)) < 1e-3
+
+
+def test_early_stop(cuda):
+    """sdc_test.cpp:142-163: residual stalls at the cutoff."""
+    f, _ = _decay()
+    st = P.SdcStepper(3, P.StepControls(50, 0.05))
+    _, _, d = st.step(P.CallbackRhs(1, f), np.array([1.0]), 0.0, 0.5)
+    assert d.early_stop and d.sweeps < 50 and len(d.residual_history) == d.sweeps
+    assert d.residual_history[1] < d.residual_history[0]
+
+
+def test_mrsdc_golden(golden, cuda):
+    l1 = np.array([-1.0, -0.5, -2.0])
+    l2 = np.array([-10.0, -4.0, -7.0])
+    f1 = P.CallbackRhs(3, lambda t, u: l1 * u)
+    f2 = P.CallbackRhs(3, lambda t, u: l2 * u + 0.1 * math.sin(t))
+    st = P.MrsdcStepper(3, 5, P.StepControls(4, 0.0))
+    u, d = st.integrate_mode1(f1, f2, golden["mr_u0"], 0.0, 0.4, 4)
+    sw, n1, n2 = (int(v) for v in golden["mr_meta"])
+    assert (d.sweeps, d.f1_evals, d.f2_evals) == (sw, n1, n2)
+    assert rel_err(u, golden["mr_u"]) <= 1e-13
+    np.testing.assert_allclose(d.residual_history, golden["mr_res"], rtol=1e-6, atol=1e-16)
+
+
+def test_mrsdc_counts_and_degenerate(cuda):
+    """mrsdc_test.cpp:46-105."""
+    f1 = P.CallbackRhs(1, lambda t, u: -1.0 * u)
+    f2 = P.CallbackRhs(1, lambda t, u: -10.0 * u)
+    st = P.MrsdcStepper(3, 5, P.StepControls(4, 0.0))
+    _, _, _, d = st.step_mode1(f1, f2, np.array([1.0]), 0.0, 0.05, np.array([-1.0]),
+                               np.array([-10.0]))
+    assert d.f1_evals == 8 and d.f2_evals == 32
+    _, _, _, d = st.step_mode1(f1, f2, np.array([1.0]), 0.0, 0.05)
+    assert d.f1_evals == 9 and d.f2_evals == 33
+    # degenerate fine level (TypeB{GL(2)}) collapses onto the coarse sweep
+    zero = P.CallbackRhs(1, lambda t, u: 0.0 * u)
+    mr = P.MrsdcStepper(3, 2, P.StepControls(4, 0.0))
+    u_mr, _, _, _ = mr.step_mode1(P.CallbackRhs(1, lambda t, u: -u), zero, np.array([1.0]), 0.0,
+                                  0.3)
+    sd = P.SdcStepper(3, P.StepControls(4, 0.0))
+    u_sr, _, _ = sd.step(P.CallbackRhs(1, lambda t, u: -u), np.array([1.0]), 0.0, 0.3)
+    assert abs(u_mr[0] - u_sr[0]) <= 1e-15
+
+
+def test_acceptance_c1_t1_error_table(cuda):
+    """acceptance_test.cpp:61-93 (c1) on the GPU path: T1, SMC stencil,
+    L-inf at 20^2 / 40^2 within 2% of PAPER.md:1606-1607."""
+    expected = {20: 4.167e-8, 40: 1.721e-10}
+    for n, target in expected.items():
+        eps = 0.1
+        x = np.arange(n) * 2 * math.pi / n
+        X, Y = np.meshgrid(x, x)
+        a = 1 + eps * np.cos(X) * np.cos(Y)
+        op = P.HeatOperator(n, n, P.StencilChoice.narrow8(*SMC), a, a,
+                            (1 + 4 * eps * np.cos(X) * np.cos(Y)) * np.sin(X) * np.sin(Y),
+                            lambda t: math.exp(-t))
+        dx = 2 * math.pi / n
+        dt_hint = 0.4 / ((2 / dx ** 2) * a.max())  # appendix_dt (pde.cpp:294-301)
+        steps = math.ceil(1.0 / dt_hint - 1e-9)
+        st = P.SdcStepper(3, P.StepControls(4, 0.0))
+        u, _ = st.integrate(op, np.sin(X) * np.sin(Y), 0.0, 1.0, steps)
+        err = np.abs(u - math.exp(-1.0) * np.sin(X) * np.sin(Y)).max()
+        assert abs(err - target) <= 0.02 * target, (n, err)
