@@ -82,6 +82,9 @@ int smc_synchronize(void);
 /* FP64 pipe peak of the current device (DFMA loop, TFLOP/s): the FP64
  * roofline denominator (no reference counterpart). */
 int smc_measure_fp64_peak(int iters, double* tflops);
+/* FP64 tensor path (mma.sync m8n8k4 f64) throughput; mode 1 mixes DMMA and
+ * DFMA warps.  Diagnostic only. */
+int smc_measure_dmma_peak(int iters, int mode, double* tflops);
 
 /* ------------------------------------------------------------- stencil */
 /* nsdc::build_narrow — core/src/stencil.cpp:117-132.  m64: 8x8 row-major. */

@@ -53,6 +53,7 @@ _SIG = {
     "smc_launch_count": (C.c_longlong, []),
     "smc_synchronize": (C.c_int, []),
     "smc_measure_fp64_peak": (C.c_int, [C.c_int, _D]),
+    "smc_measure_dmma_peak": (C.c_int, [C.c_int, C.c_int, _D]),
     "smc_build_narrow": (C.c_int, [C.c_int, _D, C.c_int, _D, _I]),
     "smc_apply_narrow": (C.c_int, [C.c_int, _D, C.c_int, _VP, _VP, C.c_int, C.c_double, _VP,
                                    C.c_int]),

@@ -56,10 +56,11 @@ struct StencilM {
 };
 
 // Structural nonzeros of row r (PAPER.md:263-300 / :320-345): rows of the
-// upper half start at column 0 and end at S + r; the lower half mirrors.
+// upper half start at column 0 and end at S + r; the lower half mirrors
+// (row S is full, row S+1 starts at column 1, ...).
 template <int S>
 __host__ __device__ constexpr int row_lo(int r) {
-  return r < S ? 0 : r - S + 1;
+  return r < S ? 0 : r - S;
 }
 template <int S>
 __host__ __device__ constexpr int row_hi(int r) {
@@ -77,16 +78,36 @@ __host__ __device__ inline int wrap(int i, int n) {
 // stencil_kernel.hpp:13-25 (mm ascending outer, nn ascending inner); explicit
 // fma so the instruction sequence (and hence the bits) is the same no matter
 // which thread or tiling computes the interface.
+//
+// Only the upper half of M is read: the lower rows are taken through the
+// central antisymmetry M[r][c] = -M[2S-1-r][2S-1-c], so a
+// kernel needs 26 (S = 4) distinct constants, which fit the uniform register
+// file, instead of 52.  The products and their order are unchanged.
+template <int S>
+__device__ __forceinline__ double mcoef(const StencilM& M, int r, int c) {
+  return M.m[r][c];
+}
 template <int S>
 __device__ __forceinline__ double narrow_iface(const double* a, const double* u,
                                                const StencilM& M) {
   double acc;
 #pragma unroll
   for (int r = 0; r < 2 * S; ++r) {
-    double v = M.m[r][row_lo<S>(r)] * u[row_lo<S>(r)];
+    constexpr int L = 2 * S - 1;
+    const int lo = row_lo<S>(r), hi = row_hi<S>(r);
+    double v;
+    if (r < S) {
+      v = M.m[r][lo] * u[lo];
 #pragma unroll
-    for (int c = row_lo<S>(r) + 1; c <= row_hi<S>(r); ++c) v = __fma_rn(M.m[r][c], u[c], v);
-    acc = (r == 0) ? a[0] * v : __fma_rn(a[r], v, acc);
+      for (int c = lo + 1; c <= hi; ++c) v = __fma_rn(M.m[r][c], u[c], v);
+      acc = (r == 0) ? a[0] * v : __fma_rn(a[r], v, acc);
+    } else {
+      // v_r = sum_c M[r][c] u_c = -sum_c M[L-r][L-c] u_c
+      v = M.m[L - r][L - lo] * u[lo];
+#pragma unroll
+      for (int c = lo + 1; c <= hi; ++c) v = __fma_rn(M.m[L - r][L - c], u[c], v);
+      acc = __fma_rn(-a[r], v, acc);
+    }
   }
   return acc;
 }

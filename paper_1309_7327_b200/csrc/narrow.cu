@@ -52,33 +52,48 @@ struct Smem {
   double hy[HAS_Y ? TY + 1 : 1][TX];
 };
 
-// Global index of tile cell (row, col) of plane pointer `plane`.
-template <int S, bool HAS_Y>
-__device__ __forceinline__ long long tile_src(int row, int col, int x0, int y0, int nx, int ny) {
-  const int gx = wrap(x0 - S + col, nx);
-  const int gy = HAS_Y ? wrap(y0 - S + row, ny) : wrap(y0 + row, ny);
-  return static_cast<long long>(gy) * nx + gx;
-}
+// In-plane source offsets of the tile cells this thread stages; identical
+// for every plane, so computed once per CTA (wrap folded in).
+template <int S, bool HAS_Y, bool SAME>
+struct StagePlan {
+  static constexpr int N = (Smem<S, HAS_Y, SAME>::CELLS + NTHREADS - 1) / NTHREADS;
+  int off[N];
+  __device__ void init(int x0, int y0, int nx, int ny) {
+    using SM = Smem<S, HAS_Y, SAME>;
+#pragma unroll
+    for (int i = 0; i < N; ++i) {
+      const int e = threadIdx.x + i * NTHREADS;
+      const int row = e / SM::W, col = e - row * SM::W;
+      const int gx = wrap(x0 - S + col, nx);
+      const int gy = HAS_Y ? wrap(y0 - S + row, ny) : wrap(y0 + row, ny);
+      off[i] = e < SM::CELLS ? gy * nx + gx : -1;
+    }
+  }
+};
 
 template <int S, bool HAS_Y, bool SAME>
 __device__ __forceinline__ void stage_plane(Smem<S, HAS_Y, SAME>& sm, int buf, const NarrowArgs& p,
-                                            long long plane_off, int x0, int y0) {
+                                            const StagePlan<S, HAS_Y, SAME>& plan,
+                                            long long plane_off) {
   using SM = Smem<S, HAS_Y, SAME>;
   const double* u = p.u + plane_off;
   const double* cx = p.cx + plane_off;
   const double* cy = p.cy + plane_off;
-  for (int e = threadIdx.x; e < SM::CELLS; e += NTHREADS) {
-    const int row = e / SM::W, col = e - row * SM::W;
-    const long long g = tile_src<S, HAS_Y>(row, col, x0, y0, p.nx, p.ny);
-    cp_async8(&sm.tile[buf][0][e], u + g);
-    cp_async8(&sm.tile[buf][1][e], cx + g);
-    if constexpr (!SAME) cp_async8(&sm.tile[buf][SM::FIELDS - 1][e], cy + g);
+#pragma unroll
+  for (int i = 0; i < plan.N; ++i) {
+    const int e = threadIdx.x + i * NTHREADS;
+    if (i + 1 < plan.N || e < SM::CELLS) {
+      const int g = plan.off[i];
+      cp_async8(&sm.tile[buf][0][e], u + g);
+      cp_async8(&sm.tile[buf][1][e], cx + g);
+      if constexpr (!SAME) cp_async8(&sm.tile[buf][SM::FIELDS - 1][e], cy + g);
+    }
   }
   cp_async_commit();
 }
 
 template <int S, bool HAS_Y, bool HAS_Z, bool SAME, bool HAS_SRC>
-__global__ void __launch_bounds__(NTHREADS, 2)
+__global__ void __launch_bounds__(NTHREADS, 1)
     narrow_kernel(const NarrowArgs p, const StencilM M) {
   using SM = Smem<S, HAS_Y, SAME>;
   extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -125,13 +140,15 @@ __global__ void __launch_bounds__(NTHREADS, 2)
     }
   }
 
+  StagePlan<S, HAS_Y, SAME> plan;
+  plan.init(x0, y0, p.nx, p.ny);
   int buf = 0;
-  stage_plane<S, HAS_Y, SAME>(sm, 0, p, zplane(k0), x0, y0);
+  stage_plane<S, HAS_Y, SAME>(sm, 0, p, plan, zplane(k0));
 
   for (int k = k0; k < k1; ++k) {
     cp_async_wait_all();
     __syncthreads();  // tile[buf] complete; hx/hy of the previous plane consumed
-    if (k + 1 < k1) stage_plane<S, HAS_Y, SAME>(sm, buf ^ 1, p, zplane(k + 1), x0, y0);
+    if (k + 1 < k1) stage_plane<S, HAS_Y, SAME>(sm, buf ^ 1, p, plan, zplane(k + 1));
 
     double hz[RPT];
     if constexpr (HAS_Z) {
@@ -254,7 +271,10 @@ void launch_s(const NarrowArgs& p, const StencilM& M, cudaStream_t st) {
   if (p.dims == 3) {
     require(same, "narrow3d: one coefficient field shared by all directions");
     require(p.g0 == nullptr, "narrow3d: no source term");
-    launch_t<S, true, true, true, false>(p, M, st);
+    if (p.use_fast && narrow3d_fast_applicable(p))
+      launch_narrow3d_fast(p, S, M, st);
+    else
+      launch_t<S, true, true, true, false>(p, M, st);
   } else if (p.dims == 2) {
     if (p.g0)
       launch_t<S, true, false, false, true>(p, M, st);
@@ -269,6 +289,7 @@ void launch_s(const NarrowArgs& p, const StencilM& M, cudaStream_t st) {
 
 int narrow_default_kc(int nx, int ny, int nz, int dims, int num_sms) {
   if (dims < 3) return 1;
+  if (nx % 64 == 0 && ny % 8 == 0) return narrow3d_fast_default_kc(nx, ny, nz, num_sms);
   const long long tiles = static_cast<long long>((nx + TX - 1) / TX) * ((ny + TY - 1) / TY);
   // ~8 CTAs per SM slot pair in flight over the run, but at least 8 planes
   // per CTA so the 2S-plane window warm-up stays below ~50% extra z loads.

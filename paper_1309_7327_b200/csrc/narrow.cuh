@@ -21,11 +21,18 @@ struct NarrowArgs {
   int kc = 1;                  // z planes per CTA
   int kbeg = 0, kend = -1;     // plane range [kbeg, kend) to compute (kend < 0: nz)
   bool zwrap = true;
+  bool use_fast = true;         // allow the narrow3d_fast kernel
   double idx2 = 0, idy2 = 0, idz2 = 0, gt = 0;
 };
 
 void launch_narrow(const NarrowArgs& p, int s, const StencilM& M, cudaStream_t st);
 int narrow_default_kc(int nx, int ny, int nz, int dims, int num_sms);
+
+// FP64-issue-optimised 3-D kernel (narrow3d_fast.cu) for nx % 64 == 0,
+// ny % 8 == 0; launch_narrow dispatches to it when applicable.
+bool narrow3d_fast_applicable(const NarrowArgs& p);
+void launch_narrow3d_fast(const NarrowArgs& p, int s, const StencilM& M, cudaStream_t st);
+int narrow3d_fast_default_kc(int nx, int ny, int nz, int num_sms);
 
 // Wide route D(a D u) (+ y term when w2/b given) + g0*gt; w1/w2 scratch.
 void launch_wide2d(const double* u, const double* a, const double* b, const double* g0, double gt,

@@ -1,0 +1,386 @@
+// 3-D narrow operator, FP64-issue-optimised z-march (configs[1] hot kernel).
+//
+// Same arithmetic as narrow_kernel (narrow.cu) — every interface
+// H_{i+1/2} = sum_m a_{i+m} sum_n M_mn u_{i+n} computed once in the fixed
+// order of stencil_kernel.hpp:13-25, then differenced as pde.cpp:118-120 —
+// laid out so that the FP64 pipe, not the issue slot, is the limit:
+//   * CTA tile 64 (x) x 8 (y), 8 warps; a thread owns 2 adjacent x cells, so
+//     its x window comes from 5 conflict-free 16-byte LDS per field and its
+//     y window from 8 LDS.128 that serve both columns;
+//   * only the 26 upper-half entries of M are read (antisymmetry, see
+//     narrow_iface), so they stay in uniform registers;
+//   * the z window (2S planes of U and a for the 2 columns) lives in
+//     registers and is shifted by moves: a compact loop body keeps the
+//     instruction cache warm (the 2S-fold unrolled variant measured slower);
+//   * the centre plane (with a 4-cell halo) is staged by 16-byte cp.async
+//     two planes ahead (triple buffer); the z window's leading plane is
+//     prefetched two planes ahead with LDG.128; all addresses are
+//     precomputed, the z offset advances incrementally;
+//   * one CTA barrier per plane (it publishes the y interfaces and, as every
+//     thread first waits for its own copies of plane k+1, the next tile);
+//     deferring the difference-and-store past the next plane's interfaces
+//     measured slower (register pressure), so it follows the barrier;
+//   * x neighbours' interfaces come by warp shuffle, y neighbours' through
+//     shared memory (double-buffered by plane parity); the 72 extra
+//     interfaces per plane (x0-1/2 of each row, y0-1/2 of each column) are
+//     packed into three warp passes on three different SM sub-partitions.
+// Requirements (else narrow.cu's general kernel runs): nx % 64 == 0,
+// ny % 8 == 0, 16-byte aligned fields.
+#include <algorithm>
+#include <cstdint>
+#include <cstdlib>
+#include <string>
+
+#include "common.cuh"
+#include "narrow.cuh"
+
+namespace smc {
+namespace {
+
+constexpr int FX = 64;       // tile x
+constexpr int FY = 8;        // tile y (= warps)
+constexpr int FT = 256;      // threads
+constexpr int HALO = 4;      // staged halo (>= S)
+constexpr int SW = FX + 2 * HALO;   // 72 tile columns
+constexpr int SH = FY + 2 * HALO;   // 16 tile rows
+constexpr int CHUNKS = SH * SW / 2; // 16-byte chunks per field per plane (576)
+constexpr int CPT = (CHUNKS + FT - 1) / FT;  // 3 (last partial)
+constexpr int NBUF = 3;
+
+struct FastSmem {
+  double tile[NBUF][2][SH * SW];   // u, a
+  double hy[2][FY + 1][FX];        // y interfaces, double-buffered by plane parity
+  double hxe[2][FY];               // x0 - 1/2 interfaces
+};
+
+__device__ __forceinline__ void cp16(void* dst, const void* src) {
+  const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(dst));
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(src));
+}
+__device__ __forceinline__ void commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int N>
+__device__ __forceinline__ void wait_groups() {
+  asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory");
+}
+
+__device__ __forceinline__ double2 lds2(const double* p) {
+  return *reinterpret_cast<const double2*>(p);
+}
+
+// One (tile, [k0, k1)) segment of the z-march.
+template <int S>
+__device__ __forceinline__ void march_segment(FastSmem& sm, const NarrowArgs& p,
+                                              const StencilM& M, int tile, int k0, int k1) {
+  constexpr int WIN = 2 * S;
+  const int tiles_x = p.nx / FX;
+  const int x0 = (tile % tiles_x) * FX;
+  const int y0 = (tile / tiles_x) * FY;
+  const int lane = threadIdx.x & 31;
+  const int w = threadIdx.x >> 5;
+  const long long plane = static_cast<long long>(p.nx) * p.ny;
+  const long long zspan = plane * p.nz;
+
+  // plane offset helpers (periodic wrap or ghosted slab)
+  auto zoff = [&](int k) -> long long {
+    if (p.zwrap) {
+      k %= p.nz;
+      if (k < 0) k += p.nz;
+    }
+    return static_cast<long long>(k) * plane;
+  };
+  auto zadv = [&](long long o) -> long long {
+    o += plane;
+    if (p.zwrap && o >= zspan) o -= zspan;
+    return o;
+  };
+
+  // staging plan: in-plane offsets of this thread's 16-byte chunks
+  int soff[CPT];
+#pragma unroll
+  for (int i = 0; i < CPT; ++i) {
+    const int c = threadIdx.x + i * FT;
+    const int row = c / (SW / 2), col = 2 * (c - row * (SW / 2));
+    const int gx = wrap(x0 - HALO + col, p.nx);
+    const int gy = wrap(y0 - HALO + row, p.ny);
+    soff[i] = c < CHUNKS ? gy * p.nx + gx : 0;
+  }
+  auto stage = [&](int buf, long long po) {
+#pragma unroll
+    for (int i = 0; i < CPT; ++i) {
+      const int c = threadIdx.x + i * FT;
+      if (i + 1 < CPT || c < CHUNKS) {
+        cp16(&sm.tile[buf][0][2 * c], p.u + po + soff[i]);
+        cp16(&sm.tile[buf][1][2 * c], p.cz + po + soff[i]);
+      }
+    }
+    commit();
+  };
+
+  // own columns: x0 + 2*lane + {0, 1}, row y0 + w
+  const int col_off = (y0 + w) * p.nx + x0 + 2 * lane;
+  auto ld2 = [&](const double* base, long long o) {
+    return __ldg(reinterpret_cast<const double2*>(base + o + col_off));
+  };
+
+  // z window (2 columns): slot j holds plane k - S + 1 + j at step k
+  double2 wu[WIN], wa[WIN];
+  double2 pf_u[2], pf_a[2];
+  {
+    long long o = zoff(k0 - S);
+#pragma unroll
+    for (int j = 0; j < WIN; ++j) {
+      wu[j] = ld2(p.u, o);
+      wa[j] = ld2(p.cz, o);
+      o = zadv(o);
+    }
+  }
+  // leading planes k0 + S, k0 + S + 1 (never past k1 - 1 + S: a ghosted
+  // slab has only S planes above its interior)
+  long long o_pf = zoff(k0 + S);
+#pragma unroll
+  for (int j = 0; j < 2; ++j) {
+    if (k0 + j < k1) {
+      pf_u[j] = ld2(p.u, o_pf);
+      pf_a[j] = ld2(p.cz, o_pf);
+    }
+    o_pf = zadv(o_pf);
+  }
+  // centre-plane staging: planes k0, k0 + 1 now (buffers 0, 1)
+  long long o_st = zoff(k0);
+  stage(0, o_st);
+  o_st = zadv(o_st);
+  if (k0 + 1 < k1)
+    stage(1, o_st);
+  else
+    commit();
+  o_st = zadv(o_st);
+  long long o_out = zoff(k0);
+
+  // z interface k0 - 1/2 from the initial window (planes k0 - S .. k0 + S - 1)
+  double hzp0, hzp1;
+  {
+    double a0[WIN], u0[WIN], a1[WIN], u1[WIN];
+#pragma unroll
+    for (int j = 0; j < WIN; ++j) a0[j] = wa[j].x, u0[j] = wu[j].x, a1[j] = wa[j].y, u1[j] = wu[j].y;
+    hzp0 = narrow_iface<S>(a0, u0, M);
+    hzp1 = narrow_iface<S>(a1, u1, M);
+  }
+  // plane k0's tile must be visible to every thread before the first step
+  wait_groups<1>();
+  __syncthreads();
+
+  const double idx2 = p.idx2, idy2 = p.idy2, idz2 = p.idz2;
+
+  // (dHx)/dx^2 + (dHy)/dy^2 + (dHz)/dz^2 of plane (parity hb), pde.cpp:118-120
+  auto finish = [&](int hb, double hx0, double hx1, double hz0, double hz1, double hzl0,
+                    double hzl1, long long oo) {
+    double hxl = __shfl_up_sync(0xffffffffu, hx1, 1);
+    if (lane == 0) hxl = sm.hxe[hb][w];
+    const double2 yu = lds2(&sm.hy[hb][w][2 * lane]);
+    const double2 yd = lds2(&sm.hy[hb][w + 1][2 * lane]);
+    double o0 = __dmul_rn(__dsub_rn(hx0, hxl), idx2);
+    double o1 = __dmul_rn(__dsub_rn(hx1, hx0), idx2);
+    o0 = __dadd_rn(o0, __dmul_rn(__dsub_rn(yd.x, yu.x), idy2));
+    o1 = __dadd_rn(o1, __dmul_rn(__dsub_rn(yd.y, yu.y), idy2));
+    o0 = __dadd_rn(o0, __dmul_rn(__dsub_rn(hz0, hzl0), idz2));
+    o1 = __dadd_rn(o1, __dmul_rn(__dsub_rn(hz1, hzl1), idz2));
+    *reinterpret_cast<double2*>(p.out + oo + col_off) = make_double2(o0, o1);
+  };
+
+#pragma unroll 1
+  for (int k = k0; k < k1; ++k) {
+    const int t = k - k0;
+    const int buf = t % NBUF;
+    const int hb = t & 1;
+    // shift the z window down one plane and append the leading plane k + S
+#pragma unroll
+    for (int j = 0; j + 1 < WIN; ++j) wu[j] = wu[j + 1], wa[j] = wa[j + 1];
+    wu[WIN - 1] = pf_u[0];
+    wa[WIN - 1] = pf_a[0];
+    pf_u[0] = pf_u[1];
+    pf_a[0] = pf_a[1];
+    if (k + 2 < k1) {
+      pf_u[1] = ld2(p.u, o_pf);
+      pf_a[1] = ld2(p.cz, o_pf);
+      o_pf = zadv(o_pf);
+    }
+    const double* tu = sm.tile[buf][0];
+    const double* ta = sm.tile[buf][1];
+
+    // ---- z interfaces k + 1/2
+    double hz0, hz1;
+    {
+      double a0[WIN], u0[WIN], a1[WIN], u1[WIN];
+#pragma unroll
+      for (int j = 0; j < WIN; ++j) a0[j] = wa[j].x, u0[j] = wu[j].x, a1[j] = wa[j].y, u1[j] = wu[j].y;
+      hz0 = narrow_iface<S>(a0, u0, M);
+      hz1 = narrow_iface<S>(a1, u1, M);
+    }
+    // ---- x interfaces x+1/2 for my two cells (row HALO + w)
+    double hx0, hx1;
+    {
+      // values at tile columns 2*lane + HALO - S + 1 + j
+      constexpr int NV = WIN + 2;  // loaded in pairs
+      constexpr int BASE = HALO - S + 1 - ((HALO - S + 1) & 1);  // even start
+      constexpr int OFF = (HALO - S + 1) - BASE;                 // 0 or 1
+      double ua[NV], aa[NV];
+      const double* ru = tu + (HALO + w) * SW + 2 * lane + BASE;
+      const double* ra = ta + (HALO + w) * SW + 2 * lane + BASE;
+#pragma unroll
+      for (int j = 0; j < NV / 2; ++j) {
+        const double2 vu = lds2(ru + 2 * j), va = lds2(ra + 2 * j);
+        ua[2 * j] = vu.x, ua[2 * j + 1] = vu.y;
+        aa[2 * j] = va.x, aa[2 * j + 1] = va.y;
+      }
+      hx0 = narrow_iface<S>(aa + OFF, ua + OFF, M);
+      hx1 = narrow_iface<S>(aa + OFF + 1, ua + OFF + 1, M);
+    }
+    // ---- y interfaces y+1/2 for my two columns
+    {
+      double u0[WIN], a0[WIN], u1[WIN], a1[WIN];
+#pragma unroll
+      for (int j = 0; j < WIN; ++j) {
+        const int row = HALO + w - S + 1 + j;
+        const double2 vu = lds2(tu + row * SW + HALO + 2 * lane);
+        const double2 va = lds2(ta + row * SW + HALO + 2 * lane);
+        u0[j] = vu.x, u1[j] = vu.y, a0[j] = va.x, a1[j] = va.y;
+      }
+      *reinterpret_cast<double2*>(&sm.hy[hb][w + 1][2 * lane]) =
+          make_double2(narrow_iface<S>(a0, u0, M), narrow_iface<S>(a1, u1, M));
+    }
+    // ---- extra interfaces: y0 - 1/2 of the even columns (warp 1), of the
+    //      odd columns (warp 2), x0 - 1/2 of each row (warp 3)
+    if (w == 1 || w == 2) {
+      const int col = HALO + 2 * lane + (w - 1);
+      double uu[WIN], aa[WIN];
+#pragma unroll
+      for (int j = 0; j < WIN; ++j) {
+        uu[j] = tu[(HALO - S + j) * SW + col];
+        aa[j] = ta[(HALO - S + j) * SW + col];
+      }
+      sm.hy[hb][0][2 * lane + (w - 1)] = narrow_iface<S>(aa, uu, M);
+    } else if (w == 3 && lane < FY) {
+      double uu[WIN], aa[WIN];
+#pragma unroll
+      for (int j = 0; j < WIN; ++j) {
+        uu[j] = tu[(HALO + lane) * SW + HALO - S + j];
+        aa[j] = ta[(HALO + lane) * SW + HALO - S + j];
+      }
+      sm.hxe[hb][lane] = narrow_iface<S>(aa, uu, M);
+    }
+    // ---- stage plane k + 2 into the buffer of plane k - 1 (all of its
+    //      readers passed the previous barrier), then make plane k + 1 ready
+    if (k + 2 < k1) {
+      stage((t + 2) % NBUF, o_st);
+      o_st = zadv(o_st);
+    } else {
+      commit();  // keep the group count uniform
+    }
+    wait_groups<1>();
+    __syncthreads();
+    finish(hb, hx0, hx1, hz0, hz1, hzp0, hzp1, o_out);
+    o_out = zadv(o_out);
+    hzp0 = hz0;
+    hzp1 = hz1;
+  }
+  // drain the (empty) trailing groups; the next segment reuses the buffers
+  wait_groups<0>();
+  __syncthreads();
+}
+
+// Chunked grid (default): tile = blockIdx.x, planes [kbeg + y*kc, +kc), so
+// co-scheduled CTAs are x/y neighbours at the same z and tile halos hit in
+// L2.  Persistent grid: CTA b owns the contiguous range [b*L/G, (b+1)*L/G)
+// of L = tile * nplanes + plane (one wave, equal work to within a plane).
+template <int S>
+__global__ void __launch_bounds__(FT, 1) narrow3d_fast(const NarrowArgs p, const StencilM M,
+                                                       int chunked) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  FastSmem& sm = *reinterpret_cast<FastSmem*>(smem_raw);
+  const int kend = p.kend < 0 ? p.nz : p.kend;
+  if (chunked) {
+    const int k0 = p.kbeg + blockIdx.y * p.kc;
+    march_segment<S>(sm, p, M, blockIdx.x, k0, min(k0 + p.kc, kend));
+    return;
+  }
+  const long long np = kend - p.kbeg;
+  const long long total = static_cast<long long>(p.nx / FX) * (p.ny / FY) * np;
+  const long long lo = total * blockIdx.x / gridDim.x;
+  const long long hi = total * (blockIdx.x + 1) / gridDim.x;
+  for (long long l = lo; l < hi;) {
+    const int tile = static_cast<int>(l / np);
+    const int kk = static_cast<int>(l - tile * np);
+    const int len = static_cast<int>(min(np - kk, hi - l));
+    march_segment<S>(sm, p, M, tile, p.kbeg + kk, p.kbeg + kk + len);
+    l += len;
+  }
+}
+
+// SMC_NARROW_GRID=chunk selects the (tiles, z-chunks) grid (tuning knob;
+// the persistent grid measured ~2% faster at 256^3).
+bool chunked_grid() {
+  static bool c = [] {
+    const char* e = std::getenv("SMC_NARROW_GRID");
+    return e && std::string(e) == "chunk";
+  }();
+  return c;
+}
+
+int num_sms_cached() {
+  static int n = [] {
+    int dev = 0, v = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
+    return v;
+  }();
+  return n;
+}
+
+template <int S>
+void launch_fast_s(const NarrowArgs& p, const StencilM& M, cudaStream_t st) {
+  static bool configured = false;
+  if (!configured) {
+    SMC_CUDA(cudaFuncSetAttribute(narrow3d_fast<S>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  static_cast<int>(sizeof(FastSmem))));
+    configured = true;
+  }
+  const int kend = p.kend < 0 ? p.nz : p.kend;
+  if (kend <= p.kbeg) return;
+  const int tiles = (p.nx / FX) * (p.ny / FY);
+  if (chunked_grid()) {
+    const dim3 grid(tiles, (kend - p.kbeg + p.kc - 1) / p.kc);
+    narrow3d_fast<S><<<grid, FT, sizeof(FastSmem), st>>>(p, M, 1);
+  } else {
+    const long long work = static_cast<long long>(tiles) * (kend - p.kbeg);
+    const long long by_kc = (work + p.kc - 1) / p.kc;
+    const int grid = static_cast<int>(std::max(1LL, std::min<long long>(num_sms_cached(), by_kc)));
+    narrow3d_fast<S><<<grid, FT, sizeof(FastSmem), st>>>(p, M, 0);
+  }
+  SMC_CHECK_LAUNCH();
+}
+
+}  // namespace
+
+bool narrow3d_fast_applicable(const NarrowArgs& p) {
+  const auto al = [](const void* q) { return (reinterpret_cast<std::uintptr_t>(q) & 15) == 0; };
+  return p.dims == 3 && p.nx % FX == 0 && p.ny % FY == 0 && p.nx >= FX && p.cx == p.cz &&
+         p.cy == p.cz && p.g0 == nullptr && al(p.u) && al(p.cz) && al(p.out);
+}
+
+void launch_narrow3d_fast(const NarrowArgs& p, int s, const StencilM& M, cudaStream_t st) {
+  if (s == 4)
+    launch_fast_s<4>(p, M, st);
+  else
+    launch_fast_s<3>(p, M, st);
+}
+
+int narrow3d_fast_default_kc(int nx, int ny, int nz, int num_sms) {
+  const long long tiles = static_cast<long long>(nx / FX) * (ny / FY);
+  // chunked grid: ~7 waves of one CTA per SM, >= 16 planes per CTA
+  long long kc = (tiles * nz + 7LL * num_sms - 1) / (7LL * num_sms);
+  if (kc < 16) kc = 16;
+  if (kc > nz) kc = nz;
+  return static_cast<int>(kc);
+}
+
+}  // namespace smc

@@ -68,6 +68,49 @@ def test_narrow3d_tiling_independent_bitwise(cuda):
         assert np.array_equal(o, outs[0])
 
 
+@pytest.mark.parametrize("order", [8, 6])
+def test_narrow3d_fast_kernel_partition_independent(cuda, order):
+    """The FP64-optimised kernel (nx % 64 == 0, ny % 8 == 0) splits the box
+    into per-CTA plane ranges; the result must not depend on the split and
+    must match the oracle."""
+    n = 64
+    a, u = W.narrow3d_inputs(n, seed=9)
+    choice = P.StencilChoice.narrow8(*SMC) if order == 8 else P.StencilChoice.narrow6(
+        P.DEFAULT_M36)
+    op = P.Narrow3DOperator(a, 1 / n, 1 / n, 1 / n, choice)
+    outs = []
+    for kc in (1, 5, 16, 64):
+        op.set_kc(kc)
+        outs.append(op(0.0, u))
+    for o in outs[1:]:
+        assert np.array_equal(o, outs[0])
+    m, s = O.build_narrow(order, SMC if order == 8 else (P.DEFAULT_M36,))
+    assert rel_err(outs[0], O.narrow3d(m, s, a, u, 1 / n, 1 / n, 1 / n)) <= TOL
+
+
+@pytest.mark.parametrize("nx,ny", [(64, 64), (40, 24)])
+def test_narrow3d_slab_matches_periodic_box(cuda, nx, ny):
+    """A z-slab with 4 ghost planes, applied in pieces (interior first, then
+    the boundary planes, as the halo-overlapped multi-GPU step does), equals
+    the periodic box bitwise (GPU-count independence)."""
+    torch = _torch()
+    nz, z0, nzl, G = 64, 16, 32, 4
+    rng = np.random.default_rng(21)
+    a = rng.uniform(0.5, 2.0, (nz, ny, nx))
+    u = rng.standard_normal((nz, ny, nx))
+    full = P.Narrow3DOperator(a, 0.1, 0.1, 0.1)(0.0, u)
+    idx = [(z0 + k - G) % nz for k in range(nzl + 2 * G)]
+    ag = torch.from_numpy(np.ascontiguousarray(a[idx])).to(cuda)
+    ug = torch.from_numpy(np.ascontiguousarray(u[idx])).to(cuda)
+    slab = P.Narrow3DSlab(ag, nzl, G, 0.1, 0.1, 0.1)
+    out = torch.empty((nzl, ny, nx), dtype=torch.float64, device=cuda)
+    slab.apply_planes(ug, out, 4, nzl - 4)
+    slab.apply_planes(ug, out, 0, 4)
+    slab.apply_planes(ug, out, nzl - 4, nzl)
+    torch.cuda.synchronize()
+    assert np.array_equal(out.cpu().numpy(), full[z0:z0 + nzl])
+
+
 def test_narrow3d_convergence_order8(cuda):
     """configs[1] check: 8th-order convergence to the analytic div(a grad U)
     (slope 8 +- 0.3 as pde_test.cpp:152), fit on 64^3 -> 128^3 -> 256^3."""
