@@ -130,6 +130,26 @@ int smc_narrow3d_apply_planes(smc_rhs* op, const double* u, double* out, int kbe
 /* z planes per CTA of the narrow kernel (tuning knob; 0 = heuristic). */
 int smc_narrow3d_set_kc(smc_rhs* op, int kc);
 
+/* Multicomponent reacting Navier-Stokes RHS (
+ * no reference implementation) with the builder-defined
+ * synthetic 9-species mechanism of include/smc_mechanism.h.  State: SMC_NVAR
+ * (= 14) fields of nx*ny*nz cells, field-major (rho, rho u, rho v, rho w,
+ * rho E, rho Y_1..9).  One workspace, three Rhs views: the full RHS, the
+ * advection-diffusion part (MRSDC f1: hypterm + diffterm) and the chemistry
+ * part (MRSDC f2: wdot) — the split of PAPER.md:732-735.  Any view pointer
+ * may be NULL.  zghost = 0: periodic box (interior-only arrays); zghost >= 4:
+ * one z-slab, arrays passed to smc_ns_rhs_ghosted carry the ghost planes. */
+int smc_ns_create(int nx, int ny, int nz, int zghost, double dx, double dy, double dz, int order,
+                  const double* params, int nparams, smc_rhs** full, smc_rhs** advdiff,
+                  smc_rhs** chem);
+/* Slab mode: out (interior) = RHS of U (SMC_NVAR ghosted fields), device. */
+int smc_ns_rhs_ghosted(smc_rhs* ns, const double* U, double* out);
+/* ctoprim: temperature and pressure of every interior cell. */
+int smc_ns_temperature_pressure(smc_rhs* ns, const double* U, double* T, double* p, int where);
+/* Conserved state from T, p, velocity (3 fields), Y (9 fields); n cells. */
+int smc_ns_conserved(const double* T, const double* p, const double* uvw, const double* Y,
+                     long long n, double* U, int where);
+
 /* Any host callback as an operator (nsdc::Rhs, core/include/nsdc/field.hpp:14-16). */
 int smc_rhs_from_callback(long long dim, smc_rhs_fn f, void* ctx, smc_rhs** out);
 

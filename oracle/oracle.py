@@ -173,3 +173,29 @@ def ref_hierarchy(coarse_family, coarse_n, fine_type, fine_family, fine_n, repea
     r.ref_nodes(coarse_family, coarse_n, dp(coarse))
     return dict(coarse=coarse, fine=fine, q21=q21, s21=s21, q22=q22, s22=s22,
                 fine_of_coarse=foc, p_map=pm)
+
+
+# ------------------------------------------------------------------ NS
+def ns_conserved(T, p, uvw, Y) -> np.ndarray:
+    n = T.size
+    U = np.empty((14,) + T.shape)
+    lib().or_ns_conserved(dp(T), dp(p), dp(uvw), dp(Y), C.c_longlong(n), dp(U))
+    return U
+
+
+def ns_rhs(U, dx, part=0, m64=None, s=4) -> np.ndarray:
+    _, nz, ny, nx = U.shape
+    if m64 is None:
+        m64, s = build_narrow(8, (3557.0 / 44100.0, -2083.0 / 117600.0))
+    out = np.empty_like(U)
+    rc = lib().or_ns_rhs(dp(U), nx, ny, nz, C.c_double(dx), C.c_double(dx), C.c_double(dx),
+                         dp(m64), s, part, dp(out))
+    assert rc == 0
+    return out
+
+
+def ns_temperature_pressure(U):
+    n = U[0].size
+    T, p = np.empty(U.shape[1:]), np.empty(U.shape[1:])
+    lib().or_ns_temperature_pressure(dp(U), C.c_longlong(n), dp(T), dp(p))
+    return T, p

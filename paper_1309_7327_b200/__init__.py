@@ -28,7 +28,8 @@ __all__ = [
     "SmcError", "SmcInvalidArgument", "SmcIntegrationError", "StencilChoice", "stencil_preset",
     "build_narrow", "apply_narrow", "apply_wide", "first_derivative8", "HeatOperator",
     "Narrow3DOperator", "Narrow3DSlab", "CallbackRhs", "SdcStepper", "MrsdcStepper", "StepControls", "nodes",
-    "integration_matrices", "build_hierarchy", "SMC_M47", "SMC_M48", "OPTIMAL_M47",
+    "integration_matrices", "build_hierarchy", "SMC_M47", "SMC_M48", "OPTIMAL_M47", "NsOperator",
+    "ns_conserved", "NS_FULL", "NS_ADVDIFF", "NS_CHEM",
     "OPTIMAL_M48", "DEFAULT_M36", "launch_count",
 ]
 
@@ -406,3 +407,62 @@ def build_hierarchy(coarse_n, inner_n, repeats=1, coarse_family=GAUSS_LOBATTO,
                                 s22.ctypes.data_as(D), foc.ctypes.data_as(I),
                                 pm.ctypes.data_as(I)))
     return dict(fine=fine, q21=q21, s21=s21, q22=q22, s22=s22, fine_of_coarse=foc, p_map=pm)
+
+
+# ------------------------------------------------------------------ NS RHS
+NVAR = 14
+NS_FULL, NS_ADVDIFF, NS_CHEM = 0, 1, 2
+
+
+class NsOperator:
+    """The reacting-NS RHS on a periodic nz x ny x nx box (zghost = 0) or on
+    one z-slab with zghost ghost planes: .full, .advdiff (MRSDC f1) and
+    .chem (MRSDC f2) are Rhs views sharing one device workspace."""
+
+    def __init__(self, nx, ny, nz, dx, dy=None, dz=None, choice: StencilChoice = None,
+                 zghost: int = 0):
+        choice = choice or StencilChoice()
+        dy = dy or dx
+        dz = dz or dx
+        self.shape = (nz, ny, nx)
+        self.zghost = zghost
+        hs = [C.c_void_p() for _ in range(3)]
+        pp, keep = _params(choice.params)
+        check(_capi.lib().smc_ns_create(nx, ny, nz, zghost, dx, dy, dz, choice.order, pp,
+                                        len(choice.params), C.byref(hs[0]), C.byref(hs[1]),
+                                        C.byref(hs[2])))
+        self.full, self.advdiff, self.chem = (_Rhs(h) for h in hs)
+
+    def set_stream(self, stream) -> None:
+        for r in (self.full, self.advdiff, self.chem):
+            r.set_stream(stream)
+
+    def rhs_ghosted(self, U, out, part: int = NS_FULL) -> None:
+        h = (self.full, self.advdiff, self.chem)[part].handle
+        check(_capi.lib().smc_ns_rhs_ghosted(h, dptr(U), dptr(out)))
+
+    def temperature_pressure(self, U):
+        nz, ny, nx = self.shape
+        if hasattr(U, "is_cuda"):
+            import torch
+            T = torch.empty((nz, ny, nx), dtype=torch.float64, device=U.device)
+            p = torch.empty_like(T)
+        else:
+            T, p = np.empty((nz, ny, nx)), np.empty((nz, ny, nx))
+        check(_capi.lib().smc_ns_temperature_pressure(self.full.handle, dptr(U), dptr(T),
+                                                      dptr(p), where_of(U)))
+        return T, p
+
+
+def ns_conserved(T, p, uvw, Y):
+    """Conserved state (14 fields) from T, p, velocity (3 fields), Y (9 fields)."""
+    n = T.size if not hasattr(T, "numel") else T.numel()
+    shape = (NVAR,) + tuple(T.shape)
+    if hasattr(T, "is_cuda"):
+        import torch
+        U = torch.empty(shape, dtype=torch.float64, device=T.device)
+    else:
+        U = np.empty(shape)
+    check(_capi.lib().smc_ns_conserved(dptr(T), dptr(p), dptr(uvw), dptr(Y), n, dptr(U),
+                                       where_of(T)))
+    return U

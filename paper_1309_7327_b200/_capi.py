@@ -70,6 +70,12 @@ _SIG = {
                                            C.c_double, C.c_double, C.c_int, _D, C.c_int, _VP,
                                            C.c_int, C.POINTER(_VP)]),
     "smc_narrow3d_apply_planes": (C.c_int, [_VP, _VP, _VP, C.c_int, C.c_int]),
+    "smc_ns_create": (C.c_int, [C.c_int, C.c_int, C.c_int, C.c_int, C.c_double, C.c_double,
+                                C.c_double, C.c_int, _D, C.c_int, C.POINTER(_VP), C.POINTER(_VP),
+                                C.POINTER(_VP)]),
+    "smc_ns_rhs_ghosted": (C.c_int, [_VP, _VP, _VP]),
+    "smc_ns_temperature_pressure": (C.c_int, [_VP, _VP, _VP, _VP, C.c_int]),
+    "smc_ns_conserved": (C.c_int, [_VP, _VP, _VP, _VP, C.c_longlong, _VP, C.c_int]),
     "smc_rhs_from_callback": (C.c_int, [C.c_longlong, RHS_FN, _VP, C.POINTER(_VP)]),
     "smc_rhs_eval": (C.c_int, [_VP, C.c_double, _VP, _VP, C.c_int]),
     "smc_rhs_dim": (C.c_longlong, [_VP]),

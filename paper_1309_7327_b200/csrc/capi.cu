@@ -6,6 +6,7 @@
 
 #include "../../include/smc_b200.h"
 #include "narrow.cuh"
+#include "ns.cuh"
 #include "ops.hpp"
 #include "quadrature.hpp"
 #include "sweeps.hpp"
@@ -278,6 +279,68 @@ int smc_rhs_set_stream(smc_rhs* h, void* stream) {
 int smc_rhs_destroy(smc_rhs* h) {
   delete h;
   return SMC_OK;
+}
+
+// ------------------------------------------------------------ NS RHS
+int smc_ns_create(int nx, int ny, int nz, int zghost, double dx, double dy, double dz, int order,
+                  const double* params, int nparams, smc_rhs** full, smc_rhs** advdiff,
+                  smc_rhs** chem) {
+  return guarded([&] {
+    need(params, "params");
+    int s = 0;
+    smc::StencilM M = smc::make_stencil(order, params, nparams, &s);
+    smc::NsBox box;
+    box.nx = nx, box.ny = ny, box.nz = nz, box.G = zghost;
+    auto ws = std::make_shared<smc::NsWorkspace>(box, dx, dy, dz, M, s);
+    smc_rhs** outs[3] = {full, advdiff, chem};
+    for (int part = 0; part < 3; ++part) {
+      if (!outs[part]) continue;
+      auto h = std::make_unique<smc_rhs>();
+      h->op = std::make_unique<smc::NsRhsOp>(ws, part);
+      *outs[part] = h.release();
+    }
+  });
+}
+
+static smc::NsRhsOp& ns_of(smc_rhs* h) {
+  auto* op = dynamic_cast<smc::NsRhsOp*>(&op_of(h));
+  if (!op) throw smc::InvalidArgument("not an NS operator");
+  return *op;
+}
+
+int smc_ns_rhs_ghosted(smc_rhs* h, const double* U, double* out) {
+  return guarded([&] {
+    need(U, "U"), need(out, "out");
+    smc::NsRhsOp& op = ns_of(h);
+    op.workspace().rhs(U, out, op.part(), op.stream());
+  });
+}
+
+int smc_ns_temperature_pressure(smc_rhs* h, const double* U, double* T, double* p, int where) {
+  return guarded([&] {
+    need(U, "U"), need(T, "T"), need(p, "p");
+    smc::NsRhsOp& op = ns_of(h);
+    const smc::NsBox& b = op.workspace().box();
+    cudaStream_t st = op.stream();
+    Staged dU(U, SMC_NVAR * b.field_len(), where, st);
+    StagedOut oT(T, b.cells(), where), op_(p, b.cells(), where);
+    op.workspace().temperature_pressure(dU.dev, oT.dev, op_.dev, st);
+    oT.finish(st), op_.finish(st);
+    SMC_CUDA(cudaStreamSynchronize(st));
+  });
+}
+
+int smc_ns_conserved(const double* T, const double* p, const double* uvw, const double* Y,
+                     long long n, double* U, int where) {
+  return guarded([&] {
+    need(T, "T"), need(p, "p"), need(uvw, "uvw"), need(Y, "Y"), need(U, "U");
+    Staged dT(T, n, where, nullptr), dp(p, n, where, nullptr), du(uvw, 3 * n, where, nullptr),
+        dY(Y, SMC_NSP * n, where, nullptr);
+    StagedOut oU(U, SMC_NVAR * n, where);
+    smc::ns_conserved_from_primitives(dT.dev, dp.dev, du.dev, dY.dev, n, oU.dev, nullptr);
+    oU.finish(nullptr);
+    SMC_CUDA(cudaStreamSynchronize(nullptr));
+  });
 }
 
 // ---------------------------------------------------------- quadrature

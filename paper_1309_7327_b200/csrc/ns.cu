@@ -1,0 +1,598 @@
+// NS right-hand side kernels (see ns.cuh).  v1 layout: one thread per cell,
+// neighbour values gathered through L1/L2; the same decomposition as the CPU
+// oracle (oracle/ns_oracle.c) so every intermediate is comparable:
+//   prim    : ctoprim (Newton for T) + transport + derived coefficient fields
+//   hyp     : -div F with 8th-order centred first derivatives  -> out
+//   narrow  : same-direction second derivatives, narrow stencil -> acc
+//   grad    : velocity gradients -> mixed-term fields, tau:grad u, V_c
+//   assemble: mixed viscous terms, correction-velocity terms  -> out
+//   wdot    : rho omega_k                                       -> out
+#include <cmath>
+
+#include "ns.cuh"
+
+namespace smc {
+
+namespace {
+
+constexpr int NSP = SMC_NSP;
+constexpr int NV = SMC_NVAR;
+
+// prim_ field indices (same roles as the oracle's F_* enum)
+enum : int {
+  F_U = 0, F_T = 3, F_P, F_ETA, F_ETA43, F_LAM2, F_LAM, F_DHP, F_HYS, F_Y,
+  F_X = F_Y + NSP, F_D = F_X + NSP, F_DH = F_D + NSP, F_DP = F_DH + NSP, F_COUNT = F_DP + NSP
+};
+// acc_ field indices (interior)
+enum : int { A_DM = 0, A_DE = 3, A_DY = 4, A_VC = A_DY + NSP, A_HEAT = A_VC + 3, A_COUNT };
+// mixed_ fields (all planes): M_ij = eta d_i u_j for (i, j), i != j; L_i
+constexpr int MX_COUNT = 9;
+__host__ __device__ constexpr int mx_index(int i, int j) { return 3 * i + j - (j > i) - i; }
+
+struct Tables {
+  double W[NSP], th[NSP][4], mu0[NSP], lam0[NSP], rhoD0[NSP];
+  double kf[SMC_NREAC][3], kr[SMC_NREAC][3];
+  int reac[SMC_NREAC][3], prod[SMC_NREAC][3], tb[SMC_NREAC];
+};
+__constant__ Tables cT;
+
+struct Geo {
+  int nx, ny, nz, G;
+  long long plane, flen;
+  double d1[3], d2[3];
+};
+
+__device__ __forceinline__ long long zo(const Geo& g, int k) {
+  if (g.G == 0) k = wrap(k, g.nz);
+  return static_cast<long long>(k) * g.plane;
+}
+// offset of cell (i, j, k) + o along dir d (periodic in x, y; z periodic or ghosted)
+__device__ __forceinline__ long long nb(const Geo& g, int i, int j, int k, int d, int o) {
+  if (d == 0) i = wrap(i + o, g.nx);
+  else if (d == 1) j = wrap(j + o, g.ny);
+  else k += o;
+  return zo(g, k) + static_cast<long long>(j) * g.nx + i;
+}
+
+__device__ __forceinline__ double spec_e(int k, double T) {
+  const double R = SMC_RU / cT.W[k];
+  const double* a = cT.th[k];
+  return R * (a[0] * T + a[1] * T * T / 2.0 + a[2] * T * T * T / 3.0 + a[3] - T);
+}
+__device__ __forceinline__ double spec_h(int k, double T) {
+  const double R = SMC_RU / cT.W[k];
+  const double* a = cT.th[k];
+  return R * (a[0] * T + a[1] * T * T / 2.0 + a[2] * T * T * T / 3.0 + a[3]);
+}
+__device__ __forceinline__ double spec_cv(int k, double T) {
+  const double R = SMC_RU / cT.W[k];
+  const double* a = cT.th[k];
+  return R * (a[0] + a[1] * T + a[2] * T * T - 1.0);
+}
+
+// T from e by Newton, same start and stopping rule as the oracle.
+__device__ double temperature(const double* Y, double e) {
+  double T = 1000.0;
+  for (int it = 0; it < 50; ++it) {
+    double f = -e, df = 0.0;
+#pragma unroll
+    for (int k = 0; k < NSP; ++k) {
+      f += Y[k] * spec_e(k, T);
+      df += Y[k] * spec_cv(k, T);
+    }
+    const double dT = f / df;
+    T -= dT;
+    if (fabs(dT) <= 1e-9 * T) break;
+  }
+  return T;
+}
+
+// ---------------------------------------------------------------- prim
+__global__ void __launch_bounds__(256) prim_kernel(const double* __restrict__ U,
+                                                   double* __restrict__ F, Geo g) {
+  const long long n = g.flen;  // all planes incl. ghosts
+  const long long c = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
+  if (c >= n) return;
+  const double rho = U[c];
+  const double ri = 1.0 / rho;
+  double u[3], Y[NSP], X[NSP];
+  for (int i = 0; i < 3; ++i) u[i] = U[(1 + i) * n + c] * ri;
+  double wsum = 0.0;
+#pragma unroll
+  for (int k = 0; k < NSP; ++k) {
+    Y[k] = U[(5 + k) * n + c] * ri;
+    wsum += Y[k] / cT.W[k];
+  }
+  const double e = U[4 * n + c] * ri - 0.5 * (u[0] * u[0] + u[1] * u[1] + u[2] * u[2]);
+  const double T = temperature(Y, e);
+  const double p = rho * SMC_RU * T * wsum;
+  const double s = pow(T / SMC_T_REF, SMC_TRANSPORT_EXP);
+  double eta = 0.0, lam = 0.0, dhp = 0.0, hys = 0.0;
+  const double pinv = 1.0 / p;
+#pragma unroll
+  for (int k = 0; k < NSP; ++k) {
+    X[k] = (Y[k] / cT.W[k]) / wsum;
+    eta += X[k] * cT.mu0[k];
+    lam += X[k] * cT.lam0[k];
+  }
+  eta *= s;
+  lam *= s;
+  const double xi = SMC_XI_OVER_ETA * eta;
+  for (int i = 0; i < 3; ++i) F[(F_U + i) * n + c] = u[i];
+  F[F_T * n + c] = T;
+  F[F_P * n + c] = p;
+  F[F_ETA * n + c] = eta;
+  F[F_ETA43 * n + c] = 4.0 / 3.0 * eta + xi;
+  F[F_LAM2 * n + c] = xi - 2.0 / 3.0 * eta;
+  F[F_LAM * n + c] = lam;
+#pragma unroll
+  for (int k = 0; k < NSP; ++k) {
+    const double h = spec_h(k, T);
+    const double rd = cT.rhoD0[k] * s;
+    F[(F_Y + k) * n + c] = Y[k];
+    F[(F_X + k) * n + c] = X[k];
+    F[(F_D + k) * n + c] = rd;
+    F[(F_DH + k) * n + c] = rd * h;
+    F[(F_DP + k) * n + c] = rd * (X[k] - Y[k]) * pinv;
+    dhp += rd * h * (X[k] - Y[k]) * pinv;
+    hys += h * Y[k];
+  }
+  F[F_DHP * n + c] = dhp;
+  F[F_HYS * n + c] = hys;
+}
+
+__device__ __forceinline__ void cell_ijk(long long c, const Geo& g, int& i, int& j, int& k) {
+  i = static_cast<int>(c % g.nx);
+  const long long r = c / g.nx;
+  j = static_cast<int>(r % g.ny);
+  k = static_cast<int>(r / g.ny);
+}
+
+constexpr double C1 = 4.0 / 5.0, C2 = -1.0 / 5.0, C3 = 4.0 / 105.0, C4 = -1.0 / 280.0;
+__device__ __forceinline__ double dcoef(int o) {  // antisymmetric 8th-order weights
+  const int a = o < 0 ? -o : o;
+  const double c = a == 1 ? C1 : a == 2 ? C2 : a == 3 ? C3 : C4;
+  return o < 0 ? -c : c;
+}
+
+// d/dx_d of field f (plane-0 pointer) at interior cell (i, j, k)
+__device__ __forceinline__ double d8(const double* f, const Geo& g, int i, int j, int k, int d) {
+  double w[9];
+#pragma unroll
+  for (int o = -4; o <= 4; ++o) w[o + 4] = o == 0 ? 0.0 : __ldg(f + nb(g, i, j, k, d, o));
+  return deriv8_w(w, g.d1[d]);
+}
+
+// ----------------------------------------------------------------- hyp
+// out = -sum_d d_d F_d, fluxes formed at the neighbours.
+__global__ void __launch_bounds__(256) hyp_kernel(const double* __restrict__ U,
+                                                  const double* __restrict__ F,
+                                                  double* __restrict__ out, Geo g, int init) {
+  const long long n = g.plane * g.nz;
+  const long long c = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
+  if (c >= n) return;
+  int i, j, k;
+  cell_ijk(c, g, i, j, k);
+  const double* U0 = U + g.G * g.plane;  // plane 0 of interior, field stride flen
+  const double* F0 = F + g.G * g.plane;
+  double acc[NV];
+#pragma unroll
+  for (int v = 0; v < NV; ++v) acc[v] = 0.0;
+  for (int d = 0; d < 3; ++d) {
+    double dv[NV];
+#pragma unroll
+    for (int v = 0; v < NV; ++v) dv[v] = 0.0;
+    // per offset pair (o, -o): c_o (F(+o) - F(-o))
+#pragma unroll
+    for (int a = 4; a >= 1; --a) {
+      double fp[NV], fm[NV];
+#pragma unroll
+      for (int sgn = 0; sgn < 2; ++sgn) {
+        const long long q = nb(g, i, j, k, d, sgn ? -a : a);
+        const double ud = __ldg(F0 + F_U * 0 + (F_U + d) * g.flen + q);
+        const double p = __ldg(F0 + F_P * g.flen + q);
+        double* f = sgn ? fm : fp;
+        f[0] = __ldg(U0 + (1 + d) * g.flen + q);
+#pragma unroll
+        for (int m = 0; m < 3; ++m) f[1 + m] = __ldg(U0 + (1 + m) * g.flen + q) * ud + (m == d ? p : 0.0);
+        f[4] = (__ldg(U0 + 4 * g.flen + q) + p) * ud;
+#pragma unroll
+        for (int s = 0; s < NSP; ++s) f[5 + s] = __ldg(U0 + (5 + s) * g.flen + q) * ud;
+      }
+      const double ca = a == 1 ? C1 : a == 2 ? C2 : a == 3 ? C3 : C4;
+#pragma unroll
+      for (int v = 0; v < NV; ++v) dv[v] = __fma_rn(ca, fp[v] - fm[v], dv[v]);
+    }
+#pragma unroll
+    for (int v = 0; v < NV; ++v) acc[v] -= dv[v] * g.d1[d];
+  }
+#pragma unroll
+  for (int v = 0; v < NV; ++v) {
+    double* o = out + v * n + c;
+    *o = init ? acc[v] : *o + acc[v];
+  }
+}
+
+// ------------------------------------------------------------ narrow
+// v'_r of the interface whose window starts at u[0] (antisymmetric form of
+// narrow_iface: rows r >= S carry the sign flip, see common.cuh).
+template <int S>
+__device__ __forceinline__ void narrow_v(const double* u, const StencilM& M, double* v) {
+  constexpr int L = 2 * S - 1;
+#pragma unroll
+  for (int r = 0; r < 2 * S; ++r) {
+    const int lo = row_lo<S>(r), hi = row_hi<S>(r);
+    double acc;
+    if (r < S) {
+      acc = M.m[r][lo] * u[lo];
+#pragma unroll
+      for (int c = lo + 1; c <= hi; ++c) acc = __fma_rn(M.m[r][c], u[c], acc);
+    } else {
+      acc = M.m[L - r][L - lo] * u[lo];
+#pragma unroll
+      for (int c = lo + 1; c <= hi; ++c) acc = __fma_rn(M.m[L - r][L - c], u[c], acc);
+    }
+    v[r] = acc;
+  }
+}
+template <int S>
+__device__ __forceinline__ double narrow_dot(const double* a, const double* v) {
+  double acc = a[0] * v[0];
+#pragma unroll
+  for (int r = 1; r < 2 * S; ++r) acc = __fma_rn(r < S ? a[r] : -a[r], v[r], acc);
+  return acc;
+}
+
+// All same-direction second-derivative terms of one cell (PAPER.md:150-156,
+// :170-213): both interfaces of the cell are formed here (v1).
+template <int S>
+__global__ void __launch_bounds__(256) narrow_kernel(const double* __restrict__ F,
+                                                     double* __restrict__ A, Geo g,
+                                                     const StencilM M) {
+  const long long n = g.plane * g.nz;
+  const long long c = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
+  if (c >= n) return;
+  int i, j, k;
+  cell_ijk(c, g, i, j, k);
+  const double* F0 = F + g.G * g.plane;
+  double dm[3] = {0, 0, 0}, dE = 0.0, dY[NSP];
+#pragma unroll
+  for (int s = 0; s < NSP; ++s) dY[s] = 0.0;
+  constexpr int WN = 2 * S + 1;  // window covering both interfaces
+  for (int d = 0; d < 3; ++d) {
+    long long q[WN];
+#pragma unroll
+    for (int o = 0; o < WN; ++o) q[o] = nb(g, i, j, k, d, o - S);
+    const double id2 = g.d2[d];
+    auto win = [&](int fld, double* w) {
+      const double* f = F0 + static_cast<long long>(fld) * g.flen;
+#pragma unroll
+      for (int o = 0; o < WN; ++o) w[o] = __ldg(f + q[o]);
+    };
+    // (coef a, field u): (H(i+1/2) - H(i-1/2)) / d^2 via the shared v'
+    double u[WN], a[WN], vl[2 * S], vr[2 * S];
+    // velocities
+#pragma unroll 1
+    for (int m = 0; m < 3; ++m) {
+      win(F_U + m, u);
+      win(m == d ? F_ETA43 : F_ETA, a);
+      narrow_v<S>(u, M, vl);
+      narrow_v<S>(u + 1, M, vr);
+      dm[m] += (narrow_dot<S>(a + 1, vr) - narrow_dot<S>(a, vl)) * id2;
+    }
+    // temperature
+    win(F_T, u);
+    win(F_LAM, a);
+    narrow_v<S>(u, M, vl);
+    narrow_v<S>(u + 1, M, vr);
+    dE += (narrow_dot<S>(a + 1, vr) - narrow_dot<S>(a, vl)) * id2;
+    // mole fractions: rhoD_k and rhoD_k h_k
+#pragma unroll 1
+    for (int s = 0; s < NSP; ++s) {
+      win(F_X + s, u);
+      narrow_v<S>(u, M, vl);
+      narrow_v<S>(u + 1, M, vr);
+      win(F_D + s, a);
+      dY[s] += (narrow_dot<S>(a + 1, vr) - narrow_dot<S>(a, vl)) * id2;
+      win(F_DH + s, a);
+      dE += (narrow_dot<S>(a + 1, vr) - narrow_dot<S>(a, vl)) * id2;
+    }
+    // pressure: rhoD_k (X_k - Y_k) / p and sum_k rhoD_k h_k (X_k - Y_k) / p
+    win(F_P, u);
+    narrow_v<S>(u, M, vl);
+    narrow_v<S>(u + 1, M, vr);
+#pragma unroll 1
+    for (int s = 0; s < NSP; ++s) {
+      win(F_DP + s, a);
+      dY[s] += (narrow_dot<S>(a + 1, vr) - narrow_dot<S>(a, vl)) * id2;
+    }
+    win(F_DHP, a);
+    dE += (narrow_dot<S>(a + 1, vr) - narrow_dot<S>(a, vl)) * id2;
+  }
+  for (int m = 0; m < 3; ++m) A[(A_DM + m) * n + c] = dm[m];
+  A[A_DE * n + c] = dE;
+#pragma unroll
+  for (int s = 0; s < NSP; ++s) A[(A_DY + s) * n + c] = dY[s];
+}
+
+// ------------------------------------------------------------- grad
+// Interior: tau:grad u, V_c, and the mixed-term fields; ghost planes (slab
+// mode): the mixed-term fields that are differentiated along z, from in-plane
+// derivatives only.
+__global__ void __launch_bounds__(256) grad_kernel(const double* __restrict__ F,
+                                                   double* __restrict__ A,
+                                                   double* __restrict__ MX, Geo g) {
+  const long long n = g.plane * g.nz;
+  const long long all = g.plane * (g.nz + 2 * g.G);
+  const long long t = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
+  if (t >= all) return;
+  // t indexes planes -G .. nz+G-1
+  const long long cg = t;  // offset within the field including ghosts
+  int i, j, kk;
+  cell_ijk(t, g, i, j, kk);
+  const int k = kk - g.G;
+  const bool interior = k >= 0 && k < g.nz;
+  const double* F0 = F + g.G * g.plane;
+  const double* fu[3] = {F0 + F_U * g.flen, F0 + (F_U + 1) * g.flen, F0 + (F_U + 2) * g.flen};
+  const double eta = __ldg(F + F_ETA * g.flen + cg);
+  const double lam2 = __ldg(F + F_LAM2 * g.flen + cg);
+  if (!interior) {
+    // eta d_x w, eta d_y w (differentiated along z), lam2 (d_x u + d_y v)
+    MX[mx_index(0, 2) * g.flen + cg] = eta * d8(fu[2], g, i, j, k, 0);
+    MX[mx_index(1, 2) * g.flen + cg] = eta * d8(fu[2], g, i, j, k, 1);
+    MX[(6 + 2) * g.flen + cg] = lam2 * (d8(fu[0], g, i, j, k, 0) + d8(fu[1], g, i, j, k, 1));
+    return;
+  }
+  double G[3][3];
+  for (int a = 0; a < 3; ++a)
+    for (int b = 0; b < 3; ++b) G[a][b] = d8(fu[a], g, i, j, k, b);
+  const long long c = static_cast<long long>(k) * g.plane + static_cast<long long>(j) * g.nx + i;
+  // mixed-term fields M_ij = eta d_i u_j = eta G[j][i]; L_i = lam2 sum_{j!=i} G[j][j]
+  for (int a = 0; a < 3; ++a)
+    for (int b = 0; b < 3; ++b)
+      if (a != b) MX[mx_index(a, b) * g.flen + cg] = eta * G[b][a];
+  for (int a = 0; a < 3; ++a) {
+    double sd = 0.0;
+    for (int b = 0; b < 3; ++b)
+      if (b != a) sd += G[b][b];
+    MX[(6 + a) * g.flen + cg] = lam2 * sd;
+  }
+  // tau : grad u
+  const double div = G[0][0] + G[1][1] + G[2][2];
+  double heat = 0.0;
+  for (int a = 0; a < 3; ++a)
+    for (int b = 0; b < 3; ++b) {
+      const double tau = eta * (G[a][b] + G[b][a]) + (a == b ? lam2 * div : 0.0);
+      heat += tau * G[a][b];
+    }
+  A[A_HEAT * n + c] = heat;
+  // V_c = -sum_l (rhoD_l grad X_l + rhoD_l (X_l - Y_l)/p grad p)
+  double gp[3];
+  for (int b = 0; b < 3; ++b) gp[b] = d8(F0 + F_P * g.flen, g, i, j, k, b);
+  double vc[3] = {0, 0, 0};
+  for (int l = 0; l < NSP; ++l) {
+    const double D = __ldg(F + (F_D + l) * g.flen + cg);
+    const double DP = __ldg(F + (F_DP + l) * g.flen + cg);
+    for (int b = 0; b < 3; ++b)
+      vc[b] -= D * d8(F0 + (F_X + l) * g.flen, g, i, j, k, b) + DP * gp[b];
+  }
+  for (int b = 0; b < 3; ++b) A[(A_VC + b) * n + c] = vc[b];
+}
+
+// --------------------------------------------------------- assemble
+__global__ void __launch_bounds__(256) assemble_kernel(const double* __restrict__ F,
+                                                       const double* __restrict__ A,
+                                                       const double* __restrict__ MX,
+                                                       double* __restrict__ out, Geo g) {
+  const long long n = g.plane * g.nz;
+  const long long c = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
+  if (c >= n) return;
+  int i, j, k;
+  cell_ijk(c, g, i, j, k);
+  const long long cg = c + g.G * g.plane;
+  const double* MX0 = MX + g.G * g.plane;
+  const double* F0 = F + g.G * g.plane;
+  // div tau = narrow part + sum_{j!=i} d_j(eta d_i u_j) + d_i(lam2 sum_{j!=i} d_j u_j)
+  double dm[3];
+  for (int a = 0; a < 3; ++a) {
+    double v = A[(A_DM + a) * n + c];
+    for (int b = 0; b < 3; ++b)
+      if (b != a) v += d8(MX0 + mx_index(a, b) * g.flen, g, i, j, k, b);
+    v += d8(MX0 + (6 + a) * g.flen, g, i, j, k, a);
+    dm[a] = v;
+  }
+  double divvc = 0.0;
+  for (int s = 0; s < NSP; ++s) divvc -= A[(A_DY + s) * n + c];
+  const double vc[3] = {A[A_VC * n + c], A[(A_VC + 1) * n + c], A[(A_VC + 2) * n + c]};
+  for (int s = 0; s < NSP; ++s) {
+    double v = A[(A_DY + s) * n + c] + __ldg(F + (F_Y + s) * g.flen + cg) * divvc;
+    for (int b = 0; b < 3; ++b) v += vc[b] * d8(F0 + (F_Y + s) * g.flen, g, i, j, k, b);
+    out[(5 + s) * n + c] += v;
+  }
+  double e = A[A_DE * n + c] + A[A_HEAT * n + c];
+  for (int a = 0; a < 3; ++a) e += __ldg(F + (F_U + a) * g.flen + cg) * dm[a];
+  e += __ldg(F + F_HYS * g.flen + cg) * divvc;
+  for (int b = 0; b < 3; ++b) e += vc[b] * d8(F0 + F_HYS * g.flen, g, i, j, k, b);
+  out[4 * n + c] += e;
+  for (int a = 0; a < 3; ++a) out[(1 + a) * n + c] += dm[a];
+}
+
+// ------------------------------------------------------------- wdot
+__global__ void __launch_bounds__(256) wdot_kernel(const double* __restrict__ U,
+                                                   const double* __restrict__ F,
+                                                   double* __restrict__ out, Geo g, int init) {
+  const long long n = g.plane * g.nz;
+  const long long c = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
+  if (c >= n) return;
+  const long long cg = c + g.G * g.plane;
+  const double rho = U[cg];
+  const double T = F[F_T * g.flen + cg];
+  double C[NSP], M = 0.0, om[NSP];
+#pragma unroll
+  for (int s = 0; s < NSP; ++s) {
+    C[s] = rho * F[(F_Y + s) * g.flen + cg] / cT.W[s];
+    M += C[s];
+    om[s] = 0.0;
+  }
+  const double lnT = log(T), invRT = 1.0 / (SMC_RU * T);
+#pragma unroll
+  for (int r = 0; r < SMC_NREAC; ++r) {
+    const double kf = cT.kf[r][0] * exp(cT.kf[r][1] * lnT - cT.kf[r][2] * invRT);
+    const double kr = cT.kr[r][0] * exp(cT.kr[r][1] * lnT - cT.kr[r][2] * invRT);
+    double qf = kf, qr = kr;
+#pragma unroll
+    for (int m = 0; m < 3; ++m) {
+      if (cT.reac[r][m] >= 0) qf *= C[cT.reac[r][m]];
+      if (cT.prod[r][m] >= 0) qr *= C[cT.prod[r][m]];
+    }
+    if (cT.tb[r]) {
+      qf *= M;
+      qr *= M;
+    }
+    const double q = qf - qr;
+#pragma unroll
+    for (int m = 0; m < 3; ++m) {
+      if (cT.reac[r][m] >= 0) om[cT.reac[r][m]] -= q;
+      if (cT.prod[r][m] >= 0) om[cT.prod[r][m]] += q;
+    }
+  }
+  if (init)
+    for (int v = 0; v < 5; ++v) out[v * n + c] = 0.0;
+#pragma unroll
+  for (int s = 0; s < NSP; ++s) {
+    double* o = out + (5 + s) * n + c;
+    const double w = cT.W[s] * om[s];
+    *o = init ? w : *o + w;
+  }
+}
+
+__global__ void __launch_bounds__(256) tp_kernel(const double* __restrict__ F, double* T,
+                                                 double* p, Geo g) {
+  const long long n = g.plane * g.nz;
+  const long long c = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
+  if (c >= n) return;
+  const long long cg = c + g.G * g.plane;
+  T[c] = F[F_T * g.flen + cg];
+  p[c] = F[F_P * g.flen + cg];
+}
+
+__global__ void __launch_bounds__(256) conserved_kernel(const double* __restrict__ T,
+                                                        const double* __restrict__ p,
+                                                        const double* __restrict__ uvw,
+                                                        const double* __restrict__ Y, long long n,
+                                                        double* __restrict__ U) {
+  const long long c = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
+  if (c >= n) return;
+  double Yc[NSP], rinv = 0.0, e = 0.0;
+#pragma unroll
+  for (int s = 0; s < NSP; ++s) {
+    Yc[s] = Y[s * n + c];
+    rinv += Yc[s] / cT.W[s];
+  }
+  const double rho = p[c] / (SMC_RU * T[c] * rinv);
+#pragma unroll
+  for (int s = 0; s < NSP; ++s) e += Yc[s] * spec_e(s, T[c]);
+  const double u = uvw[c], v = uvw[n + c], w = uvw[2 * n + c];
+  U[c] = rho;
+  U[n + c] = rho * u;
+  U[2 * n + c] = rho * v;
+  U[3 * n + c] = rho * w;
+  U[4 * n + c] = rho * (e + 0.5 * (u * u + v * v + w * w));
+#pragma unroll
+  for (int s = 0; s < NSP; ++s) U[(5 + s) * n + c] = rho * Yc[s];
+}
+
+void upload_tables() {
+  static bool done = false;
+  if (done) return;
+  Tables t{};
+  for (int s = 0; s < NSP; ++s) {
+    t.W[s] = SMC_W[s];
+    for (int q = 0; q < 4; ++q) t.th[s][q] = SMC_THERMO[s][q];
+    t.mu0[s] = SMC_MU0[s];
+    t.lam0[s] = SMC_LAM0[s];
+    t.rhoD0[s] = SMC_RHOD0[s];
+  }
+  for (int r = 0; r < SMC_NREAC; ++r) {
+    for (int q = 0; q < 3; ++q) {
+      t.kf[r][q] = SMC_REACTIONS[r].fwd[q];
+      t.kr[r][q] = SMC_REACTIONS[r].rev[q];
+      t.reac[r][q] = SMC_REACTIONS[r].reac[q];
+      t.prod[r][q] = SMC_REACTIONS[r].prod[q];
+    }
+    t.tb[r] = SMC_REACTIONS[r].third_body;
+  }
+  SMC_CUDA(cudaMemcpyToSymbol(cT, &t, sizeof(t)));
+  done = true;
+}
+
+int blocks(long long n) { return static_cast<int>((n + 255) / 256); }
+
+}  // namespace
+
+NsWorkspace::NsWorkspace(const NsBox& box, double dx, double dy, double dz, const StencilM& M,
+                         int s)
+    : box_(box), M_(M), s_(s) {
+  require(box.nx >= 9 && box.ny >= 9, "ns: need at least 9 cells in x and y");
+  require(box.G == 0 ? box.nz >= 9 : (box.G >= 4 && box.nz >= 1),
+          "ns: need nz >= 9 (periodic) or >= 4 ghost planes (slab)");
+  require(s == 4 || s == 3, "ns: narrow half width must be 3 or 4");
+  require(dx > 0 && dy > 0 && dz > 0, "ns: spacings must be positive");
+  dx_[0] = dx, dx_[1] = dy, dx_[2] = dz;
+  upload_tables();
+  prim_.resize(static_cast<std::size_t>(F_COUNT) * box.field_len());
+  acc_.resize(static_cast<std::size_t>(A_COUNT) * box.cells());
+  mixed_.resize(static_cast<std::size_t>(MX_COUNT) * box.field_len());
+}
+
+static Geo make_geo(const NsBox& b, const double* d) {
+  Geo g;
+  g.nx = b.nx, g.ny = b.ny, g.nz = b.nz, g.G = b.G;
+  g.plane = b.plane();
+  g.flen = b.field_len();
+  for (int q = 0; q < 3; ++q) g.d1[q] = 1.0 / d[q], g.d2[q] = 1.0 / (d[q] * d[q]);
+  return g;
+}
+
+void NsWorkspace::rhs(const double* U, double* out, int part, cudaStream_t st) {
+  const Geo g = make_geo(box_, dx_);
+  const long long n = box_.cells();
+  double* F = prim_.get();
+  double* A = acc_.get();
+  prim_kernel<<<blocks(g.flen), 256, 0, st>>>(U, F, g);
+  SMC_CHECK_LAUNCH();
+  if (part != kNsChem) {
+    hyp_kernel<<<blocks(n), 256, 0, st>>>(U, F, out, g, 1);
+    SMC_CHECK_LAUNCH();
+    if (s_ == 4)
+      narrow_kernel<4><<<blocks(n), 256, 0, st>>>(F, A, g, M_);
+    else
+      narrow_kernel<3><<<blocks(n), 256, 0, st>>>(F, A, g, M_);
+    SMC_CHECK_LAUNCH();
+    grad_kernel<<<blocks(g.plane * (g.nz + 2 * g.G)), 256, 0, st>>>(F, A, mixed_.get(), g);
+    SMC_CHECK_LAUNCH();
+    assemble_kernel<<<blocks(n), 256, 0, st>>>(F, A, mixed_.get(), out, g);
+    SMC_CHECK_LAUNCH();
+  }
+  if (part != kNsAdvDiff) {
+    wdot_kernel<<<blocks(n), 256, 0, st>>>(U, F, out, g, part == kNsChem ? 1 : 0);
+    SMC_CHECK_LAUNCH();
+  }
+}
+
+void NsWorkspace::temperature_pressure(const double* U, double* T, double* p, cudaStream_t st) {
+  const Geo g = make_geo(box_, dx_);
+  prim_kernel<<<blocks(g.flen), 256, 0, st>>>(U, prim_.get(), g);
+  SMC_CHECK_LAUNCH();
+  tp_kernel<<<blocks(box_.cells()), 256, 0, st>>>(prim_.get(), T, p, g);
+  SMC_CHECK_LAUNCH();
+}
+
+void ns_conserved_from_primitives(const double* T, const double* p, const double* uvw,
+                                  const double* Y, long long n, double* U, cudaStream_t st) {
+  upload_tables();
+  conserved_kernel<<<blocks(n), 256, 0, st>>>(T, p, uvw, Y, n, U);
+  SMC_CHECK_LAUNCH();
+}
+
+}  // namespace smc

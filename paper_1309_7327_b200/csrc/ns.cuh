@@ -1,0 +1,69 @@
+// Multicomponent reacting Navier-Stokes RHS on
+// sm_100a: ctoprim + transport, hypterm, diffterm (narrow stencil for
+// same-direction second derivatives, 8th-order first derivatives for mixed
+// and correction terms), wdot with the synthetic mechanism of
+// include/smc_mechanism.h.  The reference has no NS code;
+// oracle/ns_oracle.c is the CPU restatement the kernels are checked against.
+#pragma once
+
+#include "../../include/smc_mechanism.h"
+#include "common.cuh"
+#include "ops.hpp"
+
+namespace smc {
+
+// Periodic box or one z-slab with G ghost planes per field (multi-GPU).
+struct NsBox {
+  int nx = 0, ny = 0, nz = 0;  // interior
+  int G = 0;                   // ghost planes below/above (0: periodic wrap in z)
+  long long plane() const { return static_cast<long long>(nx) * ny; }
+  long long cells() const { return plane() * nz; }
+  long long field_len() const { return plane() * (nz + 2 * G); }
+};
+
+enum NsPart : int { kNsFull = 0, kNsAdvDiff = 1, kNsChem = 2 };
+
+// Device workspace shared by the three RHS views (full / f1 / f2).
+class NsWorkspace {
+ public:
+  NsWorkspace(const NsBox& box, double dx, double dy, double dz, const StencilM& M, int s);
+  // out (interior, SMC_NVAR fields) = part of the RHS at state U.  U holds
+  // SMC_NVAR fields of box.field_len() each (ghosts filled by the caller
+  // when box.G > 0).
+  void rhs(const double* U, double* out, int part, cudaStream_t st);
+  // T and p of every interior cell (ctoprim), for tests / diagnostics.
+  void temperature_pressure(const double* U, double* T, double* p, cudaStream_t st);
+  const NsBox& box() const { return box_; }
+
+ private:
+  NsBox box_;
+  double dx_[3];
+  StencilM M_;
+  int s_;
+  DevBuf prim_;   // primitive + coefficient fields (all planes)
+  DevBuf acc_;    // narrow-stencil accumulators + gradients (interior)
+  DevBuf mixed_;  // eta d_i u_j, lam2 sum d_j u_j (all planes)
+};
+
+// Conserved state from primitives (T, p, u, v, w, Y_k), n cells, device ptrs.
+void ns_conserved_from_primitives(const double* T, const double* p, const double* uvw,
+                                  const double* Y, long long n, double* U, cudaStream_t st);
+
+class NsRhsOp final : public RhsOp {
+ public:
+  NsRhsOp(std::shared_ptr<NsWorkspace> ws, int part) : ws_(std::move(ws)), part_(part) {}
+  long long dim() const override { return SMC_NVAR * ws_->box().cells(); }
+  void eval_device(double, const double* u, double* out) override {
+    ws_->rhs(u, out, part_, stream_);
+    ++evals_;
+  }
+  const char* name() const override { return "ns"; }
+  NsWorkspace& workspace() { return *ws_; }
+  int part() const { return part_; }
+
+ private:
+  std::shared_ptr<NsWorkspace> ws_;
+  int part_;
+};
+
+}  // namespace smc

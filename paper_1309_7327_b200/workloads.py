@@ -70,3 +70,84 @@ def narrow3d_exact(n: int, seed: int = 1309, xp=np, device=None):
         out = out + ax * g * k[0] + ay * g * k[1] + az * g * k[2] \
             - a * (A * TWO_PI ** 2 * float(k @ k)) * s(th)
     return out
+
+
+# --------------------------------------------------------------------------
+# NS states (configs[0], [2], [3], [4]); primitive fields on a periodic
+# n^3 box of spacing dx: T [K], p [Pa], velocity [m/s], mass fractions.
+NSP = 9
+SP = dict(H2=0, O2=1, H2O=2, H=3, O=4, OH=5, HO2=6, H2O2=7, N2=8)
+
+
+def _smooth_modes(rng, count, kmax):
+    ks, ph = [], []
+    while len(ks) < count:
+        k = rng.integers(-kmax, kmax + 1, size=3)
+        if 0 < (k * k).sum() <= kmax * kmax:
+            ks.append(k.astype(np.float64))
+            ph.append(rng.random() * TWO_PI)
+    return ks, ph
+
+
+def ns_primitives(n: int, seed: int = 1309, hot_spot: bool = False, ignition: bool = False,
+                  ny: int = None, nz: int = None, z0: int = 0, nz_global: int = None):
+    """configs[0] generator: T = 1200 K + 300 K x (sum of 4 random-phase
+    sinusoids, normalised), p = 1 atm, velocity = 8 random Fourier modes of
+    amplitude 10 m/s, Y = smooth seeded H2/O2/N2 blend + 1e-6 radicals,
+    normalised.  hot_spot: Gaussian T bump to 1800 K, radius 20 cells
+    (configs[3]).  ignition: 600 K stoichiometric H2/air with a 1500 K
+    Gaussian kernel (configs[4]).  ny/nz/z0/nz_global select a z-slab of a
+    larger periodic box (multi-GPU)."""
+    ny = ny or n
+    nz = nz or n
+    nzg = nz_global or nz
+    rng = np.random.default_rng(seed)
+    i = np.arange(n, dtype=np.float64)[None, None, :] / n
+    j = np.arange(ny, dtype=np.float64)[None, :, None] / ny
+    kz = ((z0 + np.arange(nz)) % nzg).astype(np.float64)[:, None, None] / nzg
+
+    def field(ks, ph):
+        out = np.zeros((nz, ny, n))
+        for k, p_ in zip(ks, ph):
+            out = out + np.sin(TWO_PI * (k[0] * i + k[1] * j + k[2] * kz) + p_)
+        return out
+
+    ks, ph = _smooth_modes(rng, 4, 2)
+    sT = field(ks, ph)
+    T = 1200.0 + 300.0 * sT / 4.0  # |sum of 4 unit sinusoids| <= 4
+    u = []
+    for _ in range(3):
+        ks, ph = _smooth_modes(rng, 8, 2)
+        s = field(ks, ph)
+        u.append(10.0 * s / 8.0)
+    ks, ph = _smooth_modes(rng, 2, 1)
+    s1 = field(ks, ph)
+    ks, ph = _smooth_modes(rng, 2, 1)
+    s2 = field(ks, ph)
+    Y = np.zeros((NSP, nz, ny, n))
+    Y[SP["H2"]] = 0.02 + 0.01 * (s1 / 2.0)
+    Y[SP["O2"]] = 0.22 + 0.02 * (s2 / 2.0)
+    for sp in ("H2O", "H", "O", "OH", "HO2", "H2O2"):
+        Y[SP[sp]] = 1e-6
+    if ignition:
+        T = np.full((nz, ny, n), 600.0)
+        Y[SP["H2"]] = 0.0285
+        Y[SP["O2"]] = 0.2264
+    if hot_spot or ignition:
+        c = np.array([n / 2.0, ny / 2.0, nzg / 2.0])
+
+        def pdist(a, L):
+            d = np.abs(a - 0.0)
+            return np.minimum(d, L - d)
+        xi = np.arange(n, dtype=np.float64)[None, None, :]
+        yj = np.arange(ny, dtype=np.float64)[None, :, None]
+        zk = ((z0 + np.arange(nz)) % nzg).astype(np.float64)[:, None, None]
+        r2 = pdist(xi - c[0], n) ** 2 + pdist(yj - c[1], ny) ** 2 + pdist(zk - c[2], nzg) ** 2
+        g = np.exp(-r2 / 20.0 ** 2)
+        peak = 1500.0 if ignition else 1800.0
+        T = T + (peak - T) * g
+    Y[SP["N2"]] = 1.0 - Y[:SP["N2"]].sum(axis=0)
+    Y = Y / Y.sum(axis=0)
+    p = np.full((nz, ny, n), 101325.0)
+    return (np.ascontiguousarray(T), np.ascontiguousarray(p),
+            np.ascontiguousarray(np.stack(u)), np.ascontiguousarray(Y))

@@ -1,0 +1,89 @@
+"""GPU parity of the reacting-NS right-hand side (ctoprim, hypterm, narrow
+diffterm + transport, wdot) against the CPU oracle oracle/ns_oracle.c on the
+configs[0] state generator.  Tolerance (BASELINE.json north_star): per-
+component max error <= 1e-10 of the component's max magnitude.  The oracle is
+"parity unpinned" beyond its building blocks (no reference NS exists)."""
+import numpy as np
+import pytest
+
+import paper_1309_7327_b200 as P
+from paper_1309_7327_b200 import workloads as W
+from oracle import oracle as O
+
+pytestmark = pytest.mark.gpu
+TOL = 1e-10
+DX = 1e-4
+
+
+def _state(n, **kw):
+    T, p, uvw, Y = W.ns_primitives(n, **kw)
+    return O.ns_conserved(T, p, uvw, Y), (T, p, uvw, Y)
+
+
+def _percomp(a, b):
+    return [float(np.abs(a[v] - b[v]).max() / max(np.abs(b[v]).max(), 1e-300))
+            for v in range(a.shape[0])]
+
+
+def test_conserved_from_primitives(cuda):
+    U, prims = _state(12)
+    Ug = P.ns_conserved(*prims)
+    assert max(_percomp(Ug, U)) <= 1e-14
+
+
+@pytest.mark.parametrize("part", [P.NS_FULL, P.NS_ADVDIFF, P.NS_CHEM])
+@pytest.mark.parametrize("n,kw", [(16, {}), (24, {"hot_spot": True})])
+def test_ns_rhs_vs_oracle(cuda, part, n, kw):
+    U, _ = _state(n, **kw)
+    ref = O.ns_rhs(U, DX, part)
+    op = P.NsOperator(n, n, n, DX)
+    got = (op.full, op.advdiff, op.chem)[part](0.0, U)
+    errs = _percomp(got, ref)
+    assert max(errs) <= TOL, errs
+
+
+def test_ns_temperature_pressure(cuda):
+    U, (T, p, _, _) = _state(12)
+    op = P.NsOperator(12, 12, 12, DX)
+    Tg, pg = op.temperature_pressure(U)
+    assert np.abs(Tg - T).max() <= 1e-9 and np.abs(pg - p).max() / 1e5 <= 1e-12
+
+
+def test_ns_split_sums_to_full(cuda):
+    U, _ = _state(16)
+    op = P.NsOperator(16, 16, 16, DX)
+    full = op.full(0.0, U)
+    s = op.advdiff(0.0, U) + op.chem(0.0, U)
+    assert max(_percomp(s, full)) <= 1e-13
+
+
+def test_ns_invariants(cuda):
+    """Physics-independent checks: continuity/momentum conserve the total
+    (telescoping), species RHS sums to the continuity RHS (mass consistency
+    of the corrected diffusion fluxes), chemistry conserves mass."""
+    n = 16
+    U, _ = _state(n, hot_spot=True)
+    op = P.NsOperator(n, n, n, DX)
+    r = op.advdiff(0.0, U)
+    for v in range(4):
+        assert abs(r[v].sum()) <= 1e-12 * np.abs(r[v]).max() * r[v].size
+    assert np.abs(r[5:].sum(0) - r[0]).max() <= 1e-12 * np.abs(r[0]).max()
+    c = op.chem(0.0, U)
+    assert np.abs(c[5:].sum(0)).max() <= 1e-12 * np.abs(c[5:]).max()
+
+
+def test_ns_slab_matches_periodic(cuda):
+    """One z-slab with 4 ghost planes (multi-GPU layout) equals the periodic
+    box on its planes."""
+    import torch
+    n, z0, nzl, G = 16, 4, 8, 4
+    U, _ = _state(n)
+    full = P.NsOperator(n, n, n, DX).full(0.0, U)
+    idx = [(z0 + k - G) % n for k in range(nzl + 2 * G)]
+    Ug = torch.from_numpy(np.ascontiguousarray(U[:, idx])).to(cuda)
+    slab = P.NsOperator(n, n, nzl, DX, zghost=G)
+    out = torch.empty((14, nzl, n, n), dtype=torch.float64, device=cuda)
+    slab.rhs_ghosted(Ug, out)
+    torch.cuda.synchronize()
+    got = out.cpu().numpy()
+    assert max(_percomp(got, full[:, z0:z0 + nzl])) <= 1e-13
