@@ -45,6 +45,8 @@ def parse():
     p.add_argument("--kc", type=int, default=0)
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--e2e-steps", type=int, default=20)
+    p.add_argument("--no-ns", action="store_true")
+    p.add_argument("--ns-steps", type=int, default=5)
     return p.parse_args()
 
 
@@ -194,6 +196,61 @@ def run_reference(args):
                 "d2h_bytes_per_step": 0},
     }
     print(json.dumps(out), flush=True)
+
+
+# ---------------------------------------------------------- NS secondary
+NS_FLOP_PER_CELL = 8850   # frozen algorithmic count, DESIGN.md "NS RHS flop count"
+NS_BYTES_PER_CELL = 224   # 14 conserved fp64 in + 14 out (fully fused minimum)
+
+
+def ns_rhs_measurement(n, dev, stream, fp64_peak, hbm_peak, steps):
+    """Full NS RHS (ctoprim, hypterm, narrow diffterm + transport, wdot) on
+    the configs[3] state generator (hot spot), n^3 periodic, dx = 1e-4 m."""
+    import torch
+    import paper_1309_7327_b200 as P
+    from paper_1309_7327_b200 import workloads as W
+    T, p, uvw, Y = W.ns_primitives(n, hot_spot=True)
+    U = P.ns_conserved(*(torch.from_numpy(a).to(dev) for a in (T, p, uvw, Y)))
+    del T, p, uvw, Y
+    op = P.NsOperator(n, n, n, 1e-4)
+    op.set_stream(stream)
+    out = torch.empty_like(U)
+    op.full(0.0, U, out)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(steps):
+        op.full(0.0, U, out)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / steps
+    cells = n ** 3
+    tf = NS_FLOP_PER_CELL * cells / (ms * 1e-3) / 1e12
+    gbs = NS_BYTES_PER_CELL * cells / (ms * 1e-3) / 1e9
+    res = {"workload": f"configs[3] full reacting-NS RHS, {n}^3, hot spot, 9-species synthetic "
+                       "mechanism, periodic", "value": cells / (ms * 1e-3),
+           "unit": "cell-RHS/s", "ms_per_rhs": ms, "steps": steps,
+           "roofline": {"bound": "fp64", "achieved": tf, "peak": fp64_peak, "unit": "TFLOP/s",
+                        "frac": tf / fp64_peak, "flop_per_cell": NS_FLOP_PER_CELL,
+                        "hbm": {"achieved": gbs, "peak": hbm_peak, "frac": gbs / hbm_peak,
+                                "bytes_per_cell": NS_BYTES_PER_CELL}}}
+    # the oracle (C restatement, 1 thread) on a 24^3 sample of the same generator
+    try:
+        import time as _t
+        from oracle import oracle as O
+        Tn, pn, un, Yn = W.ns_primitives(24, hot_spot=True)
+        Uh = O.ns_conserved(Tn, pn, un, Yn)
+        O.ns_rhs(Uh, 1e-4, 0)
+        t0 = _t.perf_counter()
+        O.ns_rhs(Uh, 1e-4, 0)
+        res["cpu_baseline"] = {"value": 24 ** 3 / (_t.perf_counter() - t0), "unit": "cell-RHS/s",
+                               "cores": 1, "kind": "port",
+                               "sample": "24^3 box, oracle/ns_oracle.c (no reference NS exists)"}
+    except Exception as exc:  # noqa: BLE001
+        res["cpu_baseline"] = {"value": None, "kind": "unavailable", "sample": str(exc)}
+    del U, out
+    torch.cuda.empty_cache()
+    return res
 
 
 # ------------------------------------------------------------------- ours
@@ -349,6 +406,14 @@ def main():
     e2e_ms = max_over_ranks(f0.elapsed_time(f1)) / e2e_steps
     e2e_value = cells_total / (e2e_ms * 1e-3)
 
+    # ---- secondary: the full reacting-NS RHS (configs[3] state, this GPU's block)
+    ns = None
+    if not args.no_ns and world == 1:
+        try:
+            ns = ns_rhs_measurement(n, dev, stream, fp64_peak, hbm_peak, args.ns_steps)
+        except Exception as exc:  # noqa: BLE001
+            ns = {"error": str(exc)}
+
     # ---- CPU baseline (rank 0, N = 1 only)
     cpu = None
     if world == 1 and rank == 0 and not args.no_cpu_baseline:
@@ -391,6 +456,7 @@ def main():
             "gpu_launches": launches,
             "clocks": clocks,
             "cpu_baseline": cpu,
+            "ns_rhs": ns,
         }
         print(json.dumps(line), flush=True)
     if world > 1:
