@@ -19,7 +19,12 @@
  * lambda_k; bulk viscosity xi = XI_OVER_ETA * eta.
  * Kinetics: k = A T^b exp(-Ea / (R_u T)) for forward and reverse
  * directions independently (no equilibrium constants), third body
- * [M] = sum_k C_k with unit efficiencies.
+ * [M] = sum_k C_k with unit efficiencies.  The prefactors are sized so that
+ * at 1200-1800 K the fastest radical time scale is ~50-200 acoustic steps at
+ * dx = 1e-4 m (CFL 0.5): explicit SDC on the full RHS (configs[2]) stays
+ * well inside its stability region, and a 100x faster chemistry (which made
+ * explicit SDC at CFL 0.5 blow up on the configs[3] hot spot) remains a
+ * one-line change for MRSDC studies.
  */
 #ifndef SMC_MECHANISM_H
 #define SMC_MECHANISM_H
@@ -53,12 +58,15 @@ static const double SMC_THERMO[SMC_NSP][4] = {
 };
 
 /* transport prefactors at 300 K (self-chosen): mu0 [Pa s], lam0 [W/m/K],
- * rhoD0 [kg/m/s] */
+ * rhoD0 [kg/m/s].  rhoD_k multiplies grad X_k in Fbar_k,
+ * so it already carries the W_k / W factor of a mass-based mixture
+ * coefficient: light species (H, H2) get small rhoD0 and every species'
+ * effective mass diffusivity rhoD_k W / (rho W_k) stays ~1e-4..2e-3 m^2/s. */
 static const double SMC_MU0[SMC_NSP] = {9.0e-6, 2.0e-5, 1.0e-5, 6.0e-6, 1.5e-5,
                                         1.5e-5, 2.0e-5, 1.9e-5, 1.8e-5};
 static const double SMC_LAM0[SMC_NSP] = {0.18, 0.026, 0.018, 0.40, 0.05, 0.05, 0.027, 0.025, 0.026};
-static const double SMC_RHOD0[SMC_NSP] = {8.0e-5, 2.2e-5, 2.6e-5, 1.2e-4, 3.5e-5,
-                                          3.4e-5, 2.2e-5, 2.2e-5, 2.1e-5};
+static const double SMC_RHOD0[SMC_NSP] = {5.7e-6, 2.5e-5, 1.7e-5, 4.3e-6, 2.0e-5,
+                                          2.1e-5, 2.6e-5, 2.7e-5, 2.1e-5};
 
 /* Reactions: up to 3 reactant / product species indices (-1 = none),
  * third-body flag, forward {A, b, Ea}, reverse {A, b, Ea} (self-chosen). */
@@ -72,31 +80,31 @@ typedef struct {
 
 static const smc_reaction SMC_REACTIONS[SMC_NREAC] = {
     /* H + O2 = O + OH */
-    {{SP_H, SP_O2, -1}, {SP_O, SP_OH, -1}, 0, {2.0e8, 0.0, 70000.0}, {1.2e7, 0.2, 2000.0}},
+    {{SP_H, SP_O2, -1}, {SP_O, SP_OH, -1}, 0, {2e+06, 0.0, 70000.0}, {1.2e+05, 0.2, 2000.0}},
     /* O + H2 = H + OH */
-    {{SP_O, SP_H2, -1}, {SP_H, SP_OH, -1}, 0, {5.0e-2, 2.6, 26000.0}, {2.2e-2, 2.6, 18000.0}},
+    {{SP_O, SP_H2, -1}, {SP_H, SP_OH, -1}, 0, {0.0005, 2.6, 26000.0}, {0.00022, 2.6, 18000.0}},
     /* OH + H2 = H2O + H */
-    {{SP_OH, SP_H2, -1}, {SP_H2O, SP_H, -1}, 0, {2.0e2, 1.5, 14000.0}, {9.0e2, 1.5, 77000.0}},
+    {{SP_OH, SP_H2, -1}, {SP_H2O, SP_H, -1}, 0, {2, 1.5, 14000.0}, {9, 1.5, 77000.0}},
     /* O + H2O = OH + OH */
-    {{SP_O, SP_H2O, -1}, {SP_OH, SP_OH, -1}, 0, {3.0e0, 2.0, 56000.0}, {1.0e0, 2.0, 3000.0}},
+    {{SP_O, SP_H2O, -1}, {SP_OH, SP_OH, -1}, 0, {0.03, 2.0, 56000.0}, {0.01, 2.0, 3000.0}},
     /* H2 + M = H + H + M */
-    {{SP_H2, -1, -1}, {SP_H, SP_H, -1}, 1, {4.5e13, -1.4, 436000.0}, {1.0e6, -1.0, 0.0}},
+    {{SP_H2, -1, -1}, {SP_H, SP_H, -1}, 1, {4.5e+11, -1.4, 436000.0}, {1e+04, -1.0, 0.0}},
     /* O + O + M = O2 + M */
-    {{SP_O, SP_O, -1}, {SP_O2, -1, -1}, 1, {6.0e3, -0.5, 0.0}, {2.0e12, -0.9, 495000.0}},
+    {{SP_O, SP_O, -1}, {SP_O2, -1, -1}, 1, {60, -0.5, 0.0}, {2e+10, -0.9, 495000.0}},
     /* H + OH + M = H2O + M */
-    {{SP_H, SP_OH, -1}, {SP_H2O, -1, -1}, 1, {2.2e10, -2.0, 0.0}, {3.0e17, -2.5, 500000.0}},
+    {{SP_H, SP_OH, -1}, {SP_H2O, -1, -1}, 1, {2.2e+08, -2.0, 0.0}, {3e+15, -2.5, 500000.0}},
     /* H + O2 + M = HO2 + M */
-    {{SP_H, SP_O2, -1}, {SP_HO2, -1, -1}, 1, {6.0e5, -0.8, 0.0}, {2.0e12, -0.6, 205000.0}},
+    {{SP_H, SP_O2, -1}, {SP_HO2, -1, -1}, 1, {6e+03, -0.8, 0.0}, {2e+10, -0.6, 205000.0}},
     /* HO2 + H = OH + OH */
-    {{SP_HO2, SP_H, -1}, {SP_OH, SP_OH, -1}, 0, {7.0e7, 0.0, 1200.0}, {2.0e4, 0.6, 150000.0}},
+    {{SP_HO2, SP_H, -1}, {SP_OH, SP_OH, -1}, 0, {7e+05, 0.0, 1200.0}, {200, 0.6, 150000.0}},
     /* HO2 + H = H2 + O2 */
-    {{SP_HO2, SP_H, -1}, {SP_H2, SP_O2, -1}, 0, {2.8e7, 0.0, 4500.0}, {5.0e6, 0.3, 230000.0}},
+    {{SP_HO2, SP_H, -1}, {SP_H2, SP_O2, -1}, 0, {2.8e+05, 0.0, 4500.0}, {5e+04, 0.3, 230000.0}},
     /* HO2 + OH = H2O + O2 */
-    {{SP_HO2, SP_OH, -1}, {SP_H2O, SP_O2, -1}, 0, {2.9e7, 0.0, 0.0}, {1.0e8, 0.2, 290000.0}},
+    {{SP_HO2, SP_OH, -1}, {SP_H2O, SP_O2, -1}, 0, {2.9e+05, 0.0, 0.0}, {1e+06, 0.2, 290000.0}},
     /* HO2 + HO2 = H2O2 + O2 */
-    {{SP_HO2, SP_HO2, -1}, {SP_H2O2, SP_O2, -1}, 0, {4.0e6, 0.0, 5000.0}, {1.0e8, 0.0, 160000.0}},
+    {{SP_HO2, SP_HO2, -1}, {SP_H2O2, SP_O2, -1}, 0, {4e+04, 0.0, 5000.0}, {1e+06, 0.0, 160000.0}},
     /* H2O2 + M = OH + OH + M */
-    {{SP_H2O2, -1, -1}, {SP_OH, SP_OH, -1}, 1, {1.2e11, 0.0, 190000.0}, {2.3e6, -0.8, 0.0}},
+    {{SP_H2O2, -1, -1}, {SP_OH, SP_OH, -1}, 1, {1.2e+09, 0.0, 190000.0}, {2.3e+04, -0.8, 0.0}},
 };
 
 #endif /* SMC_MECHANISM_H */

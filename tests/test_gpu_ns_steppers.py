@@ -56,7 +56,7 @@ def _cb(n, part):
 
 def test_sdc_ten_steps_vs_oracle(cuda, golden):
     n, steps = 12, 10
-    U0, prims = _state(n, hot_spot=True)
+    U0, prims = _state(n)  # configs[2]: the configs[0] generator (T = 1200 +- 300 K)
     dt = acoustic_dt(prims, DX)
     t1 = steps * dt
     # oracle: integrate_sdc restated (sdc.cpp:38-127) over the NS oracle
@@ -83,7 +83,7 @@ def test_sdc_ten_steps_vs_oracle(cuda, golden):
 
 def test_mrsdc_mode1_vs_oracle(cuda, golden):
     n, steps = 12, 3
-    U0, prims = _state(n, hot_spot=True)
+    U0, prims = _state(n, ignition=True)  # configs[4]: 1500 K kernel in 600 K H2/air
     dt = acoustic_dt(prims, DX)
     t1 = steps * dt
     c1, c2 = _cb(n, 1), _cb(n, 2)
