@@ -55,6 +55,10 @@ typedef void (*smc_rhs_fn)(double t, const double* u, double* out, long long n, 
 typedef double (*smc_time_fn)(double t, void* ctx);
 typedef void (*smc_field_fn)(double t, double* field, void* ctx);
 typedef double (*smc_reduce_fn)(double local, void* ctx);
+/* device-side callback: u, out are device pointers, stream the handle's
+ * cudaStream_t; must be stream-ordered on it */
+typedef void (*smc_dev_rhs_fn)(double t, const double* u, double* out, long long n, void* stream,
+                               void* ctx);
 
 /* Sweep diagnostics: SweepDiagnostics (core/include/nsdc/sdc.hpp:30-35) and
  * MrsdcDiagnostics (core/include/nsdc/mrsdc.hpp:30-38).  `residuals` is a
@@ -152,6 +156,11 @@ int smc_ns_conserved(const double* T, const double* p, const double* uvw, const 
 
 /* Any host callback as an operator (nsdc::Rhs, core/include/nsdc/field.hpp:14-16). */
 int smc_rhs_from_callback(long long dim, smc_rhs_fn f, void* ctx, smc_rhs** out);
+
+/* A callback that works on device buffers itself (e.g. a multi-GPU RHS whose
+ * halo exchange is issued by the host through NCCL) — lets the device
+ * steppers drive any RHS without host round trips. */
+int smc_rhs_from_device_callback(long long dim, smc_dev_rhs_fn f, void* ctx, smc_rhs** out);
 
 /* Rhs call: out = f(t, u) — HeatOperator::rhs / as_rhs (pde.cpp:266-284). */
 int smc_rhs_eval(smc_rhs* op, double t, const double* u, double* out, int where);

@@ -27,7 +27,7 @@ from ._capi import (CLENSHAW_CURTIS, DEVICE, GAUSS_LOBATTO, HOST, NARROW6, NARRO
 __all__ = [
     "SmcError", "SmcInvalidArgument", "SmcIntegrationError", "StencilChoice", "stencil_preset",
     "build_narrow", "apply_narrow", "apply_wide", "first_derivative8", "HeatOperator",
-    "Narrow3DOperator", "Narrow3DSlab", "CallbackRhs", "SdcStepper", "MrsdcStepper", "StepControls", "nodes",
+    "Narrow3DOperator", "Narrow3DSlab", "CallbackRhs", "DeviceCallbackRhs", "SdcStepper", "MrsdcStepper", "StepControls", "nodes",
     "integration_matrices", "build_hierarchy", "SMC_M47", "SMC_M48", "OPTIMAL_M47", "NsOperator",
     "ns_conserved", "NS_FULL", "NS_ADVDIFF", "NS_CHEM",
     "OPTIMAL_M48", "DEFAULT_M36", "launch_count",
@@ -235,6 +235,41 @@ class Narrow3DSlab(_Rhs):
 
     def set_kc(self, kc: int) -> None:
         check(_capi.lib().smc_narrow3d_set_kc(self._h, kc))
+
+
+class _CudaPtr:
+    """Minimal __cuda_array_interface__ view of a raw device pointer."""
+
+    def __init__(self, ptr: int, n: int, stream: int):
+        self.__cuda_array_interface__ = {"shape": (n,), "typestr": "<f8", "data": (ptr, False),
+                                         "version": 3, "strides": None,
+                                         "stream": stream if stream else None}
+
+
+def device_tensor(ptr: int, n: int, stream: int = 0):
+    """torch.float64 CUDA tensor aliasing n doubles at device pointer ptr."""
+    import torch
+    return torch.as_tensor(_CudaPtr(ptr, n, stream), device="cuda")
+
+
+class DeviceCallbackRhs(_Rhs):
+    """fn(t, u, out) on torch CUDA tensors (views of the stepper's buffers),
+    called with the operator's stream current; for RHS whose work includes
+    host-issued collectives (multi-GPU halo exchange)."""
+
+    def __init__(self, dim: int, fn):
+        import torch
+
+        def tramp(t, u, out, n, stream, ctx):
+            s = torch.cuda.ExternalStream(stream) if stream else torch.cuda.default_stream()
+            with torch.cuda.stream(s):
+                fn(t, device_tensor(u, n, stream), device_tensor(out, n, stream))
+
+        cb = _capi.DEV_RHS_FN(tramp)
+        h = C.c_void_p()
+        check(_capi.lib().smc_rhs_from_device_callback(dim, cb, None, C.byref(h)))
+        super().__init__(h)
+        self._keep.append(cb)
 
 
 class CallbackRhs(_Rhs):

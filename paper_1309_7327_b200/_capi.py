@@ -24,6 +24,8 @@ RHS_FN = C.CFUNCTYPE(None, C.c_double, _D, _D, C.c_longlong, C.c_void_p)
 TIME_FN = C.CFUNCTYPE(C.c_double, C.c_double, C.c_void_p)
 FIELD_FN = C.CFUNCTYPE(None, C.c_double, _D, C.c_void_p)
 REDUCE_FN = C.CFUNCTYPE(C.c_double, C.c_double, C.c_void_p)
+DEV_RHS_FN = C.CFUNCTYPE(None, C.c_double, C.c_void_p, C.c_void_p, C.c_longlong, C.c_void_p,
+                         C.c_void_p)
 
 
 class SmcError(RuntimeError):
@@ -77,6 +79,7 @@ _SIG = {
     "smc_ns_temperature_pressure": (C.c_int, [_VP, _VP, _VP, _VP, C.c_int]),
     "smc_ns_conserved": (C.c_int, [_VP, _VP, _VP, _VP, C.c_longlong, _VP, C.c_int]),
     "smc_rhs_from_callback": (C.c_int, [C.c_longlong, RHS_FN, _VP, C.POINTER(_VP)]),
+    "smc_rhs_from_device_callback": (C.c_int, [C.c_longlong, DEV_RHS_FN, _VP, C.POINTER(_VP)]),
     "smc_rhs_eval": (C.c_int, [_VP, C.c_double, _VP, _VP, C.c_int]),
     "smc_rhs_dim": (C.c_longlong, [_VP]),
     "smc_rhs_set_stream": (C.c_int, [_VP, _VP]),

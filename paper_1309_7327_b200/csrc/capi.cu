@@ -263,6 +263,16 @@ int smc_rhs_from_callback(long long dim, smc_rhs_fn f, void* ctx, smc_rhs** out)
   });
 }
 
+int smc_rhs_from_device_callback(long long dim, smc_dev_rhs_fn f, void* ctx, smc_rhs** out) {
+  return guarded([&] {
+    need(out, "out");
+    *out = nullptr;
+    auto h = std::make_unique<smc_rhs>();
+    h->op = std::make_unique<smc::DeviceCallbackOp>(dim, f, ctx);
+    *out = h.release();
+  });
+}
+
 int smc_rhs_eval(smc_rhs* h, double t, const double* u, double* out, int where) {
   return guarded([&] {
     need(u, "u"), need(out, "out");

@@ -143,6 +143,29 @@ class HostCallbackOp final : public RhsOp {
   std::vector<double> hu_, ho_;
 };
 
+// A callback that computes on device buffers itself (e.g. a multi-GPU RHS
+// whose halo exchange runs through torch.distributed / NCCL on the host).
+class DeviceCallbackOp final : public RhsOp {
+ public:
+  using Cb = void (*)(double t, const double* u, double* out, long long n, void* stream,
+                      void* ctx);
+  DeviceCallbackOp(long long dim, Cb cb, void* ctx) : dim_(dim), cb_(cb), ctx_(ctx) {
+    require(dim >= 1, "device callback rhs: dim must be positive");
+    require(cb != nullptr, "device callback rhs: null callback");
+  }
+  long long dim() const override { return dim_; }
+  void eval_device(double t, const double* u, double* out) override {
+    cb_(t, u, out, dim_, static_cast<void*>(stream_), ctx_);
+    ++evals_;
+  }
+  const char* name() const override { return "device_callback"; }
+
+ private:
+  long long dim_;
+  Cb cb_;
+  void* ctx_;
+};
+
 StencilM make_stencil(int order, const double* params, int nparams, int* s);
 int num_sms();
 

@@ -120,3 +120,76 @@ class DistributedNarrow3D:
             r.wait()                                     # current stream waits on NCCL
         self.op.apply_planes(u_ghosted, out, 0, lo)
         self.op.apply_planes(u_ghosted, out, hi, self.slab.nz)
+
+
+# -------------------------------------------------- multi-component (NS)
+def exchange_halo_fields(U, slab: Slab, dist) -> None:
+    """Halo exchange of a field-major state U[v, plane, y, x] (e.g. the 14
+    conserved NS fields): the 4 boundary planes of every field are packed
+    into one contiguous message per direction, sent in the order of
+    exchange_ops, and unpacked into the ghost planes.  Blocking (the NS
+    kernels need every ghost before ctoprim)."""
+    a, b = slab.send_up()
+    c, d = slab.recv_down()
+    e, f = slab.send_down()
+    g, h = slab.recv_up()
+    if slab.world == 1:
+        U[:, c:d].copy_(U[:, a:b])
+        U[:, g:h].copy_(U[:, e:f])
+        return
+    up = U[:, a:b].contiguous()
+    down = U[:, e:f].contiguous()
+    from_below = up.new_empty(up.shape)
+    from_above = down.new_empty(down.shape)
+    ops = [dist.P2POp(dist.isend, up, slab.next), dist.P2POp(dist.irecv, from_below, slab.prev),
+           dist.P2POp(dist.isend, down, slab.prev), dist.P2POp(dist.irecv, from_above, slab.next)]
+    for r in dist.batch_isend_irecv(ops):
+        r.wait()
+    U[:, c:d].copy_(from_below)
+    U[:, g:h].copy_(from_above)
+
+
+def allreduce_max(dist, device=None):
+    """Reducer for the device steppers' residual (max over ranks, one double
+    per sweep, sdc.cpp:20-30 / mrsdc.cpp:23-35)."""
+    import torch
+
+    def fn(v: float) -> float:
+        if dist is None or not dist.is_initialized() or dist.get_world_size() == 1:
+            return v
+        t = torch.tensor([v], dtype=torch.float64, device=device)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    return fn
+
+
+class DistributedNs:
+    """configs[3]/[4]: the reacting-NS RHS on this rank's z-slab of a periodic
+    nx x ny x (nz * world) box; ghosts of the 14 conserved fields are
+    exchanged once per RHS and ctoprim/transport are recomputed on them (the
+    paper's choice).  .rhs(part) returns an Rhs usable by
+    the device steppers (state = the rank's interior cells)."""
+
+    def __init__(self, slab: Slab, nx: int, ny: int, dx: float, dist=None, choice=None):
+        import torch
+        from . import NsOperator
+        self.slab, self.dist = slab, dist
+        self.nx, self.ny = nx, ny
+        self.ns = NsOperator(nx, ny, slab.nz, dx, choice=choice, zghost=slab.ghost)
+        self.U = torch.zeros((14, slab.nz + 2 * slab.ghost, ny, nx), dtype=torch.float64,
+                             device="cuda")
+        self.dim = 14 * slab.nz * ny * nx
+
+    def apply(self, U_interior, out, part: int = 0) -> None:
+        """out = RHS(U) on interior cells (device tensors, 14 x nz x ny x nx)."""
+        G, nz = self.slab.ghost, self.slab.nz
+        self.U[:, G:G + nz].copy_(U_interior.view(14, nz, self.ny, self.nx))
+        exchange_halo_fields(self.U, self.slab, self.dist)
+        import torch
+        self.ns.set_stream(torch.cuda.current_stream())
+        self.ns.rhs_ghosted(self.U, out.view(14, nz, self.ny, self.nx), part)
+
+    def rhs(self, part: int = 0):
+        from . import DeviceCallbackRhs
+        return DeviceCallbackRhs(self.dim, lambda t, u, out: self.apply(u, out, part))

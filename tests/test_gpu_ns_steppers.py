@@ -128,3 +128,26 @@ def test_sdc_device_buffers_and_stream(cuda):
     host, _ = st.integrate(op.full, U0, 0.0, 2 * dt, 2)
     assert np.array_equal(out.cpu().numpy(), host)
     assert math.isfinite(d.residual_history[-1])
+
+
+def test_distributed_ns_single_rank_through_device_callback(cuda):
+    """The multi-GPU NS path at world size 1 (slab with self-copied ghosts,
+    RHS as a device callback into the device-resident stepper) reproduces
+    the periodic operator's time advance bitwise."""
+    import torch
+    from paper_1309_7327_b200.distributed import DistributedNs, Slab, allreduce_max
+    n = 12
+    U0, prims = _state(n)
+    dt = acoustic_dt(prims, DX)
+    dns = DistributedNs(Slab(0, 1, n), n, n, DX)
+    rhs = dns.rhs(P.NS_FULL)
+    rhs.set_stream(torch.cuda.current_stream())
+    st = P.SdcStepper(3, P.StepControls(4, 0.0))
+    st.set_reducer(allreduce_max(None))
+    Ud = torch.from_numpy(U0).to(cuda)
+    got, d = st.integrate(rhs, Ud, 0.0, 3 * dt, 3)
+    torch.cuda.synchronize()
+    op = P.NsOperator(n, n, n, DX)
+    ref, _ = P.SdcStepper(3, P.StepControls(4, 0.0)).integrate(op.full, U0, 0.0, 3 * dt, 3)
+    assert np.array_equal(got.cpu().numpy(), ref)
+    assert d.fresh_evals == 3 * 8 + 1
