@@ -164,12 +164,13 @@ struct TypeC {
 };
 
 // ---------------------------------------------------------------- pde.hpp
-struct Grid2D {
+inline constexpr double kTwoPi = 2.0 * std::numbers::pi;
+struct Grid2D {  // pde.hpp:14-22: node-based periodic [0, 2pi)^2
   int nx = 0, ny = 0;
-  double dx() const { return 2.0 * std::numbers::pi / nx; }
-  double dy() const { return 2.0 * std::numbers::pi / ny; }
-  double x(int i) const { return i * 2.0 * std::numbers::pi / nx; }
-  double y(int j) const { return j * 2.0 * std::numbers::pi / ny; }
+  double dx() const { return kTwoPi / nx; }
+  double dy() const { return kTwoPi / ny; }
+  double x(int i) const { return i * kTwoPi / nx; }
+  double y(int j) const { return j * kTwoPi / ny; }
 };
 struct Field2D {
   int nx = 0, ny = 0;
