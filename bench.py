@@ -47,6 +47,10 @@ def parse():
     p.add_argument("--e2e-steps", type=int, default=20)
     p.add_argument("--no-ns", action="store_true")
     p.add_argument("--ns-steps", type=int, default=5)
+    p.add_argument("--overlap", action="store_true",
+                   help="N>1: interior planes run while the halo is in flight (split launch)")
+    p.add_argument("--slab", action="store_true",
+                   help="use the multi-GPU z-slab path also at N=1 (ghosts by self-copy)")
     return p.parse_args()
 
 
@@ -279,7 +283,8 @@ def main():
     stream = torch.cuda.current_stream()
 
     # ---- inputs resident in HBM
-    if world == 1:
+    slab_mode = world > 1 or args.slab
+    if not slab_mode:
         a, u = W.narrow3d_inputs(n, xp=torch, device=dev)
         op = P.Narrow3DOperator(a, 1 / n, 1 / n, 1 / n)
         op.set_stream(stream)
@@ -308,7 +313,7 @@ def main():
         out = torch.empty((n, n, n), dtype=torch.float64, device=dev)
 
         def step():
-            dop.apply(u, out)
+            dop.apply(u, out, overlap=args.overlap)
 
     def barrier():
         if world > 1:
@@ -349,7 +354,7 @@ def main():
     value = cells_total * args.steps / (ms * 1e-3)
 
     # ---- dominant kernel alone (for N > 1 the step also holds the exchange)
-    if world == 1:
+    if not slab_mode:
         k_ms = ms_step
     else:
         k0, k1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -378,7 +383,7 @@ def main():
 
     # ---- e2e through the public API with host buffers
     e2e_steps = max(3, min(args.e2e_steps, args.steps))
-    if world == 1:
+    if not slab_mode:
         uh = torch.empty((n, n, n), dtype=torch.float64).pin_memory()
         oh = torch.empty((n, n, n), dtype=torch.float64).pin_memory()
         uh.copy_(u.cpu())
@@ -392,7 +397,7 @@ def main():
 
         def e2e_step():
             u[4:4 + n].copy_(uh, non_blocking=True)
-            dop.apply(u, out)
+            dop.apply(u, out, overlap=args.overlap)
             oh.copy_(out, non_blocking=True)
             torch.cuda.current_stream().synchronize()
     e2e_step()
@@ -434,8 +439,8 @@ def main():
             "config": {
                 "workload": f"configs[1] narrow 8th-order (a U_x)_x+(a U_y)_y+(a U_z)_z, "
                             f"{n}^3 per GPU, periodic" +
-                            ("" if world == 1 else f", z-slabs of a {n}x{n}x{n * world} box, "
-                                                   "4-plane NCCL halo overlapped"),
+                            ("" if not slab_mode else f", z-slabs of a {n}x{n}x{n * world} box, "
+                                                      "4-plane NCCL halo" + (", overlapped" if args.overlap else "")),
                 "cells_per_gpu": cells_rank, "stencil": "SMC (m47=3557/44100, m48=-2083/117600)",
                 "l2": f"inputs larger than L2 ({(2 * 8 * cells_rank) / 1e6:.0f} MB read + "
                       f"{8 * cells_rank / 1e6:.0f} MB written per step per GPU)",

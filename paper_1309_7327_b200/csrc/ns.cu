@@ -8,6 +8,7 @@
 //   assemble: mixed viscous terms, correction-velocity terms  -> out
 //   wdot    : rho omega_k                                       -> out
 #include <cmath>
+#include <cstdlib>
 
 #include "ns.cuh"
 
@@ -528,6 +529,52 @@ void upload_tables() {
 
 int blocks(long long n) { return static_cast<int>((n + 255) / 256); }
 
+#include "ns_dir.inc"
+
+// SMC_NS_V1=1 selects the v1 one-thread-per-cell gather kernels (debug).
+bool ns_v1() {
+  static bool v = [] {
+    const char* e = std::getenv("SMC_NS_V1");
+    return e && std::atoi(e) == 1;
+  }();
+  return v;
+}
+
+template <class K>
+void set_smem(K kern, std::size_t bytes) {
+  SMC_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                static_cast<int>(bytes)));
+}
+
+template <int S>
+void rhs_v2(const Geo& g, const double* U, const double* F, double* A, double* GR, double* MX,
+            double* out, const StencilM& M, cudaStream_t st) {
+  static bool configured = false;
+  const std::size_t sm = sizeof(DirSmem);
+  if (!configured) {
+    set_smem(ns_phase_a<0, S>, sm), set_smem(ns_phase_a<1, S>, sm), set_smem(ns_phase_a<2, S>, sm);
+    set_smem(ns_phase_b<0>, sm), set_smem(ns_phase_b<1>, sm), set_smem(ns_phase_b<2>, sm);
+    configured = true;
+  }
+  const int allp = g.nz + 2 * g.G;
+  ns_phase_a<0, S><<<dir_grid<0>(g, allp), DT_THREADS, sm, st>>>(U, F, A, GR, out, g, M, -g.G, 1);
+  SMC_CHECK_LAUNCH();
+  ns_phase_a<1, S><<<dir_grid<1>(g, allp), DT_THREADS, sm, st>>>(U, F, A, GR, out, g, M, -g.G, 0);
+  SMC_CHECK_LAUNCH();
+  ns_phase_a<2, S><<<dir_grid<2>(g, allp), DT_THREADS, sm, st>>>(U, F, A, GR, out, g, M, 0, 0);
+  SMC_CHECK_LAUNCH();
+  ns_mixed_fields<<<blocks(g.plane * allp), 256, 0, st>>>(F, GR, A, MX, g);
+  SMC_CHECK_LAUNCH();
+  ns_phase_b<0><<<dir_grid<0>(g, g.nz), DT_THREADS, sm, st>>>(F, A, MX, out, g);
+  SMC_CHECK_LAUNCH();
+  ns_phase_b<1><<<dir_grid<1>(g, g.nz), DT_THREADS, sm, st>>>(F, A, MX, out, g);
+  SMC_CHECK_LAUNCH();
+  ns_phase_b<2><<<dir_grid<2>(g, g.nz), DT_THREADS, sm, st>>>(F, A, MX, out, g);
+  SMC_CHECK_LAUNCH();
+  ns_assemble2<<<blocks(g.plane * g.nz), 256, 0, st>>>(F, A, out, g);
+  SMC_CHECK_LAUNCH();
+}
+
 }  // namespace
 
 NsWorkspace::NsWorkspace(const NsBox& box, double dx, double dy, double dz, const StencilM& M,
@@ -543,6 +590,7 @@ NsWorkspace::NsWorkspace(const NsBox& box, double dx, double dy, double dz, cons
   prim_.resize(static_cast<std::size_t>(F_COUNT) * box.field_len());
   acc_.resize(static_cast<std::size_t>(A_COUNT) * box.cells());
   mixed_.resize(static_cast<std::size_t>(MX_COUNT) * box.field_len());
+  grad_.resize(static_cast<std::size_t>(9) * box.field_len());
 }
 
 static Geo make_geo(const NsBox& b, const double* d) {
@@ -561,7 +609,12 @@ void NsWorkspace::rhs(const double* U, double* out, int part, cudaStream_t st) {
   double* A = acc_.get();
   prim_kernel<<<blocks(g.flen), 256, 0, st>>>(U, F, g);
   SMC_CHECK_LAUNCH();
-  if (part != kNsChem) {
+  if (part != kNsChem && !ns_v1()) {
+    if (s_ == 4)
+      rhs_v2<4>(g, U, F, A, grad_.get(), mixed_.get(), out, M_, st);
+    else
+      rhs_v2<3>(g, U, F, A, grad_.get(), mixed_.get(), out, M_, st);
+  } else if (part != kNsChem) {
     hyp_kernel<<<blocks(n), 256, 0, st>>>(U, F, out, g, 1);
     SMC_CHECK_LAUNCH();
     if (s_ == 4)

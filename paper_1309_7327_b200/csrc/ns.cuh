@@ -43,6 +43,7 @@ class NsWorkspace {
   DevBuf prim_;   // primitive + coefficient fields (all planes)
   DevBuf acc_;    // narrow-stencil accumulators + gradients (interior)
   DevBuf mixed_;  // eta d_i u_j, lam2 sum d_j u_j (all planes)
+  DevBuf grad_;   // d_j u_i (all planes; v2 pipeline)
 };
 
 // Conserved state from primitives (T, p, u, v, w, Y_k), n cells, device ptrs.
