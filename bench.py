@@ -46,6 +46,8 @@ def parse():
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--e2e-steps", type=int, default=20)
     p.add_argument("--no-ns", action="store_true")
+    p.add_argument("--no-advance", action="store_true",
+                   help="skip the configs[2] SDC / configs[4] MRSDC time-advance blocks")
     p.add_argument("--ns-steps", type=int, default=5)
     p.add_argument("--overlap", action="store_true",
                    help="N>1: interior planes run while the halo is in flight (split launch)")
@@ -257,6 +259,66 @@ def ns_rhs_measurement(n, dev, stream, fp64_peak, hbm_peak, steps):
     return res
 
 
+def acoustic_dt(T, p, uvw, Y, dx, cfl=0.5):
+    """CFL 0.5 on max(|u_i| + c) (the synthetic thermodynamics of
+    include/smc_mechanism.h), host side."""
+    import numpy as np
+    W_ = np.array([2.01588e-3, 31.9988e-3, 18.01528e-3, 1.00794e-3, 15.9994e-3, 17.00734e-3,
+                   33.00674e-3, 34.01468e-3, 28.0134e-3])
+    a = np.array([[3.40, 1.0e-4, 1.0e-8], [3.30, 6.0e-4, -1.0e-7], [3.60, 9.0e-4, -1.0e-7],
+                  [2.50, 0.0, 0.0], [2.60, -1.0e-4, 2.0e-8], [3.50, 1.0e-4, 1.0e-8],
+                  [4.00, 1.2e-3, -2.0e-7], [4.50, 2.0e-3, -3.0e-7], [3.25, 5.0e-4, -8.0e-8]])
+    Ru = 8.314462618
+    cp = sum(Y[k] * Ru / W_[k] * (a[k, 0] + a[k, 1] * T + a[k, 2] * T * T) for k in range(9))
+    Rm = sum(Y[k] * Ru / W_[k] for k in range(9))
+    c = np.sqrt(cp / (cp - Rm) * Rm * T)
+    return cfl * dx / float((np.abs(uvw).max(axis=0) + c).max())
+
+
+def advance_measurement(dev, stream):
+    """configs[2]: 10 SDC steps (3 Gauss-Lobatto nodes, 4 sweeps) at CFL 0.5
+    of the configs[0] generator on 128^3; configs[4] (one GPU point): one
+    MRSDC mode-1 step (GL(3) coarse advection-diffusion, GL(5) fine
+    chemistry per coarse interval) on the ignition state at 128^3."""
+    import torch
+    import paper_1309_7327_b200 as P
+    from paper_1309_7327_b200 import workloads as W
+    n, dx, res = 128, 1e-4, {}
+    for name, kw in (("sdc_configs2", {}), ("mrsdc_configs4", {"ignition": True})):
+        T, p, uvw, Y = W.ns_primitives(n, **kw)
+        dt = acoustic_dt(T, p, uvw, Y, dx)
+        U = P.ns_conserved(*(torch.from_numpy(x).to(dev) for x in (T, p, uvw, Y)))
+        op = P.NsOperator(n, n, n, dx)
+        op.set_stream(stream)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        if name.startswith("sdc"):
+            st = P.SdcStepper(3, P.StepControls(4, 0.0))
+            st.integrate(op.full, U, 0.0, dt, 1)  # warm-up (buffers)
+            torch.cuda.synchronize()
+            e0.record(stream)
+            out, d = st.integrate(op.full, U, 0.0, 10 * dt, 10)
+            e1.record(stream)
+            torch.cuda.synchronize()
+            steps, evals = 10, d.fresh_evals
+        else:
+            st = P.MrsdcStepper(3, 5, P.StepControls(4, 0.0))
+            st.integrate_mode1(op.advdiff, op.chem, U, 0.0, dt, 1)
+            torch.cuda.synchronize()
+            e0.record(stream)
+            out, d = st.integrate_mode1(op.advdiff, op.chem, U, 0.0, dt, 1)
+            e1.record(stream)
+            torch.cuda.synchronize()
+            steps, evals = 1, d.f1_evals + d.f2_evals
+        ms = e0.elapsed_time(e1)
+        res[name] = {"cells": n ** 3, "steps": steps, "dt_s": dt, "ms_per_step": ms / steps,
+                     "rhs_evals": evals, "sweeps": d.sweeps,
+                     "final_residual": d.residual_history[-1] if d.residual_history else None,
+                     "finite": bool(torch.isfinite(out).all().item())}
+        del U, out, op, st
+        torch.cuda.empty_cache()
+    return res
+
+
 # ------------------------------------------------------------------- ours
 def main():
     args = parse()
@@ -419,6 +481,13 @@ def main():
         except Exception as exc:  # noqa: BLE001
             ns = {"error": str(exc)}
 
+    adv = None
+    if not args.no_advance and world == 1:
+        try:
+            adv = advance_measurement(dev, stream)
+        except Exception as exc:  # noqa: BLE001
+            adv = {"error": str(exc)}
+
     # ---- CPU baseline (rank 0, N = 1 only)
     cpu = None
     if world == 1 and rank == 0 and not args.no_cpu_baseline:
@@ -462,6 +531,7 @@ def main():
             "clocks": clocks,
             "cpu_baseline": cpu,
             "ns_rhs": ns,
+            "time_advance": adv,
         }
         print(json.dumps(line), flush=True)
     if world > 1:
