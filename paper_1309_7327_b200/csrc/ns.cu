@@ -419,19 +419,12 @@ __global__ void __launch_bounds__(256) assemble_kernel(const double* __restrict_
 }
 
 // ------------------------------------------------------------- wdot
-__global__ void __launch_bounds__(256) wdot_kernel(const double* __restrict__ U,
-                                                   const double* __restrict__ F,
-                                                   double* __restrict__ out, Geo g, int init) {
-  const long long n = g.plane * g.nz;
-  const long long c = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
-  if (c >= n) return;
-  const long long cg = c + g.G * g.plane;
-  const double rho = U[cg];
-  const double T = F[F_T * g.flen + cg];
+// rho omega_k W_k of one cell (smc_mechanism.h kinetics)
+__device__ __forceinline__ void wdot_cell(double rho, double T, const double* Y, double* w) {
   double C[NSP], M = 0.0, om[NSP];
 #pragma unroll
   for (int s = 0; s < NSP; ++s) {
-    C[s] = rho * F[(F_Y + s) * g.flen + cg] / cT.W[s];
+    C[s] = rho * Y[s] / cT.W[s];
     M += C[s];
     om[s] = 0.0;
   }
@@ -457,14 +450,47 @@ __global__ void __launch_bounds__(256) wdot_kernel(const double* __restrict__ U,
       if (cT.prod[r][m] >= 0) om[cT.prod[r][m]] += q;
     }
   }
-  if (init)
-    for (int v = 0; v < 5; ++v) out[v * n + c] = 0.0;
 #pragma unroll
-  for (int s = 0; s < NSP; ++s) {
-    double* o = out + (5 + s) * n + c;
-    const double w = cT.W[s] * om[s];
-    *o = init ? w : *o + w;
-  }
+  for (int s = 0; s < NSP; ++s) w[s] = cT.W[s] * om[s];
+}
+
+// full RHS: += wdot, from the primitive fields
+__global__ void __launch_bounds__(256) wdot_kernel(const double* __restrict__ U,
+                                                   const double* __restrict__ F,
+                                                   double* __restrict__ out, Geo g) {
+  const long long n = g.plane * g.nz;
+  const long long c = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
+  if (c >= n) return;
+  const long long cg = c + g.G * g.plane;
+  double Y[NSP], w[NSP];
+#pragma unroll
+  for (int s = 0; s < NSP; ++s) Y[s] = F[(F_Y + s) * g.flen + cg];
+  wdot_cell(U[cg], F[F_T * g.flen + cg], Y, w);
+#pragma unroll
+  for (int s = 0; s < NSP; ++s) out[(5 + s) * n + c] += w[s];
+}
+
+// chemistry part alone (MRSDC f2): ctoprim's temperature + wdot fused, so the
+// 32 chemistry calls of an MRSDC step read the 14 conserved fields and write
+// the RHS without materialising the primitive workspace.
+__global__ void __launch_bounds__(256) chem_kernel(const double* __restrict__ U,
+                                                   double* __restrict__ out, Geo g) {
+  const long long n = g.plane * g.nz;
+  const long long c = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
+  if (c >= n) return;
+  const long long cg = c + g.G * g.plane;
+  const long long fl = g.flen;
+  const double rho = U[cg];
+  const double ri = 1.0 / rho;
+  double u[3], Y[NSP], w[NSP];
+  for (int i = 0; i < 3; ++i) u[i] = U[(1 + i) * fl + cg] * ri;
+#pragma unroll
+  for (int k = 0; k < NSP; ++k) Y[k] = U[(5 + k) * fl + cg] * ri;
+  const double e = U[4 * fl + cg] * ri - 0.5 * (u[0] * u[0] + u[1] * u[1] + u[2] * u[2]);
+  wdot_cell(rho, temperature(Y, e), Y, w);
+  for (int v = 0; v < 5; ++v) out[v * n + c] = 0.0;
+#pragma unroll
+  for (int s = 0; s < NSP; ++s) out[(5 + s) * n + c] = w[s];
 }
 
 __global__ void __launch_bounds__(256) tp_kernel(const double* __restrict__ F, double* T,
@@ -607,6 +633,11 @@ void NsWorkspace::rhs(const double* U, double* out, int part, cudaStream_t st) {
   const long long n = box_.cells();
   double* F = prim_.get();
   double* A = acc_.get();
+  if (part == kNsChem) {
+    chem_kernel<<<blocks(n), 256, 0, st>>>(U, out, g);
+    SMC_CHECK_LAUNCH();
+    return;
+  }
   prim_kernel<<<blocks(g.flen), 256, 0, st>>>(U, F, g);
   SMC_CHECK_LAUNCH();
   if (part != kNsChem && !ns_v1()) {
@@ -627,8 +658,8 @@ void NsWorkspace::rhs(const double* U, double* out, int part, cudaStream_t st) {
     assemble_kernel<<<blocks(n), 256, 0, st>>>(F, A, mixed_.get(), out, g);
     SMC_CHECK_LAUNCH();
   }
-  if (part != kNsAdvDiff) {
-    wdot_kernel<<<blocks(n), 256, 0, st>>>(U, F, out, g, part == kNsChem ? 1 : 0);
+  if (part == kNsFull) {
+    wdot_kernel<<<blocks(n), 256, 0, st>>>(U, F, out, g);
     SMC_CHECK_LAUNCH();
   }
 }
