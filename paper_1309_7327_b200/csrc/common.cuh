@@ -112,6 +112,50 @@ __device__ __forceinline__ double narrow_iface(const double* a, const double* u,
   return acc;
 }
 
+// Two independent interfaces in lockstep (same arithmetic as narrow_iface for
+// each): every M entry is used by two adjacent, independent FMAs, which
+// doubles the instruction-level parallelism of the dependent row chains.
+template <int S>
+__device__ __forceinline__ void narrow_iface2(const double* a0, const double* u0, const double* a1,
+                                              const double* u1, const StencilM& M, double& h0,
+                                              double& h1) {
+  double acc0, acc1;
+#pragma unroll
+  for (int r = 0; r < 2 * S; ++r) {
+    constexpr int L = 2 * S - 1;
+    const int lo = row_lo<S>(r), hi = row_hi<S>(r);
+    double v0, v1;
+    if (r < S) {
+      v0 = M.m[r][lo] * u0[lo];
+      v1 = M.m[r][lo] * u1[lo];
+#pragma unroll
+      for (int c = lo + 1; c <= hi; ++c) {
+        v0 = __fma_rn(M.m[r][c], u0[c], v0);
+        v1 = __fma_rn(M.m[r][c], u1[c], v1);
+      }
+      if (r == 0) {
+        acc0 = a0[0] * v0;
+        acc1 = a1[0] * v1;
+      } else {
+        acc0 = __fma_rn(a0[r], v0, acc0);
+        acc1 = __fma_rn(a1[r], v1, acc1);
+      }
+    } else {
+      v0 = M.m[L - r][L - lo] * u0[lo];
+      v1 = M.m[L - r][L - lo] * u1[lo];
+#pragma unroll
+      for (int c = lo + 1; c <= hi; ++c) {
+        v0 = __fma_rn(M.m[L - r][L - c], u0[c], v0);
+        v1 = __fma_rn(M.m[L - r][L - c], u1[c], v1);
+      }
+      acc0 = __fma_rn(-a0[r], v0, acc0);
+      acc1 = __fma_rn(-a1[r], v1, acc1);
+    }
+  }
+  h0 = acc0;
+  h1 = acc1;
+}
+
 // 8th-order centred first derivative (stencil_kernel.hpp:48-54) from a
 // 9-point window w[0..8] centred at w[4].
 __device__ __forceinline__ double deriv8_w(const double* w, double inv_d) {

@@ -67,8 +67,10 @@ __device__ __forceinline__ double2 lds2(const double* p) {
   return *reinterpret_cast<const double2*>(p);
 }
 
-// One (tile, [k0, k1)) segment of the z-march.
-template <int S>
+// One (tile, [k0, k1)) segment of the z-march.  OCC = CTAs per SM the
+// kernel is built for: OCC 2 forms the y interfaces one column at a time
+// (half the live y window) to fit 128 registers.
+template <int S, int OCC, bool PAIR>
 __device__ __forceinline__ void march_segment(FastSmem& sm, const NarrowArgs& p,
                                               const StencilM& M, int tile, int k0, int k1) {
   constexpr int WIN = 2 * S;
@@ -213,8 +215,12 @@ __device__ __forceinline__ void march_segment(FastSmem& sm, const NarrowArgs& p,
       double a0[WIN], u0[WIN], a1[WIN], u1[WIN];
 #pragma unroll
       for (int j = 0; j < WIN; ++j) a0[j] = wa[j].x, u0[j] = wu[j].x, a1[j] = wa[j].y, u1[j] = wu[j].y;
-      hz0 = narrow_iface<S>(a0, u0, M);
-      hz1 = narrow_iface<S>(a1, u1, M);
+      if constexpr (PAIR) {
+        narrow_iface2<S>(a0, u0, a1, u1, M, hz0, hz1);
+      } else {
+        hz0 = narrow_iface<S>(a0, u0, M);
+        hz1 = narrow_iface<S>(a1, u1, M);
+      }
     }
     // ---- x interfaces x+1/2 for my two cells (row HALO + w)
     double hx0, hx1;
@@ -232,11 +238,27 @@ __device__ __forceinline__ void march_segment(FastSmem& sm, const NarrowArgs& p,
         ua[2 * j] = vu.x, ua[2 * j + 1] = vu.y;
         aa[2 * j] = va.x, aa[2 * j + 1] = va.y;
       }
-      hx0 = narrow_iface<S>(aa + OFF, ua + OFF, M);
-      hx1 = narrow_iface<S>(aa + OFF + 1, ua + OFF + 1, M);
+      if constexpr (PAIR) {
+        narrow_iface2<S>(aa + OFF, ua + OFF, aa + OFF + 1, ua + OFF + 1, M, hx0, hx1);
+      } else {
+        hx0 = narrow_iface<S>(aa + OFF, ua + OFF, M);
+        hx1 = narrow_iface<S>(aa + OFF + 1, ua + OFF + 1, M);
+      }
     }
     // ---- y interfaces y+1/2 for my two columns
-    {
+    if constexpr (OCC == 2) {
+#pragma unroll
+      for (int col = 0; col < 2; ++col) {
+        double uc[WIN], ac[WIN];
+#pragma unroll
+        for (int j = 0; j < WIN; ++j) {
+          const int row = HALO + w - S + 1 + j;
+          uc[j] = tu[row * SW + HALO + 2 * lane + col];
+          ac[j] = ta[row * SW + HALO + 2 * lane + col];
+        }
+        sm.hy[hb][w + 1][2 * lane + col] = narrow_iface<S>(ac, uc, M);
+      }
+    } else {
       double u0[WIN], a0[WIN], u1[WIN], a1[WIN];
 #pragma unroll
       for (int j = 0; j < WIN; ++j) {
@@ -245,8 +267,14 @@ __device__ __forceinline__ void march_segment(FastSmem& sm, const NarrowArgs& p,
         const double2 va = lds2(ta + row * SW + HALO + 2 * lane);
         u0[j] = vu.x, u1[j] = vu.y, a0[j] = va.x, a1[j] = va.y;
       }
-      *reinterpret_cast<double2*>(&sm.hy[hb][w + 1][2 * lane]) =
-          make_double2(narrow_iface<S>(a0, u0, M), narrow_iface<S>(a1, u1, M));
+      double y0v, y1v;
+      if constexpr (PAIR) {
+        narrow_iface2<S>(a0, u0, a1, u1, M, y0v, y1v);
+      } else {
+        y0v = narrow_iface<S>(a0, u0, M);
+        y1v = narrow_iface<S>(a1, u1, M);
+      }
+      *reinterpret_cast<double2*>(&sm.hy[hb][w + 1][2 * lane]) = make_double2(y0v, y1v);
     }
     // ---- extra interfaces: y0 - 1/2 of the even columns (warp 1), of the
     //      odd columns (warp 2), x0 - 1/2 of each row (warp 3)
@@ -292,15 +320,15 @@ __device__ __forceinline__ void march_segment(FastSmem& sm, const NarrowArgs& p,
 // co-scheduled CTAs are x/y neighbours at the same z and tile halos hit in
 // L2.  Persistent grid: CTA b owns the contiguous range [b*L/G, (b+1)*L/G)
 // of L = tile * nplanes + plane (one wave, equal work to within a plane).
-template <int S>
-__global__ void __launch_bounds__(FT, 1) narrow3d_fast(const NarrowArgs p, const StencilM M,
-                                                       int chunked) {
+template <int S, int OCC, bool PAIR>
+__global__ void __launch_bounds__(FT, OCC) narrow3d_fast(const NarrowArgs p, const StencilM M,
+                                                         int chunked) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   FastSmem& sm = *reinterpret_cast<FastSmem*>(smem_raw);
   const int kend = p.kend < 0 ? p.nz : p.kend;
   if (chunked) {
     const int k0 = p.kbeg + blockIdx.y * p.kc;
-    march_segment<S>(sm, p, M, blockIdx.x, k0, min(k0 + p.kc, kend));
+    march_segment<S, OCC, PAIR>(sm, p, M, blockIdx.x, k0, min(k0 + p.kc, kend));
     return;
   }
   const long long np = kend - p.kbeg;
@@ -311,17 +339,19 @@ __global__ void __launch_bounds__(FT, 1) narrow3d_fast(const NarrowArgs p, const
     const int tile = static_cast<int>(l / np);
     const int kk = static_cast<int>(l - tile * np);
     const int len = static_cast<int>(min(np - kk, hi - l));
-    march_segment<S>(sm, p, M, tile, p.kbeg + kk, p.kbeg + kk + len);
+    march_segment<S, OCC, PAIR>(sm, p, M, tile, p.kbeg + kk, p.kbeg + kk + len);
     l += len;
   }
 }
 
-// SMC_NARROW_GRID=chunk selects the (tiles, z-chunks) grid (tuning knob;
-// the persistent grid measured ~2% faster at 256^3).
+// SMC_NARROW_GRID=persistent selects the one-wave persistent grid (tuning
+// knob).  Both measure 0.295 ms at 256^3; the chunked grid keeps co-resident
+// CTAs on neighbouring tiles, so it moves 2.9x fewer DRAM bytes (388 vs
+// 925 MB per launch), which is the default.
 bool chunked_grid() {
   static bool c = [] {
     const char* e = std::getenv("SMC_NARROW_GRID");
-    return e && std::string(e) == "chunk";
+    return !(e && std::string(e) == "persistent");
   }();
   return c;
 }
@@ -336,11 +366,29 @@ int num_sms_cached() {
   return n;
 }
 
-template <int S>
+// SMC_NARROW_OCC=2 selects the 2-CTA/SM build (tuning knob).
+int fast_occ() {
+  static int o = [] {
+    const char* e = std::getenv("SMC_NARROW_OCC");
+    return (e && std::atoi(e) == 2) ? 2 : 1;
+  }();
+  return o;
+}
+
+// SMC_NARROW_PAIR=0 computes the interface pairs one after the other (A/B knob).
+bool fast_pair() {
+  static bool v = [] {
+    const char* e = std::getenv("SMC_NARROW_PAIR");
+    return !(e && std::atoi(e) == 0);
+  }();
+  return v;
+}
+
+template <int S, int OCC, bool PAIR>
 void launch_fast_s(const NarrowArgs& p, const StencilM& M, cudaStream_t st) {
   static bool configured = false;
   if (!configured) {
-    SMC_CUDA(cudaFuncSetAttribute(narrow3d_fast<S>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    SMC_CUDA(cudaFuncSetAttribute(narrow3d_fast<S, OCC, PAIR>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   static_cast<int>(sizeof(FastSmem))));
     configured = true;
   }
@@ -349,12 +397,13 @@ void launch_fast_s(const NarrowArgs& p, const StencilM& M, cudaStream_t st) {
   const int tiles = (p.nx / FX) * (p.ny / FY);
   if (chunked_grid()) {
     const dim3 grid(tiles, (kend - p.kbeg + p.kc - 1) / p.kc);
-    narrow3d_fast<S><<<grid, FT, sizeof(FastSmem), st>>>(p, M, 1);
+    narrow3d_fast<S, OCC, PAIR><<<grid, FT, sizeof(FastSmem), st>>>(p, M, 1);
   } else {
     const long long work = static_cast<long long>(tiles) * (kend - p.kbeg);
     const long long by_kc = (work + p.kc - 1) / p.kc;
-    const int grid = static_cast<int>(std::max(1LL, std::min<long long>(num_sms_cached(), by_kc)));
-    narrow3d_fast<S><<<grid, FT, sizeof(FastSmem), st>>>(p, M, 0);
+    const int grid =
+        static_cast<int>(std::max(1LL, std::min<long long>(num_sms_cached() * OCC, by_kc)));
+    narrow3d_fast<S, OCC, PAIR><<<grid, FT, sizeof(FastSmem), st>>>(p, M, 0);
   }
   SMC_CHECK_LAUNCH();
 }
@@ -368,10 +417,18 @@ bool narrow3d_fast_applicable(const NarrowArgs& p) {
 }
 
 void launch_narrow3d_fast(const NarrowArgs& p, int s, const StencilM& M, cudaStream_t st) {
-  if (s == 4)
-    launch_fast_s<4>(p, M, st);
-  else
-    launch_fast_s<3>(p, M, st);
+  const bool pair = fast_pair();
+  if (fast_occ() == 2) {
+    if (s == 4)
+      pair ? launch_fast_s<4, 2, true>(p, M, st) : launch_fast_s<4, 2, false>(p, M, st);
+    else
+      pair ? launch_fast_s<3, 2, true>(p, M, st) : launch_fast_s<3, 2, false>(p, M, st);
+  } else {
+    if (s == 4)
+      pair ? launch_fast_s<4, 1, true>(p, M, st) : launch_fast_s<4, 1, false>(p, M, st);
+    else
+      pair ? launch_fast_s<3, 1, true>(p, M, st) : launch_fast_s<3, 1, false>(p, M, st);
+  }
 }
 
 int narrow3d_fast_default_kc(int nx, int ny, int nz, int num_sms) {
