@@ -70,7 +70,7 @@ __device__ __forceinline__ double2 lds2(const double* p) {
 // One (tile, [k0, k1)) segment of the z-march.  OCC = CTAs per SM the
 // kernel is built for: OCC 2 forms the y interfaces one column at a time
 // (half the live y window) to fit 128 registers.
-template <int S, int OCC, bool PAIR>
+template <int S, int OCC, bool LATE>
 __device__ __forceinline__ void march_segment(FastSmem& sm, const NarrowArgs& p,
                                               const StencilM& M, int tile, int k0, int k1) {
   constexpr int WIN = 2 * S;
@@ -126,7 +126,7 @@ __device__ __forceinline__ void march_segment(FastSmem& sm, const NarrowArgs& p,
 
   // z window (2 columns): slot j holds plane k - S + 1 + j at step k
   double2 wu[WIN], wa[WIN];
-  double2 pf_u[2], pf_a[2];
+  double2 pf_u[2], pf_a[2];  // (LATE: unused) leading planes prefetched two ahead
   {
     long long o = zoff(k0 - S);
 #pragma unroll
@@ -141,11 +141,11 @@ __device__ __forceinline__ void march_segment(FastSmem& sm, const NarrowArgs& p,
   long long o_pf = zoff(k0 + S);
 #pragma unroll
   for (int j = 0; j < 2; ++j) {
-    if (k0 + j < k1) {
+    if (!LATE && k0 + j < k1) {
       pf_u[j] = ld2(p.u, o_pf);
       pf_a[j] = ld2(p.cz, o_pf);
     }
-    o_pf = zadv(o_pf);
+    if (!LATE) o_pf = zadv(o_pf);
   }
   // centre-plane staging: planes k0, k0 + 1 now (buffers 0, 1)
   long long o_st = zoff(k0);
@@ -194,34 +194,37 @@ __device__ __forceinline__ void march_segment(FastSmem& sm, const NarrowArgs& p,
     const int t = k - k0;
     const int buf = t % NBUF;
     const int hb = t & 1;
-    // shift the z window down one plane and append the leading plane k + S
-#pragma unroll
-    for (int j = 0; j + 1 < WIN; ++j) wu[j] = wu[j + 1], wa[j] = wa[j + 1];
-    wu[WIN - 1] = pf_u[0];
-    wa[WIN - 1] = pf_a[0];
-    pf_u[0] = pf_u[1];
-    pf_a[0] = pf_a[1];
-    if (k + 2 < k1) {
-      pf_u[1] = ld2(p.u, o_pf);
-      pf_a[1] = ld2(p.cz, o_pf);
+    // z window: LATE issues the leading plane k + S now and forms the z
+    // interfaces after x and y (the load is hidden behind them, no prefetch
+    // registers); otherwise the plane prefetched two steps ago is shifted in.
+    double2 lead_u, lead_a;
+    if constexpr (LATE) {
+      lead_u = ld2(p.u, o_pf);
+      lead_a = ld2(p.cz, o_pf);
       o_pf = zadv(o_pf);
+    } else {
+#pragma unroll
+      for (int j = 0; j + 1 < WIN; ++j) wu[j] = wu[j + 1], wa[j] = wa[j + 1];
+      wu[WIN - 1] = pf_u[0];
+      wa[WIN - 1] = pf_a[0];
+      pf_u[0] = pf_u[1];
+      pf_a[0] = pf_a[1];
+      if (k + 2 < k1) {
+        pf_u[1] = ld2(p.u, o_pf);
+        pf_a[1] = ld2(p.cz, o_pf);
+        o_pf = zadv(o_pf);
+      }
     }
     const double* tu = sm.tile[buf][0];
     const double* ta = sm.tile[buf][1];
-
-    // ---- z interfaces k + 1/2
     double hz0, hz1;
-    {
+    auto z_interfaces = [&]() {
       double a0[WIN], u0[WIN], a1[WIN], u1[WIN];
 #pragma unroll
       for (int j = 0; j < WIN; ++j) a0[j] = wa[j].x, u0[j] = wu[j].x, a1[j] = wa[j].y, u1[j] = wu[j].y;
-      if constexpr (PAIR) {
-        narrow_iface2<S>(a0, u0, a1, u1, M, hz0, hz1);
-      } else {
-        hz0 = narrow_iface<S>(a0, u0, M);
-        hz1 = narrow_iface<S>(a1, u1, M);
-      }
-    }
+      narrow_iface2<S>(a0, u0, a1, u1, M, hz0, hz1);
+    };
+    if constexpr (!LATE) z_interfaces();
     // ---- x interfaces x+1/2 for my two cells (row HALO + w)
     double hx0, hx1;
     {
@@ -238,12 +241,7 @@ __device__ __forceinline__ void march_segment(FastSmem& sm, const NarrowArgs& p,
         ua[2 * j] = vu.x, ua[2 * j + 1] = vu.y;
         aa[2 * j] = va.x, aa[2 * j + 1] = va.y;
       }
-      if constexpr (PAIR) {
-        narrow_iface2<S>(aa + OFF, ua + OFF, aa + OFF + 1, ua + OFF + 1, M, hx0, hx1);
-      } else {
-        hx0 = narrow_iface<S>(aa + OFF, ua + OFF, M);
-        hx1 = narrow_iface<S>(aa + OFF + 1, ua + OFF + 1, M);
-      }
+      narrow_iface2<S>(aa + OFF, ua + OFF, aa + OFF + 1, ua + OFF + 1, M, hx0, hx1);
     }
     // ---- y interfaces y+1/2 for my two columns
     if constexpr (OCC == 2) {
@@ -268,12 +266,7 @@ __device__ __forceinline__ void march_segment(FastSmem& sm, const NarrowArgs& p,
         u0[j] = vu.x, u1[j] = vu.y, a0[j] = va.x, a1[j] = va.y;
       }
       double y0v, y1v;
-      if constexpr (PAIR) {
-        narrow_iface2<S>(a0, u0, a1, u1, M, y0v, y1v);
-      } else {
-        y0v = narrow_iface<S>(a0, u0, M);
-        y1v = narrow_iface<S>(a1, u1, M);
-      }
+      narrow_iface2<S>(a0, u0, a1, u1, M, y0v, y1v);
       *reinterpret_cast<double2*>(&sm.hy[hb][w + 1][2 * lane]) = make_double2(y0v, y1v);
     }
     // ---- extra interfaces: y0 - 1/2 of the even columns (warp 1), of the
@@ -295,6 +288,13 @@ __device__ __forceinline__ void march_segment(FastSmem& sm, const NarrowArgs& p,
         aa[j] = ta[(HALO + lane) * SW + HALO - S + j];
       }
       sm.hxe[hb][lane] = narrow_iface<S>(aa, uu, M);
+    }
+    if constexpr (LATE) {
+#pragma unroll
+      for (int j = 0; j + 1 < WIN; ++j) wu[j] = wu[j + 1], wa[j] = wa[j + 1];
+      wu[WIN - 1] = lead_u;
+      wa[WIN - 1] = lead_a;
+      z_interfaces();
     }
     // ---- stage plane k + 2 into the buffer of plane k - 1 (all of its
     //      readers passed the previous barrier), then make plane k + 1 ready
@@ -320,7 +320,7 @@ __device__ __forceinline__ void march_segment(FastSmem& sm, const NarrowArgs& p,
 // co-scheduled CTAs are x/y neighbours at the same z and tile halos hit in
 // L2.  Persistent grid: CTA b owns the contiguous range [b*L/G, (b+1)*L/G)
 // of L = tile * nplanes + plane (one wave, equal work to within a plane).
-template <int S, int OCC, bool PAIR>
+template <int S, int OCC, bool LATE>
 __global__ void __launch_bounds__(FT, OCC) narrow3d_fast(const NarrowArgs p, const StencilM M,
                                                          int chunked) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -328,7 +328,7 @@ __global__ void __launch_bounds__(FT, OCC) narrow3d_fast(const NarrowArgs p, con
   const int kend = p.kend < 0 ? p.nz : p.kend;
   if (chunked) {
     const int k0 = p.kbeg + blockIdx.y * p.kc;
-    march_segment<S, OCC, PAIR>(sm, p, M, blockIdx.x, k0, min(k0 + p.kc, kend));
+    march_segment<S, OCC, LATE>(sm, p, M, blockIdx.x, k0, min(k0 + p.kc, kend));
     return;
   }
   const long long np = kend - p.kbeg;
@@ -339,7 +339,7 @@ __global__ void __launch_bounds__(FT, OCC) narrow3d_fast(const NarrowArgs p, con
     const int tile = static_cast<int>(l / np);
     const int kk = static_cast<int>(l - tile * np);
     const int len = static_cast<int>(min(np - kk, hi - l));
-    march_segment<S, OCC, PAIR>(sm, p, M, tile, p.kbeg + kk, p.kbeg + kk + len);
+    march_segment<S, OCC, LATE>(sm, p, M, tile, p.kbeg + kk, p.kbeg + kk + len);
     l += len;
   }
 }
@@ -375,20 +375,21 @@ int fast_occ() {
   return o;
 }
 
-// SMC_NARROW_PAIR=0 computes the interface pairs one after the other (A/B knob).
-bool fast_pair() {
+// SMC_NARROW_LATEZ=1: z interfaces after x/y with the leading plane loaded at
+// the step start instead of prefetched (A/B knob).
+bool fast_latez() {
   static bool v = [] {
-    const char* e = std::getenv("SMC_NARROW_PAIR");
-    return !(e && std::atoi(e) == 0);
+    const char* e = std::getenv("SMC_NARROW_LATEZ");
+    return e && std::atoi(e) == 1;
   }();
   return v;
 }
 
-template <int S, int OCC, bool PAIR>
+template <int S, int OCC, bool LATE>
 void launch_fast_s(const NarrowArgs& p, const StencilM& M, cudaStream_t st) {
   static bool configured = false;
   if (!configured) {
-    SMC_CUDA(cudaFuncSetAttribute(narrow3d_fast<S, OCC, PAIR>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    SMC_CUDA(cudaFuncSetAttribute(narrow3d_fast<S, OCC, LATE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   static_cast<int>(sizeof(FastSmem))));
     configured = true;
   }
@@ -397,13 +398,13 @@ void launch_fast_s(const NarrowArgs& p, const StencilM& M, cudaStream_t st) {
   const int tiles = (p.nx / FX) * (p.ny / FY);
   if (chunked_grid()) {
     const dim3 grid(tiles, (kend - p.kbeg + p.kc - 1) / p.kc);
-    narrow3d_fast<S, OCC, PAIR><<<grid, FT, sizeof(FastSmem), st>>>(p, M, 1);
+    narrow3d_fast<S, OCC, LATE><<<grid, FT, sizeof(FastSmem), st>>>(p, M, 1);
   } else {
     const long long work = static_cast<long long>(tiles) * (kend - p.kbeg);
     const long long by_kc = (work + p.kc - 1) / p.kc;
     const int grid =
         static_cast<int>(std::max(1LL, std::min<long long>(num_sms_cached() * OCC, by_kc)));
-    narrow3d_fast<S, OCC, PAIR><<<grid, FT, sizeof(FastSmem), st>>>(p, M, 0);
+    narrow3d_fast<S, OCC, LATE><<<grid, FT, sizeof(FastSmem), st>>>(p, M, 0);
   }
   SMC_CHECK_LAUNCH();
 }
@@ -417,7 +418,7 @@ bool narrow3d_fast_applicable(const NarrowArgs& p) {
 }
 
 void launch_narrow3d_fast(const NarrowArgs& p, int s, const StencilM& M, cudaStream_t st) {
-  const bool pair = fast_pair();
+  const bool pair = fast_latez();
   if (fast_occ() == 2) {
     if (s == 4)
       pair ? launch_fast_s<4, 2, true>(p, M, st) : launch_fast_s<4, 2, false>(p, M, st);
