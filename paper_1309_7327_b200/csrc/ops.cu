@@ -1,3 +1,5 @@
+#include <algorithm>
+#include <cstdlib>
 #include <cstring>
 
 #include "narrow.cuh"
@@ -69,10 +71,13 @@ int num_sms() {
 
 // ------------------------------------------------------------------ RhsOp
 void RhsOp::eval(double t, const double* u, double* out, int where) {
-  if (where == kDevice) {
+  if (where == kDevice)
     eval_device(t, u, out);
-    return;
-  }
+  else
+    eval_host(t, u, out);
+}
+
+void RhsOp::eval_host(double t, const double* u, double* out) {
   const std::size_t n = static_cast<std::size_t>(dim());
   stage_u_.resize(n);
   stage_out_.resize(n);
@@ -119,6 +124,92 @@ void Narrow3DOp::eval_planes(const double* u, double* out, int kb, int ke) {
 void Narrow3DOp::eval_device(double, const double* u, double* out) {
   require(zghost_ == 0, "narrow3d: a ghosted (slab) operator is applied with apply_planes");
   eval_planes(u, out, 0, nz_);
+  ++evals_;
+}
+
+Narrow3DOp::~Narrow3DOp() {
+  for (cudaEvent_t e : ev_in_) cudaEventDestroy(e);
+  for (cudaEvent_t e : ev_done_) cudaEventDestroy(e);
+  if (h2d_) cudaStreamDestroy(h2d_);
+  if (d2h_) cudaStreamDestroy(d2h_);
+}
+
+void Narrow3DOp::eval_host(double t, const double* u, double* out) {
+  require(zghost_ == 0, "narrow3d: a ghosted (slab) operator is applied with apply_planes");
+  // Chunk boundaries: short chunks at both ends (the pipeline's fill and
+  // drain are one chunk each), SMC_E2E_CHUNK_PLANES (default 32) planes in
+  // the middle; every chunk holds >= 8 >= S planes.
+  static const int mid_planes = [] {
+    const char* e = std::getenv("SMC_E2E_CHUNK_PLANES");
+    return e ? std::max(8, std::atoi(e)) : 32;
+  }();
+  std::vector<int> bnd{0};
+  if (nz_ >= 48 + mid_planes) {
+    bnd.push_back(8);
+    bnd.push_back(24);
+    const int mid = nz_ - 48, nm = (mid + mid_planes - 1) / mid_planes;
+    for (int i = 1; i <= nm; ++i) bnd.push_back(24 + static_cast<int>((1LL * mid * i) / nm));
+    bnd.push_back(nz_ - 8);
+    bnd.push_back(nz_);
+  } else {
+    const int n = std::min(8, nz_ / 8);
+    for (int i = 1; i <= n; ++i) bnd.push_back(static_cast<int>((1LL * nz_ * i) / std::max(n, 1)));
+  }
+  const int nchunk = static_cast<int>(bnd.size()) - 1;
+  if (nchunk < 2) {
+    RhsOp::eval_host(t, u, out);
+    return;
+  }
+  const std::size_t plane = static_cast<std::size_t>(nx_) * ny_;
+  stage_u_.resize(plane * nz_);
+  stage_out_.resize(plane * nz_);
+  if (!h2d_) {
+    SMC_CUDA(cudaStreamCreateWithFlags(&h2d_, cudaStreamNonBlocking));
+    SMC_CUDA(cudaStreamCreateWithFlags(&d2h_, cudaStreamNonBlocking));
+  }
+  while (static_cast<int>(ev_in_.size()) < nchunk) {
+    cudaEvent_t a, b;
+    SMC_CUDA(cudaEventCreateWithFlags(&a, cudaEventDisableTiming));
+    SMC_CUDA(cudaEventCreateWithFlags(&b, cudaEventDisableTiming));
+    ev_in_.push_back(a);
+    ev_done_.push_back(b);
+  }
+  auto lo = [&](int c) { return bnd[c]; };
+  auto h2d = [&](int k0, int k1) {
+    const std::size_t off = plane * k0, cnt = plane * (k1 - k0);
+    SMC_CUDA(cudaMemcpyAsync(stage_u_.get() + off, u + off, cnt * sizeof(double),
+                             cudaMemcpyHostToDevice, h2d_));
+  };
+  // Host->device: first the top S planes (the periodic neighbours of plane
+  // 0), then the chunks in order.  Once chunk c is resident, interior planes
+  // [lo(c) - S, lo(c+1) - S) have their whole stencil (the last range runs to
+  // nz and wraps onto chunk 0), so the stencil lags the copy by S planes and
+  // the device->host copy of each range starts as soon as it is computed.
+  h2d(nz_ - s_, nz_);
+  for (int c = 0; c < nchunk; ++c) {
+    h2d(lo(c), c == nchunk - 1 ? nz_ - s_ : lo(c + 1));
+    SMC_CUDA(cudaEventRecord(ev_in_[c], h2d_));
+  }
+  auto range = [&](int c, int& k0, int& k1) {
+    k0 = c == 0 ? 0 : lo(c) - s_;
+    k1 = c == nchunk - 1 ? nz_ : lo(c + 1) - s_;
+  };
+  for (int c = 0; c < nchunk; ++c) {
+    int k0, k1;
+    range(c, k0, k1);
+    SMC_CUDA(cudaStreamWaitEvent(stream_, ev_in_[c], 0));
+    eval_planes(stage_u_.get(), stage_out_.get(), k0, k1);
+    SMC_CUDA(cudaEventRecord(ev_done_[c], stream_));
+  }
+  for (int c = 0; c < nchunk; ++c) {
+    int k0, k1;
+    range(c, k0, k1);
+    SMC_CUDA(cudaStreamWaitEvent(d2h_, ev_done_[c], 0));
+    const std::size_t off = plane * k0, cnt = plane * (k1 - k0);
+    SMC_CUDA(cudaMemcpyAsync(out + off, stage_out_.get() + off, cnt * sizeof(double),
+                             cudaMemcpyDeviceToHost, d2h_));
+  }
+  SMC_CUDA(cudaStreamSynchronize(d2h_));
   ++evals_;
 }
 
