@@ -418,3 +418,246 @@ int or_integrate_mrsdc1(or_rhs_cb f1, void* c1, or_rhs_cb f2, void* c2, long lon
   free(hist); free(coarse_at);
   return 0;
 }
+
+/* ------------------------------------------------- implicit (mode 2) */
+static double max_keep(double a, double b) { return (a < b) ? b : a; } /* std::max(a, b) */
+
+static long long blk_at(long long b, long long j, long long B, long long nb, int inter) {
+  return inter ? j * nb + b : b * B + j;
+}
+
+/* lu_factor (core/src/matrix.cpp:9-33) on one row-major n x n block */
+static int lu_factor_blk(double* m, int n, int* piv) {
+  for (int col = 0; col < n; ++col) {
+    int best = col;
+    double best_mag = fabs(m[col * n + col]);
+    for (int r = col + 1; r < n; ++r) {
+      const double mag = fabs(m[r * n + col]);
+      if (mag > best_mag) {
+        best = r;
+        best_mag = mag;
+      }
+    }
+    piv[col] = best;
+    if (best_mag == 0.0) return 0;
+    if (best != col)
+      for (int c = 0; c < n; ++c) {
+        const double tmp = m[col * n + c];
+        m[col * n + c] = m[best * n + c];
+        m[best * n + c] = tmp;
+      }
+    const double inv = 1.0 / m[col * n + col];
+    for (int r = col + 1; r < n; ++r) {
+      const double l = m[r * n + col] * inv;
+      m[r * n + col] = l;
+      for (int c = col + 1; c < n; ++c) m[r * n + c] -= l * m[col * n + c];
+    }
+  }
+  return 1;
+}
+
+/* lu_solve (core/src/matrix.cpp:35-51) */
+static void lu_solve_blk(const double* m, int n, const int* piv, double* b) {
+  for (int i = 0; i < n; ++i)
+    if (piv[i] != i) {
+      const double tmp = b[i];
+      b[i] = b[piv[i]];
+      b[piv[i]] = tmp;
+    }
+  for (int i = 1; i < n; ++i) {
+    double s = b[i];
+    for (int j = 0; j < i; ++j) s -= m[i * n + j] * b[j];
+    b[i] = s;
+  }
+  for (int i = n - 1; i >= 0; --i) {
+    double s = b[i];
+    for (int j = i + 1; j < n; ++j) s -= m[i * n + j] * b[j];
+    b[i] = s / m[i * n + i];
+  }
+}
+
+int or_solve_backward_euler(or_rhs_cb f, void* ctx, long long dim, double t, double beta,
+                            const double* c, const double* guess, const or_stiff* o, double* w,
+                            or_newton_report* rep) {
+  const long long B = o->block > 0 ? o->block : dim;
+  if (dim < 1 || B < 1 || dim % B != 0 || B > 4096) return 1;
+  const long long nb = dim / B;
+  const int inter = o->block > 0 && o->interleaved;
+  const size_t bytes = sizeof(double) * dim;
+  double* fw = malloc(bytes);
+  double* fp = malloc(bytes);
+  double* wp = malloc(bytes);
+  double* delta = malloc(bytes);
+  double* jac = malloc(sizeof(double) * nb * B * B);
+  double* hcol = malloc(sizeof(double) * nb);
+  double* rhs = malloc(sizeof(double) * B);
+  int* piv = malloc(sizeof(int) * nb * B);
+  const double root_eps = sqrt(2.220446049250313e-16); /* sqrt(DBL_EPSILON), stiff.cpp:19 */
+  memcpy(w, guess, bytes);
+  rep->iterations = 0;
+  rep->final_residual = 0.0;
+  rep->converged = 0;
+  rep->f_evals = 0;
+  for (int iter = 0; iter < o->max_newton_iters; ++iter) {
+    f(t, w, fw, dim, ctx);
+    ++rep->f_evals;
+    double rnorm = 0.0;
+    for (long long i = 0; i < dim; ++i) {
+      delta[i] = w[i] - beta * fw[i] - c[i];
+      rnorm = max_keep(rnorm, fabs(delta[i]));
+    }
+    rep->final_residual = rnorm;
+    double wn = 0.0; /* max_norm, field.hpp:18-22 */
+    for (long long i = 0; i < dim; ++i) wn = max_keep(wn, fabs(w[i]));
+    if (rnorm <= o->atol + o->rtol * wn) {
+      rep->converged = 1;
+      break;
+    }
+    /* fd_jacobian (stiff.cpp:16-30), one block column at a time */
+    memcpy(wp, w, bytes);
+    for (long long j = 0; j < B; ++j) {
+      for (long long b = 0; b < nb; ++b) {
+        const long long i = blk_at(b, j, B, nb, inter);
+        hcol[b] = root_eps * max_keep(fabs(w[i]), o->atol);
+        wp[i] = w[i] + hcol[b];
+      }
+      f(t, wp, fp, dim, ctx);
+      ++rep->f_evals;
+      for (long long b = 0; b < nb; ++b) {
+        const long long i = blk_at(b, j, B, nb, inter);
+        wp[i] = w[i];
+        const double inv = 1.0 / hcol[b];
+        for (long long r = 0; r < B; ++r) {
+          const long long k = blk_at(b, r, B, nb, inter);
+          jac[(b * B + r) * B + j] = (fp[k] - fw[k]) * inv;
+        }
+      }
+    }
+    /* jg = I - beta J (stiff.cpp:63-65), factored block by block */
+    int ok = 1;
+    for (long long b = 0; b < nb && ok; ++b) {
+      double* m = jac + b * B * B;
+      for (long long r = 0; r < B; ++r)
+        for (long long cc = 0; cc < B; ++cc)
+          m[r * B + cc] = (r == cc ? 1.0 : 0.0) - beta * m[r * B + cc];
+      ok = lu_factor_blk(m, (int)B, piv + b * B);
+    }
+    if (!ok) break;
+    for (long long b = 0; b < nb; ++b) {
+      for (long long r = 0; r < B; ++r) rhs[r] = delta[blk_at(b, r, B, nb, inter)];
+      lu_solve_blk(jac + b * B * B, (int)B, piv + b * B, rhs);
+      for (long long r = 0; r < B; ++r) delta[blk_at(b, r, B, nb, inter)] = rhs[r];
+    }
+    for (long long i = 0; i < dim; ++i) w[i] -= delta[i];
+    rep->iterations = iter + 1;
+  }
+  free(fw); free(fp); free(wp); free(delta); free(jac); free(hcol); free(rhs); free(piv);
+  return 0;
+}
+
+int or_integrate_mrsdc2(or_rhs_cb f1, void* c1, or_rhs_cb f2, void* c2, long long dim,
+                        const double* u0, double t0, double tend, int nsteps, int m1,
+                        const double* t1, int m2, const double* t2, const double* s21,
+                        const double* q21, const double* s22, const double* q22,
+                        const int* fine_of_coarse, int iterations, double cutoff,
+                        const or_stiff* opts, double* u_out, double* residuals, int max_res,
+                        int* sweeps, int* f1_evals, int* f2_evals, int* implicit_solves,
+                        int* newton_f1_evals, int* fail_node, int* fail_sweep) {
+  if (nsteps < 0 || iterations < 1) return 1;
+  const size_t bytes = sizeof(double) * dim;
+  double* U = malloc(bytes * (m2 + 1));
+  double* F1 = malloc(bytes * (m1 + 1));
+  double* F2 = malloc(bytes * (m2 + 1));
+  double* OF1 = malloc(bytes * (m1 + 1));
+  double* SO = malloc(bytes * m2);
+  double* fold = malloc(bytes);
+  double* cvec = malloc(bytes);
+  double* wsol = malloc(bytes);
+  double* u = malloc(bytes);
+  double* c1s = malloc(bytes);
+  double* c2s = malloc(bytes);
+  double* hist = malloc(sizeof(double) * (iterations + 1));
+  int rc = 0;
+  memcpy(u, u0, bytes);
+  *sweeps = *f1_evals = *f2_evals = *implicit_solves = *newton_f1_evals = 0;
+  *fail_node = *fail_sweep = -1;
+  int nres = 0;
+  const double dt = (tend - t0) / (nsteps > 1 ? nsteps : 1);
+  for (int step = 0; step < nsteps && rc == 0; ++step) {
+    const double tn = t0 + step * dt;
+    /* provisional, mrsdc.cpp:43-66 */
+    for (int q = 0; q <= m2; ++q) memcpy(U + q * dim, u, bytes);
+    if (step > 0) memcpy(F1, c1s, bytes); else { f1(tn, u, F1, dim, c1); ++*f1_evals; }
+    if (step > 0) memcpy(F2, c2s, bytes); else { f2(tn, u, F2, dim, c2); ++*f2_evals; }
+    for (int p = 1; p <= m1; ++p) memcpy(F1 + p * dim, F1, bytes);
+    for (int q = 1; q <= m2; ++q) memcpy(F2 + q * dim, F2, bytes);
+    int hl = 0;
+    for (int it = 1; it <= iterations && rc == 0; ++it) {
+      /* accumulate_node_terms, mrsdc.cpp:69-82 */
+      for (int q = 0; q < m2; ++q)
+        for (long long i = 0; i < dim; ++i) {
+          double acc = 0.0;
+          for (int j = 0; j <= m1; ++j) acc += s21[q * (m1 + 1) + j] * F1[j * dim + i];
+          for (int j = 0; j <= m2; ++j) acc += s22[q * (m2 + 1) + j] * F2[j * dim + i];
+          SO[q * dim + i] = dt * acc;
+        }
+      memcpy(OF1, F1, bytes * (m1 + 1));
+      memcpy(fold, F2, bytes);
+      /* step_mode2 coarse intervals, mrsdc.cpp:156-194 */
+      for (int p = 0; p < m1; ++p) {
+        const int qa = fine_of_coarse[p], qb = fine_of_coarse[p + 1];
+        const double dt1 = (t1[p + 1] - t1[p]) * dt;
+        const double t_right = tn + t1[p + 1] * dt;
+        for (long long i = 0; i < dim; ++i) {
+          double acc = 0.0;
+          for (int q = qa; q < qb; ++q) acc += SO[q * dim + i];
+          cvec[i] = U[qa * dim + i] + acc - dt1 * OF1[(p + 1) * dim + i];
+        }
+        or_newton_report rep;
+        or_solve_backward_euler(f1, c1, dim, t_right, dt1, cvec, U + qb * dim, opts, wsol, &rep);
+        ++*implicit_solves;
+        *newton_f1_evals += rep.f_evals;
+        if (!rep.converged) {
+          *fail_node = p + 1;
+          *fail_sweep = it;
+          rc = 2;
+          break;
+        }
+        f1(t_right, wsol, F1 + (p + 1) * dim, dim, c1);
+        ++*f1_evals;
+        for (int q = qa; q < qb; ++q) {
+          const double dtq = (t2[q + 1] - t2[q]) * dt;
+          double* next = U + (q + 1) * dim;
+          const double* cur = U + q * dim;
+          for (long long i = 0; i < dim; ++i)
+            next[i] = cur[i] + dtq * (F1[(p + 1) * dim + i] - OF1[(p + 1) * dim + i]) +
+                      dtq * (F2[q * dim + i] - fold[i]) + SO[q * dim + i];
+          memcpy(fold, F2 + (q + 1) * dim, bytes);
+          f2(tn + t2[q + 1] * dt, next, F2 + (q + 1) * dim, dim, c2);
+          ++*f2_evals;
+        }
+      }
+      if (rc) break;
+      /* mrsdc_residual, mrsdc.cpp:23-35 */
+      double res = 0.0;
+      for (long long i = 0; i < dim; ++i) {
+        double acc = 0.0;
+        for (int j = 0; j <= m1; ++j) acc += q21[(m2 - 1) * (m1 + 1) + j] * F1[j * dim + i];
+        for (int j = 0; j <= m2; ++j) acc += q22[(m2 - 1) * (m2 + 1) + j] * F2[j * dim + i];
+        res = max_keep(res, fabs(u[i] + dt * acc - U[m2 * dim + i]));
+      }
+      hist[hl++] = res;
+      if (residuals && nres < max_res) residuals[nres] = res;
+      ++nres;
+      ++*sweeps;
+      if (stalled(hist, hl, cutoff)) break;
+    }
+    memcpy(u, U + m2 * dim, bytes);
+    memcpy(c1s, F1 + m1 * dim, bytes);
+    memcpy(c2s, F2 + m2 * dim, bytes);
+  }
+  memcpy(u_out, u, bytes);
+  free(U); free(F1); free(F2); free(OF1); free(SO); free(fold); free(cvec); free(wsol);
+  free(u); free(c1s); free(c2s); free(hist);
+  return rc;
+}

@@ -77,6 +77,48 @@ int or_integrate_mrsdc1(or_rhs_cb f1, void* c1, or_rhs_cb f2, void* c2, long lon
                         double cutoff, double* u_out, double* residuals, int max_res,
                         int* sweeps, int* f1_evals, int* f2_evals);
 
+/* StiffOptions (core/include/nsdc/stiff.hpp:10-20) plus the block structure
+ * the device solver exploits: f couples only the `block` components of one
+ * block (block 0 = dense, the reference's case).  Component j of block b sits
+ * at j*nb + b when `interleaved` (structure-of-arrays, the NS state) and at
+ * b*block + j otherwise. */
+typedef struct {
+  double rtol, atol;
+  int max_newton_iters;
+  long long block;
+  int interleaved;
+} or_stiff;
+
+/* NewtonReport (stiff.hpp:22-27) */
+typedef struct {
+  int iterations;
+  double final_residual;
+  int converged;
+  int f_evals;
+} or_newton_report;
+
+/* solve_backward_euler (core/src/stiff.cpp:34-76, fd_jacobian :16-30,
+ * lu_factor/lu_solve core/src/matrix.cpp:9-51): w = c + beta f(t, w) by
+ * Newton from guess.  With block > 0 the finite-difference Jacobian is formed
+ * one block column at a time (every block perturbed at once) and factored
+ * per block; for a block-local f this equals the dense computation bit for
+ * bit.  Returns 0, or 1 on bad arguments; convergence is in *rep. */
+int or_solve_backward_euler(or_rhs_cb f, void* ctx, long long dim, double t, double beta,
+                            const double* c, const double* guess, const or_stiff* opts,
+                            double* w, or_newton_report* rep);
+
+/* integrate_mrsdc, mode 2 (core/src/mrsdc.cpp:137-206, :227-259): f1 implicit
+ * on the coarse nodes.  Returns 0, 1 on bad arguments, 2 when a Newton solve
+ * fails (*fail_node = coarse node, *fail_sweep = sweep). */
+int or_integrate_mrsdc2(or_rhs_cb f1, void* c1, or_rhs_cb f2, void* c2, long long dim,
+                        const double* u0, double t0, double tend, int nsteps, int m1,
+                        const double* t1, int m2, const double* t2, const double* s21,
+                        const double* q21, const double* s22, const double* q22,
+                        const int* fine_of_coarse, int iterations, double cutoff,
+                        const or_stiff* opts, double* u_out, double* residuals, int max_res,
+                        int* sweeps, int* f1_evals, int* f2_evals, int* implicit_solves,
+                        int* newton_f1_evals, int* fail_node, int* fail_sweep);
+
 #ifdef __cplusplus
 }
 #endif

@@ -199,3 +199,92 @@ def ns_temperature_pressure(U):
     T, p = np.empty(U.shape[1:]), np.empty(U.shape[1:])
     lib().or_ns_temperature_pressure(dp(U), C.c_longlong(n), dp(T), dp(p))
     return T, p
+
+
+# ------------------------------------------------ implicit (MRSDC mode 2)
+class Stiff(C.Structure):
+    """or_stiff (oracle.h): StiffOptions + the block structure of f1."""
+    _fields_ = [("rtol", C.c_double), ("atol", C.c_double), ("max_newton_iters", C.c_int),
+                ("block", C.c_longlong), ("interleaved", C.c_int)]
+
+
+class NewtonReport(C.Structure):
+    _fields_ = [("iterations", C.c_int), ("final_residual", C.c_double), ("converged", C.c_int),
+                ("f_evals", C.c_int)]
+
+
+def _stiff(rtol=1e-8, atol=1e-10, max_newton_iters=16, block=0, interleaved=False) -> Stiff:
+    return Stiff(rtol, atol, max_newton_iters, block, int(interleaved))
+
+
+def solve_backward_euler(fcb, dim, t, beta, c, guess, **stiff):
+    """or_solve_backward_euler; fcb is an RHS_CB.  Returns (w, report)."""
+    w = np.empty(dim)
+    rep = NewtonReport()
+    st = _stiff(**stiff)
+    rc = lib().or_solve_backward_euler(fcb, None, C.c_longlong(dim), C.c_double(t),
+                                       C.c_double(beta), dp(c), dp(guess), C.byref(st), dp(w),
+                                       C.byref(rep))
+    assert rc == 0
+    return w, rep
+
+
+def ref_solve_backward_euler(fcb, dim, t, beta, c, guess, rtol=1e-8, atol=1e-10,
+                             max_newton_iters=16):
+    w = np.empty(dim)
+    ints = np.zeros(3, dtype=np.int32)
+    fr = C.c_double()
+    rc = ref().ref_solve_backward_euler(fcb, None, C.c_longlong(dim), C.c_double(t),
+                                        C.c_double(beta), dp(c), dp(guess), C.c_double(rtol),
+                                        C.c_double(atol), max_newton_iters, dp(w), ip(ints),
+                                        C.byref(fr))
+    if rc:
+        raise RuntimeError(ref().ref_last_error().decode())
+    return w, dict(iterations=int(ints[0]), converged=bool(ints[1]), f_evals=int(ints[2]),
+                   final_residual=fr.value)
+
+
+def integrate_mrsdc2(f1cb, f2cb, u0, t0, t1, nsteps, h, iterations=4, cutoff=0.0, **stiff):
+    """or_integrate_mrsdc2 with hierarchy h (ref_hierarchy dict).  Returns
+    (rc, u, diag dict)."""
+    D = lambda a: np.ascontiguousarray(a, dtype=np.float64)  # noqa: E731
+    u0 = D(u0)
+    dim = u0.size
+    m1, m2 = len(h["coarse"]) - 1, len(h["fine"]) - 1
+    uo = np.empty(dim)
+    res = np.zeros(4096)
+    ints = [C.c_int() for _ in range(7)]
+    st = _stiff(**stiff)
+    foc = np.ascontiguousarray(h["fine_of_coarse"], dtype=np.int32)
+    arrs = [D(h[k]) for k in ("coarse", "fine", "s21", "q21", "s22", "q22")]
+    rc = lib().or_integrate_mrsdc2(
+        f1cb, None, f2cb, None, C.c_longlong(dim), dp(u0), C.c_double(t0), C.c_double(t1), nsteps,
+        m1, dp(arrs[0]), m2, dp(arrs[1]), dp(arrs[2]), dp(arrs[3]), dp(arrs[4]), dp(arrs[5]),
+        ip(foc), iterations, C.c_double(cutoff), C.byref(st), dp(uo), dp(res), res.size,
+        *[C.byref(i) for i in ints])
+    sw, n1, n2, imp, nf1, fnode, fsweep = (i.value for i in ints)
+    return rc, uo, dict(sweeps=sw, f1_evals=n1, f2_evals=n2, implicit_solves=imp,
+                        newton_f1_evals=nf1, residuals=res[:sw].copy(), fail_node=fnode,
+                        fail_sweep=fsweep)
+
+
+def ref_integrate_mrsdc2(f1cb, f2cb, u0, t0, t1, nsteps, coarse_n=3, fine_type=1, fine_n=5,
+                         repeats=1, iterations=4, cutoff=0.0, rtol=1e-8, atol=1e-10,
+                         max_newton_iters=16, coarse_family=0, fine_family=0):
+    """The reference's integrate_mrsdc with f1 implicit.  Returns (rc, u, diag
+    dict, error message)."""
+    u0 = np.ascontiguousarray(u0, dtype=np.float64)
+    dim = u0.size
+    uo = np.empty(dim)
+    res = np.zeros(4096)
+    ints = [C.c_int() for _ in range(5)]
+    r = ref()
+    rc = r.ref_integrate_mrsdc2(
+        f1cb, None, f2cb, None, C.c_longlong(dim), dp(u0), C.c_double(t0), C.c_double(t1), nsteps,
+        coarse_family, coarse_n, fine_type, fine_family, fine_n, repeats, iterations,
+        C.c_double(cutoff), C.c_double(rtol), C.c_double(atol), max_newton_iters, dp(uo), dp(res),
+        res.size, *[C.byref(i) for i in ints])
+    sw, n1, n2, imp, nf1 = (i.value for i in ints)
+    msg = r.ref_last_error().decode() if rc else ""
+    return rc, uo, dict(sweeps=sw, f1_evals=n1, f2_evals=n2, implicit_solves=imp,
+                        newton_f1_evals=nf1, residuals=res[:sw].copy()), msg

@@ -25,6 +25,7 @@
 #include "nsdc/quadrature.hpp"
 #include "nsdc/sdc.hpp"
 #include "nsdc/stencil.hpp"
+#include "nsdc/stiff.hpp"
 #include "stencil_kernel.hpp"  // proj/core/src (private kernels, -I on the src dir)
 
 using namespace nsdc;
@@ -374,6 +375,66 @@ int ref_integrate_mrsdc1(rhs_cb f1, void* ctx1, rhs_cb f2, void* ctx2, long long
     *sweeps = diag.sweeps;
     *f1_evals = diag.f1_evals;
     *f2_evals = diag.f2_evals;
+  });
+}
+
+// integrate_mrsdc with f1 implicit (mode 2, mrsdc.cpp:137-206, :227-259) and
+// StiffOptions{rtol, atol, max_newton_iters} (stiff.hpp:10-20).  Returns 2
+// with ref_last_error() on IntegrationError (e.g. Newton failure).
+int ref_integrate_mrsdc2(rhs_cb f1, void* ctx1, rhs_cb f2, void* ctx2, long long dim,
+                         const double* u0, double t0, double t1, int nsteps, int coarse_family,
+                         int coarse_nodes, int fine_type, int fine_family, int fine_nodes,
+                         int repeats, int iterations, double cutoff, double rtol, double atol,
+                         int max_newton_iters, double* u_out, double* residuals, int max_res,
+                         int* sweeps, int* f1_evals, int* f2_evals, int* implicit_solves,
+                         int* newton_f1_evals) {
+  return guarded([&] {
+    StepControls c;
+    c.num_iterations = iterations;
+    c.residual_ratio_cutoff = cutoff;
+    StiffOptions so;
+    so.rtol = rtol;
+    so.atol = atol;
+    so.max_newton_iters = max_newton_iters;
+    FineSpec spec = fine_type == 2 ? FineSpec{TypeC{nodes_from(fine_family, fine_nodes), repeats}}
+                                   : FineSpec{TypeB{nodes_from(fine_family, fine_nodes)}};
+    MultirateHierarchy h = build_hierarchy(nodes_from(coarse_family, coarse_nodes), spec);
+    SplitRHS rhs;
+    rhs.f1 = wrap_cb(f1, ctx1);
+    rhs.f2 = wrap_cb(f2, ctx2);
+    rhs.f1_stiffness = SplitRHS::Stiffness::Implicit;
+    auto [u, diag] = integrate_mrsdc(rhs, Field(u0, u0 + dim), t0, t1, nsteps, h, c, so);
+    std::memcpy(u_out, u.data(), sizeof(double) * dim);
+    if (residuals)
+      for (int i = 0; i < std::min<int>(max_res, diag.residual_history.size()); ++i)
+        residuals[i] = diag.residual_history[i];
+    *sweeps = diag.sweeps;
+    *f1_evals = diag.f1_evals;
+    *f2_evals = diag.f2_evals;
+    *implicit_solves = diag.implicit_solves;
+    *newton_f1_evals = diag.newton_f1_evals;
+  });
+}
+
+// solve_backward_euler (stiff.cpp:34-76) with a report: out_int = {iterations,
+// converged, f_evals}, *final_residual.
+int ref_solve_backward_euler(rhs_cb f, void* ctx, long long dim, double t, double beta,
+                             const double* c, const double* guess, double rtol, double atol,
+                             int max_newton_iters, double* w, int* out_int,
+                             double* final_residual) {
+  return guarded([&] {
+    StiffOptions so;
+    so.rtol = rtol;
+    so.atol = atol;
+    so.max_newton_iters = max_newton_iters;
+    NewtonReport rep;
+    Field r = solve_backward_euler(wrap_cb(f, ctx), t, beta, Field(c, c + dim),
+                                   Field(guess, guess + dim), so, &rep);
+    std::memcpy(w, r.data(), sizeof(double) * dim);
+    out_int[0] = rep.iterations;
+    out_int[1] = rep.converged ? 1 : 0;
+    out_int[2] = rep.f_evals;
+    *final_residual = rep.final_residual;
   });
 }
 

@@ -13,6 +13,14 @@ Contents (all fp64):
                                              cutoff 0, 10 steps at appendix_dt
   mr_u0 / mr_u / mr_res / mr_meta            integrate_mrsdc mode 1, dim 3 linear split
                                              problem, GL(3) / TypeB GL(5), K=4, 4 steps
+  m2_<case>_u0 / _u / _res / _meta           integrate_mrsdc mode 2 (f1 implicit, dense
+                                             FD-Jacobian Newton): osc = Prothero-Robinson
+                                             sigma 1e4, GL(3)/TypeB GL(5), K=6, 5 steps of
+                                             0.02, rtol 1e-12 atol 1e-13; rob = 4 Robertson
+                                             cells (tests/mode2_problems.py), K=4, 5 steps
+                                             of 0.01; oscc = sigma 1e3, GL(5)/TypeC{GL(3),2},
+                                             K=4, 2 steps of 0.01.  meta = sweeps, f1, f2,
+                                             implicit solves, Newton f1 evals
   q_gl3, s_gl3, q_gl5, s_gl5, nodes_gl9,     quadrature tables
   q_cc5, s_cc5, h_*                          build_hierarchy(GL3, TypeB GL5)
 """
@@ -101,6 +109,28 @@ def main():
     assert rc == 0, O.ref().ref_last_error()
     g["mr_u0"], g["mr_u"], g["mr_res"] = u0, uo, res[: sw.value]
     g["mr_meta"] = np.array([sw.value, n1.value, n2.value], dtype=np.float64)
+
+    # integrate_mrsdc mode 2 (mrsdc.cpp:137-206) on the reference's own stiff
+    # problem and on block-local Robertson kinetics
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    import mode2_problems as MP
+    cases = {
+        "osc": (("oscillator", dict(sigma=1.0e4)), np.array([1.0]), 0.1, 5,
+                dict(coarse_n=3, fine_type=1, fine_n=5, iterations=6, rtol=1e-12, atol=1e-13)),
+        "rob": (("robertson", dict(ncell=4, inter=False)), MP.robertson_u0(4, False), 0.05, 5,
+                dict(coarse_n=3, fine_type=1, fine_n=5, iterations=4)),
+        "oscc": (("oscillator", dict(sigma=1.0e3)), np.array([1.0]), 0.02, 2,
+                 dict(coarse_n=5, fine_type=2, fine_n=3, repeats=2, iterations=4)),
+    }
+    for name, ((pname, pkw), u0m, t1m, nst, kw) in cases.items():
+        f1, f2 = MP.np_callbacks(pname, **pkw)
+        rc, um, dg, msg = O.ref_integrate_mrsdc2(O.RHS_CB(f1), O.RHS_CB(f2), u0m, 0.0, t1m, nst,
+                                                 **kw)
+        assert rc == 0, msg
+        g[f"m2_{name}_u0"], g[f"m2_{name}_u"], g[f"m2_{name}_res"] = u0m, um, dg["residuals"]
+        g[f"m2_{name}_meta"] = np.array([dg[k] for k in ("sweeps", "f1_evals", "f2_evals",
+                                                         "implicit_solves", "newton_f1_evals")],
+                                        dtype=np.float64)
 
     for fam, nm, sz in ((0, "gl", 3), (0, "gl", 5), (1, "cc", 5)):
         nodes, q, s = O.ref_integration_matrices(fam, sz)
