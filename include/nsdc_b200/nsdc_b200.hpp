@@ -22,6 +22,7 @@
 #include <string>
 #include <string_view>
 #include <utility>
+#include <variant>
 #include <vector>
 
 #include "../smc_b200.h"
@@ -162,6 +163,52 @@ struct TypeC {
   NodeSet inner;
   int repeats = 1;
 };
+using FineSpec = std::variant<TypeB, TypeC>;
+
+// matrix.hpp: dense row-major matrix
+struct Matrix {
+  int rows = 0, cols = 0;
+  std::vector<double> a;
+  Matrix() = default;
+  Matrix(int r, int c) : rows(r), cols(c), a(static_cast<std::size_t>(r) * c) {}
+  double& operator()(int r, int c) { return a[static_cast<std::size_t>(r) * cols + c]; }
+  double operator()(int r, int c) const { return a[static_cast<std::size_t>(r) * cols + c]; }
+};
+
+// MultirateHierarchy (quadrature.hpp:70-77) from the library's builder
+// (quadrature.cpp:178-248); `spec` records what the device stepper is built
+// from (TypeB == TypeC with one repeat).
+struct MultirateHierarchy {
+  NodeSet coarse;
+  NodeSet fine;
+  Matrix q21, s21;
+  Matrix q22, s22;
+  std::vector<int> fine_of_coarse;
+  std::vector<int> p_map;
+  TypeC spec;
+};
+inline MultirateHierarchy build_hierarchy(const NodeSet& coarse, const FineSpec& fs) {
+  const TypeC c = std::holds_alternative<TypeB>(fs) ? TypeC{std::get<TypeB>(fs).inner, 1}
+                                                    : std::get<TypeC>(fs);
+  MultirateHierarchy h;
+  h.coarse = coarse;
+  h.spec = c;
+  int m2p1 = 0;
+  detail::check(smc_build_hierarchy(family_of(coarse), coarse.count(), family_of(c.inner),
+                                    c.inner.count(), c.repeats, &m2p1, nullptr, nullptr, nullptr,
+                                    nullptr, nullptr, nullptr, nullptr));
+  const int m1 = coarse.intervals(), m2 = m2p1 - 1;
+  h.fine = NodeSet{std::vector<double>(m2p1), NodeKind::Composite};
+  h.q21 = Matrix(m2, m1 + 1), h.s21 = Matrix(m2, m1 + 1);
+  h.q22 = Matrix(m2, m2p1), h.s22 = Matrix(m2, m2p1);
+  h.fine_of_coarse.resize(coarse.count());
+  h.p_map.resize(m2p1);
+  detail::check(smc_build_hierarchy(family_of(coarse), coarse.count(), family_of(c.inner),
+                                    c.inner.count(), c.repeats, &m2p1, h.fine.nodes.data(),
+                                    h.q21.a.data(), h.s21.a.data(), h.q22.a.data(),
+                                    h.s22.a.data(), h.fine_of_coarse.data(), h.p_map.data()));
+  return h;
+}
 
 // ---------------------------------------------------------------- pde.hpp
 inline constexpr double kTwoPi = 2.0 * std::numbers::pi;
@@ -360,6 +407,28 @@ struct MrsdcDiagnostics {
   bool early_stop = false;
 };
 
+// stiff.hpp:10-27.  `block` / `interleaved` declare the block structure of
+// the implicit term for the device Newton (0 = dense, the reference's case;
+// see smc_stiff in smc_b200.h).  A user-supplied Jacobian is not on the
+// device path.
+struct StiffOptions {
+  double rtol = 1e-8;
+  double atol = 1e-10;
+  int max_newton_iters = 16;
+  double initial_step_fraction = 1e-3;
+  enum class Jacobian { FiniteDifference, UserSupplied };
+  Jacobian jacobian = Jacobian::FiniteDifference;
+  std::function<void(double t, const Field& u, Matrix& j)> user_jacobian;
+  long long block = 0;
+  bool interleaved = false;
+};
+struct NewtonReport {
+  int iterations = 0;
+  double final_residual = 0.0;
+  bool converged = false;
+  int f_evals = 0;
+};
+
 namespace detail {
 // Any nsdc::Rhs as a device operator (host round trip per call); the
 // overloads below taking a GPU operator skip it.
@@ -390,6 +459,11 @@ struct DiagBuf {
     return {res.begin(), res.begin() + std::min(d.n_residuals, d.residual_capacity)};
   }
 };
+inline smc_stiff to_c(const StiffOptions& o) {
+  if (o.jacobian == StiffOptions::Jacobian::UserSupplied)
+    throw std::invalid_argument("StiffOptions: a user-supplied Jacobian is not on the device path");
+  return smc_stiff{o.rtol, o.atol, o.max_newton_iters, o.block, o.interleaved ? 1 : 0};
+}
 struct SdcDeleter {
   void operator()(smc_sdc* s) const { smc_sdc_destroy(s); }
 };
@@ -469,18 +543,25 @@ inline auto integrate_sdc(const Op& op, const Field& u0, double t0, double t1, i
   return s.integrate(op.handle(), u0, t0, t1, nsteps);
 }
 
-// Device-resident MrsdcStepper, mode 1 (mrsdc.hpp:51-82), hierarchy
-// build_hierarchy(coarse, TypeB/TypeC{inner}).
+// Device-resident MrsdcStepper (mrsdc.hpp:51-82): mode 1 and mode 2 (f1
+// implicit through the device Newton), hierarchy build_hierarchy(coarse,
+// TypeB/TypeC{inner}).
 class MrsdcStepper {
  public:
-  MrsdcStepper(const NodeSet& coarse, const TypeC& fine, StepControls c) : c_(c) {
+  MrsdcStepper(MultirateHierarchy h, StepControls c, StiffOptions stiff = {})
+      : c_(c), h_(std::move(h)), stiff_(std::move(stiff)) {
     if (c.num_iterations < 1) throw std::invalid_argument("MrsdcStepper: need at least one sweep");
     smc_mrsdc* m = nullptr;
-    detail::check(smc_mrsdc_create(family_of(coarse), coarse.count(), family_of(fine.inner),
-                                   fine.inner.count(), fine.repeats, c.num_iterations,
-                                   c.residual_ratio_cutoff, c.reuse_first_eval ? 1 : 0, &m));
+    detail::check(smc_mrsdc_create(family_of(h_.coarse), h_.coarse.count(),
+                                   family_of(h_.spec.inner), h_.spec.inner.count(),
+                                   h_.spec.repeats, c.num_iterations, c.residual_ratio_cutoff,
+                                   c.reuse_first_eval ? 1 : 0, &m));
     m_.reset(m);
+    const smc_stiff so = detail::to_c(stiff_);
+    detail::check(smc_mrsdc_set_stiff(m_.get(), &so));
   }
+  MrsdcStepper(const NodeSet& coarse, const TypeC& fine, StepControls c)
+      : MrsdcStepper(build_hierarchy(coarse, fine), c) {}
   MrsdcStepper(const NodeSet& coarse, const TypeB& fine, StepControls c)
       : MrsdcStepper(coarse, TypeC{fine.inner, 1}, c) {}
   struct Result {
@@ -489,58 +570,117 @@ class MrsdcStepper {
   };
   Result step_mode1(smc_rhs* f1, smc_rhs* f2, const Field& u0, double t_n, double dt,
                     const Field* f01 = nullptr, const Field* f02 = nullptr) {
-    const std::size_t n = u0.size();
-    Result r{Field(n), Field(n), Field(n), {}};
-    detail::DiagBuf db;
-    detail::check(smc_mrsdc_step_mode1(m_.get(), f1, f2, u0.data(), t_n, dt,
-                                       f01 ? f01->data() : nullptr, f02 ? f02->data() : nullptr,
-                                       r.u.data(), r.f1_end.data(), r.f2_end.data(), SMC_HOST,
-                                       &db.d));
-    r.diag = to_diag(db);
-    return r;
+    return step(smc_mrsdc_step_mode1, f1, f2, u0, t_n, dt, f01, f02);
   }
   Result step_mode1(const SplitRHS& rhs, const Field& u0, double t_n, double dt,
                     const Field* f01 = nullptr, const Field* f02 = nullptr) {
     detail::CallbackRhs a(rhs.f1, u0.size()), b(rhs.f2, u0.size());
     return step_mode1(a.h.get(), b.h.get(), u0, t_n, dt, f01, f02);
   }
-  Result step_mode2(const SplitRHS&, const Field&, double, double, const Field* = nullptr,
-                    const Field* = nullptr) {
-    throw std::invalid_argument(
-        "MrsdcStepper::step_mode2: implicit f1 is not on the device path (SURVEY.md §8(f))");
+  // f1 implicit: one backward-Euler-form Newton solve per coarse interval
+  // (mrsdc.cpp:137-206); throws IntegrationError naming the coarse node.
+  Result step_mode2(smc_rhs* f1, smc_rhs* f2, const Field& u0, double t_n, double dt,
+                    const Field* f01 = nullptr, const Field* f02 = nullptr) {
+    return step(smc_mrsdc_step_mode2, f1, f2, u0, t_n, dt, f01, f02);
+  }
+  Result step_mode2(const SplitRHS& rhs, const Field& u0, double t_n, double dt,
+                    const Field* f01 = nullptr, const Field* f02 = nullptr) {
+    detail::CallbackRhs a(rhs.f1, u0.size()), b(rhs.f2, u0.size());
+    return step_mode2(a.h.get(), b.h.get(), u0, t_n, dt, f01, f02);
   }
   std::pair<Field, MrsdcDiagnostics> integrate_mode1(smc_rhs* f1, smc_rhs* f2, const Field& u0,
                                                      double t0, double t1, int nsteps) {
-    Field u(u0.size());
-    detail::DiagBuf db;
-    detail::check(smc_mrsdc_integrate_mode1(m_.get(), f1, f2, u0.data(), t0, t1, nsteps,
-                                            u.data(), SMC_HOST, &db.d));
-    return {std::move(u), to_diag(db)};
+    return integrate(smc_mrsdc_integrate_mode1, f1, f2, u0, t0, t1, nsteps);
   }
+  std::pair<Field, MrsdcDiagnostics> integrate_mode2(smc_rhs* f1, smc_rhs* f2, const Field& u0,
+                                                     double t0, double t1, int nsteps) {
+    return integrate(smc_mrsdc_integrate_mode2, f1, f2, u0, t0, t1, nsteps);
+  }
+  const MultirateHierarchy& hierarchy() const { return h_; }
 
  private:
+  using StepFn = int (*)(smc_mrsdc*, smc_rhs*, smc_rhs*, const double*, double, double,
+                         const double*, const double*, double*, double*, double*, int,
+                         smc_diag*);
+  using IntFn = int (*)(smc_mrsdc*, smc_rhs*, smc_rhs*, const double*, double, double, int,
+                        double*, int, smc_diag*);
+  Result step(StepFn fn, smc_rhs* f1, smc_rhs* f2, const Field& u0, double t_n, double dt,
+              const Field* f01, const Field* f02) {
+    const std::size_t n = u0.size();
+    Result r{Field(n), Field(n), Field(n), {}};
+    detail::DiagBuf db;
+    detail::check(fn(m_.get(), f1, f2, u0.data(), t_n, dt, f01 ? f01->data() : nullptr,
+                     f02 ? f02->data() : nullptr, r.u.data(), r.f1_end.data(), r.f2_end.data(),
+                     SMC_HOST, &db.d));
+    r.diag = to_diag(db);
+    return r;
+  }
+  std::pair<Field, MrsdcDiagnostics> integrate(IntFn fn, smc_rhs* f1, smc_rhs* f2,
+                                               const Field& u0, double t0, double t1,
+                                               int nsteps) {
+    Field u(u0.size());
+    detail::DiagBuf db;
+    detail::check(fn(m_.get(), f1, f2, u0.data(), t0, t1, nsteps, u.data(), SMC_HOST, &db.d));
+    return {std::move(u), to_diag(db)};
+  }
   static MrsdcDiagnostics to_diag(const detail::DiagBuf& db) {
     MrsdcDiagnostics d;
     d.residual_history = db.history();
     d.sweeps = db.d.sweeps, d.f1_evals = db.d.f1_evals, d.f2_evals = db.d.f2_evals;
+    d.implicit_solves = db.d.implicit_solves, d.newton_f1_evals = db.d.newton_f1_evals;
     d.early_stop = db.d.early_stop != 0;
     return d;
   }
   StepControls c_;
+  MultirateHierarchy h_;
+  StiffOptions stiff_;
   std::unique_ptr<smc_mrsdc, detail::MrsdcDeleter> m_;
 };
 
+// mrsdc.hpp:97-101: fixed-step integration, mode selected by f1_stiffness.
+inline std::pair<Field, MrsdcDiagnostics> integrate_mrsdc(const SplitRHS& rhs, const Field& u0,
+                                                          double t0, double t1, int nsteps,
+                                                          const MultirateHierarchy& h,
+                                                          const StepControls& c,
+                                                          const StiffOptions& stiff = {}) {
+  if (nsteps < 0) throw std::invalid_argument("integrate_mrsdc: negative step count");
+  detail::CallbackRhs a(rhs.f1, u0.size()), b(rhs.f2, u0.size());
+  MrsdcStepper m(h, c, stiff);
+  return rhs.f1_stiffness == SplitRHS::Stiffness::Implicit
+             ? m.integrate_mode2(a.h.get(), b.h.get(), u0, t0, t1, nsteps)
+             : m.integrate_mode1(a.h.get(), b.h.get(), u0, t0, t1, nsteps);
+}
 inline std::pair<Field, MrsdcDiagnostics> integrate_mrsdc(const SplitRHS& rhs, const Field& u0,
                                                           double t0, double t1, int nsteps,
                                                           const NodeSet& coarse,
                                                           const TypeB& fine,
                                                           const StepControls& c) {
-  if (nsteps < 0) throw std::invalid_argument("integrate_mrsdc: negative step count");
-  if (rhs.f1_stiffness == SplitRHS::Stiffness::Implicit)
-    throw std::invalid_argument("integrate_mrsdc: mode 2 is not on the device path");
-  detail::CallbackRhs a(rhs.f1, u0.size()), b(rhs.f2, u0.size());
-  MrsdcStepper m(coarse, fine, c);
-  return m.integrate_mode1(a.h.get(), b.h.get(), u0, t0, t1, nsteps);
+  return integrate_mrsdc(rhs, u0, t0, t1, nsteps, build_hierarchy(coarse, fine), c);
+}
+inline std::pair<Field, MrsdcDiagnostics> mrsdc_step_mode2(const SplitRHS& rhs, const Field& u0,
+                                                           double t_n, double dt,
+                                                           const MultirateHierarchy& h,
+                                                           const StepControls& c,
+                                                           const StiffOptions& stiff) {
+  MrsdcStepper m(h, c, stiff);
+  MrsdcStepper::Result r = m.step_mode2(rhs, u0, t_n, dt);
+  return {std::move(r.u), std::move(r.diag)};
+}
+
+// stiff.hpp:29-40: w = c + beta f(t_eval, w) by Newton from guess, on the
+// device.  Throws IntegrationError on non-convergence when report is null.
+inline Field solve_backward_euler(const Rhs& f, double t_eval, double beta, const Field& c,
+                                  const Field& guess, const StiffOptions& opts,
+                                  NewtonReport* report = nullptr) {
+  detail::CallbackRhs op(f, c.size());
+  Field w(c.size());
+  const smc_stiff so = detail::to_c(opts);
+  smc_newton_report rep{};
+  detail::check(smc_solve_backward_euler(op.h.get(), t_eval, beta, c.data(), guess.data(),
+                                         w.data(), SMC_HOST, &so, report ? &rep : nullptr));
+  if (report) *report = NewtonReport{rep.iterations, rep.final_residual, rep.converged != 0,
+                                     rep.f_evals};
+  return w;
 }
 
 }  // namespace nsdc_b200

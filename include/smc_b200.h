@@ -74,7 +74,33 @@ typedef struct {
   int n_residuals;
   int residual_capacity;
   double* residuals;
+  int implicit_solves;  /* MRSDC mode 2 */
+  int newton_f1_evals;  /* f1 evaluations inside Newton, counted apart */
 } smc_diag;
+
+/* StiffOptions (core/include/nsdc/stiff.hpp:10-20) plus the block structure
+ * of the implicit term: f couples only the `block` components of one block
+ * (0 = dense, the reference's case).  Component j of block b lives at
+ * j*(n/block) + b when `interleaved` (structure-of-arrays, e.g. the 14 NS
+ * fields of one cell), else at b*block + j.  The finite-difference Jacobian
+ * then costs `block` evaluations per Newton step instead of n, and the LU is
+ * batched per block; for a block-local f the result equals the dense
+ * computation bit for bit. */
+typedef struct {
+  double rtol;          /* 1e-8 */
+  double atol;          /* 1e-10 */
+  int max_newton_iters; /* 16 */
+  long long block;
+  int interleaved;
+} smc_stiff;
+
+/* NewtonReport (core/include/nsdc/stiff.hpp:22-27) */
+typedef struct {
+  int iterations;
+  double final_residual;
+  int converged;
+  int f_evals;
+} smc_newton_report;
 
 /* ------------------------------------------------------------- library */
 int smc_version(void);
@@ -169,6 +195,14 @@ long long smc_rhs_dim(const smc_rhs* op);
 int smc_rhs_set_stream(smc_rhs* op, void* stream);
 int smc_rhs_destroy(smc_rhs* op);
 
+/* solve_backward_euler — core/src/stiff.cpp:34-76: w = c + beta f(t, w) by
+ * Newton from guess (n = the rhs dimension).  With report == NULL a
+ * non-converged solve returns SMC_EINTEGRATION (the reference throws
+ * IntegrationError); with a report the caller inspects report->converged. */
+int smc_solve_backward_euler(smc_rhs* f, double t, double beta, const double* c,
+                             const double* guess, double* w, int where, const smc_stiff* opts,
+                             smc_newton_report* report);
+
 /* ------------------------------------------------------- quadrature */
 /* gauss_lobatto / clenshaw_curtis — core/src/quadrature.cpp:101-132 */
 int smc_nodes(int family, int n, double* t);
@@ -206,6 +240,18 @@ int smc_mrsdc_step_mode1(smc_mrsdc* m, smc_rhs* f1, smc_rhs* f2, const double* u
                          double* f1_end, double* f2_end, int where, smc_diag* diag);
 /* integrate_mrsdc, mode 1 — core/src/mrsdc.cpp:227-259. */
 int smc_mrsdc_integrate_mode1(smc_mrsdc* m, smc_rhs* f1, smc_rhs* f2, const double* u0,
+                              double t0, double t1, int nsteps, double* u_out, int where,
+                              smc_diag* diag);
+/* StiffOptions of mode 2 (MrsdcStepper(h, controls, stiff), mrsdc.hpp:51). */
+int smc_mrsdc_set_stiff(smc_mrsdc* m, const smc_stiff* opts);
+/* MrsdcStepper::step_mode2 — core/src/mrsdc.cpp:137-206: f1 implicit on the
+ * coarse nodes, one backward-Euler-form Newton solve per coarse interval.
+ * Newton failure returns SMC_EINTEGRATION naming the coarse node and sweep. */
+int smc_mrsdc_step_mode2(smc_mrsdc* m, smc_rhs* f1, smc_rhs* f2, const double* u0, double t_n,
+                         double dt, const double* f0_1, const double* f0_2, double* u_out,
+                         double* f1_end, double* f2_end, int where, smc_diag* diag);
+/* integrate_mrsdc with rhs.f1_stiffness == Implicit — core/src/mrsdc.cpp:227-259. */
+int smc_mrsdc_integrate_mode2(smc_mrsdc* m, smc_rhs* f1, smc_rhs* f2, const double* u0,
                               double t0, double t1, int nsteps, double* u_out, int where,
                               smc_diag* diag);
 int smc_mrsdc_set_reducer(smc_mrsdc* m, smc_reduce_fn fn, void* ctx);

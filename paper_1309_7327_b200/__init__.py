@@ -27,7 +27,8 @@ from ._capi import (CLENSHAW_CURTIS, DEVICE, GAUSS_LOBATTO, HOST, NARROW6, NARRO
 __all__ = [
     "SmcError", "SmcInvalidArgument", "SmcIntegrationError", "StencilChoice", "stencil_preset",
     "build_narrow", "apply_narrow", "apply_wide", "first_derivative8", "HeatOperator",
-    "Narrow3DOperator", "Narrow3DSlab", "CallbackRhs", "DeviceCallbackRhs", "SdcStepper", "MrsdcStepper", "StepControls", "nodes",
+    "Narrow3DOperator", "Narrow3DSlab", "CallbackRhs", "DeviceCallbackRhs", "SdcStepper",
+    "MrsdcStepper", "StepControls", "StiffOptions", "NewtonReport", "solve_backward_euler", "nodes",
     "integration_matrices", "build_hierarchy", "SMC_M47", "SMC_M48", "OPTIMAL_M47", "NsOperator",
     "ns_conserved", "NS_FULL", "NS_ADVDIFF", "NS_CHEM",
     "OPTIMAL_M48", "DEFAULT_M36", "launch_count",
@@ -305,6 +306,8 @@ class SweepDiagnostics:
     f2_evals: int = 0
     early_stop: bool = False
     nonfinite: bool = False
+    implicit_solves: int = 0     # MRSDC mode 2 (mrsdc.hpp:30-38)
+    newton_f1_evals: int = 0
 
 
 def _diag(cap=4096):
@@ -318,7 +321,48 @@ def _diag(cap=4096):
 def _from_diag(d, buf) -> SweepDiagnostics:
     n = min(d.n_residuals, d.residual_capacity)
     return SweepDiagnostics(list(buf[:n]), d.sweeps, d.fresh_evals, d.f1_evals, d.f2_evals,
-                            bool(d.early_stop), bool(d.nonfinite))
+                            bool(d.early_stop), bool(d.nonfinite), d.implicit_solves,
+                            d.newton_f1_evals)
+
+
+@dataclass
+class StiffOptions:
+    """StiffOptions (stiff.hpp:10-20) plus the block structure of the implicit
+    term: f couples only the `block` components of one block (0 = dense).
+    `interleaved`: component j of block b at j*(n/block) + b (structure of
+    arrays — NsOperator state: block=14, interleaved=True), else b*block + j."""
+    rtol: float = 1e-8
+    atol: float = 1e-10
+    max_newton_iters: int = 16
+    block: int = 0
+    interleaved: bool = False
+
+    def c(self):
+        return _capi.Stiff(self.rtol, self.atol, self.max_newton_iters, self.block,
+                           int(self.interleaved))
+
+
+@dataclass
+class NewtonReport:
+    """NewtonReport (stiff.hpp:22-27)."""
+    iterations: int = 0
+    final_residual: float = 0.0
+    converged: bool = False
+    f_evals: int = 0
+
+
+def solve_backward_euler(f: "_Rhs", t: float, beta: float, c, guess, stiff: "StiffOptions" = None,
+                         report: bool = True):
+    """solve_backward_euler (stiff.cpp:34-76): w = c + beta f(t, w) by Newton
+    from guess, on the device.  Returns (w, NewtonReport) with report=True;
+    with report=False a failed solve raises SmcIntegrationError."""
+    w = _out_like(c)
+    rep = _capi.NewtonReport()
+    so = (stiff or StiffOptions()).c()
+    check(_capi.lib().smc_solve_backward_euler(f.handle, t, beta, dptr(c), dptr(guess), dptr(w),
+                                               where_of(c), C.byref(so),
+                                               C.byref(rep) if report else None))
+    return w, NewtonReport(rep.iterations, rep.final_residual, bool(rep.converged), rep.f_evals)
 
 
 def _reducer(fn):
@@ -367,11 +411,14 @@ class SdcStepper:
 
 
 class MrsdcStepper:
-    """Device-resident MrsdcStepper, mode 1 (mrsdc.hpp:51-82), hierarchy
-    build_hierarchy(coarse, TypeB{inner}) (repeats=1) or TypeC{inner, repeats}."""
+    """Device-resident MrsdcStepper (mrsdc.hpp:51-82), modes 1 and 2, hierarchy
+    build_hierarchy(coarse, TypeB{inner}) (repeats=1) or TypeC{inner, repeats}.
+    Mode 2 solves f1 implicitly with StiffOptions `stiff` (block structure:
+    see StiffOptions)."""
 
     def __init__(self, coarse_nodes=3, inner_nodes=5, controls: StepControls = None, repeats=1,
-                 coarse_family=GAUSS_LOBATTO, inner_family=GAUSS_LOBATTO):
+                 coarse_family=GAUSS_LOBATTO, inner_family=GAUSS_LOBATTO,
+                 stiff: StiffOptions = None):
         c = controls or StepControls()
         h = C.c_void_p()
         check(_capi.lib().smc_mrsdc_create(coarse_family, coarse_nodes, inner_family, inner_nodes,
@@ -379,6 +426,12 @@ class MrsdcStepper:
                                            int(c.reuse_first_eval), C.byref(h)))
         self._h = h
         self._keep = []
+        if stiff is not None:
+            self.set_stiff(stiff)
+
+    def set_stiff(self, stiff: StiffOptions) -> None:
+        so = stiff.c()
+        check(_capi.lib().smc_mrsdc_set_stiff(self._h, C.byref(so)))
 
     def set_reducer(self, fn) -> None:
         cb = _reducer(fn)
@@ -394,11 +447,26 @@ class MrsdcStepper:
         return u, e1, e2, _from_diag(d, buf)
 
     def integrate_mode1(self, f1: _Rhs, f2: _Rhs, u0, t0, t1, nsteps, out=None):
+        return self._integrate(1, f1, f2, u0, t0, t1, nsteps, out)
+
+    def step_mode2(self, f1: _Rhs, f2: _Rhs, u0, t_n, dt, f0_1=None, f0_2=None):
+        u, e1, e2 = _out_like(u0), _out_like(u0), _out_like(u0)
+        d, buf = _diag()
+        check(_capi.lib().smc_mrsdc_step_mode2(self._h, f1.handle, f2.handle, dptr(u0), t_n, dt,
+                                               dptr(f0_1), dptr(f0_2), dptr(u), dptr(e1),
+                                               dptr(e2), where_of(u0), C.byref(d)))
+        return u, e1, e2, _from_diag(d, buf)
+
+    def integrate_mode2(self, f1: _Rhs, f2: _Rhs, u0, t0, t1, nsteps, out=None):
+        return self._integrate(2, f1, f2, u0, t0, t1, nsteps, out)
+
+    def _integrate(self, mode, f1, f2, u0, t0, t1, nsteps, out):
         u = out if out is not None else _out_like(u0)
         d, buf = _diag()
-        check(_capi.lib().smc_mrsdc_integrate_mode1(self._h, f1.handle, f2.handle, dptr(u0), t0,
-                                                    t1, nsteps, dptr(u), where_of(u0),
-                                                    C.byref(d)))
+        fn = _capi.lib().smc_mrsdc_integrate_mode2 if mode == 2 else \
+            _capi.lib().smc_mrsdc_integrate_mode1
+        check(fn(self._h, f1.handle, f2.handle, dptr(u0), t0, t1, nsteps, dptr(u), where_of(u0),
+                 C.byref(d)))
         return u, _from_diag(d, buf)
 
     def __del__(self):

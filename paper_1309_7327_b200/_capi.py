@@ -43,7 +43,19 @@ class SmcIntegrationError(SmcError):
 class Diag(C.Structure):
     _fields_ = [("sweeps", C.c_int), ("fresh_evals", C.c_int), ("f1_evals", C.c_int),
                 ("f2_evals", C.c_int), ("early_stop", C.c_int), ("nonfinite", C.c_int),
-                ("n_residuals", C.c_int), ("residual_capacity", C.c_int), ("residuals", _D)]
+                ("n_residuals", C.c_int), ("residual_capacity", C.c_int), ("residuals", _D),
+                ("implicit_solves", C.c_int), ("newton_f1_evals", C.c_int)]
+
+
+class Stiff(C.Structure):
+    """smc_stiff: StiffOptions (stiff.hpp:10-20) + block structure of f."""
+    _fields_ = [("rtol", C.c_double), ("atol", C.c_double), ("max_newton_iters", C.c_int),
+                ("block", C.c_longlong), ("interleaved", C.c_int)]
+
+
+class NewtonReport(C.Structure):
+    _fields_ = [("iterations", C.c_int), ("final_residual", C.c_double), ("converged", C.c_int),
+                ("f_evals", C.c_int)]
 
 
 _lib = None
@@ -102,6 +114,13 @@ _SIG = {
                                        _VP, _VP, _VP, C.c_int, C.POINTER(Diag)]),
     "smc_mrsdc_integrate_mode1": (C.c_int, [_VP, _VP, _VP, _VP, C.c_double, C.c_double, C.c_int,
                                             _VP, C.c_int, C.POINTER(Diag)]),
+    "smc_mrsdc_set_stiff": (C.c_int, [_VP, C.POINTER(Stiff)]),
+    "smc_mrsdc_step_mode2": (C.c_int, [_VP, _VP, _VP, _VP, C.c_double, C.c_double, _VP, _VP,
+                                       _VP, _VP, _VP, C.c_int, C.POINTER(Diag)]),
+    "smc_mrsdc_integrate_mode2": (C.c_int, [_VP, _VP, _VP, _VP, C.c_double, C.c_double, C.c_int,
+                                            _VP, C.c_int, C.POINTER(Diag)]),
+    "smc_solve_backward_euler": (C.c_int, [_VP, C.c_double, C.c_double, _VP, _VP, _VP, C.c_int,
+                                           C.POINTER(Stiff), C.POINTER(NewtonReport)]),
     "smc_mrsdc_set_reducer": (C.c_int, [_VP, REDUCE_FN, _VP]),
     "smc_mrsdc_destroy": (C.c_int, [_VP]),
 }

@@ -98,6 +98,8 @@ void fill_diag(const smc::SweepDiag& d, smc_diag* out) {
   out->early_stop = d.early_stop ? 1 : 0;
   out->nonfinite = d.nonfinite ? 1 : 0;
   out->n_residuals = static_cast<int>(d.residuals.size());
+  out->implicit_solves = d.implicit_solves;
+  out->newton_f1_evals = d.newton_f1_evals;
   if (out->residuals)
     for (int i = 0; i < out->residual_capacity && i < out->n_residuals; ++i)
       out->residuals[i] = d.residuals[i];
@@ -476,9 +478,13 @@ int smc_mrsdc_set_reducer(smc_mrsdc* m, smc_reduce_fn fn, void* ctx) {
   });
 }
 
-int smc_mrsdc_step_mode1(smc_mrsdc* m, smc_rhs* f1, smc_rhs* f2, const double* u0, double t_n,
-                         double dt, const double* f0_1, const double* f0_2, double* u_out,
-                         double* f1_end, double* f2_end, int where, smc_diag* diag) {
+}  // extern "C"
+
+namespace {
+
+int mrsdc_step(int mode, smc_mrsdc* m, smc_rhs* f1, smc_rhs* f2, const double* u0, double t_n,
+               double dt, const double* f0_1, const double* f0_2, double* u_out, double* f1_end,
+               double* f2_end, int where, smc_diag* diag) {
   return guarded([&] {
     need(m, "mrsdc handle"), need(u0, "u0"), need(u_out, "u_out");
     smc::RhsOp& a = op_of(f1);
@@ -488,16 +494,18 @@ int smc_mrsdc_step_mode1(smc_mrsdc* m, smc_rhs* f1, smc_rhs* f2, const double* u
     Staged du(u0, n, where, st), d1(f0_1, n, where, st), d2(f0_2, n, where, st);
     StagedOut ou(u_out, n, where), o1(f1_end, n, where), o2(f2_end, n, where);
     smc::SweepDiag d;
-    m->m->step_mode1(a, b, du.dev, t_n, dt, d1.dev, d2.dev, ou.dev, o1.dev, o2.dev, d);
+    if (mode == 2)
+      m->m->step_mode2(a, b, du.dev, t_n, dt, d1.dev, d2.dev, ou.dev, o1.dev, o2.dev, d);
+    else
+      m->m->step_mode1(a, b, du.dev, t_n, dt, d1.dev, d2.dev, ou.dev, o1.dev, o2.dev, d);
     ou.finish(st), o1.finish(st), o2.finish(st);
     if (where == SMC_HOST) SMC_CUDA(cudaStreamSynchronize(st));
     fill_diag(d, diag);
   });
 }
 
-int smc_mrsdc_integrate_mode1(smc_mrsdc* m, smc_rhs* f1, smc_rhs* f2, const double* u0,
-                              double t0, double t1, int nsteps, double* u_out, int where,
-                              smc_diag* diag) {
+int mrsdc_integrate(int mode, smc_mrsdc* m, smc_rhs* f1, smc_rhs* f2, const double* u0, double t0,
+                    double t1, int nsteps, double* u_out, int where, smc_diag* diag) {
   return guarded([&] {
     need(m, "mrsdc handle"), need(u0, "u0"), need(u_out, "u_out");
     smc::RhsOp& a = op_of(f1);
@@ -507,10 +515,88 @@ int smc_mrsdc_integrate_mode1(smc_mrsdc* m, smc_rhs* f1, smc_rhs* f2, const doub
     Staged du(u0, n, where, st);
     StagedOut ou(u_out, n, where);
     smc::SweepDiag d;
-    m->m->integrate_mode1(a, b, du.dev, t0, t1, nsteps, ou.dev, d);
+    if (mode == 2)
+      m->m->integrate_mode2(a, b, du.dev, t0, t1, nsteps, ou.dev, d);
+    else
+      m->m->integrate_mode1(a, b, du.dev, t0, t1, nsteps, ou.dev, d);
     ou.finish(st);
     if (where == SMC_HOST) SMC_CUDA(cudaStreamSynchronize(st));
     fill_diag(d, diag);
+  });
+}
+
+smc::StiffOpts stiff_of(const smc_stiff* o) {
+  smc::StiffOpts s;
+  if (o) {
+    s.rtol = o->rtol, s.atol = o->atol, s.max_newton_iters = o->max_newton_iters;
+    s.block = o->block, s.interleaved = o->interleaved;
+  }
+  smc::require(s.rtol >= 0.0 && s.atol >= 0.0, "StiffOptions: negative tolerance");
+  smc::require(s.block >= 0, "StiffOptions: negative block size");
+  return s;
+}
+
+}  // namespace
+
+extern "C" {
+
+int smc_mrsdc_step_mode1(smc_mrsdc* m, smc_rhs* f1, smc_rhs* f2, const double* u0, double t_n,
+                         double dt, const double* f0_1, const double* f0_2, double* u_out,
+                         double* f1_end, double* f2_end, int where, smc_diag* diag) {
+  return mrsdc_step(1, m, f1, f2, u0, t_n, dt, f0_1, f0_2, u_out, f1_end, f2_end, where, diag);
+}
+
+int smc_mrsdc_integrate_mode1(smc_mrsdc* m, smc_rhs* f1, smc_rhs* f2, const double* u0,
+                              double t0, double t1, int nsteps, double* u_out, int where,
+                              smc_diag* diag) {
+  return mrsdc_integrate(1, m, f1, f2, u0, t0, t1, nsteps, u_out, where, diag);
+}
+
+int smc_mrsdc_set_stiff(smc_mrsdc* m, const smc_stiff* opts) {
+  return guarded([&] {
+    need(m, "mrsdc handle");
+    m->m->set_stiff(stiff_of(opts));
+  });
+}
+
+int smc_mrsdc_step_mode2(smc_mrsdc* m, smc_rhs* f1, smc_rhs* f2, const double* u0, double t_n,
+                         double dt, const double* f0_1, const double* f0_2, double* u_out,
+                         double* f1_end, double* f2_end, int where, smc_diag* diag) {
+  return mrsdc_step(2, m, f1, f2, u0, t_n, dt, f0_1, f0_2, u_out, f1_end, f2_end, where, diag);
+}
+
+int smc_mrsdc_integrate_mode2(smc_mrsdc* m, smc_rhs* f1, smc_rhs* f2, const double* u0,
+                              double t0, double t1, int nsteps, double* u_out, int where,
+                              smc_diag* diag) {
+  return mrsdc_integrate(2, m, f1, f2, u0, t0, t1, nsteps, u_out, where, diag);
+}
+
+int smc_solve_backward_euler(smc_rhs* f, double t, double beta, const double* c,
+                             const double* guess, double* w, int where, const smc_stiff* opts,
+                             smc_newton_report* report) {
+  return guarded([&] {
+    need(c, "c"), need(guess, "guess"), need(w, "w");
+    smc::RhsOp& op = op_of(f);
+    const long long n = op.dim();
+    cudaStream_t st = op.stream();
+    const smc::StiffOpts so = stiff_of(opts);
+    Staged dc(c, n, where, st), dg(guess, n, where, st);
+    StagedOut ow(w, n, where);
+    smc::DeviceNewton newton;
+    smc::NewtonReport rep;
+    newton.solve(op, t, beta, dc.dev, dg.dev, ow.dev, so, rep);
+    ow.finish(st);
+    SMC_CUDA(cudaStreamSynchronize(st));
+    if (report) {
+      report->iterations = rep.iterations;
+      report->final_residual = rep.final_residual;
+      report->converged = rep.converged ? 1 : 0;
+      report->f_evals = rep.f_evals;
+    } else if (!rep.converged) {
+      throw smc::IntegrationFailure("backward-Euler Newton failed: residual " +
+                                    std::to_string(rep.final_residual) + " after " +
+                                    std::to_string(rep.iterations) + " iterations");
+    }
   });
 }
 

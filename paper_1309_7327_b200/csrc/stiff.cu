@@ -1,0 +1,267 @@
+// Device backward-Euler Newton with a block-structured finite-difference
+// Jacobian (see stiff.hpp).  Arithmetic follows the reference operation by
+// operation without contraction (explicit _rn intrinsics), so the dense case
+// reproduces stiff.cpp / matrix.cpp exactly.
+#include <cfloat>
+#include <cmath>
+#include <cstring>
+
+#include "stiff.hpp"
+
+namespace smc {
+namespace {
+
+struct BlockMap {
+  long long B, nb;
+  int inter;
+  __device__ __forceinline__ long long at(long long b, long long j) const {
+    return inter ? j * nb + b : b * B + j;
+  }
+};
+
+int grid_for(long long n) {
+  const long long want = (n + 255) / 256;
+  const long long cap = static_cast<long long>(num_sms()) * 8;
+  return static_cast<int>(std::max(1LL, std::min(want, cap)));
+}
+
+// delta = w - beta f(w) - c (stiff.cpp:54-58); slots[0] = max |delta|,
+// slots[1] = max |w| (field.hpp:18-22).  A NaN never wins the max, as with
+// std::max(r, NaN) == r in the reference.
+__global__ void __launch_bounds__(256) be_residual_kernel(const double* w, const double* fw,
+                                                          const double* c, double beta,
+                                                          double* delta, long long n,
+                                                          unsigned long long* slots) {
+  double r = 0.0, m = 0.0;
+  const long long stride = static_cast<long long>(gridDim.x) * blockDim.x;
+  for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < n;
+       i += stride) {
+    const double d = __dsub_rn(__dsub_rn(w[i], __dmul_rn(beta, fw[i])), c[i]);
+    delta[i] = d;
+    const double ad = fabs(d), aw = fabs(w[i]);
+    if (ad > r) r = ad;
+    if (aw > m) m = aw;
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    r = fmax(r, __shfl_xor_sync(0xffffffffu, r, o));
+    m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
+  }
+  if ((threadIdx.x & 31) == 0) {
+    atomicMax(slots, static_cast<unsigned long long>(__double_as_longlong(r)));
+    atomicMax(slots + 1, static_cast<unsigned long long>(__double_as_longlong(m)));
+  }
+}
+
+// Column j of every block: h_b = sqrt(eps) max(|w|, atol), wp += h
+// (fd_jacobian, stiff.cpp:19-24).
+__global__ void __launch_bounds__(256) fd_perturb_kernel(const double* w, double* wp, double* h,
+                                                         long long j, BlockMap bm, double atol,
+                                                         double root_eps) {
+  const long long stride = static_cast<long long>(gridDim.x) * blockDim.x;
+  for (long long b = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; b < bm.nb;
+       b += stride) {
+    const long long i = bm.at(b, j);
+    const double a = fabs(w[i]);
+    const double hv = __dmul_rn(root_eps, (a < atol) ? atol : a);
+    h[b] = hv;
+    wp[i] = __dadd_rn(w[i], hv);
+  }
+}
+
+// J_b(r, j) = (f(wp) - f(w)) * (1 / h_b) (stiff.cpp:25-28); jac laid out
+// [r][c][b] so the per-block threads of the LU read it coalesced.  Restores
+// wp for the next column.
+__global__ void __launch_bounds__(256) fd_column_kernel(const double* fp, const double* fw,
+                                                        const double* w, double* wp,
+                                                        const double* h, double* jac, long long j,
+                                                        BlockMap bm) {
+  const long long total = bm.B * bm.nb;
+  const long long stride = static_cast<long long>(gridDim.x) * blockDim.x;
+  for (long long t = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; t < total;
+       t += stride) {
+    const long long r = t / bm.nb, b = t - r * bm.nb;
+    const long long k = bm.at(b, r);
+    const double inv = 1.0 / h[b];
+    jac[(r * bm.B + j) * bm.nb + b] = __dmul_rn(__dsub_rn(fp[k], fw[k]), inv);
+    if (r == 0) {
+      const long long i = bm.at(b, j);
+      wp[i] = w[i];
+    }
+  }
+}
+
+// jg = I - beta J (stiff.cpp:63-65), then lu_factor (matrix.cpp:9-33) per
+// block; a zero pivot in any block raises *flag.
+__global__ void __launch_bounds__(128) lu_factor_kernel(double* jac, int* piv, double beta,
+                                                        BlockMap bm, unsigned long long* flag) {
+  const long long B = bm.B, nb = bm.nb;
+  const long long stride = static_cast<long long>(gridDim.x) * blockDim.x;
+  for (long long b = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; b < nb;
+       b += stride) {
+    auto m = [&](long long r, long long c) -> double& { return jac[(r * B + c) * nb + b]; };
+    for (long long r = 0; r < B; ++r)
+      for (long long c = 0; c < B; ++c)
+        m(r, c) = __dsub_rn(r == c ? 1.0 : 0.0, __dmul_rn(beta, m(r, c)));
+    for (long long col = 0; col < B; ++col) {
+      long long best = col;
+      double best_mag = fabs(m(col, col));
+      for (long long r = col + 1; r < B; ++r) {
+        const double mag = fabs(m(r, col));
+        if (mag > best_mag) {
+          best = r;
+          best_mag = mag;
+        }
+      }
+      piv[col * nb + b] = static_cast<int>(best);
+      if (best_mag == 0.0) {
+        atomicMax(flag, 1ull);
+        break;
+      }
+      if (best != col)
+        for (long long c = 0; c < B; ++c) {
+          const double tmp = m(col, c);
+          m(col, c) = m(best, c);
+          m(best, c) = tmp;
+        }
+      const double inv = 1.0 / m(col, col);
+      for (long long r = col + 1; r < B; ++r) {
+        const double l = __dmul_rn(m(r, col), inv);
+        m(r, col) = l;
+        for (long long c = col + 1; c < B; ++c)
+          m(r, c) = __dsub_rn(m(r, c), __dmul_rn(l, m(col, c)));
+      }
+    }
+  }
+}
+
+// lu_solve (matrix.cpp:35-51) on each block of delta, then w -= delta
+// (stiff.cpp:68).
+__global__ void __launch_bounds__(128) lu_solve_update_kernel(const double* jac, const int* piv,
+                                                              double* delta, double* w,
+                                                              BlockMap bm) {
+  const long long B = bm.B, nb = bm.nb;
+  const long long stride = static_cast<long long>(gridDim.x) * blockDim.x;
+  for (long long b = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; b < nb;
+       b += stride) {
+    auto m = [&](long long r, long long c) { return jac[(r * B + c) * nb + b]; };
+    auto x = [&](long long r) -> double& { return delta[bm.at(b, r)]; };
+    for (long long i = 0; i < B; ++i) {
+      const long long p = piv[i * nb + b];
+      if (p != i) {
+        const double tmp = x(i);
+        x(i) = x(p);
+        x(p) = tmp;
+      }
+    }
+    for (long long i = 1; i < B; ++i) {
+      double s = x(i);
+      for (long long j = 0; j < i; ++j) s = __dsub_rn(s, __dmul_rn(m(i, j), x(j)));
+      x(i) = s;
+    }
+    for (long long i = B - 1; i >= 0; --i) {
+      double s = x(i);
+      for (long long j = i + 1; j < B; ++j) s = __dsub_rn(s, __dmul_rn(m(i, j), x(j)));
+      x(i) = s / m(i, i);
+    }
+    for (long long r = 0; r < B; ++r) {
+      const long long k = bm.at(b, r);
+      w[k] = __dsub_rn(w[k], delta[k]);
+    }
+  }
+}
+
+double bits_to_double(unsigned long long u) {
+  double d;
+  std::memcpy(&d, &u, sizeof(d));
+  return d;
+}
+
+}  // namespace
+
+DeviceNewton::DeviceNewton() {
+  SMC_CUDA(cudaMallocHost(&host_slots_, 4 * sizeof(double)));
+}
+
+DeviceNewton::~DeviceNewton() {
+  if (piv_) cudaFree(piv_);
+  if (host_slots_) cudaFreeHost(host_slots_);
+}
+
+void DeviceNewton::ensure(long long dim, long long block) {
+  if (dim == dim_ && block == block_) return;
+  const long long nb = dim / block;
+  fw_.resize(dim), fp_.resize(dim), wp_.resize(dim), delta_.resize(dim);
+  jac_.resize(static_cast<std::size_t>(block) * block * nb);
+  h_.resize(nb);
+  slots_.resize(4);
+  if (piv_n_ != block * nb) {
+    if (piv_) cudaFree(piv_);
+    piv_ = nullptr;
+    SMC_CUDA(cudaMalloc(&piv_, sizeof(int) * block * nb));
+    piv_n_ = block * nb;
+  }
+  dim_ = dim, block_ = block;
+}
+
+void DeviceNewton::solve(RhsOp& f, double t, double beta, const double* c, const double* guess,
+                         double* w, const StiffOpts& o, NewtonReport& rep) {
+  const long long dim = f.dim();
+  const long long B = o.block > 0 ? o.block : dim;
+  require(dim >= 1 && dim % B == 0, "solve_backward_euler: block must divide the dimension");
+  require(o.max_newton_iters >= 0, "solve_backward_euler: negative iteration limit");
+  ensure(dim, B);
+  const BlockMap bm{B, dim / B, o.block > 0 && o.interleaved ? 1 : 0};
+  cudaStream_t st = f.stream();
+  const double root_eps = std::sqrt(DBL_EPSILON);  // stiff.cpp:19
+  auto* slots = reinterpret_cast<unsigned long long*>(slots_.get());
+  auto read_slots = [&](int n) {
+    SMC_CUDA(cudaMemcpyAsync(host_slots_, slots_.get(), n * sizeof(double),
+                             cudaMemcpyDeviceToHost, st));
+    SMC_CUDA(cudaStreamSynchronize(st));
+  };
+  if (w != guess)
+    SMC_CUDA(cudaMemcpyAsync(w, guess, dim * sizeof(double), cudaMemcpyDeviceToDevice, st));
+  rep = NewtonReport{};
+  for (int iter = 0; iter < o.max_newton_iters; ++iter) {
+    f.eval_device(t, w, fw_.get());
+    ++rep.f_evals;
+    SMC_CUDA(cudaMemsetAsync(slots_.get(), 0, 3 * sizeof(double), st));
+    be_residual_kernel<<<grid_for(dim), 256, 0, st>>>(w, fw_.get(), c, beta, delta_.get(), dim,
+                                                     slots);
+    SMC_CHECK_LAUNCH();
+    read_slots(2);
+    unsigned long long u[2];
+    std::memcpy(u, host_slots_, sizeof(u));
+    const double rnorm = bits_to_double(u[0]), wnorm = bits_to_double(u[1]);
+    rep.final_residual = rnorm;
+    if (rnorm <= o.atol + o.rtol * wnorm) {
+      rep.converged = true;
+      break;
+    }
+    SMC_CUDA(cudaMemcpyAsync(wp_.get(), w, dim * sizeof(double), cudaMemcpyDeviceToDevice, st));
+    for (long long j = 0; j < B; ++j) {
+      fd_perturb_kernel<<<grid_for(bm.nb), 256, 0, st>>>(w, wp_.get(), h_.get(), j, bm, o.atol,
+                                                        root_eps);
+      SMC_CHECK_LAUNCH();
+      f.eval_device(t, wp_.get(), fp_.get());
+      ++rep.f_evals;
+      fd_column_kernel<<<grid_for(B * bm.nb), 256, 0, st>>>(fp_.get(), fw_.get(), w, wp_.get(),
+                                                           h_.get(), jac_.get(), j, bm);
+      SMC_CHECK_LAUNCH();
+    }
+    const int lu_grid = static_cast<int>(std::max(1LL, std::min((bm.nb + 127) / 128,
+                                                                 static_cast<long long>(num_sms()) * 16)));
+    lu_factor_kernel<<<lu_grid, 128, 0, st>>>(jac_.get(), piv_, beta, bm, slots + 2);
+    SMC_CHECK_LAUNCH();
+    read_slots(3);
+    unsigned long long flag;
+    std::memcpy(&flag, host_slots_ + 2, sizeof(flag));
+    if (flag) break;  // singular iteration matrix (stiff.cpp:66)
+    lu_solve_update_kernel<<<lu_grid, 128, 0, st>>>(jac_.get(), piv_, delta_.get(), w, bm);
+    SMC_CHECK_LAUNCH();
+    rep.iterations = iter + 1;
+  }
+}
+
+}  // namespace smc

@@ -1,6 +1,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstring>
+#include <string>
 #include <utility>
 
 #include "sweeps.hpp"
@@ -126,6 +127,26 @@ __global__ void __launch_bounds__(256) residual_kernel(const ResidualP p) {
   }
 }
 
+struct BeRhsP {
+  double* c;
+  const double* u;
+  const double* so[kMaxRows];
+  const double* old;
+  double dt1;
+  long long n;
+  int nso;
+};
+
+__global__ void __launch_bounds__(256) be_rhs_kernel(const BeRhsP p) {
+  const long long stride = static_cast<long long>(gridDim.x) * blockDim.x;
+  for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < p.n;
+       i += stride) {
+    double acc = 0.0;
+    for (int q = 0; q < p.nso; ++q) acc = __dadd_rn(acc, p.so[q][i]);
+    p.c[i] = __dsub_rn(__dadd_rn(p.u[i], acc), __dmul_rn(p.dt1, p.old[i]));
+  }
+}
+
 int blocks_for(long long n) {
   const long long want = (n + 255) / 256;
   const long long cap = static_cast<long long>(num_sms()) * 8;
@@ -186,6 +207,16 @@ void launch_integrals(int rows, double* const* out, int ng, const double* const*
   SMC_CHECK_LAUNCH();
 }
 
+void launch_be_rhs(double* c, const double* u, int nso, const double* const* so, const double* old,
+                   double dt1, long long n, cudaStream_t st) {
+  require(nso >= 1 && nso <= kMaxRows, "mrsdc mode 2: too many fine sub-steps per coarse interval");
+  BeRhsP p{};
+  p.c = c, p.u = u, p.old = old, p.dt1 = dt1, p.n = n, p.nso = nso;
+  for (int q = 0; q < nso; ++q) p.so[q] = so[q];
+  be_rhs_kernel<<<blocks_for(n), 256, 0, st>>>(p);
+  SMC_CHECK_LAUNCH();
+}
+
 void launch_residual(const double* u0, const double* um, int ng, const double* const* g,
                      const double* q, double dt, long long n, double* slot, cudaStream_t st) {
   require(ng >= 1 && ng <= kMaxTerms, "residual: too many terms");
@@ -203,6 +234,8 @@ void SweepDiag::add(const SweepDiag& o) {
   fresh_evals += o.fresh_evals;
   f1_evals += o.f1_evals;
   f2_evals += o.f2_evals;
+  implicit_solves += o.implicit_solves;
+  newton_f1_evals += o.newton_f1_evals;
   early_stop = early_stop || o.early_stop;
   nonfinite = nonfinite || o.nonfinite;
 }
@@ -478,8 +511,118 @@ void DeviceMrsdc::step_mode1(RhsOp& f1, RhsOp& f2, const double* u0, double t_n,
   if (f2_end) d2d(f2_end, f2_last_, n, st);
 }
 
-void DeviceMrsdc::integrate_mode1(RhsOp& f1, RhsOp& f2, const double* u0, double t0, double t1,
-                                  int nsteps, double* u_out, SweepDiag& total) {
+// MrsdcStepper::step_mode2 (mrsdc.cpp:137-206) on the internal buffers.
+void DeviceMrsdc::run2(RhsOp& f1, RhsOp& f2, double t_n, double dt, bool have1, bool have2,
+                       SweepDiag& d) {
+  const int m1 = h_.coarse.intervals(), m2 = h_.fine.intervals();
+  const long long n = dim_;
+  const auto& t1 = h_.coarse.t;
+  const auto& t2 = h_.fine.t;
+  cudaStream_t st = f2.stream();
+  require(f1.stream() == st, "mrsdc: f1 and f2 must share a stream");
+  C_.resize(n);
+  W_.resize(n);
+  // provisional U at every fine node (mrsdc.cpp:49): mode 2 reads U_q1 as the
+  // Newton guess before the sweep has written it
+  for (int q = 1; q <= m2; ++q) d2d(u_[q], u_[0], n, st);
+  if (!have1) {
+    f1.eval_device(t_n, u_[0], f10_);
+    ++d.f1_evals;
+  }
+  if (!have2) {
+    f2.eval_device(t_n, u_[0], f20_);
+    ++d.f2_evals;
+  }
+  std::vector<const double*> o1(m1 + 1, f10_), n1(m1 + 1, f10_), o2(m2 + 1, f20_),
+      n2(m2 + 1, f20_);
+  const int ng = m1 + 1 + m2 + 1;
+  std::vector<double> w(static_cast<std::size_t>(m2) * ng);
+  for (int q = 0; q < m2; ++q) {
+    for (int j = 0; j <= m1; ++j) w[q * ng + j] = h_.s21(q, j);
+    for (int j = 0; j <= m2; ++j) w[q * ng + m1 + 1 + j] = h_.s22(q, j);
+  }
+  std::vector<double> qrow(ng);
+  for (int j = 0; j <= m1; ++j) qrow[j] = h_.q21(m2 - 1, j);
+  for (int j = 0; j <= m2; ++j) qrow[m1 + 1 + j] = h_.q22(m2 - 1, j);
+  SMC_CUDA(cudaMemsetAsync(res_.get(), 0, res_.size() * sizeof(double), st));
+  int collected = 0;
+  for (int k = 1; k <= iterations_; ++k) {
+    std::vector<double*>& s1 = (k % 2) ? f1a_ : f1b_;
+    std::vector<double*>& s2 = (k % 2) ? f2a_ : f2b_;
+    std::vector<const double*> g(o1.begin(), o1.end());
+    g.insert(g.end(), o2.begin(), o2.end());
+    launch_integrals(m2, so_.data(), ng, g.data(), w.data(), dt, n, st);
+    for (int p = 0; p < m1; ++p) {
+      const int q0 = h_.fine_of_coarse[p], q1 = h_.fine_of_coarse[p + 1];
+      const double dt1 = (t1[p + 1] - t1[p]) * dt;
+      const double t_right = t_n + t1[p + 1] * dt;
+      // backward-Euler-form correction at the right coarse node
+      launch_be_rhs(C_.get(), u_[q0], q1 - q0, so_.data() + q0, o1[p + 1], dt1, n, st);
+      NewtonReport rep;
+      newton_.solve(f1, t_right, dt1, C_.get(), u_[q1], W_.get(), stiff_, rep);
+      ++d.implicit_solves;
+      d.newton_f1_evals += rep.f_evals;
+      if (!rep.converged)
+        throw IntegrationFailure("mrsdc mode 2: Newton failed at coarse node " +
+                                 std::to_string(p + 1) + ", sweep " + std::to_string(k) +
+                                 ", residual " + std::to_string(rep.final_residual));
+      f1.eval_device(t_right, W_.get(), s1[p]);
+      n1[p + 1] = s1[p];
+      ++d.f1_evals;
+      for (int q = q0; q < q1; ++q) {
+        const double dtq = (t2[q + 1] - t2[q]) * dt;
+        const double* da[2];
+        const double* db[2];
+        double dc[2];
+        int nd = 0;
+        da[nd] = n1[p + 1], db[nd] = o1[p + 1], dc[nd] = dtq, ++nd;
+        if (n2[q] != o2[q]) da[nd] = n2[q], db[nd] = o2[q], dc[nd] = dtq, ++nd;
+        launch_sweep_update(u_[q + 1], u_[q], nd, da, db, dc, 0, nullptr, nullptr, dt, so_[q], n,
+                            st);
+        f2.eval_device(t_n + t2[q + 1] * dt, u_[q + 1], s2[q]);
+        n2[q + 1] = s2[q];
+        ++d.f2_evals;
+      }
+    }
+    std::vector<const double*> gn(n1.begin(), n1.end());
+    gn.insert(gn.end(), n2.begin(), n2.end());
+    launch_residual(u_[0], u_[m2], ng, gn.data(), qrow.data(), dt, n, res_.get() + 2 * (k - 1), st);
+    d.sweeps = k;
+    o1 = n1;
+    o2 = n2;
+    if (cutoff_ > 0.0) {
+      collect(res_, k - 1, 1, st, reduce_, d);
+      collected = k;
+      if (stalled(d.residuals, cutoff_)) {
+        d.early_stop = true;
+        break;
+      }
+    }
+  }
+  if (collected < d.sweeps) collect(res_, collected, d.sweeps - collected, st, reduce_, d);
+  f1_last_ = const_cast<double*>(o1[m1]);
+  f2_last_ = const_cast<double*>(o2[m2]);
+}
+
+void DeviceMrsdc::step_mode2(RhsOp& f1, RhsOp& f2, const double* u0, double t_n, double dt,
+                             const double* f01, const double* f02, double* u_out, double* f1_end,
+                             double* f2_end, SweepDiag& d) {
+  require(f1.dim() == f2.dim(), "mrsdc: f1/f2 dimension mismatch");
+  ensure(f1.dim());
+  const long long n = dim_;
+  cudaStream_t st = f2.stream();
+  d2d(u_[0], u0, n, st);
+  const bool h1 = f01 && reuse_first_, h2 = f02 && reuse_first_;
+  if (h1) d2d(f10_, f01, n, st);
+  if (h2) d2d(f20_, f02, n, st);
+  run2(f1, f2, t_n, dt, h1, h2, d);
+  d2d(u_out, u_[h_.fine.intervals()], n, st);
+  if (f1_end) d2d(f1_end, f1_last_, n, st);
+  if (f2_end) d2d(f2_end, f2_last_, n, st);
+}
+
+void DeviceMrsdc::integrate(int mode, RhsOp& f1, RhsOp& f2, const double* u0, double t0,
+                            double t1, int nsteps, double* u_out, SweepDiag& total) {
   require(nsteps >= 0, "integrate_mrsdc: negative step count");
   require(f1.dim() == f2.dim(), "mrsdc: f1/f2 dimension mismatch");
   ensure(f1.dim());
@@ -490,7 +633,11 @@ void DeviceMrsdc::integrate_mode1(RhsOp& f1, RhsOp& f2, const double* u0, double
   const double dt = (t1 - t0) / std::max(nsteps, 1);
   for (int step = 0; step < nsteps; ++step) {
     SweepDiag d;
-    run(f1, f2, t0 + step * dt, dt, step > 0 && reuse_first_, step > 0 && reuse_first_, d);
+    const bool reuse = step > 0 && reuse_first_;
+    if (mode == 2)
+      run2(f1, f2, t0 + step * dt, dt, reuse, reuse, d);
+    else
+      run(f1, f2, t0 + step * dt, dt, reuse, reuse, d);
     std::swap(u_[0], u_[m2]);
     for (auto* set : {&f1a_, &f1b_})
       for (auto& p : *set)
@@ -501,6 +648,16 @@ void DeviceMrsdc::integrate_mode1(RhsOp& f1, RhsOp& f2, const double* u0, double
     total.add(d);
   }
   d2d(u_out, u_[0], n, st);
+}
+
+void DeviceMrsdc::integrate_mode1(RhsOp& f1, RhsOp& f2, const double* u0, double t0, double t1,
+                                  int nsteps, double* u_out, SweepDiag& total) {
+  integrate(1, f1, f2, u0, t0, t1, nsteps, u_out, total);
+}
+
+void DeviceMrsdc::integrate_mode2(RhsOp& f1, RhsOp& f2, const double* u0, double t0, double t1,
+                                  int nsteps, double* u_out, SweepDiag& total) {
+  integrate(2, f1, f2, u0, t0, t1, nsteps, u_out, total);
 }
 
 }  // namespace smc

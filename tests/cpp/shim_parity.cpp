@@ -18,6 +18,7 @@
 #include "nsdc/quadrature.hpp"
 #include "nsdc/sdc.hpp"
 #include "nsdc/stencil.hpp"
+#include "nsdc/stiff.hpp"
 #include "nsdc_b200/nsdc_b200.hpp"
 
 namespace B = nsdc_b200;
@@ -110,6 +111,71 @@ int main() {
     check(std::fabs(u_b[0] - u_ref[0]) <= 1e-14 && d_b.f1_evals == d_ref.f1_evals &&
               d_b.f2_evals == d_ref.f2_evals,
           "integrate_mrsdc mode 1 split linear", std::fabs(u_b[0] - u_ref[0]));
+  }
+  // MRSDC mode 2 (f1 implicit, mrsdc.cpp:137-206) on the reference's stiff
+  // Prothero-Robinson split (mrsdc_test.cpp:23-35, acceptance_test.cpp:357-371),
+  // reference vs the mirror's drop-in signatures
+  {
+    const double sigma = 1.0e4;
+    nsdc::SplitRHS r;
+    r.f1 = [sigma](double t, const nsdc::Field& u, nsdc::Field& out) {
+      out.resize(u.size());
+      for (std::size_t i = 0; i < u.size(); ++i) out[i] = -sigma * (u[i] - std::cos(t));
+    };
+    r.f2 = [](double t, const nsdc::Field& u, nsdc::Field& out) {
+      out.assign(u.size(), -std::sin(t));
+    };
+    r.f1_stiffness = nsdc::SplitRHS::Stiffness::Implicit;
+    auto h = nsdc::build_hierarchy(nsdc::gauss_lobatto(3), nsdc::TypeB{nsdc::gauss_lobatto(5)});
+    nsdc::StepControls c;
+    c.num_iterations = 6;
+    c.residual_ratio_cutoff = 0.0;
+    nsdc::StiffOptions so;
+    so.rtol = 1e-12;
+    so.atol = 1e-13;
+    auto [u_ref, d_ref] = nsdc::integrate_mrsdc(r, {1.0}, 0.0, 0.2, 10, h, c, so);
+
+    B::SplitRHS s{r.f1, r.f2, B::SplitRHS::Stiffness::Implicit};
+    auto bh = B::build_hierarchy(B::gauss_lobatto(3), B::TypeB{B::gauss_lobatto(5)});
+    B::StepControls bc;
+    bc.num_iterations = 6;
+    bc.residual_ratio_cutoff = 0.0;
+    B::StiffOptions bso;
+    bso.rtol = 1e-12;
+    bso.atol = 1e-13;
+    auto [u_b, d_b] = B::integrate_mrsdc(s, {1.0}, 0.0, 0.2, 10, bh, bc, bso);
+    check(std::fabs(u_b[0] - u_ref[0]) <= 1e-10 * std::fabs(u_ref[0]) &&
+              d_b.implicit_solves == d_ref.implicit_solves && d_b.f1_evals == d_ref.f1_evals &&
+              d_b.f2_evals == d_ref.f2_evals,
+          "integrate_mrsdc mode 2 stiff oscillator", std::fabs(u_b[0] - u_ref[0]));
+    bool same_tables = bh.fine.nodes == h.fine.nodes && bh.fine_of_coarse == h.fine_of_coarse &&
+                       bh.p_map == h.p_map;
+    for (int q = 0; q < h.s22.rows; ++q)
+      for (int j = 0; j < h.s22.cols; ++j) same_tables = same_tables && bh.s22(q, j) == h.s22(q, j);
+    check(same_tables, "build_hierarchy tables bitwise");
+
+    // Newton failure names the coarse node (mrsdc_test.cpp:215-228)
+    B::SplitRHS bad{[](double, const B::Field& u, B::Field& out) { out = {u[0] * u[0]}; },
+                    [](double, const B::Field& u, B::Field& out) { out.assign(u.size(), 0.0); },
+                    B::SplitRHS::Stiffness::Implicit};
+    std::string msg;
+    try {
+      B::mrsdc_step_mode2(bad, {5.0}, 0.0, 1.0,
+                          B::build_hierarchy(B::gauss_lobatto(3), B::TypeB{B::gauss_lobatto(2)}),
+                          bc, B::StiffOptions{});
+    } catch (const B::IntegrationError& e) {
+      msg = e.what();
+    }
+    check(msg.find("coarse node 1") != std::string::npos, "mode 2 Newton failure -> IntegrationError");
+
+    // solve_backward_euler (stiff.cpp:34-76) with a report
+    nsdc::NewtonReport rr;
+    nsdc::Field wr = nsdc::solve_backward_euler(r.f1, 0.1, 0.05, {0.5}, {0.5}, so, &rr);
+    B::NewtonReport br;
+    B::Field wb = B::solve_backward_euler(s.f1, 0.1, 0.05, {0.5}, {0.5}, bso, &br);
+    check(wb[0] == wr[0] && br.iterations == rr.iterations && br.f_evals == rr.f_evals &&
+              br.converged == rr.converged,
+          "solve_backward_euler bitwise", std::fabs(wb[0] - wr[0]));
   }
   // error behaviour mirrors the reference (pde_test.cpp:243-263)
   {
