@@ -574,7 +574,7 @@ void set_smem(K kern, std::size_t bytes) {
 
 template <int S>
 void rhs_v2(const Geo& g, const double* U, const double* F, double* A, double* GR, double* MX,
-            double* out, const StencilM& M, cudaStream_t st) {
+            double* SC, double* out, const StencilM& M, cudaStream_t st) {
   static bool configured = false;
   const std::size_t sm = sizeof(DirSmem);
   if (!configured) {
@@ -583,21 +583,31 @@ void rhs_v2(const Geo& g, const double* U, const double* F, double* A, double* G
     configured = true;
   }
   const int allp = g.nz + 2 * g.G;
-  ns_phase_a<0, S><<<dir_grid<0>(g, allp), DT_THREADS, sm, st>>>(U, F, A, GR, out, g, M, -g.G, 1);
+  const long long n = g.plane * g.nz;
+  // scratch SC (54 arrays of n): phase A of directions 1, 2 -> [NA | HY] x 2,
+  // then, once ns_mixed_fields has added them in, phase B's three blocks
+  double* na1 = SC;
+  double* hy1 = SC + 13 * n;
+  double* na2 = SC + 27 * n;
+  double* hy2 = SC + 40 * n;
+  ns_phase_a<0, S><<<dir_grid<0>(g, allp), DT_THREADS, sm, st>>>(U, F, A, A, GR, out, g, M, -g.G);
   SMC_CHECK_LAUNCH();
-  ns_phase_a<1, S><<<dir_grid<1>(g, allp), DT_THREADS, sm, st>>>(U, F, A, GR, out, g, M, -g.G, 0);
+  ns_phase_a<1, S><<<dir_grid<1>(g, allp), DT_THREADS, sm, st>>>(U, F, na1, A, GR, hy1, g, M, -g.G);
   SMC_CHECK_LAUNCH();
-  ns_phase_a<2, S><<<dir_grid<2>(g, allp), DT_THREADS, sm, st>>>(U, F, A, GR, out, g, M, 0, 0);
+  ns_phase_a<2, S><<<dir_grid<2>(g, allp), DT_THREADS, sm, st>>>(U, F, na2, A, GR, hy2, g, M, 0);
   SMC_CHECK_LAUNCH();
-  ns_mixed_fields<<<blocks(g.plane * allp), 256, 0, st>>>(F, GR, A, MX, g);
+  ns_mixed_fields<<<blocks(g.plane * allp), 256, 0, st>>>(F, GR, A, MX, SC, out, g);
   SMC_CHECK_LAUNCH();
-  ns_phase_b<0><<<dir_grid<0>(g, g.nz), DT_THREADS, sm, st>>>(F, A, MX, out, g);
+  double* pb0 = SC;
+  double* pb1 = SC + 13 * n;
+  double* pb2 = SC + 26 * n;
+  ns_phase_b<0><<<dir_grid<0>(g, g.nz), DT_THREADS, sm, st>>>(F, A, MX, pb0, g);
   SMC_CHECK_LAUNCH();
-  ns_phase_b<1><<<dir_grid<1>(g, g.nz), DT_THREADS, sm, st>>>(F, A, MX, out, g);
+  ns_phase_b<1><<<dir_grid<1>(g, g.nz), DT_THREADS, sm, st>>>(F, A, MX, pb1, g);
   SMC_CHECK_LAUNCH();
-  ns_phase_b<2><<<dir_grid<2>(g, g.nz), DT_THREADS, sm, st>>>(F, A, MX, out, g);
+  ns_phase_b<2><<<dir_grid<2>(g, g.nz), DT_THREADS, sm, st>>>(F, A, MX, pb2, g);
   SMC_CHECK_LAUNCH();
-  ns_assemble2<<<blocks(g.plane * g.nz), 256, 0, st>>>(F, A, out, g);
+  ns_assemble2<<<blocks(n), 256, 0, st>>>(F, A, pb0, pb1, pb2, out, g);
   SMC_CHECK_LAUNCH();
 }
 
@@ -617,6 +627,7 @@ NsWorkspace::NsWorkspace(const NsBox& box, double dx, double dy, double dz, cons
   acc_.resize(static_cast<std::size_t>(A_COUNT) * box.cells());
   mixed_.resize(static_cast<std::size_t>(MX_COUNT) * box.field_len());
   grad_.resize(static_cast<std::size_t>(9) * box.field_len());
+  if (!ns_v1()) scratch_.resize(static_cast<std::size_t>(54) * box.cells());
 }
 
 static Geo make_geo(const NsBox& b, const double* d) {
@@ -642,9 +653,9 @@ void NsWorkspace::rhs(const double* U, double* out, int part, cudaStream_t st) {
   SMC_CHECK_LAUNCH();
   if (part != kNsChem && !ns_v1()) {
     if (s_ == 4)
-      rhs_v2<4>(g, U, F, A, grad_.get(), mixed_.get(), out, M_, st);
+      rhs_v2<4>(g, U, F, A, grad_.get(), mixed_.get(), scratch_.get(), out, M_, st);
     else
-      rhs_v2<3>(g, U, F, A, grad_.get(), mixed_.get(), out, M_, st);
+      rhs_v2<3>(g, U, F, A, grad_.get(), mixed_.get(), scratch_.get(), out, M_, st);
   } else if (part != kNsChem) {
     hyp_kernel<<<blocks(n), 256, 0, st>>>(U, F, out, g, 1);
     SMC_CHECK_LAUNCH();
