@@ -156,6 +156,9 @@ inline int family_of(const NodeSet& s) {
     throw std::invalid_argument("device steppers take simple node sets");
   return s.kind == NodeKind::GaussLobatto ? SMC_GAUSS_LOBATTO : SMC_CLENSHAW_CURTIS;
 }
+struct TypeA {
+  NodeSet fine;  // must contain every coarse node
+};
 struct TypeB {
   NodeSet inner;
 };
@@ -163,7 +166,7 @@ struct TypeC {
   NodeSet inner;
   int repeats = 1;
 };
-using FineSpec = std::variant<TypeB, TypeC>;
+using FineSpec = std::variant<TypeA, TypeB, TypeC>;
 
 // matrix.hpp: dense row-major matrix
 struct Matrix {
@@ -177,7 +180,8 @@ struct Matrix {
 
 // MultirateHierarchy (quadrature.hpp:70-77) from the library's builder
 // (quadrature.cpp:178-248); `spec` records what the device stepper is built
-// from (TypeB == TypeC with one repeat).
+// from (TypeB == TypeC with one repeat, TypeA == repeats 0 with the fine set
+// as `inner`).
 struct MultirateHierarchy {
   NodeSet coarse;
   NodeSet fine;
@@ -188,8 +192,11 @@ struct MultirateHierarchy {
   TypeC spec;
 };
 inline MultirateHierarchy build_hierarchy(const NodeSet& coarse, const FineSpec& fs) {
-  const TypeC c = std::holds_alternative<TypeB>(fs) ? TypeC{std::get<TypeB>(fs).inner, 1}
-                                                    : std::get<TypeC>(fs);
+  const TypeC c = std::holds_alternative<TypeA>(fs)   ? TypeC{std::get<TypeA>(fs).fine, 0}
+                  : std::holds_alternative<TypeB>(fs) ? TypeC{std::get<TypeB>(fs).inner, 1}
+                                                      : std::get<TypeC>(fs);
+  if (std::holds_alternative<TypeC>(fs) && std::get<TypeC>(fs).repeats < 1)
+    throw std::invalid_argument("build_hierarchy: repeats must be >= 1");
   MultirateHierarchy h;
   h.coarse = coarse;
   h.spec = c;

@@ -208,9 +208,11 @@ int smc_solve_backward_euler(smc_rhs* f, double t, double beta, const double* c,
 int smc_nodes(int family, int n, double* t);
 /* integration_matrices — core/src/quadrature.cpp:134-158; q, s: (n-1) x n */
 int smc_integration_matrices(int family, int n, double* q, double* s);
-/* build_hierarchy(coarse, TypeB{inner}) (repeats 1) or TypeC{inner, repeats}
- * — core/src/quadrature.cpp:178-248.  *m2p1 receives the fine node count;
- * arrays may be NULL (query), else sized for m2p1 = 1 + (nc-1)*repeats*(ni-1). */
+/* build_hierarchy(coarse, TypeB{inner}) (repeats 1), TypeC{inner, repeats}
+ * (repeats > 1) or TypeA{inner} (repeats 0: inner is the fine set and must
+ * contain every coarse node) — core/src/quadrature.cpp:178-248.  *m2p1
+ * receives the fine node count; arrays may be NULL (query), else sized for
+ * m2p1 (1 + (nc-1)*repeats*(ni-1) for TypeB/C, ni for TypeA). */
 int smc_build_hierarchy(int coarse_family, int coarse_nodes, int inner_family, int inner_nodes,
                         int repeats, int* m2p1, double* fine, double* q21, double* s21,
                         double* q22, double* s22, int* fine_of_coarse, int* p_map);
@@ -230,7 +232,8 @@ int smc_sdc_set_reducer(smc_sdc* s, smc_reduce_fn fn, void* ctx);
 int smc_sdc_destroy(smc_sdc* s);
 
 /* MrsdcStepper(MultirateHierarchy, StepControls) with the hierarchy
- * build_hierarchy(coarse, TypeB/TypeC{inner}) — core/include/nsdc/mrsdc.hpp:51-82. */
+ * build_hierarchy(coarse, TypeA/TypeB/TypeC{inner}) (repeats as in
+ * smc_build_hierarchy) — core/include/nsdc/mrsdc.hpp:51-82. */
 int smc_mrsdc_create(int coarse_family, int coarse_nodes, int inner_family, int inner_nodes,
                      int repeats, int iterations, double residual_ratio_cutoff,
                      int reuse_first_eval, smc_mrsdc** out);

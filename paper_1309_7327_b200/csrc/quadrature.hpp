@@ -41,7 +41,8 @@ Nodes gauss_lobatto(int n);
 Nodes clenshaw_curtis(int n);
 Nodes make_nodes(int family, int n);  // 0 = Gauss-Lobatto, 1 = Clenshaw-Curtis
 SweepTables integration_matrices(const Nodes& nodes);
-// TypeB (repeats == 1) / TypeC fine levels (quadrature.hpp:56-67).
+// TypeB (repeats == 1) / TypeC fine levels (quadrature.hpp:56-67); repeats
+// == 0 is TypeA: `inner` is the fine set and must contain the coarse nodes.
 Hierarchy build_hierarchy(const Nodes& coarse, const Nodes& inner, int repeats);
 
 }  // namespace smc
