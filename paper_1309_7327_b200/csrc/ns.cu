@@ -584,8 +584,8 @@ void rhs_v2(const Geo& g, const double* U, const double* F, double* A, double* G
   }
   const int allp = g.nz + 2 * g.G;
   const long long n = g.plane * g.nz;
-  // scratch SC (54 arrays of n): phase A of directions 1, 2 -> [NA | HY] x 2,
-  // then, once ns_mixed_fields has added them in, phase B's three blocks
+  // scratch SC (93 arrays of n): phase A of directions 1, 2 -> [NA | HY] x 2
+  // (54), phase B of the three directions (3 x 13); ns_assemble2 adds them in
   double* na1 = SC;
   double* hy1 = SC + 13 * n;
   double* na2 = SC + 27 * n;
@@ -596,18 +596,15 @@ void rhs_v2(const Geo& g, const double* U, const double* F, double* A, double* G
   SMC_CHECK_LAUNCH();
   ns_phase_a<2, S><<<dir_grid<2>(g, allp), DT_THREADS, sm, st>>>(U, F, na2, A, GR, hy2, g, M, 0);
   SMC_CHECK_LAUNCH();
-  ns_mixed_fields<<<blocks(g.plane * allp), 256, 0, st>>>(F, GR, A, MX, SC, out, g);
+  ns_mixed_fields<<<blocks(g.plane * allp), 256, 0, st>>>(F, GR, A, MX, g);
   SMC_CHECK_LAUNCH();
-  double* pb0 = SC;
-  double* pb1 = SC + 13 * n;
-  double* pb2 = SC + 26 * n;
-  ns_phase_b<0><<<dir_grid<0>(g, g.nz), DT_THREADS, sm, st>>>(F, A, MX, pb0, g);
+  ns_phase_b<0><<<dir_grid<0>(g, g.nz), DT_THREADS, sm, st>>>(F, A, MX, SC + 54 * n, g);
   SMC_CHECK_LAUNCH();
-  ns_phase_b<1><<<dir_grid<1>(g, g.nz), DT_THREADS, sm, st>>>(F, A, MX, pb1, g);
+  ns_phase_b<1><<<dir_grid<1>(g, g.nz), DT_THREADS, sm, st>>>(F, A, MX, SC + 67 * n, g);
   SMC_CHECK_LAUNCH();
-  ns_phase_b<2><<<dir_grid<2>(g, g.nz), DT_THREADS, sm, st>>>(F, A, MX, pb2, g);
+  ns_phase_b<2><<<dir_grid<2>(g, g.nz), DT_THREADS, sm, st>>>(F, A, MX, SC + 80 * n, g);
   SMC_CHECK_LAUNCH();
-  ns_assemble2<<<blocks(n), 256, 0, st>>>(F, A, pb0, pb1, pb2, out, g);
+  ns_assemble2<<<blocks(n), 256, 0, st>>>(F, A, SC, out, g);
   SMC_CHECK_LAUNCH();
 }
 
@@ -627,7 +624,7 @@ NsWorkspace::NsWorkspace(const NsBox& box, double dx, double dy, double dz, cons
   acc_.resize(static_cast<std::size_t>(A_COUNT) * box.cells());
   mixed_.resize(static_cast<std::size_t>(MX_COUNT) * box.field_len());
   grad_.resize(static_cast<std::size_t>(9) * box.field_len());
-  if (!ns_v1()) scratch_.resize(static_cast<std::size_t>(54) * box.cells());
+  if (!ns_v1()) scratch_.resize(static_cast<std::size_t>(93) * box.cells());
 }
 
 static Geo make_geo(const NsBox& b, const double* d) {

@@ -44,7 +44,7 @@ class NsWorkspace {
   DevBuf acc_;    // narrow-stencil accumulators + gradients (interior)
   DevBuf mixed_;  // eta d_i u_j, lam2 sum d_j u_j (all planes)
   DevBuf grad_;   // d_j u_i (all planes; v2 pipeline)
-  DevBuf scratch_;  // v2: per-direction results (54 interior arrays), summed in order
+  DevBuf scratch_;  // v2: per-direction results (93 interior arrays), summed in order
 };
 
 // Conserved state from primitives (T, p, u, v, w, Y_k), n cells, device ptrs.
