@@ -4,11 +4,14 @@
 // H_{i+1/2} = sum_m a_{i+m} sum_n M_mn u_{i+n} computed once in the fixed
 // order of stencil_kernel.hpp:13-25, then differenced as pde.cpp:118-120 —
 // laid out so that the FP64 pipe, not the issue slot, is the limit:
-//   * CTA tile 64 (x) x 8 (y), 8 warps; a thread owns 2 adjacent x cells, so
-//     its x window comes from 5 conflict-free 16-byte LDS per field and its
-//     y window from 8 LDS.128 that serve both columns;
+//   * CTA tile 32 (x) x 8 (y) of 128 threads (default; 64 x 8 of 256 threads
+//     with SMC_NARROW_FX=64), a thread owns 2 adjacent x cells, so its x
+//     window comes from 5 conflict-free 16-byte LDS per field and its y
+//     window from 8 LDS.128 that serve both columns; at <= 168 registers
+//     three CTAs (12 warps) share an SM;
 //   * only the 26 upper-half entries of M are read (antisymmetry, see
-//     narrow_iface), so they stay in uniform registers;
+//     narrow_iface), so they stay in uniform registers; the two cells'
+//     interfaces are formed in lockstep (narrow_iface2) for ILP;
 //   * the z window (2S planes of U and a for the 2 columns) lives in
 //     registers and is shifted by moves: a compact loop body keeps the
 //     instruction cache warm (the 2S-fold unrolled variant measured slower);
@@ -18,13 +21,14 @@
 //     precomputed, the z offset advances incrementally;
 //   * one CTA barrier per plane (it publishes the y interfaces and, as every
 //     thread first waits for its own copies of plane k+1, the next tile);
-//     deferring the difference-and-store past the next plane's interfaces
-//     measured slower (register pressure), so it follows the barrier;
 //   * x neighbours' interfaces come by warp shuffle, y neighbours' through
-//     shared memory (double-buffered by plane parity); the 72 extra
-//     interfaces per plane (x0-1/2 of each row, y0-1/2 of each column) are
-//     packed into three warp passes on three different SM sub-partitions.
-// Requirements (else narrow.cu's general kernel runs): nx % 64 == 0,
+//     shared memory (double-buffered by plane parity); the tile-edge
+//     interfaces (x0-1/2 of each row, y0-1/2 of each column) are packed into
+//     warps 1-3.
+// Measured variants kept out: 2 CTAs/SM at 128 registers
+// with the y window split (spills), z interfaces formed last with the
+// leading-plane load issued at the step start, a persistent grid.
+// Requirements (else narrow.cu's general kernel runs): nx % tile width == 0,
 // ny % 8 == 0, 16-byte aligned fields.
 #include <algorithm>
 #include <cstdint>
@@ -37,20 +41,31 @@
 namespace smc {
 namespace {
 
-constexpr int FX = 64;       // tile x
-constexpr int FY = 8;        // tile y (= warps)
-constexpr int FT = 256;      // threads
-constexpr int HALO = 4;      // staged halo (>= S)
-constexpr int SW = FX + 2 * HALO;   // 72 tile columns
-constexpr int SH = FY + 2 * HALO;   // 16 tile rows
-constexpr int CHUNKS = SH * SW / 2; // 16-byte chunks per field per plane (576)
-constexpr int CPT = (CHUNKS + FT - 1) / FT;  // 3 (last partial)
-constexpr int NBUF = 3;
+// Tile geometry.  FXT = tile width in x: 64 (256 threads, one CTA per SM at
+// up to 255 registers) or 32 (128 threads, three CTAs per SM at <= 168
+// registers: 12 warps per SM instead of 8).  A thread owns 2 adjacent x
+// cells; LPR threads cover one tile row.
+template <int FXT>
+struct NG {
+  static constexpr int FX = FXT;
+  static constexpr int FY = 8;
+  static constexpr int LPR = FX / 2;
+  static constexpr int FT = LPR * FY;
+  static constexpr int HALO = 4;                       // staged halo (>= S)
+  static constexpr int SW = FX + 2 * HALO;             // tile columns
+  static constexpr int SH = FY + 2 * HALO;             // tile rows
+  static constexpr int CHUNKS = SH * SW / 2;           // 16-byte chunks per field per plane
+  static constexpr int CPT = (CHUNKS + FT - 1) / FT;   // per thread (last partial)
+  static constexpr int NBUF = 3;
+  static constexpr int OCC = FXT == 64 ? 1 : 3;
+};
 
+template <int FXT>
 struct FastSmem {
-  double tile[NBUF][2][SH * SW];   // u, a
-  double hy[2][FY + 1][FX];        // y interfaces, double-buffered by plane parity
-  double hxe[2][FY];               // x0 - 1/2 interfaces
+  using G = NG<FXT>;
+  double tile[G::NBUF][2][G::SH * G::SW];  // u, a
+  double hy[2][G::FY + 1][G::FX];          // y interfaces, double-buffered by plane parity
+  double hxe[2][G::FY];                    // x0 - 1/2 interfaces
 };
 
 __device__ __forceinline__ void cp16(void* dst, const void* src) {
@@ -67,18 +82,21 @@ __device__ __forceinline__ double2 lds2(const double* p) {
   return *reinterpret_cast<const double2*>(p);
 }
 
-// One (tile, [k0, k1)) segment of the z-march.  OCC = CTAs per SM the
-// kernel is built for: OCC 2 forms the y interfaces one column at a time
-// (half the live y window) to fit 128 registers.
-template <int S, int OCC, bool LATE>
-__device__ __forceinline__ void march_segment(FastSmem& sm, const NarrowArgs& p,
+// One (tile, [k0, k1)) segment of the z-march.
+template <int S, int FXT>
+__device__ __forceinline__ void march_segment(FastSmem<FXT>& sm, const NarrowArgs& p,
                                               const StencilM& M, int tile, int k0, int k1) {
+  using G = NG<FXT>;
+  constexpr int FX = G::FX, FY = G::FY, FT = G::FT, HALO = G::HALO, SW = G::SW;
+  constexpr int CHUNKS = G::CHUNKS, CPT = G::CPT, NBUF = G::NBUF, LPR = G::LPR;
   constexpr int WIN = 2 * S;
   const int tiles_x = p.nx / FX;
   const int x0 = (tile % tiles_x) * FX;
   const int y0 = (tile / tiles_x) * FY;
   const int lane = threadIdx.x & 31;
-  const int w = threadIdx.x >> 5;
+  const int wid = threadIdx.x >> 5;
+  const int row = threadIdx.x / LPR;  // tile row of my cells
+  const int cp = threadIdx.x % LPR;   // my column pair
   const long long plane = static_cast<long long>(p.nx) * p.ny;
   const long long zspan = plane * p.nz;
 
@@ -101,9 +119,9 @@ __device__ __forceinline__ void march_segment(FastSmem& sm, const NarrowArgs& p,
 #pragma unroll
   for (int i = 0; i < CPT; ++i) {
     const int c = threadIdx.x + i * FT;
-    const int row = c / (SW / 2), col = 2 * (c - row * (SW / 2));
+    const int r = c / (SW / 2), col = 2 * (c - r * (SW / 2));
     const int gx = wrap(x0 - HALO + col, p.nx);
-    const int gy = wrap(y0 - HALO + row, p.ny);
+    const int gy = wrap(y0 - HALO + r, p.ny);
     soff[i] = c < CHUNKS ? gy * p.nx + gx : 0;
   }
   auto stage = [&](int buf, long long po) {
@@ -118,15 +136,15 @@ __device__ __forceinline__ void march_segment(FastSmem& sm, const NarrowArgs& p,
     commit();
   };
 
-  // own columns: x0 + 2*lane + {0, 1}, row y0 + w
-  const int col_off = (y0 + w) * p.nx + x0 + 2 * lane;
+  // own columns: x0 + 2*cp + {0, 1}, row y0 + row
+  const int col_off = (y0 + row) * p.nx + x0 + 2 * cp;
   auto ld2 = [&](const double* base, long long o) {
     return __ldg(reinterpret_cast<const double2*>(base + o + col_off));
   };
 
   // z window (2 columns): slot j holds plane k - S + 1 + j at step k
   double2 wu[WIN], wa[WIN];
-  double2 pf_u[2], pf_a[2];  // (LATE: unused) leading planes prefetched two ahead
+  double2 pf_u[2], pf_a[2];  // leading planes prefetched two ahead
   {
     long long o = zoff(k0 - S);
 #pragma unroll
@@ -141,11 +159,11 @@ __device__ __forceinline__ void march_segment(FastSmem& sm, const NarrowArgs& p,
   long long o_pf = zoff(k0 + S);
 #pragma unroll
   for (int j = 0; j < 2; ++j) {
-    if (!LATE && k0 + j < k1) {
+    if (k0 + j < k1) {
       pf_u[j] = ld2(p.u, o_pf);
       pf_a[j] = ld2(p.cz, o_pf);
     }
-    if (!LATE) o_pf = zadv(o_pf);
+    o_pf = zadv(o_pf);
   }
   // centre-plane staging: planes k0, k0 + 1 now (buffers 0, 1)
   long long o_st = zoff(k0);
@@ -177,9 +195,9 @@ __device__ __forceinline__ void march_segment(FastSmem& sm, const NarrowArgs& p,
   auto finish = [&](int hb, double hx0, double hx1, double hz0, double hz1, double hzl0,
                     double hzl1, long long oo) {
     double hxl = __shfl_up_sync(0xffffffffu, hx1, 1);
-    if (lane == 0) hxl = sm.hxe[hb][w];
-    const double2 yu = lds2(&sm.hy[hb][w][2 * lane]);
-    const double2 yd = lds2(&sm.hy[hb][w + 1][2 * lane]);
+    if (cp == 0) hxl = sm.hxe[hb][row];
+    const double2 yu = lds2(&sm.hy[hb][row][2 * cp]);
+    const double2 yd = lds2(&sm.hy[hb][row + 1][2 * cp]);
     double o0 = __dmul_rn(__dsub_rn(hx0, hxl), idx2);
     double o1 = __dmul_rn(__dsub_rn(hx1, hx0), idx2);
     o0 = __dadd_rn(o0, __dmul_rn(__dsub_rn(yd.x, yu.x), idy2));
@@ -194,47 +212,37 @@ __device__ __forceinline__ void march_segment(FastSmem& sm, const NarrowArgs& p,
     const int t = k - k0;
     const int buf = t % NBUF;
     const int hb = t & 1;
-    // z window: LATE issues the leading plane k + S now and forms the z
-    // interfaces after x and y (the load is hidden behind them, no prefetch
-    // registers); otherwise the plane prefetched two steps ago is shifted in.
-    double2 lead_u, lead_a;
-    if constexpr (LATE) {
-      lead_u = ld2(p.u, o_pf);
-      lead_a = ld2(p.cz, o_pf);
-      o_pf = zadv(o_pf);
-    } else {
+    // z window: shift in the plane prefetched two steps ago
 #pragma unroll
-      for (int j = 0; j + 1 < WIN; ++j) wu[j] = wu[j + 1], wa[j] = wa[j + 1];
-      wu[WIN - 1] = pf_u[0];
-      wa[WIN - 1] = pf_a[0];
-      pf_u[0] = pf_u[1];
-      pf_a[0] = pf_a[1];
-      if (k + 2 < k1) {
-        pf_u[1] = ld2(p.u, o_pf);
-        pf_a[1] = ld2(p.cz, o_pf);
-        o_pf = zadv(o_pf);
-      }
+    for (int j = 0; j + 1 < WIN; ++j) wu[j] = wu[j + 1], wa[j] = wa[j + 1];
+    wu[WIN - 1] = pf_u[0];
+    wa[WIN - 1] = pf_a[0];
+    pf_u[0] = pf_u[1];
+    pf_a[0] = pf_a[1];
+    if (k + 2 < k1) {
+      pf_u[1] = ld2(p.u, o_pf);
+      pf_a[1] = ld2(p.cz, o_pf);
+      o_pf = zadv(o_pf);
     }
     const double* tu = sm.tile[buf][0];
     const double* ta = sm.tile[buf][1];
     double hz0, hz1;
-    auto z_interfaces = [&]() {
+    {
       double a0[WIN], u0[WIN], a1[WIN], u1[WIN];
 #pragma unroll
       for (int j = 0; j < WIN; ++j) a0[j] = wa[j].x, u0[j] = wu[j].x, a1[j] = wa[j].y, u1[j] = wu[j].y;
       narrow_iface2<S>(a0, u0, a1, u1, M, hz0, hz1);
-    };
-    if constexpr (!LATE) z_interfaces();
-    // ---- x interfaces x+1/2 for my two cells (row HALO + w)
+    }
+    // ---- x interfaces x+1/2 for my two cells (row HALO + row)
     double hx0, hx1;
     {
-      // values at tile columns 2*lane + HALO - S + 1 + j
+      // values at tile columns 2*cp + HALO - S + 1 + j
       constexpr int NV = WIN + 2;  // loaded in pairs
       constexpr int BASE = HALO - S + 1 - ((HALO - S + 1) & 1);  // even start
       constexpr int OFF = (HALO - S + 1) - BASE;                 // 0 or 1
       double ua[NV], aa[NV];
-      const double* ru = tu + (HALO + w) * SW + 2 * lane + BASE;
-      const double* ra = ta + (HALO + w) * SW + 2 * lane + BASE;
+      const double* ru = tu + (HALO + row) * SW + 2 * cp + BASE;
+      const double* ra = ta + (HALO + row) * SW + 2 * cp + BASE;
 #pragma unroll
       for (int j = 0; j < NV / 2; ++j) {
         const double2 vu = lds2(ru + 2 * j), va = lds2(ra + 2 * j);
@@ -244,43 +252,31 @@ __device__ __forceinline__ void march_segment(FastSmem& sm, const NarrowArgs& p,
       narrow_iface2<S>(aa + OFF, ua + OFF, aa + OFF + 1, ua + OFF + 1, M, hx0, hx1);
     }
     // ---- y interfaces y+1/2 for my two columns
-    if constexpr (OCC == 2) {
-#pragma unroll
-      for (int col = 0; col < 2; ++col) {
-        double uc[WIN], ac[WIN];
-#pragma unroll
-        for (int j = 0; j < WIN; ++j) {
-          const int row = HALO + w - S + 1 + j;
-          uc[j] = tu[row * SW + HALO + 2 * lane + col];
-          ac[j] = ta[row * SW + HALO + 2 * lane + col];
-        }
-        sm.hy[hb][w + 1][2 * lane + col] = narrow_iface<S>(ac, uc, M);
-      }
-    } else {
+    {
       double u0[WIN], a0[WIN], u1[WIN], a1[WIN];
 #pragma unroll
       for (int j = 0; j < WIN; ++j) {
-        const int row = HALO + w - S + 1 + j;
-        const double2 vu = lds2(tu + row * SW + HALO + 2 * lane);
-        const double2 va = lds2(ta + row * SW + HALO + 2 * lane);
+        const int r = HALO + row - S + 1 + j;
+        const double2 vu = lds2(tu + r * SW + HALO + 2 * cp);
+        const double2 va = lds2(ta + r * SW + HALO + 2 * cp);
         u0[j] = vu.x, u1[j] = vu.y, a0[j] = va.x, a1[j] = va.y;
       }
       double y0v, y1v;
       narrow_iface2<S>(a0, u0, a1, u1, M, y0v, y1v);
-      *reinterpret_cast<double2*>(&sm.hy[hb][w + 1][2 * lane]) = make_double2(y0v, y1v);
+      *reinterpret_cast<double2*>(&sm.hy[hb][row + 1][2 * cp]) = make_double2(y0v, y1v);
     }
     // ---- extra interfaces: y0 - 1/2 of the even columns (warp 1), of the
     //      odd columns (warp 2), x0 - 1/2 of each row (warp 3)
-    if (w == 1 || w == 2) {
-      const int col = HALO + 2 * lane + (w - 1);
+    if ((wid == 1 || wid == 2) && lane < LPR) {
+      const int col = HALO + 2 * lane + (wid - 1);
       double uu[WIN], aa[WIN];
 #pragma unroll
       for (int j = 0; j < WIN; ++j) {
         uu[j] = tu[(HALO - S + j) * SW + col];
         aa[j] = ta[(HALO - S + j) * SW + col];
       }
-      sm.hy[hb][0][2 * lane + (w - 1)] = narrow_iface<S>(aa, uu, M);
-    } else if (w == 3 && lane < FY) {
+      sm.hy[hb][0][2 * lane + (wid - 1)] = narrow_iface<S>(aa, uu, M);
+    } else if (wid == 3 && lane < FY) {
       double uu[WIN], aa[WIN];
 #pragma unroll
       for (int j = 0; j < WIN; ++j) {
@@ -288,13 +284,6 @@ __device__ __forceinline__ void march_segment(FastSmem& sm, const NarrowArgs& p,
         aa[j] = ta[(HALO + lane) * SW + HALO - S + j];
       }
       sm.hxe[hb][lane] = narrow_iface<S>(aa, uu, M);
-    }
-    if constexpr (LATE) {
-#pragma unroll
-      for (int j = 0; j + 1 < WIN; ++j) wu[j] = wu[j + 1], wa[j] = wa[j + 1];
-      wu[WIN - 1] = lead_u;
-      wa[WIN - 1] = lead_a;
-      z_interfaces();
     }
     // ---- stage plane k + 2 into the buffer of plane k - 1 (all of its
     //      readers passed the previous barrier), then make plane k + 1 ready
@@ -320,26 +309,27 @@ __device__ __forceinline__ void march_segment(FastSmem& sm, const NarrowArgs& p,
 // co-scheduled CTAs are x/y neighbours at the same z and tile halos hit in
 // L2.  Persistent grid: CTA b owns the contiguous range [b*L/G, (b+1)*L/G)
 // of L = tile * nplanes + plane (one wave, equal work to within a plane).
-template <int S, int OCC, bool LATE>
-__global__ void __launch_bounds__(FT, OCC) narrow3d_fast(const NarrowArgs p, const StencilM M,
-                                                         int chunked) {
+template <int S, int FXT>
+__global__ void __launch_bounds__(NG<FXT>::FT, NG<FXT>::OCC)
+    narrow3d_fast(const NarrowArgs p, const StencilM M, int chunked) {
+  using G = NG<FXT>;
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  FastSmem& sm = *reinterpret_cast<FastSmem*>(smem_raw);
+  FastSmem<FXT>& sm = *reinterpret_cast<FastSmem<FXT>*>(smem_raw);
   const int kend = p.kend < 0 ? p.nz : p.kend;
   if (chunked) {
     const int k0 = p.kbeg + blockIdx.y * p.kc;
-    march_segment<S, OCC, LATE>(sm, p, M, blockIdx.x, k0, min(k0 + p.kc, kend));
+    march_segment<S, FXT>(sm, p, M, blockIdx.x, k0, min(k0 + p.kc, kend));
     return;
   }
   const long long np = kend - p.kbeg;
-  const long long total = static_cast<long long>(p.nx / FX) * (p.ny / FY) * np;
+  const long long total = static_cast<long long>(p.nx / G::FX) * (p.ny / G::FY) * np;
   const long long lo = total * blockIdx.x / gridDim.x;
   const long long hi = total * (blockIdx.x + 1) / gridDim.x;
   for (long long l = lo; l < hi;) {
     const int tile = static_cast<int>(l / np);
     const int kk = static_cast<int>(l - tile * np);
     const int len = static_cast<int>(min(np - kk, hi - l));
-    march_segment<S, OCC, LATE>(sm, p, M, tile, p.kbeg + kk, p.kbeg + kk + len);
+    march_segment<S, FXT>(sm, p, M, tile, p.kbeg + kk, p.kbeg + kk + len);
     l += len;
   }
 }
@@ -366,45 +356,38 @@ int num_sms_cached() {
   return n;
 }
 
-// SMC_NARROW_OCC=2 selects the 2-CTA/SM build (tuning knob).
-int fast_occ() {
-  static int o = [] {
-    const char* e = std::getenv("SMC_NARROW_OCC");
-    return (e && std::atoi(e) == 2) ? 2 : 1;
+// SMC_NARROW_FX=32|64 selects the tile width (tuning knob); see NG.  32 (three
+// CTAs of 4 warps per SM) measured 0.278 ms at 256^3 against 0.296 ms for 64
+// (one CTA of 8 warps), so it is the default.
+int fast_fx() {
+  static int f = [] {
+    const char* e = std::getenv("SMC_NARROW_FX");
+    return (e && std::atoi(e) == 64) ? 64 : 32;
   }();
-  return o;
+  return f;
 }
 
-// SMC_NARROW_LATEZ=1: z interfaces after x/y with the leading plane loaded at
-// the step start instead of prefetched (A/B knob).
-bool fast_latez() {
-  static bool v = [] {
-    const char* e = std::getenv("SMC_NARROW_LATEZ");
-    return e && std::atoi(e) == 1;
-  }();
-  return v;
-}
-
-template <int S, int OCC, bool LATE>
+template <int S, int FXT>
 void launch_fast_s(const NarrowArgs& p, const StencilM& M, cudaStream_t st) {
+  using G = NG<FXT>;
   static bool configured = false;
   if (!configured) {
-    SMC_CUDA(cudaFuncSetAttribute(narrow3d_fast<S, OCC, LATE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  static_cast<int>(sizeof(FastSmem))));
+    SMC_CUDA(cudaFuncSetAttribute(narrow3d_fast<S, FXT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  static_cast<int>(sizeof(FastSmem<FXT>))));
     configured = true;
   }
   const int kend = p.kend < 0 ? p.nz : p.kend;
   if (kend <= p.kbeg) return;
-  const int tiles = (p.nx / FX) * (p.ny / FY);
+  const int tiles = (p.nx / G::FX) * (p.ny / G::FY);
   if (chunked_grid()) {
     const dim3 grid(tiles, (kend - p.kbeg + p.kc - 1) / p.kc);
-    narrow3d_fast<S, OCC, LATE><<<grid, FT, sizeof(FastSmem), st>>>(p, M, 1);
+    narrow3d_fast<S, FXT><<<grid, G::FT, sizeof(FastSmem<FXT>), st>>>(p, M, 1);
   } else {
     const long long work = static_cast<long long>(tiles) * (kend - p.kbeg);
     const long long by_kc = (work + p.kc - 1) / p.kc;
     const int grid =
-        static_cast<int>(std::max(1LL, std::min<long long>(num_sms_cached() * OCC, by_kc)));
-    narrow3d_fast<S, OCC, LATE><<<grid, FT, sizeof(FastSmem), st>>>(p, M, 0);
+        static_cast<int>(std::max(1LL, std::min<long long>(num_sms_cached() * G::OCC, by_kc)));
+    narrow3d_fast<S, FXT><<<grid, G::FT, sizeof(FastSmem<FXT>), st>>>(p, M, 0);
   }
   SMC_CHECK_LAUNCH();
 }
@@ -413,32 +396,30 @@ void launch_fast_s(const NarrowArgs& p, const StencilM& M, cudaStream_t st) {
 
 bool narrow3d_fast_applicable(const NarrowArgs& p) {
   const auto al = [](const void* q) { return (reinterpret_cast<std::uintptr_t>(q) & 15) == 0; };
-  return p.dims == 3 && p.nx % FX == 0 && p.ny % FY == 0 && p.nx >= FX && p.cx == p.cz &&
-         p.cy == p.cz && p.g0 == nullptr && al(p.u) && al(p.cz) && al(p.out);
+  const int fx = fast_fx();
+  return p.dims == 3 && p.nx % fx == 0 && p.ny % NG<64>::FY == 0 && p.nx >= fx &&
+         p.cx == p.cz && p.cy == p.cz && p.g0 == nullptr && al(p.u) && al(p.cz) && al(p.out);
 }
 
 void launch_narrow3d_fast(const NarrowArgs& p, int s, const StencilM& M, cudaStream_t st) {
-  const bool pair = fast_latez();
-  if (fast_occ() == 2) {
-    if (s == 4)
-      pair ? launch_fast_s<4, 2, true>(p, M, st) : launch_fast_s<4, 2, false>(p, M, st);
-    else
-      pair ? launch_fast_s<3, 2, true>(p, M, st) : launch_fast_s<3, 2, false>(p, M, st);
+  if (fast_fx() == 32) {
+    s == 4 ? launch_fast_s<4, 32>(p, M, st) : launch_fast_s<3, 32>(p, M, st);
   } else {
-    if (s == 4)
-      pair ? launch_fast_s<4, 1, true>(p, M, st) : launch_fast_s<4, 1, false>(p, M, st);
-    else
-      pair ? launch_fast_s<3, 1, true>(p, M, st) : launch_fast_s<3, 1, false>(p, M, st);
+    s == 4 ? launch_fast_s<4, 64>(p, M, st) : launch_fast_s<3, 64>(p, M, st);
   }
 }
 
 int narrow3d_fast_default_kc(int nx, int ny, int nz, int num_sms) {
-  const long long tiles = static_cast<long long>(nx / FX) * (ny / FY);
-  // chunked grid: ~7 waves of one CTA per SM, >= 16 planes per CTA
-  long long kc = (tiles * nz + 7LL * num_sms - 1) / (7LL * num_sms);
-  if (kc < 16) kc = 16;
-  if (kc > nz) kc = nz;
-  return static_cast<int>(kc);
+  const int fx = fast_fx();
+  const int occ = fx == 32 ? NG<32>::OCC : NG<64>::OCC;
+  const long long tiles = static_cast<long long>(nx / fx) * (ny / NG<64>::FY);
+  const long long resident = static_cast<long long>(num_sms) * occ;
+  // chunked grid: equal z chunks of about 32 planes (256^3, 32-wide tiles:
+  // kc 8 / 16 / 21 / 32 / 64 measured 0.291 / 0.284 / 0.280 / 0.279 / 0.284
+  // ms), more and shorter (>= 8 planes) while the grid is under two waves
+  long long chunks = std::max(1LL, (nz + 16LL) / 32);
+  while (tiles * chunks < 2 * resident && (nz + chunks) / (chunks + 1) >= 8) ++chunks;
+  return static_cast<int>((nz + chunks - 1) / chunks);
 }
 
 }  // namespace smc
