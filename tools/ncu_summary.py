@@ -15,7 +15,8 @@ FIELDS = {
     "dram_bytes_write": ("dram__bytes_write.sum", 1),
     "fp64_pipe_active_pct": ("sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active", 1),
     "issue_slots_busy_pct": ("smsp__issue_active.avg.pct_of_peak_sustained_active", 1),
-    "dram_throughput_pct": ("dram__throughput.avg.pct_of_peak_sustained_elapsed", 1),
+    "dram_throughput_pct": ("gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed", 1),
+    "dram_tbytes_per_second": ("dram__bytes.sum.per_second", 1),
     "l2_throughput_pct": ("lts__throughput.avg.pct_of_peak_sustained_elapsed", 1),
     "l1_throughput_pct": ("l1tex__throughput.avg.pct_of_peak_sustained_active", 1),
     "l2_hit_pct": ("lts__t_sector_hit_rate.pct", 1),
