@@ -32,6 +32,9 @@ __host__ __device__ constexpr int mx_index(int i, int j) { return 3 * i + j - (j
 
 struct Tables {
   double W[NSP], th[NSP][4], mu0[NSP], lam0[NSP], rhoD0[NSP];
+  // derived on the host: R_k = R_u / W_k, 1 / W_k and the enthalpy
+  // polynomial in Horner form {a0, a1/2, a2/3, a3}: no divisions per cell
+  double R[NSP], Winv[NSP], hc[NSP][4];
   double kf[SMC_NREAC][3], kr[SMC_NREAC][3];
   int reac[SMC_NREAC][3], prod[SMC_NREAC][3], tb[SMC_NREAC];
 };
@@ -55,20 +58,19 @@ __device__ __forceinline__ long long nb(const Geo& g, int i, int j, int k, int d
   return zo(g, k) + static_cast<long long>(j) * g.nx + i;
 }
 
+// e_k, h_k, cv_k of the thermodynamic polynomial (smc_mechanism.h), Horner
+// form with host-derived coefficients
 __device__ __forceinline__ double spec_e(int k, double T) {
-  const double R = SMC_RU / cT.W[k];
-  const double* a = cT.th[k];
-  return R * (a[0] * T + a[1] * T * T / 2.0 + a[2] * T * T * T / 3.0 + a[3] - T);
+  const double* c = cT.hc[k];
+  return cT.R[k] * (c[3] + T * ((c[0] - 1.0) + T * (c[1] + T * c[2])));
 }
 __device__ __forceinline__ double spec_h(int k, double T) {
-  const double R = SMC_RU / cT.W[k];
-  const double* a = cT.th[k];
-  return R * (a[0] * T + a[1] * T * T / 2.0 + a[2] * T * T * T / 3.0 + a[3]);
+  const double* c = cT.hc[k];
+  return cT.R[k] * (c[3] + T * (c[0] + T * (c[1] + T * c[2])));
 }
 __device__ __forceinline__ double spec_cv(int k, double T) {
-  const double R = SMC_RU / cT.W[k];
   const double* a = cT.th[k];
-  return R * (a[0] + a[1] * T + a[2] * T * T - 1.0);
+  return cT.R[k] * ((a[0] - 1.0) + T * (a[1] + T * a[2]));
 }
 
 // T from e by Newton, same start and stopping rule as the oracle.
@@ -102,17 +104,17 @@ __global__ void __launch_bounds__(256) prim_kernel(const double* __restrict__ U,
 #pragma unroll
   for (int k = 0; k < NSP; ++k) {
     Y[k] = U[(5 + k) * n + c] * ri;
-    wsum += Y[k] / cT.W[k];
+    wsum += Y[k] * cT.Winv[k];
   }
   const double e = U[4 * n + c] * ri - 0.5 * (u[0] * u[0] + u[1] * u[1] + u[2] * u[2]);
   const double T = temperature(Y, e);
   const double p = rho * SMC_RU * T * wsum;
   const double s = pow(T / SMC_T_REF, SMC_TRANSPORT_EXP);
   double eta = 0.0, lam = 0.0, dhp = 0.0, hys = 0.0;
-  const double pinv = 1.0 / p;
+  const double pinv = 1.0 / p, wsinv = 1.0 / wsum;
 #pragma unroll
   for (int k = 0; k < NSP; ++k) {
-    X[k] = (Y[k] / cT.W[k]) / wsum;
+    X[k] = (Y[k] * cT.Winv[k]) * wsinv;
     eta += X[k] * cT.mu0[k];
     lam += X[k] * cT.lam0[k];
   }
@@ -424,7 +426,7 @@ __device__ __forceinline__ void wdot_cell(double rho, double T, const double* Y,
   double C[NSP], M = 0.0, om[NSP];
 #pragma unroll
   for (int s = 0; s < NSP; ++s) {
-    C[s] = rho * Y[s] / cT.W[s];
+    C[s] = rho * Y[s] * cT.Winv[s];
     M += C[s];
     om[s] = 0.0;
   }
@@ -514,7 +516,7 @@ __global__ void __launch_bounds__(256) conserved_kernel(const double* __restrict
 #pragma unroll
   for (int s = 0; s < NSP; ++s) {
     Yc[s] = Y[s * n + c];
-    rinv += Yc[s] / cT.W[s];
+    rinv += Yc[s] * cT.Winv[s];
   }
   const double rho = p[c] / (SMC_RU * T[c] * rinv);
 #pragma unroll
@@ -539,6 +541,12 @@ void upload_tables() {
     t.mu0[s] = SMC_MU0[s];
     t.lam0[s] = SMC_LAM0[s];
     t.rhoD0[s] = SMC_RHOD0[s];
+    t.R[s] = SMC_RU / SMC_W[s];
+    t.Winv[s] = 1.0 / SMC_W[s];
+    t.hc[s][0] = SMC_THERMO[s][0];
+    t.hc[s][1] = SMC_THERMO[s][1] / 2.0;
+    t.hc[s][2] = SMC_THERMO[s][2] / 3.0;
+    t.hc[s][3] = SMC_THERMO[s][3];
   }
   for (int r = 0; r < SMC_NREAC; ++r) {
     for (int q = 0; q < 3; ++q) {
