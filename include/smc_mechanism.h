@@ -78,33 +78,40 @@ typedef struct {
   double rev[3];
 } smc_reaction;
 
-static const smc_reaction SMC_REACTIONS[SMC_NREAC] = {
-    /* H + O2 = O + OH */
-    {{SP_H, SP_O2, -1}, {SP_O, SP_OH, -1}, 0, {2e+06, 0.0, 70000.0}, {1.2e+05, 0.2, 2000.0}},
-    /* O + H2 = H + OH */
-    {{SP_O, SP_H2, -1}, {SP_H, SP_OH, -1}, 0, {0.0005, 2.6, 26000.0}, {0.00022, 2.6, 18000.0}},
-    /* OH + H2 = H2O + H */
-    {{SP_OH, SP_H2, -1}, {SP_H2O, SP_H, -1}, 0, {2, 1.5, 14000.0}, {9, 1.5, 77000.0}},
-    /* O + H2O = OH + OH */
-    {{SP_O, SP_H2O, -1}, {SP_OH, SP_OH, -1}, 0, {0.03, 2.0, 56000.0}, {0.01, 2.0, 3000.0}},
-    /* H2 + M = H + H + M */
-    {{SP_H2, -1, -1}, {SP_H, SP_H, -1}, 1, {4.5e+11, -1.4, 436000.0}, {1e+04, -1.0, 0.0}},
-    /* O + O + M = O2 + M */
-    {{SP_O, SP_O, -1}, {SP_O2, -1, -1}, 1, {60, -0.5, 0.0}, {2e+10, -0.9, 495000.0}},
-    /* H + OH + M = H2O + M */
-    {{SP_H, SP_OH, -1}, {SP_H2O, -1, -1}, 1, {2.2e+08, -2.0, 0.0}, {3e+15, -2.5, 500000.0}},
-    /* H + O2 + M = HO2 + M */
-    {{SP_H, SP_O2, -1}, {SP_HO2, -1, -1}, 1, {6e+03, -0.8, 0.0}, {2e+10, -0.6, 205000.0}},
-    /* HO2 + H = OH + OH */
-    {{SP_HO2, SP_H, -1}, {SP_OH, SP_OH, -1}, 0, {7e+05, 0.0, 1200.0}, {200, 0.6, 150000.0}},
-    /* HO2 + H = H2 + O2 */
-    {{SP_HO2, SP_H, -1}, {SP_H2, SP_O2, -1}, 0, {2.8e+05, 0.0, 4500.0}, {5e+04, 0.3, 230000.0}},
-    /* HO2 + OH = H2O + O2 */
-    {{SP_HO2, SP_OH, -1}, {SP_H2O, SP_O2, -1}, 0, {2.9e+05, 0.0, 0.0}, {1e+06, 0.2, 290000.0}},
-    /* HO2 + HO2 = H2O2 + O2 */
-    {{SP_HO2, SP_HO2, -1}, {SP_H2O2, SP_O2, -1}, 0, {4e+04, 0.0, 5000.0}, {1e+06, 0.0, 160000.0}},
-    /* H2O2 + M = OH + OH + M */
-    {{SP_H2O2, -1, -1}, {SP_OH, SP_OH, -1}, 1, {1.2e+09, 0.0, 190000.0}, {2.3e+04, -0.8, 0.0}},
-};
+/* The reaction list as an X-macro, so C code gets the table below and CUDA
+ * code can unroll over compile-time species indices:
+ * X(reactant0..2, product0..2, third_body, A_f, b_f, Ea_f, A_r, b_r, Ea_r). */
+#define SMC_REACTION_LIST(X) \
+  /* H + O2 = O + OH */ \
+  X(SP_H, SP_O2, -1, SP_O, SP_OH, -1, 0, 2e+06, 0.0, 70000.0, 1.2e+05, 0.2, 2000.0) \
+  /* O + H2 = H + OH */ \
+  X(SP_O, SP_H2, -1, SP_H, SP_OH, -1, 0, 0.0005, 2.6, 26000.0, 0.00022, 2.6, 18000.0) \
+  /* OH + H2 = H2O + H */ \
+  X(SP_OH, SP_H2, -1, SP_H2O, SP_H, -1, 0, 2, 1.5, 14000.0, 9, 1.5, 77000.0) \
+  /* O + H2O = OH + OH */ \
+  X(SP_O, SP_H2O, -1, SP_OH, SP_OH, -1, 0, 0.03, 2.0, 56000.0, 0.01, 2.0, 3000.0) \
+  /* H2 + M = H + H + M */ \
+  X(SP_H2, -1, -1, SP_H, SP_H, -1, 1, 4.5e+11, -1.4, 436000.0, 1e+04, -1.0, 0.0) \
+  /* O + O + M = O2 + M */ \
+  X(SP_O, SP_O, -1, SP_O2, -1, -1, 1, 60, -0.5, 0.0, 2e+10, -0.9, 495000.0) \
+  /* H + OH + M = H2O + M */ \
+  X(SP_H, SP_OH, -1, SP_H2O, -1, -1, 1, 2.2e+08, -2.0, 0.0, 3e+15, -2.5, 500000.0) \
+  /* H + O2 + M = HO2 + M */ \
+  X(SP_H, SP_O2, -1, SP_HO2, -1, -1, 1, 6e+03, -0.8, 0.0, 2e+10, -0.6, 205000.0) \
+  /* HO2 + H = OH + OH */ \
+  X(SP_HO2, SP_H, -1, SP_OH, SP_OH, -1, 0, 7e+05, 0.0, 1200.0, 200, 0.6, 150000.0) \
+  /* HO2 + H = H2 + O2 */ \
+  X(SP_HO2, SP_H, -1, SP_H2, SP_O2, -1, 0, 2.8e+05, 0.0, 4500.0, 5e+04, 0.3, 230000.0) \
+  /* HO2 + OH = H2O + O2 */ \
+  X(SP_HO2, SP_OH, -1, SP_H2O, SP_O2, -1, 0, 2.9e+05, 0.0, 0.0, 1e+06, 0.2, 290000.0) \
+  /* HO2 + HO2 = H2O2 + O2 */ \
+  X(SP_HO2, SP_HO2, -1, SP_H2O2, SP_O2, -1, 0, 4e+04, 0.0, 5000.0, 1e+06, 0.0, 160000.0) \
+  /* H2O2 + M = OH + OH + M */ \
+  X(SP_H2O2, -1, -1, SP_OH, SP_OH, -1, 1, 1.2e+09, 0.0, 190000.0, 2.3e+04, -0.8, 0.0)
+
+#define SMC_REACTION_ENTRY(r0, r1, r2, p0, p1, p2, tb, af, bf, ef, ar, br, er) \
+  {{r0, r1, r2}, {p0, p1, p2}, tb, {af, bf, ef}, {ar, br, er}},
+static const smc_reaction SMC_REACTIONS[SMC_NREAC] = {SMC_REACTION_LIST(SMC_REACTION_ENTRY)};
+#undef SMC_REACTION_ENTRY
 
 #endif /* SMC_MECHANISM_H */

@@ -9,6 +9,7 @@
 //   wdot    : rho omega_k                                       -> out
 #include <cmath>
 #include <cstdlib>
+#include <utility>
 
 #include "ns.cuh"
 
@@ -421,6 +422,48 @@ __global__ void __launch_bounds__(256) assemble_kernel(const double* __restrict_
 }
 
 // ------------------------------------------------------------- wdot
+// Species indices of every reaction as compile-time constants (the
+// mechanism's X-macro), so the concentration and production arrays stay in
+// registers; the rate parameters come from the constant bank.
+struct RxIdx {
+  int r[3], p[3], tb;
+};
+#define SMC_RX_IDX(r0, r1, r2, p0, p1, p2, tb, af, bf, ef, ar, br, er) \
+  RxIdx{{r0, r1, r2}, {p0, p1, p2}, tb},
+constexpr RxIdx kRx[SMC_NREAC] = {SMC_REACTION_LIST(SMC_RX_IDX)};
+#undef SMC_RX_IDX
+
+template <int R>
+__device__ __forceinline__ void rx_step(const double* C, double M, double lnT, double invRT,
+                                        double* om) {
+  constexpr RxIdx x = kRx[R];
+  const double kf = cT.kf[R][0] * exp(cT.kf[R][1] * lnT - cT.kf[R][2] * invRT);
+  const double kr = cT.kr[R][0] * exp(cT.kr[R][1] * lnT - cT.kr[R][2] * invRT);
+  double qf = kf, qr = kr;
+  if constexpr (x.r[0] >= 0) qf *= C[x.r[0]];
+  if constexpr (x.p[0] >= 0) qr *= C[x.p[0]];
+  if constexpr (x.r[1] >= 0) qf *= C[x.r[1]];
+  if constexpr (x.p[1] >= 0) qr *= C[x.p[1]];
+  if constexpr (x.r[2] >= 0) qf *= C[x.r[2]];
+  if constexpr (x.p[2] >= 0) qr *= C[x.p[2]];
+  if constexpr (x.tb != 0) {
+    qf *= M;
+    qr *= M;
+  }
+  const double q = qf - qr;
+  if constexpr (x.r[0] >= 0) om[x.r[0]] -= q;
+  if constexpr (x.p[0] >= 0) om[x.p[0]] += q;
+  if constexpr (x.r[1] >= 0) om[x.r[1]] -= q;
+  if constexpr (x.p[1] >= 0) om[x.p[1]] += q;
+  if constexpr (x.r[2] >= 0) om[x.r[2]] -= q;
+  if constexpr (x.p[2] >= 0) om[x.p[2]] += q;
+}
+template <int... R>
+__device__ __forceinline__ void rx_all(std::integer_sequence<int, R...>, const double* C,
+                                       double M, double lnT, double invRT, double* om) {
+  (rx_step<R>(C, M, lnT, invRT, om), ...);
+}
+
 // rho omega_k W_k of one cell (smc_mechanism.h kinetics)
 __device__ __forceinline__ void wdot_cell(double rho, double T, const double* Y, double* w) {
   double C[NSP], M = 0.0, om[NSP];
@@ -431,27 +474,7 @@ __device__ __forceinline__ void wdot_cell(double rho, double T, const double* Y,
     om[s] = 0.0;
   }
   const double lnT = log(T), invRT = 1.0 / (SMC_RU * T);
-#pragma unroll
-  for (int r = 0; r < SMC_NREAC; ++r) {
-    const double kf = cT.kf[r][0] * exp(cT.kf[r][1] * lnT - cT.kf[r][2] * invRT);
-    const double kr = cT.kr[r][0] * exp(cT.kr[r][1] * lnT - cT.kr[r][2] * invRT);
-    double qf = kf, qr = kr;
-#pragma unroll
-    for (int m = 0; m < 3; ++m) {
-      if (cT.reac[r][m] >= 0) qf *= C[cT.reac[r][m]];
-      if (cT.prod[r][m] >= 0) qr *= C[cT.prod[r][m]];
-    }
-    if (cT.tb[r]) {
-      qf *= M;
-      qr *= M;
-    }
-    const double q = qf - qr;
-#pragma unroll
-    for (int m = 0; m < 3; ++m) {
-      if (cT.reac[r][m] >= 0) om[cT.reac[r][m]] -= q;
-      if (cT.prod[r][m] >= 0) om[cT.prod[r][m]] += q;
-    }
-  }
+  rx_all(std::make_integer_sequence<int, SMC_NREAC>{}, C, M, lnT, invRT, om);
 #pragma unroll
   for (int s = 0; s < NSP; ++s) w[s] = cT.W[s] * om[s];
 }
