@@ -195,3 +195,20 @@ def test_ns_mode2_implicit_chemistry_vs_oracle(cuda):
     assert (d.sweeps, d.f1_evals, d.f2_evals, d.implicit_solves) == \
         (do["sweeps"], do["f1_evals"], do["f2_evals"], do["implicit_solves"])
     assert _percomp(got, uo.reshape(U0.shape)) <= 1e-9
+
+
+def test_mode2_acceptance_c7_stiff_forced(cuda):
+    """acceptance_test.cpp:357-420 (criterion 7) on the device: sigma = 1e4,
+    GL(3)/TypeB GL(5), rtol 1e-12, atol 1e-13; 50 steps of dt = 0.02 (100x
+    the explicit limit 2/sigma) land within 1e-3 of cos(1); 24 sweeps of one
+    step reach the collocation residual floor (<= 1e-9)."""
+    f1 = P.CallbackRhs(1, lambda t, u: MP.oscillator_f1(t, u, 1.0e4))
+    f2 = P.CallbackRhs(1, MP.oscillator_f2)
+    so = P.StiffOptions(rtol=1e-12, atol=1e-13)
+    st = P.MrsdcStepper(3, 5, P.StepControls(6, 0.0), stiff=so)
+    u, d = st.integrate_mode2(f1, f2, np.array([1.0]), 0.0, 1.0, 50)
+    assert np.isfinite(u[0]) and abs(u[0] - math.cos(1.0)) <= 1e-3
+    assert d.implicit_solves == 50 * 6 * 2
+    deep = P.MrsdcStepper(3, 5, P.StepControls(24, 0.0), stiff=so)
+    _, _, _, d2 = deep.step_mode2(f1, f2, np.array([1.0]), 0.0, 0.02)
+    assert d2.residual_history[-1] <= 1e-9
