@@ -469,7 +469,8 @@ struct DiagBuf {
 inline smc_stiff to_c(const StiffOptions& o) {
   if (o.jacobian == StiffOptions::Jacobian::UserSupplied)
     throw std::invalid_argument("StiffOptions: a user-supplied Jacobian is not on the device path");
-  return smc_stiff{o.rtol, o.atol, o.max_newton_iters, o.block, o.interleaved ? 1 : 0};
+  return smc_stiff{o.rtol, o.atol, o.max_newton_iters, o.block, o.interleaved ? 1 : 0,
+                   o.initial_step_fraction};
 }
 struct SdcDeleter {
   void operator()(smc_sdc* s) const { smc_sdc_destroy(s); }
@@ -672,6 +673,19 @@ inline std::pair<Field, MrsdcDiagnostics> mrsdc_step_mode2(const SplitRHS& rhs, 
   MrsdcStepper m(h, c, stiff);
   MrsdcStepper::Result r = m.step_mode2(rhs, u0, t_n, dt);
   return {std::move(r.u), std::move(r.diag)};
+}
+
+// stiff.hpp:42-49: adaptive BE/BDF2 integration on the device; throws
+// IntegrationError when the step size collapses, std::invalid_argument for
+// t1 < t0 or bad tolerances.
+inline Field integrate_stiff(const Rhs& f, const Field& u0, double t0, double t1,
+                             const StiffOptions& opts) {
+  detail::CallbackRhs op(f, u0.size());
+  Field u(u0.size());
+  const smc_stiff so = detail::to_c(opts);
+  detail::check(smc_integrate_stiff(op.h.get(), u0.data(), t0, t1, u.data(), SMC_HOST, &so,
+                                    nullptr, nullptr));
+  return u;
 }
 
 // stiff.hpp:29-40: w = c + beta f(t_eval, w) by Newton from guess, on the

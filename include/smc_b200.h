@@ -92,6 +92,7 @@ typedef struct {
   int max_newton_iters; /* 16 */
   long long block;
   int interleaved;
+  double initial_step_fraction; /* 1e-3: integrate_stiff's first step as a fraction of the span */
 } smc_stiff;
 
 /* NewtonReport (core/include/nsdc/stiff.hpp:22-27) */
@@ -202,6 +203,14 @@ int smc_rhs_destroy(smc_rhs* op);
 int smc_solve_backward_euler(smc_rhs* f, double t, double beta, const double* c,
                              const double* guess, double* w, int where, const smc_stiff* opts,
                              smc_newton_report* report);
+
+/* integrate_stiff — core/src/stiff.cpp:115-188: u' = f(t, u) from t0 to t1 by
+ * adaptive backward Euler / variable-step BDF2 with step doubling, every
+ * implicit stage through the device Newton (block structure from opts).
+ * SMC_EINVAL for t1 < t0 or bad tolerances, SMC_EINTEGRATION when the step
+ * size collapses.  accepted / rejected (may be NULL) count the steps. */
+int smc_integrate_stiff(smc_rhs* f, const double* u0, double t0, double t1, double* u_out,
+                        int where, const smc_stiff* opts, int* accepted, int* rejected);
 
 /* ------------------------------------------------------- quadrature */
 /* gauss_lobatto / clenshaw_curtis — core/src/quadrature.cpp:101-132 */

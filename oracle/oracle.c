@@ -661,3 +661,114 @@ int or_integrate_mrsdc2(or_rhs_cb f1, void* c1, or_rhs_cb f2, void* c2, long lon
   free(u); free(c1s); free(c2s); free(hist);
   return rc;
 }
+
+/* ------------------------------------------------- integrate_stiff */
+static double clampd(double v, double lo, double hi) { return v < lo ? lo : (hi < v ? hi : v); }
+
+/* bdf2_coeff (stiff.cpp:118-121) */
+static double bdf2_coeff(double rho) {
+  return -(1.0 + rho) * (1.0 + rho) / (6.0 * rho * (1.0 + 2.0 * rho));
+}
+
+/* be_solve / bdf2_solve (stiff.cpp:82-106): 1 when Newton converged */
+static int be_step(or_rhs_cb f, void* ctx, long long dim, double t_new, double h,
+                   const double* u_n, const or_stiff* o, double* out) {
+  or_newton_report rep;
+  or_solve_backward_euler(f, ctx, dim, t_new, h, u_n, u_n, o, out, &rep);
+  return rep.converged;
+}
+static int bdf2_step(or_rhs_cb f, void* ctx, long long dim, double t_new, double h, double rho,
+                     const double* u_nm1, const double* u_n, const or_stiff* o, double* out,
+                     double* c, double* guess) {
+  const double denom = 1.0 + 2.0 * rho;
+  for (long long i = 0; i < dim; ++i) {
+    c[i] = ((1.0 + rho) * (1.0 + rho) * u_n[i] - rho * rho * u_nm1[i]) / denom;
+    guess[i] = u_n[i] + rho * (u_n[i] - u_nm1[i]);
+  }
+  or_newton_report rep;
+  or_solve_backward_euler(f, ctx, dim, t_new, h * (1.0 + rho) / denom, c, guess, o, out, &rep);
+  return rep.converged;
+}
+
+int or_integrate_stiff(or_rhs_cb f, void* ctx, long long dim, const double* u0, double t0,
+                       double t1, const or_stiff* o, double initial_step_fraction,
+                       double* u_out, int* accepted, int* rejected, double* t_fail) {
+  const double span = t1 - t0;
+  const size_t bytes = sizeof(double) * dim;
+  *accepted = *rejected = 0;
+  *t_fail = 0.0;
+  if (span == 0.0) {
+    memcpy(u_out, u0, bytes);
+    return 0;
+  }
+  if (span < 0.0 || o->rtol <= 0.0 || o->atol < 0.0) return 1;
+  double* u = malloc(bytes);
+  double* u_prev = malloc(bytes);
+  double* y_full = malloc(bytes);
+  double* y_mid = malloc(bytes);
+  double* y_half = malloc(bytes);
+  double* c = malloc(bytes);
+  double* guess = malloc(bytes);
+  memcpy(u, u0, bytes);
+  double t = t0, h_prev = 0.0;
+  double h = clampd(initial_step_fraction, 1e-12, 1.0) * span;
+  const double h_min = 1e-14 * span;
+  int have_history = 0, rc = 0;
+  while (t < t1) {
+    h = h < t1 - t ? h : t1 - t;
+    if (h < h_min) {
+      *t_fail = t;
+      rc = 2;
+      break;
+    }
+    int ok;
+    double weight;
+    if (!have_history) {
+      ok = be_step(f, ctx, dim, t + h, h, u, o, y_full) &&
+           be_step(f, ctx, dim, t + 0.5 * h, 0.5 * h, u, o, y_mid) &&
+           be_step(f, ctx, dim, t + h, 0.5 * h, y_mid, o, y_half);
+      weight = 1.0;
+    } else {
+      const double rho_full = h / h_prev;
+      const double rho_mid = 0.5 * h / h_prev;
+      ok = bdf2_step(f, ctx, dim, t + h, h, rho_full, u_prev, u, o, y_full, c, guess) &&
+           bdf2_step(f, ctx, dim, t + 0.5 * h, 0.5 * h, rho_mid, u_prev, u, o, y_mid, c, guess) &&
+           bdf2_step(f, ctx, dim, t + h, 0.5 * h, 1.0, u, y_mid, o, y_half, c, guess);
+      const double c_full = bdf2_coeff(rho_full);
+      const double c_half = ((4.0 / 3.0) * bdf2_coeff(rho_mid) + bdf2_coeff(1.0)) / 8.0;
+      weight = clampd(c_half / (c_full - c_half), 0.05, 2.0);
+    }
+    if (!ok) {
+      h *= 0.5;
+      ++*rejected;
+      continue;
+    }
+    double diff = 0.0, yn = 0.0;
+    for (long long i = 0; i < dim; ++i) {
+      diff = max_keep(diff, fabs(y_full[i] - y_half[i]));
+      yn = max_keep(yn, fabs(y_half[i]));
+    }
+    const double err = weight * diff;
+    const double p = have_history ? 3.0 : 2.0;
+    const double tol = o->rtol * yn + o->atol;
+    if (err <= tol) {
+      for (long long i = 0; i < dim; ++i) y_half[i] += weight * (y_half[i] - y_full[i]);
+      double* tmp = u_prev;
+      u_prev = u;
+      u = y_half;
+      y_half = tmp;
+      t += h;
+      h_prev = h;
+      have_history = 1;
+      ++*accepted;
+    } else {
+      ++*rejected;
+    }
+    double factor = err > 0.0 ? 0.9 * pow(tol / err, 1.0 / p) : 5.0;
+    factor = clampd(factor, 0.2, 5.0);
+    h *= factor;
+  }
+  memcpy(u_out, u, bytes);
+  free(u); free(u_prev); free(y_full); free(y_mid); free(y_half); free(c); free(guess);
+  return rc;
+}

@@ -119,6 +119,14 @@ int or_integrate_mrsdc2(or_rhs_cb f1, void* c1, or_rhs_cb f2, void* c2, long lon
                         int* sweeps, int* f1_evals, int* f2_evals, int* implicit_solves,
                         int* newton_f1_evals, int* fail_node, int* fail_sweep);
 
+/* integrate_stiff (core/src/stiff.cpp:80-188): adaptive backward Euler /
+ * variable-step BDF2 with step doubling, over or_solve_backward_euler.
+ * Returns 0, 1 on bad arguments (span < 0, bad tolerances), 2 when the step
+ * size collapses (*t_fail = the time reached). */
+int or_integrate_stiff(or_rhs_cb f, void* ctx, long long dim, const double* u0, double t0,
+                       double t1, const or_stiff* opts, double initial_step_fraction,
+                       double* u_out, int* accepted, int* rejected, double* t_fail);
+
 #ifdef __cplusplus
 }
 #endif

@@ -288,3 +288,27 @@ def ref_integrate_mrsdc2(f1cb, f2cb, u0, t0, t1, nsteps, coarse_n=3, fine_type=1
     msg = r.ref_last_error().decode() if rc else ""
     return rc, uo, dict(sweeps=sw, f1_evals=n1, f2_evals=n2, implicit_solves=imp,
                         newton_f1_evals=nf1, residuals=res[:sw].copy()), msg
+
+
+def integrate_stiff(fcb, u0, t0, t1, initial_step_fraction=1e-3, **stiff):
+    """or_integrate_stiff: (rc, u, accepted, rejected)."""
+    u0 = np.ascontiguousarray(u0, dtype=np.float64)
+    uo = np.empty_like(u0)
+    acc, rej, tf = C.c_int(), C.c_int(), C.c_double()
+    st = _stiff(**stiff)
+    rc = lib().or_integrate_stiff(fcb, None, C.c_longlong(u0.size), dp(u0), C.c_double(t0),
+                                  C.c_double(t1), C.byref(st), C.c_double(initial_step_fraction),
+                                  dp(uo), C.byref(acc), C.byref(rej), C.byref(tf))
+    return rc, uo, acc.value, rej.value
+
+
+def ref_integrate_stiff(fcb, u0, t0, t1, rtol=1e-8, atol=1e-10, max_newton_iters=16,
+                        initial_step_fraction=1e-3):
+    """The reference's integrate_stiff: (rc, u, error message)."""
+    u0 = np.ascontiguousarray(u0, dtype=np.float64)
+    uo = np.empty_like(u0)
+    r = ref()
+    rc = r.ref_integrate_stiff(fcb, None, C.c_longlong(u0.size), dp(u0), C.c_double(t0),
+                               C.c_double(t1), C.c_double(rtol), C.c_double(atol),
+                               max_newton_iters, C.c_double(initial_step_fraction), dp(uo))
+    return rc, uo, (r.ref_last_error().decode() if rc else "")

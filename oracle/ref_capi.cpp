@@ -438,6 +438,22 @@ int ref_solve_backward_euler(rhs_cb f, void* ctx, long long dim, double t, doubl
   });
 }
 
+// integrate_stiff (stiff.cpp:115-188); returns 2 with ref_last_error() on
+// IntegrationError (step size collapse), 1 on std::invalid_argument.
+int ref_integrate_stiff(rhs_cb f, void* ctx, long long dim, const double* u0, double t0,
+                        double t1, double rtol, double atol, int max_newton_iters,
+                        double initial_step_fraction, double* u_out) {
+  return guarded([&] {
+    StiffOptions so;
+    so.rtol = rtol;
+    so.atol = atol;
+    so.max_newton_iters = max_newton_iters;
+    so.initial_step_fraction = initial_step_fraction;
+    Field r = integrate_stiff(wrap_cb(f, ctx), Field(u0, u0 + dim), t0, t1, so);
+    std::memcpy(u_out, r.data(), sizeof(double) * dim);
+  });
+}
+
 // ------------------------------------------------------------- quadrature
 int ref_nodes(int family, int n, double* out) {
   return guarded([&] {

@@ -28,7 +28,7 @@ __all__ = [
     "SmcError", "SmcInvalidArgument", "SmcIntegrationError", "StencilChoice", "stencil_preset",
     "build_narrow", "apply_narrow", "apply_wide", "first_derivative8", "HeatOperator",
     "Narrow3DOperator", "Narrow3DSlab", "CallbackRhs", "DeviceCallbackRhs", "SdcStepper",
-    "MrsdcStepper", "StepControls", "StiffOptions", "NewtonReport", "solve_backward_euler", "nodes",
+    "MrsdcStepper", "StepControls", "StiffOptions", "NewtonReport", "solve_backward_euler", "integrate_stiff", "nodes",
     "integration_matrices", "build_hierarchy", "SMC_M47", "SMC_M48", "OPTIMAL_M47", "NsOperator",
     "ns_conserved", "NS_FULL", "NS_ADVDIFF", "NS_CHEM",
     "OPTIMAL_M48", "DEFAULT_M36", "launch_count",
@@ -336,10 +336,11 @@ class StiffOptions:
     max_newton_iters: int = 16
     block: int = 0
     interleaved: bool = False
+    initial_step_fraction: float = 1e-3
 
     def c(self):
         return _capi.Stiff(self.rtol, self.atol, self.max_newton_iters, self.block,
-                           int(self.interleaved))
+                           int(self.interleaved), self.initial_step_fraction)
 
 
 @dataclass
@@ -349,6 +350,17 @@ class NewtonReport:
     final_residual: float = 0.0
     converged: bool = False
     f_evals: int = 0
+
+
+def integrate_stiff(f: "_Rhs", u0, t0: float, t1: float, stiff: "StiffOptions" = None):
+    """integrate_stiff (stiff.cpp:115-188) on the device: adaptive backward Euler
+    / variable-step BDF2 with step doubling.  Returns (u, (accepted, rejected))."""
+    u = _out_like(u0)
+    so = (stiff or StiffOptions()).c()
+    acc, rej = C.c_int(), C.c_int()
+    check(_capi.lib().smc_integrate_stiff(f.handle, dptr(u0), t0, t1, dptr(u), where_of(u0),
+                                          C.byref(so), C.byref(acc), C.byref(rej)))
+    return u, (acc.value, rej.value)
 
 
 def solve_backward_euler(f: "_Rhs", t: float, beta: float, c, guess, stiff: "StiffOptions" = None,

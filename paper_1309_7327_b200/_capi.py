@@ -50,7 +50,8 @@ class Diag(C.Structure):
 class Stiff(C.Structure):
     """smc_stiff: StiffOptions (stiff.hpp:10-20) + block structure of f."""
     _fields_ = [("rtol", C.c_double), ("atol", C.c_double), ("max_newton_iters", C.c_int),
-                ("block", C.c_longlong), ("interleaved", C.c_int)]
+                ("block", C.c_longlong), ("interleaved", C.c_int),
+                ("initial_step_fraction", C.c_double)]
 
 
 class NewtonReport(C.Structure):
@@ -121,6 +122,8 @@ _SIG = {
                                             _VP, C.c_int, C.POINTER(Diag)]),
     "smc_solve_backward_euler": (C.c_int, [_VP, C.c_double, C.c_double, _VP, _VP, _VP, C.c_int,
                                            C.POINTER(Stiff), C.POINTER(NewtonReport)]),
+    "smc_integrate_stiff": (C.c_int, [_VP, _VP, C.c_double, C.c_double, _VP, C.c_int,
+                                      C.POINTER(Stiff), _I, _I]),
     "smc_mrsdc_set_reducer": (C.c_int, [_VP, REDUCE_FN, _VP]),
     "smc_mrsdc_destroy": (C.c_int, [_VP]),
 }

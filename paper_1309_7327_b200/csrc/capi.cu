@@ -530,6 +530,7 @@ smc::StiffOpts stiff_of(const smc_stiff* o) {
   if (o) {
     s.rtol = o->rtol, s.atol = o->atol, s.max_newton_iters = o->max_newton_iters;
     s.block = o->block, s.interleaved = o->interleaved;
+    s.initial_step_fraction = o->initial_step_fraction;
   }
   smc::require(s.rtol >= 0.0 && s.atol >= 0.0, "StiffOptions: negative tolerance");
   smc::require(s.block >= 0, "StiffOptions: negative block size");
@@ -569,6 +570,25 @@ int smc_mrsdc_integrate_mode2(smc_mrsdc* m, smc_rhs* f1, smc_rhs* f2, const doub
                               double t0, double t1, int nsteps, double* u_out, int where,
                               smc_diag* diag) {
   return mrsdc_integrate(2, m, f1, f2, u0, t0, t1, nsteps, u_out, where, diag);
+}
+
+int smc_integrate_stiff(smc_rhs* f, const double* u0, double t0, double t1, double* u_out,
+                        int where, const smc_stiff* opts, int* accepted, int* rejected) {
+  return guarded([&] {
+    need(u0, "u0"), need(u_out, "u_out");
+    smc::RhsOp& op = op_of(f);
+    const long long n = op.dim();
+    cudaStream_t st = op.stream();
+    const smc::StiffOpts so = stiff_of(opts);
+    Staged du(u0, n, where, st);
+    StagedOut ou(u_out, n, where);
+    smc::StiffStats stats;
+    smc::integrate_stiff(op, du.dev, t0, t1, ou.dev, so, &stats);
+    ou.finish(st);
+    SMC_CUDA(cudaStreamSynchronize(st));
+    if (accepted) *accepted = stats.accepted;
+    if (rejected) *rejected = stats.rejected;
+  });
 }
 
 int smc_solve_backward_euler(smc_rhs* f, double t, double beta, const double* c,

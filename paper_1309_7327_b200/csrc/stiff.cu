@@ -2,9 +2,11 @@
 // Jacobian (see stiff.hpp).  Arithmetic follows the reference operation by
 // operation without contraction (explicit _rn intrinsics), so the dense case
 // reproduces stiff.cpp / matrix.cpp exactly.
+#include <algorithm>
 #include <cfloat>
 #include <cmath>
 #include <cstring>
+#include <string>
 
 #include "stiff.hpp"
 
@@ -261,6 +263,51 @@ __global__ void __launch_bounds__(256) sub_kernel(double* w, const double* delta
     w[i] = __dsub_rn(w[i], delta[i]);
 }
 
+// bdf2_solve's right-hand side and guess (stiff.cpp:94-99)
+__global__ void __launch_bounds__(256) bdf2_prep_kernel(const double* u_nm1, const double* u_n,
+                                                        double rho, double denom, double* c,
+                                                        double* guess, long long n) {
+  const double a = __dmul_rn(__dadd_rn(1.0, rho), __dadd_rn(1.0, rho)), b = __dmul_rn(rho, rho);
+  const long long stride = static_cast<long long>(gridDim.x) * blockDim.x;
+  for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < n;
+       i += stride) {
+    c[i] = __dsub_rn(__dmul_rn(a, u_n[i]), __dmul_rn(b, u_nm1[i])) / denom;
+    guess[i] = __dadd_rn(u_n[i], __dmul_rn(rho, __dsub_rn(u_n[i], u_nm1[i])));
+  }
+}
+
+// slots[0] = max |full - half| (diff_norm), slots[1] = max |half| (max_norm)
+__global__ void __launch_bounds__(256) stiff_norms_kernel(const double* full, const double* half,
+                                                          long long n,
+                                                          unsigned long long* slots) {
+  double d = 0.0, m = 0.0;
+  const long long stride = static_cast<long long>(gridDim.x) * blockDim.x;
+  for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < n;
+       i += stride) {
+    const double a = fabs(__dsub_rn(full[i], half[i])), b = fabs(half[i]);
+    if (a > d) d = a;
+    if (b > m) m = b;
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    d = fmax(d, __shfl_xor_sync(0xffffffffu, d, o));
+    m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
+  }
+  if ((threadIdx.x & 31) == 0) {
+    atomicMax(slots, static_cast<unsigned long long>(__double_as_longlong(d)));
+    atomicMax(slots + 1, static_cast<unsigned long long>(__double_as_longlong(m)));
+  }
+}
+
+// Richardson correction on acceptance: half += w (half - full) (stiff.cpp:171-172)
+__global__ void __launch_bounds__(256) stiff_correct_kernel(double* half, const double* full,
+                                                            double w, long long n) {
+  const long long stride = static_cast<long long>(gridDim.x) * blockDim.x;
+  for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < n;
+       i += stride)
+    half[i] = __dadd_rn(half[i], __dmul_rn(w, __dsub_rn(half[i], full[i])));
+}
+
 double bits_to_double(unsigned long long u) {
   double d;
   std::memcpy(&d, &u, sizeof(d));
@@ -371,6 +418,108 @@ void DeviceNewton::solve(RhsOp& f, double t, double beta, const double* c, const
     }
     rep.iterations = iter + 1;
   }
+}
+
+namespace {
+
+double bdf2_coeff(double rho) {  // stiff.cpp:118-121
+  return -(1.0 + rho) * (1.0 + rho) / (6.0 * rho * (1.0 + 2.0 * rho));
+}
+
+}  // namespace
+
+void integrate_stiff(RhsOp& f, const double* u0, double t0, double t1, double* u_out,
+                     const StiffOpts& o, StiffStats* stats) {
+  const long long dim = f.dim();
+  cudaStream_t st = f.stream();
+  StiffStats local;
+  StiffStats& ss = stats ? *stats : local;
+  ss = StiffStats{};
+  const double span = t1 - t0;
+  if (span == 0.0) {
+    if (u_out != u0)
+      SMC_CUDA(cudaMemcpyAsync(u_out, u0, dim * sizeof(double), cudaMemcpyDeviceToDevice, st));
+    return;
+  }
+  require(!(span < 0.0), "integrate_stiff: t1 must be >= t0");
+  require(!(o.rtol <= 0.0 || o.atol < 0.0), "integrate_stiff: bad tolerances");
+  DevBuf U(dim), Up(dim), Yf(dim), Ym(dim), Yh(dim), C(dim), Gs(dim), slots(2);
+  double* u = U.get();
+  double* u_prev = Up.get();
+  double* y_half = Yh.get();
+  SMC_CUDA(cudaMemcpyAsync(u, u0, dim * sizeof(double), cudaMemcpyDeviceToDevice, st));
+  DeviceNewton newton;
+  auto be = [&](double t_new, double h, const double* un, double* out) {
+    NewtonReport rep;
+    newton.solve(f, t_new, h, un, un, out, o, rep);
+    return rep.converged;
+  };
+  auto bdf2 = [&](double t_new, double h, double rho, const double* unm1, const double* un,
+                  double* out) {
+    const double denom = 1.0 + 2.0 * rho;
+    bdf2_prep_kernel<<<grid_for(dim), 256, 0, st>>>(unm1, un, rho, denom, C.get(), Gs.get(), dim);
+    SMC_CHECK_LAUNCH();
+    NewtonReport rep;
+    newton.solve(f, t_new, h * (1.0 + rho) / denom, C.get(), Gs.get(), out, o, rep);
+    return rep.converged;
+  };
+  double host[2];
+  double t = t0, h_prev = 0.0;
+  double h = std::clamp(o.initial_step_fraction, 1e-12, 1.0) * span;
+  const double h_min = 1e-14 * span;
+  bool have_history = false;
+  while (t < t1) {
+    h = std::min(h, t1 - t);
+    if (h < h_min)
+      throw IntegrationFailure("integrate_stiff: step size collapsed at t = " + std::to_string(t));
+    bool ok;
+    double weight;
+    if (!have_history) {
+      ok = be(t + h, h, u, Yf.get()) && be(t + 0.5 * h, 0.5 * h, u, Ym.get()) &&
+           be(t + h, 0.5 * h, Ym.get(), y_half);
+      weight = 1.0;
+    } else {
+      const double rho_full = h / h_prev;
+      const double rho_mid = 0.5 * h / h_prev;
+      ok = bdf2(t + h, h, rho_full, u_prev, u, Yf.get()) &&
+           bdf2(t + 0.5 * h, 0.5 * h, rho_mid, u_prev, u, Ym.get()) &&
+           bdf2(t + h, 0.5 * h, 1.0, u, Ym.get(), y_half);
+      const double c_full = bdf2_coeff(rho_full);
+      const double c_half = ((4.0 / 3.0) * bdf2_coeff(rho_mid) + bdf2_coeff(1.0)) / 8.0;
+      weight = std::clamp(c_half / (c_full - c_half), 0.05, 2.0);
+    }
+    if (!ok) {
+      h *= 0.5;
+      ++ss.rejected;
+      continue;
+    }
+    SMC_CUDA(cudaMemsetAsync(slots.get(), 0, 2 * sizeof(double), st));
+    stiff_norms_kernel<<<grid_for(dim), 256, 0, st>>>(
+        Yf.get(), y_half, dim, reinterpret_cast<unsigned long long*>(slots.get()));
+    SMC_CHECK_LAUNCH();
+    SMC_CUDA(cudaMemcpyAsync(host, slots.get(), sizeof(host), cudaMemcpyDeviceToHost, st));
+    SMC_CUDA(cudaStreamSynchronize(st));
+    const double err = weight * host[0];
+    const double p = have_history ? 3.0 : 2.0;
+    const double tol = o.rtol * host[1] + o.atol;
+    if (err <= tol) {
+      stiff_correct_kernel<<<grid_for(dim), 256, 0, st>>>(y_half, Yf.get(), weight, dim);
+      SMC_CHECK_LAUNCH();
+      std::swap(u_prev, u);
+      std::swap(u, y_half);
+      t += h;
+      h_prev = h;
+      have_history = true;
+      ++ss.accepted;
+    } else {
+      ++ss.rejected;
+    }
+    double factor = err > 0.0 ? 0.9 * std::pow(tol / err, 1.0 / p) : 5.0;
+    factor = std::clamp(factor, 0.2, 5.0);
+    h *= factor;
+  }
+  SMC_CUDA(cudaMemcpyAsync(u_out, u, dim * sizeof(double), cudaMemcpyDeviceToDevice, st));
+  SMC_CUDA(cudaStreamSynchronize(st));
 }
 
 }  // namespace smc

@@ -26,6 +26,7 @@ struct StiffOpts {
   int max_newton_iters = 16;
   long long block = 0;   // 0: dense
   int interleaved = 0;   // component j of block b at j*nb + b (else b*block + j)
+  double initial_step_fraction = 1e-3;  // integrate_stiff's first step / span
 };
 
 // NewtonReport (stiff.hpp:22-27)
@@ -56,5 +57,17 @@ class DeviceNewton {
   long long piv_n_ = 0;
   double* host_slots_ = nullptr;  // pinned readback
 };
+
+// integrate_stiff (proj/core/src/stiff.cpp:80-188): adaptive backward Euler,
+// then variable-step BDF2, error-controlled by step doubling, every implicit
+// stage through DeviceNewton (so a block-local f gets the batched solver).
+// Device pointers of f.dim() doubles; the step control runs on the host and
+// reads two norms per attempted step.  Throws InvalidArgument for t1 < t0 or
+// bad tolerances and IntegrationFailure when the step size collapses.
+struct StiffStats {
+  int accepted = 0, rejected = 0;
+};
+void integrate_stiff(RhsOp& f, const double* u0, double t0, double t1, double* u_out,
+                     const StiffOpts& o, StiffStats* stats = nullptr);
 
 }  // namespace smc

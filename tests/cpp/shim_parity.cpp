@@ -177,6 +177,19 @@ int main() {
               br.converged == rr.converged,
           "solve_backward_euler bitwise", std::fabs(wb[0] - wr[0]));
   }
+  // integrate_stiff (stiff.cpp:115-188) on the stiff forced oscillator
+  {
+    const double sigma = 1.0e4;
+    nsdc::Rhs f = [sigma](double t, const nsdc::Field& u, nsdc::Field& out) {
+      out.resize(u.size());
+      for (std::size_t i = 0; i < u.size(); ++i) out[i] = -sigma * (u[i] - std::cos(t)) - std::sin(t);
+    };
+    nsdc::StiffOptions so;
+    B::StiffOptions bso;
+    const nsdc::Field ur = nsdc::integrate_stiff(f, {1.0}, 0.0, 1.0, so);
+    const B::Field ub = B::integrate_stiff(f, {1.0}, 0.0, 1.0, bso);
+    check(ub[0] == ur[0], "integrate_stiff bitwise", std::fabs(ub[0] - ur[0]));
+  }
   // error behaviour mirrors the reference (pde_test.cpp:243-263)
   {
     bool threw = false;

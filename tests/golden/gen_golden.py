@@ -21,6 +21,10 @@ Contents (all fp64):
                                              of 0.01; oscc = sigma 1e3, GL(5)/TypeC{GL(3),2},
                                              K=4, 2 steps of 0.01.  meta = sweeps, f1, f2,
                                              implicit solves, Newton f1 evals
+  st_<case>_u0 / _u                          integrate_stiff: rob1 = one Robertson cell
+                                             to t = 1, rob4 = four interleaved cells to
+                                             t = 0.5 (rtol 1e-6), osc = sigma 1e4 forced
+                                             oscillator (f1 + f2) to t = 1
   q_gl3, s_gl3, q_gl5, s_gl5, nodes_gl9,     quadrature tables
   q_cc5, s_cc5, h_*                          build_hierarchy(GL3, TypeB GL5)
 """
@@ -131,6 +135,24 @@ def main():
         g[f"m2_{name}_meta"] = np.array([dg[k] for k in ("sweeps", "f1_evals", "f2_evals",
                                                          "implicit_solves", "newton_f1_evals")],
                                         dtype=np.float64)
+
+    # integrate_stiff (stiff.cpp:115-188): one Robertson cell to t = 1, four
+    # interleaved cells to t = 0.5 (rtol 1e-6), the forced oscillator to t = 1
+    import math
+    def osc_full(t, up, op, nd, ctx):
+        for i in range(nd):
+            op[i] = -1.0e4 * (up[i] - math.cos(t)) - math.sin(t)
+    rob1, _ = MP.np_callbacks("robertson", ncell=1, inter=False)
+    rob4, _ = MP.np_callbacks("robertson", ncell=4, inter=True)
+    stiff_cases = {
+        "rob1": (rob1, MP.robertson_u0(1, False), 1.0, {}),
+        "rob4": (rob4, MP.robertson_u0(4, True), 0.5, dict(rtol=1e-6, atol=1e-10)),
+        "osc": (osc_full, np.array([1.0]), 1.0, {}),
+    }
+    for name, (fn, u0s, t1s, kw) in stiff_cases.items():
+        rc, us, msg = O.ref_integrate_stiff(O.RHS_CB(fn), u0s, 0.0, t1s, **kw)
+        assert rc == 0, msg
+        g[f"st_{name}_u0"], g[f"st_{name}_u"] = u0s, us
 
     for fam, nm, sz in ((0, "gl", 3), (0, "gl", 5), (1, "cc", 5)):
         nodes, q, s = O.ref_integration_matrices(fam, sz)

@@ -140,3 +140,45 @@ def test_mode2_with_vanishing_implicit_term_equals_mode1():
         O.dp(arrs[5]), O.ip(foc), O.ip(pm), 4, C.c_double(0.0), O.dp(uo), O.dp(res), 16,
         C.byref(sw), C.byref(n1), C.byref(n2)) == 0
     assert abs(u2[0] - uo[0]) <= 1e-15
+
+
+STIFF = {"rob1": ({}, 1.0, 1, False), "rob4": (dict(rtol=1e-6, atol=1e-10), 0.5, 4, True),
+         "osc": ({}, 1.0, 0, False)}
+
+
+def _stiff_cb(name):
+    import math
+    if name == "osc":
+        def f(t, up, op, n, ctx):
+            for i in range(n):
+                op[i] = -1.0e4 * (up[i] - math.cos(t)) - math.sin(t)
+        return O.RHS_CB(f)
+    ncell, inter = STIFF[name][2], STIFF[name][3]
+    return O.RHS_CB(MP.np_callbacks("robertson", ncell=ncell, inter=inter)[0])
+
+
+@pytest.mark.parametrize("name", list(STIFF))
+def test_integrate_stiff_oracle_equals_reference_golden(golden, name):
+    """or_integrate_stiff (oracle.c) restates stiff.cpp:80-188 bit for bit;
+    rob4 also through the block (3, interleaved) Newton."""
+    kw, t1, ncell, inter = STIFF[name]
+    cb = _stiff_cb(name)
+    rc, u, acc, rej = O.integrate_stiff(cb, golden[f"st_{name}_u0"], 0.0, t1, **kw)
+    assert rc == 0 and acc > 0
+    assert np.array_equal(u, golden[f"st_{name}_u"])
+    if inter:
+        rc, ub, _, _ = O.integrate_stiff(cb, golden[f"st_{name}_u0"], 0.0, t1, block=3,
+                                         interleaved=True, **kw)
+        assert rc == 0 and np.array_equal(ub, golden[f"st_{name}_u"])
+
+
+@pytest.mark.skipif(not O.have_ref(), reason="oracle/_ref not built (no /root/reference)")
+def test_integrate_stiff_errors_match_reference():
+    cb = _stiff_cb("rob1")
+    u0 = MP.robertson_u0(1, False)
+    rc, _, msg = O.ref_integrate_stiff(cb, u0, 1.0, 0.0)
+    assert rc == 1 and "t1 must be >= t0" in msg
+    assert O.integrate_stiff(cb, u0, 1.0, 0.0)[0] == 1
+    rc, _, msg = O.ref_integrate_stiff(cb, u0, 0.0, 1.0, rtol=0.0)
+    assert rc == 1 and "bad tolerances" in msg
+    assert O.integrate_stiff(cb, u0, 0.0, 1.0, rtol=0.0)[0] == 1
