@@ -53,7 +53,7 @@ def main():
     bw = 6531.9e9
     try:
         bw = json.load(open(os.path.join(os.path.dirname(__file__), "..",
-                                         "MEASURED_PEAKS.json")))["hbm_copy_gbps"] * 1e9
+                                         "MEASURED_PEAKS.json")))["hbm_gbs"] * 1e9
     except Exception:
         pass
     flops = peak * 1e12 if peak else 34.2e12
