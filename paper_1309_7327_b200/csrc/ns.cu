@@ -605,7 +605,7 @@ void set_smem(K kern, std::size_t bytes) {
 
 template <int S>
 void rhs_v2(const Geo& g, const double* U, const double* F, double* A, double* GR, double* MX,
-            double* SC, double* out, const StencilM& M, cudaStream_t st) {
+            double* SC, double* out, const StencilM& M, int chem, cudaStream_t st) {
   static bool configured = false;
   const std::size_t sm = sizeof(DirSmem);
   if (!configured) {
@@ -636,7 +636,7 @@ void rhs_v2(const Geo& g, const double* U, const double* F, double* A, double* G
   SMC_CHECK_LAUNCH();
   ns_phase_b<2><<<dir_grid<2>(g, g.nz), DT_THREADS, sizeof(PBSmem), st>>>(F, A, MX, SC + 80 * n, g);
   SMC_CHECK_LAUNCH();
-  ns_assemble2<<<blocks(n), 256, 0, st>>>(F, A, SC, out, g);
+  ns_assemble2<<<blocks(n), 256, 0, st>>>(F, A, SC, U, out, g, chem);
   SMC_CHECK_LAUNCH();
 }
 
@@ -682,9 +682,11 @@ void NsWorkspace::rhs(const double* U, double* out, int part, cudaStream_t st) {
   SMC_CHECK_LAUNCH();
   if (part != kNsChem && !ns_v1()) {
     if (s_ == 4)
-      rhs_v2<4>(g, U, F, A, grad_.get(), mixed_.get(), scratch_.get(), out, M_, st);
+      rhs_v2<4>(g, U, F, A, grad_.get(), mixed_.get(), scratch_.get(), out, M_,
+                part == kNsFull, st);
     else
-      rhs_v2<3>(g, U, F, A, grad_.get(), mixed_.get(), scratch_.get(), out, M_, st);
+      rhs_v2<3>(g, U, F, A, grad_.get(), mixed_.get(), scratch_.get(), out, M_,
+                part == kNsFull, st);
   } else if (part != kNsChem) {
     hyp_kernel<<<blocks(n), 256, 0, st>>>(U, F, out, g, 1);
     SMC_CHECK_LAUNCH();
@@ -698,7 +700,7 @@ void NsWorkspace::rhs(const double* U, double* out, int part, cudaStream_t st) {
     assemble_kernel<<<blocks(n), 256, 0, st>>>(F, A, mixed_.get(), out, g);
     SMC_CHECK_LAUNCH();
   }
-  if (part == kNsFull) {
+  if (part == kNsFull && ns_v1()) {  // v2 forms wdot inside ns_assemble2
     wdot_kernel<<<blocks(n), 256, 0, st>>>(U, F, out, g);
     SMC_CHECK_LAUNCH();
   }
