@@ -58,7 +58,13 @@ struct IntegralP {
   int rows, ng;
 };
 
+// The weight table is copied to shared memory once per block: indexed by the
+// runtime row it would otherwise be a dependent constant-bank load per FMA.
 __global__ void __launch_bounds__(256) integrals_kernel(const IntegralP p) {
+  __shared__ double ws[kMaxRows][kMaxTerms];
+  for (int t = threadIdx.x; t < kMaxRows * kMaxTerms; t += blockDim.x)
+    ws[t / kMaxTerms][t % kMaxTerms] = p.w[t / kMaxTerms][t % kMaxTerms];
+  __syncthreads();
   const long long stride = static_cast<long long>(gridDim.x) * blockDim.x;
   for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < p.n;
        i += stride) {
@@ -67,10 +73,10 @@ __global__ void __launch_bounds__(256) integrals_kernel(const IntegralP p) {
     for (int j = 0; j < kMaxTerms; ++j)
       if (j < p.ng) gv[j] = p.g[j][i];
     for (int r = 0; r < p.rows; ++r) {
-      double acc = p.w[r][0] * gv[0];
+      double acc = ws[r][0] * gv[0];
 #pragma unroll
       for (int j = 1; j < kMaxTerms; ++j)
-        if (j < p.ng) acc = __fma_rn(p.w[r][j], gv[j], acc);
+        if (j < p.ng) acc = __fma_rn(ws[r][j], gv[j], acc);
       p.out[r][i] = __dmul_rn(p.dt, acc);
     }
   }
