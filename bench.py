@@ -53,6 +53,10 @@ def parse():
                    help="N>1: interior planes run while the halo is in flight (split launch)")
     p.add_argument("--slab", action="store_true",
                    help="use the multi-GPU z-slab path also at N=1 (ghosts by self-copy)")
+    p.add_argument("--halo", choices=["peer", "nccl"], default="peer",
+                   help="slab halo: peer = the kernel reads the neighbours' planes over "
+                        "CUDA IPC / NVLink (falls back to nccl if the mapping fails); "
+                        "nccl = send/recv into ghost planes before the kernel")
     return p.parse_args()
 
 
@@ -363,6 +367,7 @@ def main():
 
     # ---- inputs resident in HBM
     slab_mode = world > 1 or args.slab
+    halo = None
     if not slab_mode:
         a, u = W.narrow3d_inputs(n, xp=torch, device=dev)
         op = P.Narrow3DOperator(a, 1 / n, 1 / n, 1 / n)
@@ -385,14 +390,35 @@ def main():
         for k, A, p in zip(ks, amps, ph):
             u += A * torch.sin(tw * (k[0] * x.view(1, 1, n) + k[1] * x.view(1, n, 1)
                                      + k[2] * zg.view(-1, 1, 1)) + p)
-        dop = DistributedNarrow3D(a, slab, 1 / n, 1 / n, 1 / n, dist, exchange_a=False)
-        if args.kc:
-            dop.op.set_kc(args.kc)
-        op = dop.op
         out = torch.empty((n, n, n), dtype=torch.float64, device=dev)
+        halo = args.halo
+        if halo == "peer":
+            try:
+                from paper_1309_7327_b200.distributed import PeerNarrow3D
+                pdop = PeerNarrow3D(a, slab, 1 / n, 1 / n, 1 / n, dist if world > 1 else None,
+                                    exchange_a=False, sync="nccl")
+                for b in pdop.bufs:
+                    b.copy_(u[4:4 + n])
+            except Exception as exc:  # noqa: BLE001  (a GPU path either way)
+                print(f"peer halo unavailable ({exc}); using the NCCL exchange", file=sys.stderr)
+                halo = "nccl"
+        if halo == "peer":
+            if args.kc:
+                pdop.op.set_kc(args.kc)
+            op = pdop.op
+            counter = [0]
 
-        def step():
-            dop.apply(u, out, overlap=args.overlap)
+            def step():
+                pdop.apply(counter[0], out)
+                counter[0] += 1
+        else:
+            dop = DistributedNarrow3D(a, slab, 1 / n, 1 / n, 1 / n, dist, exchange_a=False)
+            if args.kc:
+                dop.op.set_kc(args.kc)
+            op = dop.op
+
+            def step():
+                dop.apply(u, out, overlap=args.overlap)
 
     def barrier():
         if world > 1:
@@ -474,11 +500,20 @@ def main():
         oh = torch.empty((n, n, n), dtype=torch.float64).pin_memory()
         uh.copy_(u[4:4 + n].cpu())
 
-        def e2e_step():
-            u[4:4 + n].copy_(uh, non_blocking=True)
-            dop.apply(u, out, overlap=args.overlap)
-            oh.copy_(out, non_blocking=True)
-            torch.cuda.current_stream().synchronize()
+        if halo == "peer":
+            def e2e_step():
+                i = counter[0]
+                pdop.buffer(i).copy_(uh, non_blocking=True)
+                pdop.apply(i, out)
+                counter[0] += 1
+                oh.copy_(out, non_blocking=True)
+                torch.cuda.current_stream().synchronize()
+        else:
+            def e2e_step():
+                u[4:4 + n].copy_(uh, non_blocking=True)
+                dop.apply(u, out, overlap=args.overlap)
+                oh.copy_(out, non_blocking=True)
+                torch.cuda.current_stream().synchronize()
     e2e_step()
     barrier()
     f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -526,7 +561,9 @@ def main():
                 "workload": f"configs[1] narrow 8th-order (a U_x)_x+(a U_y)_y+(a U_z)_z, "
                             f"{n}^3 per GPU, periodic" +
                             ("" if not slab_mode else f", z-slabs of a {n}x{n}x{n * world} box, "
-                                                      "4-plane NCCL halo" + (", overlapped" if args.overlap else "")),
+                                                      + ("4-plane halo read by the kernel over peer memory (CUDA IPC / NVLink)"
+                                                         if halo == "peer" else
+                                                         "4-plane NCCL halo" + (", overlapped" if args.overlap else ""))),
                 "cells_per_gpu": cells_rank, "stencil": "SMC (m47=3557/44100, m48=-2083/117600)",
                 "l2": f"inputs larger than L2 ({(2 * 8 * cells_rank) / 1e6:.0f} MB read + "
                       f"{8 * cells_rank / 1e6:.0f} MB written per step per GPU)",

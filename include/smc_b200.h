@@ -158,6 +158,26 @@ int smc_narrow3d_create_slab(int nx, int ny, int nz, int zghost, double dx, doub
 /* Interior planes [kbeg, kend) only, so the interior can run while the halo
  * is in flight and the boundary planes after it lands. */
 int smc_narrow3d_apply_planes(smc_rhs* op, const double* u, double* out, int kbeg, int kend);
+/* Peer halo (multi-GPU without an exchange step): apply a slab operator
+ * (smc_narrow3d_create_slab, zghost >= S, coefficient ghosts filled once) to
+ * u holding only the nz interior planes; the S planes below / above are read
+ * inside the kernel from the neighbours' interior arrays u_lo (nz_lo planes,
+ * its top planes are used) and u_hi (its bottom planes).  The pointers are
+ * device addresses valid in this process: a neighbour GPU's buffer opened
+ * with smc_ipc_import (peer loads over NVLink) or another buffer on this
+ * device.  The caller orders the neighbours' writes before the call (e.g. a
+ * stream-ordered NCCL all-reduce of one element) and keeps the buffers alive. */
+int smc_narrow3d_apply_peer(smc_rhs* h, const double* u, const double* u_lo, int nz_lo,
+                            const double* u_hi, double* out, int kbeg, int kend);
+/* CUDA IPC of device buffers between the processes of one node.  Export
+ * whole allocations (e.g. from smc_device_alloc): the importer maps the
+ * allocation base. */
+#define SMC_IPC_HANDLE_BYTES 64
+int smc_device_alloc(long long nbytes, void** dptr);
+int smc_device_free(void* dptr);
+int smc_ipc_export(const void* dptr, unsigned char* handle /* SMC_IPC_HANDLE_BYTES */);
+int smc_ipc_import(const unsigned char* handle, void** dptr);
+int smc_ipc_close(void* dptr);
 /* z planes per CTA of the narrow kernel (tuning knob; 0 = heuristic). */
 int smc_narrow3d_set_kc(smc_rhs* op, int kc);
 

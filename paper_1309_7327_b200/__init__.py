@@ -234,8 +234,21 @@ class Narrow3DSlab(_Rhs):
     def apply_planes(self, u, out, kbeg: int, kend: int) -> None:
         check(_capi.lib().smc_narrow3d_apply_planes(self._h, dptr(u), dptr(out), kbeg, kend))
 
+    def apply_peer(self, u, u_lo, nz_lo: int, u_hi, out, kbeg: int = 0, kend: int = None) -> None:
+        """Peer halo: u holds only the nz interior planes; the ghost planes are
+        read in the kernel from the neighbours' interior arrays u_lo / u_hi
+        (tensors on this device or raw device pointers, e.g. IPC-mapped)."""
+        kend = self.nz if kend is None else kend
+        check(_capi.lib().smc_narrow3d_apply_peer(self._h, dptr(u), _ptr(u_lo), nz_lo, _ptr(u_hi),
+                                                  dptr(out), kbeg, kend))
+
     def set_kc(self, kc: int) -> None:
         check(_capi.lib().smc_narrow3d_set_kc(self._h, kc))
+
+
+def _ptr(x):
+    """device pointer of a tensor, or a raw integer pointer as given"""
+    return x if isinstance(x, int) else dptr(x)
 
 
 class _CudaPtr:

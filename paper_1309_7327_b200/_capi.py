@@ -85,6 +85,12 @@ _SIG = {
                                            C.c_double, C.c_double, C.c_int, _D, C.c_int, _VP,
                                            C.c_int, C.POINTER(_VP)]),
     "smc_narrow3d_apply_planes": (C.c_int, [_VP, _VP, _VP, C.c_int, C.c_int]),
+    "smc_narrow3d_apply_peer": (C.c_int, [_VP, _VP, _VP, C.c_int, _VP, _VP, C.c_int, C.c_int]),
+    "smc_ipc_export": (C.c_int, [_VP, C.c_char_p]),
+    "smc_ipc_import": (C.c_int, [C.c_char_p, C.POINTER(_VP)]),
+    "smc_ipc_close": (C.c_int, [_VP]),
+    "smc_device_alloc": (C.c_int, [C.c_longlong, C.POINTER(_VP)]),
+    "smc_device_free": (C.c_int, [_VP]),
     "smc_ns_create": (C.c_int, [C.c_int, C.c_int, C.c_int, C.c_int, C.c_double, C.c_double,
                                 C.c_double, C.c_int, _D, C.c_int, C.POINTER(_VP), C.POINTER(_VP),
                                 C.POINTER(_VP)]),

@@ -246,6 +246,53 @@ int smc_narrow3d_apply_planes(smc_rhs* h, const double* u, double* out, int kbeg
   });
 }
 
+int smc_narrow3d_apply_peer(smc_rhs* h, const double* u, const double* u_lo, int nz_lo,
+                            const double* u_hi, double* out, int kbeg, int kend) {
+  return guarded([&] {
+    need(u, "u"), need(u_lo, "u_lo"), need(u_hi, "u_hi"), need(out, "out");
+    auto* op = dynamic_cast<smc::Narrow3DOp*>(&op_of(h));
+    if (!op) throw smc::InvalidArgument("smc_narrow3d_apply_peer: not a narrow3d operator");
+    op->eval_planes_peer(u, u_lo, nz_lo, u_hi, out, kbeg, kend);
+  });
+}
+
+int smc_ipc_export(const void* dptr, unsigned char* handle) {
+  return guarded([&] {
+    need(dptr, "dptr"), need(handle, "handle");
+    cudaIpcMemHandle_t hd;
+    SMC_CUDA(cudaIpcGetMemHandle(&hd, const_cast<void*>(dptr)));
+    static_assert(sizeof(hd) == SMC_IPC_HANDLE_BYTES, "IPC handle size");
+    std::memcpy(handle, &hd, sizeof(hd));
+  });
+}
+
+int smc_ipc_import(const unsigned char* handle, void** dptr) {
+  return guarded([&] {
+    need(handle, "handle"), need(dptr, "dptr");
+    cudaIpcMemHandle_t hd;
+    std::memcpy(&hd, handle, sizeof(hd));
+    SMC_CUDA(cudaIpcOpenMemHandle(dptr, hd, cudaIpcMemLazyEnablePeerAccess));
+  });
+}
+
+int smc_ipc_close(void* dptr) {
+  return guarded([&] { SMC_CUDA(cudaIpcCloseMemHandle(dptr)); });
+}
+
+int smc_device_alloc(long long nbytes, void** dptr) {
+  return guarded([&] {
+    need(dptr, "dptr");
+    smc::require(nbytes > 0, "smc_device_alloc: size must be positive");
+    SMC_CUDA(cudaMalloc(dptr, static_cast<std::size_t>(nbytes)));
+  });
+}
+
+int smc_device_free(void* dptr) {
+  return guarded([&] {
+    if (dptr) SMC_CUDA(cudaFree(dptr));
+  });
+}
+
 int smc_narrow3d_set_kc(smc_rhs* h, int kc) {
   return guarded([&] {
     auto* op = dynamic_cast<smc::Narrow3DOp*>(&op_of(h));

@@ -303,6 +303,9 @@ int narrow_default_kc(int nx, int ny, int nz, int dims, int num_sms) {
 void launch_narrow(const NarrowArgs& p, int s, const StencilM& M, cudaStream_t st) {
   require(s == 3 || s == 4, "narrow: half width must be 3 or 4");
   require(p.kc >= 1, "narrow: kc >= 1");
+  require(!p.zpeer || (p.use_fast && narrow3d_fast_applicable(p) && p.u_lo && p.u_hi),
+          "narrow: the peer halo needs the fast 3-D kernel (nx % 32, ny % 8, 16-byte "
+          "aligned fields) and both neighbour arrays");
   if (s == 4)
     launch_s<4>(p, M, st);
   else

@@ -22,6 +22,15 @@ struct NarrowArgs {
   int kbeg = 0, kend = -1;     // plane range [kbeg, kend) to compute (kend < 0: nz)
   bool zwrap = true;
   bool use_fast = true;         // allow the narrow3d_fast kernel
+  // Peer halo (multi-GPU, narrow3d_fast only): u holds the nz interior planes
+  // and the planes below / above come straight from the neighbours' interior
+  // arrays (device pointers valid here: CUDA IPC / peer access over NVLink,
+  // or another buffer on this device), so no exchange step precedes the
+  // kernel.  u_lo + lo_len is the end of the lower neighbour's interior.
+  const double* u_lo = nullptr;
+  const double* u_hi = nullptr;
+  long long lo_len = 0;
+  bool zpeer = false;
   double idx2 = 0, idy2 = 0, idz2 = 0, gt = 0;
 };
 

@@ -114,6 +114,15 @@ __device__ __forceinline__ void march_segment(FastSmem<FXT>& sm, const NarrowArg
     return o;
   };
 
+  // plane base of U (offset o = k * plane from the interior start): the peer
+  // halo reads ghost planes from the neighbours' arrays
+  auto ub = [&](long long o) -> const double* {
+    if (!p.zpeer) return p.u + o;
+    if (o < 0) return p.u_lo + (p.lo_len + o);
+    if (o >= zspan) return p.u_hi + (o - zspan);
+    return p.u + o;
+  };
+
   // staging plan: in-plane offsets of this thread's 16-byte chunks
   int soff[CPT];
 #pragma unroll
@@ -129,7 +138,7 @@ __device__ __forceinline__ void march_segment(FastSmem<FXT>& sm, const NarrowArg
     for (int i = 0; i < CPT; ++i) {
       const int c = threadIdx.x + i * FT;
       if (i + 1 < CPT || c < CHUNKS) {
-        cp16(&sm.tile[buf][0][2 * c], p.u + po + soff[i]);
+        cp16(&sm.tile[buf][0][2 * c], ub(po) + soff[i]);
         cp16(&sm.tile[buf][1][2 * c], p.cz + po + soff[i]);
       }
     }
@@ -141,6 +150,9 @@ __device__ __forceinline__ void march_segment(FastSmem<FXT>& sm, const NarrowArg
   auto ld2 = [&](const double* base, long long o) {
     return __ldg(reinterpret_cast<const double2*>(base + o + col_off));
   };
+  auto ld2u = [&](long long o) {
+    return __ldg(reinterpret_cast<const double2*>(ub(o) + col_off));
+  };
 
   // z window (2 columns): slot j holds plane k - S + 1 + j at step k
   double2 wu[WIN], wa[WIN];
@@ -149,7 +161,7 @@ __device__ __forceinline__ void march_segment(FastSmem<FXT>& sm, const NarrowArg
     long long o = zoff(k0 - S);
 #pragma unroll
     for (int j = 0; j < WIN; ++j) {
-      wu[j] = ld2(p.u, o);
+      wu[j] = ld2u(o);
       wa[j] = ld2(p.cz, o);
       o = zadv(o);
     }
@@ -160,7 +172,7 @@ __device__ __forceinline__ void march_segment(FastSmem<FXT>& sm, const NarrowArg
 #pragma unroll
   for (int j = 0; j < 2; ++j) {
     if (k0 + j < k1) {
-      pf_u[j] = ld2(p.u, o_pf);
+      pf_u[j] = ld2u(o_pf);
       pf_a[j] = ld2(p.cz, o_pf);
     }
     o_pf = zadv(o_pf);
@@ -220,7 +232,7 @@ __device__ __forceinline__ void march_segment(FastSmem<FXT>& sm, const NarrowArg
     pf_u[0] = pf_u[1];
     pf_a[0] = pf_a[1];
     if (k + 2 < k1) {
-      pf_u[1] = ld2(p.u, o_pf);
+      pf_u[1] = ld2u(o_pf);
       pf_a[1] = ld2(p.cz, o_pf);
       o_pf = zadv(o_pf);
     }

@@ -121,6 +121,27 @@ void Narrow3DOp::eval_planes(const double* u, double* out, int kb, int ke) {
   launch_narrow(p, s_, M_, stream_);
 }
 
+void Narrow3DOp::eval_planes_peer(const double* u, const double* u_lo, int nz_lo,
+                                  const double* u_hi, double* out, int kb, int ke) {
+  require(zghost_ >= s_, "narrow3d: the peer halo needs a slab operator");
+  require(nz_lo >= s_, "narrow3d: the lower neighbour holds fewer than S planes");
+  require(nz_ >= s_, "narrow3d: the peer halo needs at least S interior planes");
+  const long long plane = static_cast<long long>(nx_) * ny_;
+  NarrowArgs p;
+  p.u = u;
+  p.cx = p.cy = p.cz = a_.get() + zghost_ * plane;
+  p.out = out;
+  p.nx = nx_, p.ny = ny_, p.nz = nz_;
+  p.dims = 3;
+  p.kc = kc_;
+  p.kbeg = kb, p.kend = ke;
+  p.zwrap = false;
+  p.zpeer = true;
+  p.u_lo = u_lo, p.u_hi = u_hi, p.lo_len = nz_lo * plane;
+  p.idx2 = 1.0 / (dx_ * dx_), p.idy2 = 1.0 / (dy_ * dy_), p.idz2 = 1.0 / (dz_ * dz_);
+  launch_narrow(p, s_, M_, stream_);
+}
+
 void Narrow3DOp::eval_device(double, const double* u, double* out) {
   require(zghost_ == 0, "narrow3d: a ghosted (slab) operator is applied with apply_planes");
   eval_planes(u, out, 0, nz_);

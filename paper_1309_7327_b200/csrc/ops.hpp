@@ -93,6 +93,11 @@ class Narrow3DOp final : public RhsOp {
   int zghost() const { return zghost_; }
   // interior planes [kb, ke) only (overlap of halo exchange and compute)
   void eval_planes(const double* u, double* out, int kb, int ke);
+  // slab operator, peer halo: u holds the nz interior planes, the S planes
+  // below / above are read from the neighbours' interior arrays u_lo (nz_lo
+  // planes) and u_hi in the kernel itself
+  void eval_planes_peer(const double* u, const double* u_lo, int nz_lo, const double* u_hi,
+                        double* out, int kb, int ke);
   // Host buffers: z-chunked pipeline, so the host->device copy of chunk c+1,
   // the stencil on chunk c and the device->host copy of chunk c-1 overlap
   // (the link is full duplex; the kernel is ~10x faster than either copy).

@@ -205,3 +205,107 @@ class DistributedNs:
     def rhs(self, part: int = 0):
         from . import DeviceCallbackRhs
         return DeviceCallbackRhs(self.dim, lambda t, u, out: self.apply(u, out, part))
+
+
+# ----------------------------------------------- peer halo (no exchange step)
+def ipc_export(t) -> bytes:
+    """CUDA IPC handle (64 bytes) of a device tensor's allocation base."""
+    import ctypes as C
+    from . import _capi, check
+    buf = C.create_string_buffer(64)
+    check(_capi.lib().smc_ipc_export(C.c_void_p(t.data_ptr()), buf))
+    return buf.raw
+
+
+def ipc_import(handle: bytes) -> int:
+    """Device pointer (int) of a buffer exported by another process."""
+    import ctypes as C
+    from . import _capi, check
+    p = C.c_void_p()
+    check(_capi.lib().smc_ipc_import(handle, C.byref(p)))
+    return p.value
+
+
+class PeerNarrow3D:
+    """configs[1]/[3] with the halo read over peer memory: every rank owns two
+    interior-only u buffers (double-buffered by step parity) exported by CUDA
+    IPC; the slab kernel loads its S ghost planes straight from the
+    neighbours' buffers (NVLink peer loads), so there is no exchange step and
+    no ghost copy of u.  Per step one stream-ordered one-element all-reduce
+    (sync="nccl") orders every rank's writes of buffer (step % 2) before the
+    kernels that read it; the other buffer is free for the next step's writes.
+    sync="host" (gloo, tests) synchronises the device and uses a host barrier.
+    With one rank the neighbours are the rank itself (periodic)."""
+
+    def __init__(self, a_local, slab: Slab, dx, dy, dz, dist=None, choice=None,
+                 exchange_a=True, sync: str = "nccl"):
+        import torch
+        from . import Narrow3DSlab
+        self.slab, self.dist, self.sync = slab, dist, sync
+        if exchange_a and slab.world > 1:
+            for r in exchange_halo(a_local, slab, dist):
+                r.wait()
+        elif exchange_a:
+            exchange_halo(a_local, slab, dist)
+        self.op = Narrow3DSlab(a_local, slab.nz, slab.ghost, dx, dy, dz, choice)
+        self.op.set_stream(torch.cuda.current_stream())
+        import ctypes as C
+        from . import _capi, check, device_tensor
+        nzg, ny, nx = a_local.shape
+        n = slab.nz * ny * nx
+        # whole cudaMalloc allocations: an IPC handle maps the allocation base
+        self._raw = []
+        self.bufs = []
+        for _ in range(2):
+            p = C.c_void_p()
+            check(_capi.lib().smc_device_alloc(8 * n, C.byref(p)))
+            self._raw.append(p.value)
+            self.bufs.append(device_tensor(p.value, n).view(slab.nz, ny, nx))
+            self.bufs[-1].zero_()
+        self._imported = []
+        if slab.world == 1:
+            self.lo = [b.data_ptr() for b in self.bufs]
+            self.hi = list(self.lo)
+        else:
+            mine = [ipc_export(b) for b in self.bufs]
+            allh = [None] * slab.world
+            dist.all_gather_object(allh, mine)
+            cache = {}
+
+            def open_rank(r):
+                if r not in cache:
+                    cache[r] = [ipc_import(h) for h in allh[r]]
+                    self._imported += cache[r]
+                return cache[r]
+            self.lo = open_rank(slab.prev)
+            self.hi = open_rank(slab.next)
+        self._tick = torch.zeros(1, dtype=torch.float64, device=a_local.device)
+
+    def buffer(self, step: int):
+        """The interior u buffer to fill for this step."""
+        return self.bufs[step % 2]
+
+    def apply(self, step: int, out) -> None:
+        """out (nz planes) = operator(u of this step) over the peer halo."""
+        import torch
+        i = step % 2
+        if self.slab.world > 1:
+            if self.sync == "nccl":
+                self.dist.all_reduce(self._tick)        # stream-ordered across GPUs
+            else:
+                torch.cuda.synchronize()
+                self.dist.barrier()
+        self.op.apply_peer(self.bufs[i], self.lo[i], self.slab.nz, self.hi[i], out)
+
+    def close(self) -> None:
+        """Unmap the neighbours' buffers and free this rank's (after every
+        rank's last kernel that reads them)."""
+        import ctypes as C
+        from . import _capi
+        for p in self._imported:
+            _capi.lib().smc_ipc_close(C.c_void_p(p))
+        self._imported = []
+        self.bufs = []
+        for p in self._raw:
+            _capi.lib().smc_device_free(C.c_void_p(p))
+        self._raw = []

@@ -273,3 +273,105 @@ def test_narrow3d_host_pipeline_matches_device(cuda, nz):
         m, s = O.build_narrow(8, SMC)
         ref = O.narrow3d(m, s, a, u, 1.0 / nx, 1.0 / ny, 1.0 / nz)
         assert rel_err(out_h, ref) <= TOL
+
+
+def _slab_inputs(nx, ny, nzl, nslab, G=4, seed=7):
+    rng = np.random.default_rng(seed)
+    nz = nzl * nslab
+    a = 1.0 + 0.5 * rng.random((nz, ny, nx))
+    u = rng.standard_normal((nz, ny, nx))
+    return a, u, nz
+
+
+def test_peer_halo_slabs_equal_periodic(cuda):
+    """Three z-slabs on one device whose kernels read their ghost planes
+    straight from the neighbours' interior buffers (the peer-halo path a
+    multi-GPU run takes over NVLink) equal the periodic box bit for bit."""
+    torch = _torch()
+    nx, ny, nzl, G = 64, 16, 16, 4
+    a, u, nz = _slab_inputs(nx, ny, nzl, 3)
+    ch = P.StencilChoice.narrow8(*SMC)
+    full = P.Narrow3DOperator(a, 1.0 / nx, 1.0 / ny, 1.0 / nz, ch)(0.0, u)
+    us = [torch.from_numpy(np.ascontiguousarray(u[s * nzl:(s + 1) * nzl])).to(cuda)
+          for s in range(3)]
+    for s in range(3):
+        idx = [(s * nzl + k - G) % nz for k in range(nzl + 2 * G)]
+        ag = torch.from_numpy(np.ascontiguousarray(a[idx])).to(cuda)
+        op = P.Narrow3DSlab(ag, nzl, G, 1.0 / nx, 1.0 / ny, 1.0 / nz, ch)
+        out = torch.empty((nzl, ny, nx), dtype=torch.float64, device=cuda)
+        op.apply_peer(us[s], us[(s - 1) % 3], nzl, us[(s + 1) % 3], out)
+        torch.cuda.synchronize()
+        assert np.array_equal(out.cpu().numpy(), full[s * nzl:(s + 1) * nzl])
+
+
+def test_peer_narrow_single_rank_is_periodic(cuda):
+    """PeerNarrow3D at world 1 (its own neighbour, IPC-exportable buffers)."""
+    torch = _torch()
+    from paper_1309_7327_b200.distributed import PeerNarrow3D, Slab
+    nx, ny, nz, G = 64, 16, 32, 4
+    a, u, _ = _slab_inputs(nx, ny, nz, 1, seed=11)
+    ch = P.StencilChoice.narrow8(*SMC)
+    full = P.Narrow3DOperator(a, 1.0 / nx, 1.0 / ny, 1.0 / nz, ch)(0.0, u)
+    idx = [(k - G) % nz for k in range(nz + 2 * G)]
+    ag = torch.from_numpy(np.ascontiguousarray(a[idx])).to(cuda)
+    pn = PeerNarrow3D(ag, Slab(0, 1, nz), 1.0 / nx, 1.0 / ny, 1.0 / nz, choice=ch,
+                      exchange_a=False)
+    out = torch.empty((nz, ny, nx), dtype=torch.float64, device=cuda)
+    for step in range(3):
+        pn.buffer(step).copy_(torch.from_numpy(u).to(cuda))
+        pn.apply(step, out)
+        torch.cuda.synchronize()
+        assert np.array_equal(out.cpu().numpy(), full)
+    pn.close()
+
+
+def _peer_worker(rank, world, port, nx, ny, nzl, q):
+    import os
+    import torch
+    import torch.distributed as dist
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    try:
+        dist.init_process_group("gloo", rank=rank, world_size=world)
+        from paper_1309_7327_b200.distributed import PeerNarrow3D, Slab
+        G = 4
+        a, u, nz = _slab_inputs(nx, ny, nzl, world)
+        ch = P.StencilChoice.narrow8(*SMC)
+        full = P.Narrow3DOperator(a, 1.0 / nx, 1.0 / ny, 1.0 / nz, ch)(0.0, u)
+        z0 = rank * nzl
+        idx = [(z0 + k - G) % nz for k in range(nzl + 2 * G)]
+        ag = torch.from_numpy(np.ascontiguousarray(a[idx])).cuda()
+        pn = PeerNarrow3D(ag, Slab(rank, world, nzl), 1.0 / nx, 1.0 / ny, 1.0 / nz, dist=dist,
+                          choice=ch, exchange_a=False, sync="host")
+        out = torch.empty((nzl, ny, nx), dtype=torch.float64, device="cuda")
+        ok = True
+        for step in range(2):
+            pn.buffer(step).copy_(torch.from_numpy(np.ascontiguousarray(u[z0:z0 + nzl])).cuda())
+            pn.apply(step, out)
+            torch.cuda.synchronize()
+            ok = ok and np.array_equal(out.cpu().numpy(), full[z0:z0 + nzl])
+        dist.barrier()           # every rank's reads are done before unmapping
+        pn.close()
+        dist.destroy_process_group()
+        q.put((rank, ok, ""))
+    except Exception as exc:  # noqa: BLE001
+        q.put((rank, False, repr(exc)))
+
+
+def test_peer_halo_two_processes_ipc(cuda):
+    """Two ranks (processes) sharing this GPU: each maps its neighbours'
+    buffers through CUDA IPC and runs the slab kernel over the peer halo;
+    ordering by a host barrier (no kernel waits on another)."""
+    import socket
+    import torch.multiprocessing as mp
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_peer_worker, args=(r, 2, port, 64, 16, 16, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=300) for _ in procs]
+    for p in procs:
+        p.join(timeout=60)
+    assert all(ok for _, ok, _ in res), res
