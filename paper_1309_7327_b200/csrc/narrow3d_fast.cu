@@ -82,8 +82,10 @@ __device__ __forceinline__ double2 lds2(const double* p) {
   return *reinterpret_cast<const double2*>(p);
 }
 
-// One (tile, [k0, k1)) segment of the z-march.
-template <int S, int FXT>
+// One (tile, [k0, k1)) segment of the z-march.  PEER: ghost planes of U come
+// from the neighbours' arrays (a separate instantiation, so the common path
+// carries no per-plane pointer selection).
+template <int S, int FXT, bool PEER>
 __device__ __forceinline__ void march_segment(FastSmem<FXT>& sm, const NarrowArgs& p,
                                               const StencilM& M, int tile, int k0, int k1) {
   using G = NG<FXT>;
@@ -117,7 +119,7 @@ __device__ __forceinline__ void march_segment(FastSmem<FXT>& sm, const NarrowArg
   // plane base of U (offset o = k * plane from the interior start): the peer
   // halo reads ghost planes from the neighbours' arrays
   auto ub = [&](long long o) -> const double* {
-    if (!p.zpeer) return p.u + o;
+    if constexpr (!PEER) return p.u + o;
     if (o < 0) return p.u_lo + (p.lo_len + o);
     if (o >= zspan) return p.u_hi + (o - zspan);
     return p.u + o;
@@ -321,7 +323,7 @@ __device__ __forceinline__ void march_segment(FastSmem<FXT>& sm, const NarrowArg
 // co-scheduled CTAs are x/y neighbours at the same z and tile halos hit in
 // L2.  Persistent grid: CTA b owns the contiguous range [b*L/G, (b+1)*L/G)
 // of L = tile * nplanes + plane (one wave, equal work to within a plane).
-template <int S, int FXT>
+template <int S, int FXT, bool PEER>
 __global__ void __launch_bounds__(NG<FXT>::FT, NG<FXT>::OCC)
     narrow3d_fast(const NarrowArgs p, const StencilM M, int chunked) {
   using G = NG<FXT>;
@@ -330,7 +332,7 @@ __global__ void __launch_bounds__(NG<FXT>::FT, NG<FXT>::OCC)
   const int kend = p.kend < 0 ? p.nz : p.kend;
   if (chunked) {
     const int k0 = p.kbeg + blockIdx.y * p.kc;
-    march_segment<S, FXT>(sm, p, M, blockIdx.x, k0, min(k0 + p.kc, kend));
+    march_segment<S, FXT, PEER>(sm, p, M, blockIdx.x, k0, min(k0 + p.kc, kend));
     return;
   }
   const long long np = kend - p.kbeg;
@@ -341,7 +343,7 @@ __global__ void __launch_bounds__(NG<FXT>::FT, NG<FXT>::OCC)
     const int tile = static_cast<int>(l / np);
     const int kk = static_cast<int>(l - tile * np);
     const int len = static_cast<int>(min(np - kk, hi - l));
-    march_segment<S, FXT>(sm, p, M, tile, p.kbeg + kk, p.kbeg + kk + len);
+    march_segment<S, FXT, PEER>(sm, p, M, tile, p.kbeg + kk, p.kbeg + kk + len);
     l += len;
   }
 }
@@ -379,12 +381,12 @@ int fast_fx() {
   return f;
 }
 
-template <int S, int FXT>
+template <int S, int FXT, bool PEER>
 void launch_fast_s(const NarrowArgs& p, const StencilM& M, cudaStream_t st) {
   using G = NG<FXT>;
   static bool configured = false;
   if (!configured) {
-    SMC_CUDA(cudaFuncSetAttribute(narrow3d_fast<S, FXT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    SMC_CUDA(cudaFuncSetAttribute(narrow3d_fast<S, FXT, PEER>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   static_cast<int>(sizeof(FastSmem<FXT>))));
     configured = true;
   }
@@ -393,13 +395,13 @@ void launch_fast_s(const NarrowArgs& p, const StencilM& M, cudaStream_t st) {
   const int tiles = (p.nx / G::FX) * (p.ny / G::FY);
   if (chunked_grid()) {
     const dim3 grid(tiles, (kend - p.kbeg + p.kc - 1) / p.kc);
-    narrow3d_fast<S, FXT><<<grid, G::FT, sizeof(FastSmem<FXT>), st>>>(p, M, 1);
+    narrow3d_fast<S, FXT, PEER><<<grid, G::FT, sizeof(FastSmem<FXT>), st>>>(p, M, 1);
   } else {
     const long long work = static_cast<long long>(tiles) * (kend - p.kbeg);
     const long long by_kc = (work + p.kc - 1) / p.kc;
     const int grid =
         static_cast<int>(std::max(1LL, std::min<long long>(num_sms_cached() * G::OCC, by_kc)));
-    narrow3d_fast<S, FXT><<<grid, G::FT, sizeof(FastSmem<FXT>), st>>>(p, M, 0);
+    narrow3d_fast<S, FXT, PEER><<<grid, G::FT, sizeof(FastSmem<FXT>), st>>>(p, M, 0);
   }
   SMC_CHECK_LAUNCH();
 }
@@ -415,9 +417,15 @@ bool narrow3d_fast_applicable(const NarrowArgs& p) {
 
 void launch_narrow3d_fast(const NarrowArgs& p, int s, const StencilM& M, cudaStream_t st) {
   if (fast_fx() == 32) {
-    s == 4 ? launch_fast_s<4, 32>(p, M, st) : launch_fast_s<3, 32>(p, M, st);
+    if (p.zpeer)
+      s == 4 ? launch_fast_s<4, 32, true>(p, M, st) : launch_fast_s<3, 32, true>(p, M, st);
+    else
+      s == 4 ? launch_fast_s<4, 32, false>(p, M, st) : launch_fast_s<3, 32, false>(p, M, st);
   } else {
-    s == 4 ? launch_fast_s<4, 64>(p, M, st) : launch_fast_s<3, 64>(p, M, st);
+    if (p.zpeer)
+      s == 4 ? launch_fast_s<4, 64, true>(p, M, st) : launch_fast_s<3, 64, true>(p, M, st);
+    else
+      s == 4 ? launch_fast_s<4, 64, false>(p, M, st) : launch_fast_s<3, 64, false>(p, M, st);
   }
 }
 
