@@ -53,10 +53,12 @@ def parse():
                    help="N>1: interior planes run while the halo is in flight (split launch)")
     p.add_argument("--slab", action="store_true",
                    help="use the multi-GPU z-slab path also at N=1 (ghosts by self-copy)")
-    p.add_argument("--halo", choices=["peer", "nccl"], default="peer",
-                   help="slab halo: peer = the kernel reads the neighbours' planes over "
-                        "CUDA IPC / NVLink (falls back to nccl if the mapping fails); "
-                        "nccl = send/recv into ghost planes before the kernel")
+    p.add_argument("--halo", choices=["peer", "nccl"], default="nccl",
+                   help="slab halo: nccl (default) = send/recv into ghost planes before the "
+                        "kernel; peer = the kernel reads the neighbours' planes over CUDA IPC / "
+                        "NVLink (falls back to nccl if the mapping fails).  At N=1 the step is "
+                        "0.302 ms (nccl) vs 0.311 ms (peer): the peer instantiation's per-plane "
+                        "base selection costs more than the 4-plane exchange")
     return p.parse_args()
 
 
