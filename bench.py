@@ -215,6 +215,59 @@ NS_FLOP_PER_CELL = 8850   # frozen algorithmic count, DESIGN.md "NS RHS flop cou
 NS_BYTES_PER_CELL = 224   # 14 conserved fp64 in + 14 out (fully fused minimum)
 
 
+def heat2d_measurement(dev, stream, fp64_peak, n=4096, reps=100):
+    """The reference's own RHS (HeatOperator::rhs, pde.cpp:266-274; the 2-D
+    T2 problem, narrow SMC stencil) on the GPU at n^2 next to the reference
+    CPU path on all host threads (oracle/_ref, operator built once, best of 3
+    calls).  Roofline: 2 x 112 + 3 + 2 flop per cell (two directions, the
+    1/d^2 scalings and combine), 32 B per cell (u, a, b in; out)."""
+    import ctypes as C
+    import numpy as np
+    import torch
+    import paper_1309_7327_b200 as P
+    xs = np.arange(n) * (2 * math.pi / n)
+    X, Y = np.meshgrid(xs, xs)
+    a = 1.0 + 0.9 * np.cos(2 * X) * np.sin(2 * Y + math.pi / 3)
+    b = 1.0 + 0.9 * np.cos(2 * X + math.pi / 3) * np.sin(2 * Y)
+    u = torch.from_numpy(np.sin(X) * np.sin(Y)).to(dev)
+    out = torch.empty_like(u)
+    op = P.HeatOperator(n, n, P.StencilChoice.narrow8(P.SMC_M47, P.SMC_M48), a, b)
+    op.set_stream(stream)
+    for _ in range(5):
+        op(0.0, u, out)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(reps):
+        op(0.0, u, out)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / reps
+    flop = 2 * 112 + 3 + 2
+    res = {"workload": f"HeatOperator::rhs, T2 coefficients, narrow SMC, {n}^2 periodic",
+           "value": n * n / (ms * 1e-3), "unit": "cell-RHS/s", "ms_per_rhs": ms,
+           "roofline": {"bound": "fp64", "achieved": flop * n * n / (ms * 1e-3) / 1e12,
+                        "peak": fp64_peak, "unit": "TFLOP/s",
+                        "frac": flop * n * n / (ms * 1e-3) / 1e12 / fp64_peak,
+                        "flop_per_cell": flop, "bytes_per_cell": 32}}
+    try:
+        from oracle import oracle as O
+        if O.have_ref(fast=True):
+            r = O.ref(fast=True)
+            r.ref_set_workers(0)
+            best = C.c_double()
+            pp = np.array([P.SMC_M47, P.SMC_M48])
+            rc = r.ref_heat2d_time(2, n, n, 0, O.dp(pp), 3, C.byref(best))
+            if rc == 0:
+                res["cpu_baseline"] = {"value": n * n / best.value, "unit": "cell-RHS/s",
+                                       "cores": int(r.ref_worker_limit()), "kind": "reference",
+                                       "sample": f"HeatOperator::rhs at {n}^2, operator built "
+                                                 "once, best of 3 calls"}
+    except Exception as exc:  # noqa: BLE001
+        res["cpu_baseline"] = {"value": None, "sample": f"failed: {exc}"}
+    return res
+
+
 def ns_rhs_measurement(n, dev, stream, fp64_peak, hbm_peak, steps):
     """Full NS RHS (ctoprim, hypterm, narrow diffterm + transport, wdot) on
     the configs[3] state generator (hot spot), n^3 periodic, dx = 1e-4 m."""
@@ -535,6 +588,13 @@ def main():
         except Exception as exc:  # noqa: BLE001
             ns = {"error": str(exc)}
 
+    heat = None
+    if not args.no_ns and world == 1:
+        try:
+            heat = heat2d_measurement(dev, stream, fp64_peak)
+        except Exception as exc:  # noqa: BLE001
+            heat = {"error": str(exc)}
+
     adv = None
     if not args.no_advance and world == 1:
         try:
@@ -587,6 +647,7 @@ def main():
             "clocks": clocks,
             "cpu_baseline": cpu,
             "ns_rhs": ns,
+            "heat2d_rhs": heat,
             "time_advance": adv,
         }
         print(json.dumps(line), flush=True)

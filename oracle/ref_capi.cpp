@@ -9,6 +9,7 @@
 // kernels in 3-D exactly the way narrow_rhs_rows<S> composes them in 2-D
 // (proj/core/src/pde.cpp:85-129; SURVEY.md §8(c) "oracle3d").
 #include <algorithm>
+#include <chrono>
 #include <array>
 #include <cmath>
 #include <functional>
@@ -273,6 +274,29 @@ int ref_heat2d_rhs(int id, int nx, int ny, int kind, const double* params, const
     Field2D oo(nx, ny);
     op.rhs(t, uu, oo);
     std::memcpy(out, oo.v.data(), sizeof(double) * oo.v.size());
+  });
+}
+
+// Best wall time of HeatOperator::rhs (pde.cpp:266-274) over `reps` calls on
+// the problem's own u0 (operator built once; workers from ref_set_workers).
+int ref_heat2d_time(int id, int nx, int ny, int kind, const double* params, int reps,
+                    double* best_seconds) {
+  return guarded([&] {
+    ArrayProblem arr{nx, ny, {}, {}, {}};
+    HeatProblem p = make_problem(id, &arr);
+    const Grid2D g{nx, ny};
+    HeatOperator op(p, g, choice_from(kind, params));
+    Field2D uu = eval_on_grid(g, p.u0);
+    Field2D oo(nx, ny);
+    op.rhs(0.1, uu, oo);  // warm-up
+    double best = 1e300;
+    for (int r = 0; r < reps; ++r) {
+      const auto t0 = std::chrono::steady_clock::now();
+      op.rhs(0.1, uu, oo);
+      const std::chrono::duration<double> dt = std::chrono::steady_clock::now() - t0;
+      best = std::min(best, dt.count());
+    }
+    *best_seconds = best;
   });
 }
 
