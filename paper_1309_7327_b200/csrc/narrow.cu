@@ -276,7 +276,9 @@ void launch_s(const NarrowArgs& p, const StencilM& M, cudaStream_t st) {
     else
       launch_t<S, true, true, true, false>(p, M, st);
   } else if (p.dims == 2) {
-    if (p.g0)
+    if (p.use_fast && narrow2d_fast_applicable(p))
+      launch_narrow2d_fast(p, S, M, st);
+    else if (p.g0)
       launch_t<S, true, false, false, true>(p, M, st);
     else
       launch_t<S, true, false, false, false>(p, M, st);

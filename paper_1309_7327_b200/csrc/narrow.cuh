@@ -43,6 +43,10 @@ bool narrow3d_fast_applicable(const NarrowArgs& p);
 void launch_narrow3d_fast(const NarrowArgs& p, int s, const StencilM& M, cudaStream_t st);
 int narrow3d_fast_default_kc(int nx, int ny, int nz, int num_sms);
 
+// 2-D heat operator tiles (narrow2d_fast.cu) for nx % 32 == 0, ny % 8 == 0.
+bool narrow2d_fast_applicable(const NarrowArgs& p);
+void launch_narrow2d_fast(const NarrowArgs& p, int s, const StencilM& M, cudaStream_t st);
+
 // Wide route D(a D u) (+ y term when w2/b given) + g0*gt; w1/w2 scratch.
 void launch_wide2d(const double* u, const double* a, const double* b, const double* g0, double gt,
                    double* w1, double* w2, double* out, int nx, int ny, double dx, double dy,

@@ -1,0 +1,170 @@
+// 2-D heat operator RHS (HeatOperator::rhs, proj/core/src/pde.cpp:85-129:
+// (a u_x)_x + (b u_y)_y + g0 g(t) on the periodic grid), FP64-issue-optimised
+// like narrow3d_fast.cu's per-plane step, without the z march:
+//   * a CTA owns a 32 x 8 tile (128 threads, 2 adjacent x cells per thread),
+//     stages u, a and b with a 4-cell halo by 16-byte cp.async;
+//   * x interfaces of a thread's two cells from 5 LDS.128 per field, y
+//     interfaces of its two columns from 8 LDS.128 per field, each pair
+//     formed in lockstep (narrow_iface2) from the 26 upper-half M entries;
+//   * the tile-edge interfaces (x0 - 1/2 of each row, y0 - 1/2 of each
+//     column) are packed into warps 1-3, neighbours' interfaces come by
+//     shuffle (x) and through shared memory (y);
+//   * ~18 KB of shared memory and no z window: several CTAs per SM.
+// Same interface sums and differencing order as the general kernel
+// (narrow.cu); requires nx % 32 == 0, ny % 8 == 0 and 16-byte aligned fields.
+#include <cstdint>
+
+#include "common.cuh"
+#include "narrow.cuh"
+
+namespace smc {
+namespace {
+
+constexpr int TX2 = 32;
+constexpr int TY2 = 8;
+constexpr int LPR2 = TX2 / 2;          // threads per tile row
+constexpr int FT2 = LPR2 * TY2;        // 128 threads
+constexpr int HALO2 = 4;
+constexpr int SW2 = TX2 + 2 * HALO2;   // 40
+constexpr int SH2 = TY2 + 2 * HALO2;   // 16
+constexpr int CH2 = SH2 * SW2 / 2;     // 16-byte chunks per field (320)
+constexpr int CPT2 = (CH2 + FT2 - 1) / FT2;
+
+struct Smem2 {
+  double t[3][SH2 * SW2];  // u, a (x sweep), b (y sweep)
+  double hy[TY2 + 1][TX2];
+  double hxe[TY2];
+};
+
+__device__ __forceinline__ void cp16_2(void* dst, const void* src) {
+  const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(dst));
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(src));
+}
+
+__device__ __forceinline__ double2 lds2_2(const double* p) {
+  return *reinterpret_cast<const double2*>(p);
+}
+
+template <int S, bool SRC>
+__global__ void __launch_bounds__(FT2) narrow2d_fast(const NarrowArgs p, const StencilM M) {
+  constexpr int WIN = 2 * S;
+  __shared__ __align__(16) Smem2 sm;
+  const int tiles_x = p.nx / TX2;
+  const int x0 = (blockIdx.x % tiles_x) * TX2;
+  const int y0 = (blockIdx.x / tiles_x) * TY2;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int row = threadIdx.x / LPR2, cp = threadIdx.x % LPR2;
+
+  // stage u, a, b (periodic wrap folded into the chunk offsets)
+#pragma unroll
+  for (int i = 0; i < CPT2; ++i) {
+    const int c = threadIdx.x + i * FT2;
+    if (i + 1 < CPT2 || c < CH2) {
+      const int r = c / (SW2 / 2), col = 2 * (c - r * (SW2 / 2));
+      const long long off = static_cast<long long>(wrap(y0 - HALO2 + r, p.ny)) * p.nx +
+                            wrap(x0 - HALO2 + col, p.nx);
+      cp16_2(&sm.t[0][2 * c], p.u + off);
+      cp16_2(&sm.t[1][2 * c], p.cx + off);
+      cp16_2(&sm.t[2][2 * c], p.cy + off);
+    }
+  }
+  asm volatile("cp.async.commit_group;\n" ::);
+  asm volatile("cp.async.wait_group 0;\n" ::: "memory");
+  __syncthreads();
+
+  const double* tu = sm.t[0];
+  const double* ta = sm.t[1];
+  const double* tb = sm.t[2];
+  // ---- x interfaces x+1/2 of my two cells (row HALO2 + row)
+  double hx0, hx1;
+  {
+    constexpr int NV = WIN + 2;
+    constexpr int BASE = HALO2 - S + 1 - ((HALO2 - S + 1) & 1);
+    constexpr int OFF = (HALO2 - S + 1) - BASE;
+    double ua[NV], aa[NV];
+    const double* ru = tu + (HALO2 + row) * SW2 + 2 * cp + BASE;
+    const double* ra = ta + (HALO2 + row) * SW2 + 2 * cp + BASE;
+#pragma unroll
+    for (int j = 0; j < NV / 2; ++j) {
+      const double2 vu = lds2_2(ru + 2 * j), va = lds2_2(ra + 2 * j);
+      ua[2 * j] = vu.x, ua[2 * j + 1] = vu.y;
+      aa[2 * j] = va.x, aa[2 * j + 1] = va.y;
+    }
+    narrow_iface2<S>(aa + OFF, ua + OFF, aa + OFF + 1, ua + OFF + 1, M, hx0, hx1);
+  }
+  // ---- y interfaces y+1/2 of my two columns
+  {
+    double u0[WIN], b0[WIN], u1[WIN], b1[WIN];
+#pragma unroll
+    for (int j = 0; j < WIN; ++j) {
+      const int r = HALO2 + row - S + 1 + j;
+      const double2 vu = lds2_2(tu + r * SW2 + HALO2 + 2 * cp);
+      const double2 vb = lds2_2(tb + r * SW2 + HALO2 + 2 * cp);
+      u0[j] = vu.x, u1[j] = vu.y, b0[j] = vb.x, b1[j] = vb.y;
+    }
+    double y0v, y1v;
+    narrow_iface2<S>(b0, u0, b1, u1, M, y0v, y1v);
+    *reinterpret_cast<double2*>(&sm.hy[row + 1][2 * cp]) = make_double2(y0v, y1v);
+  }
+  // ---- tile-edge interfaces: y0 - 1/2 of the even columns (warp 1), of the
+  //      odd columns (warp 2), x0 - 1/2 of each row (warp 3)
+  if ((wid == 1 || wid == 2) && lane < LPR2) {
+    const int col = HALO2 + 2 * lane + (wid - 1);
+    double uu[WIN], bb[WIN];
+#pragma unroll
+    for (int j = 0; j < WIN; ++j) {
+      uu[j] = tu[(HALO2 - S + j) * SW2 + col];
+      bb[j] = tb[(HALO2 - S + j) * SW2 + col];
+    }
+    sm.hy[0][2 * lane + (wid - 1)] = narrow_iface<S>(bb, uu, M);
+  } else if (wid == 3 && lane < TY2) {
+    double uu[WIN], aa[WIN];
+#pragma unroll
+    for (int j = 0; j < WIN; ++j) {
+      uu[j] = tu[(HALO2 + lane) * SW2 + HALO2 - S + j];
+      aa[j] = ta[(HALO2 + lane) * SW2 + HALO2 - S + j];
+    }
+    sm.hxe[lane] = narrow_iface<S>(aa, uu, M);
+  }
+  __syncthreads();
+  // ---- (dHx)/dx^2 + (dHy)/dy^2 (+ g0 g(t)), pde.cpp:118-124
+  double hxl = __shfl_up_sync(0xffffffffu, hx1, 1);
+  if (cp == 0) hxl = sm.hxe[row];
+  const double2 yu = lds2_2(&sm.hy[row][2 * cp]);
+  const double2 yd = lds2_2(&sm.hy[row + 1][2 * cp]);
+  double o0 = __dmul_rn(__dsub_rn(hx0, hxl), p.idx2);
+  double o1 = __dmul_rn(__dsub_rn(hx1, hx0), p.idx2);
+  o0 = __dadd_rn(o0, __dmul_rn(__dsub_rn(yd.x, yu.x), p.idy2));
+  o1 = __dadd_rn(o1, __dmul_rn(__dsub_rn(yd.y, yu.y), p.idy2));
+  const long long oo = static_cast<long long>(y0 + row) * p.nx + x0 + 2 * cp;
+  if constexpr (SRC) {
+    const double2 g = __ldg(reinterpret_cast<const double2*>(p.g0 + oo));
+    o0 = __dadd_rn(o0, __dmul_rn(g.x, p.gt));
+    o1 = __dadd_rn(o1, __dmul_rn(g.y, p.gt));
+  }
+  *reinterpret_cast<double2*>(p.out + oo) = make_double2(o0, o1);
+}
+
+template <int S, bool SRC>
+void launch2(const NarrowArgs& p, const StencilM& M, cudaStream_t st) {
+  const int tiles = (p.nx / TX2) * (p.ny / TY2);
+  narrow2d_fast<S, SRC><<<tiles, FT2, 0, st>>>(p, M);
+  SMC_CHECK_LAUNCH();
+}
+
+}  // namespace
+
+bool narrow2d_fast_applicable(const NarrowArgs& p) {
+  const auto al = [](const void* q) { return (reinterpret_cast<std::uintptr_t>(q) & 15) == 0; };
+  return p.dims == 2 && p.nx % TX2 == 0 && p.ny % TY2 == 0 && p.nx >= TX2 && p.ny >= TY2 &&
+         al(p.u) && al(p.cx) && al(p.cy) && al(p.out) && (p.g0 == nullptr || al(p.g0));
+}
+
+void launch_narrow2d_fast(const NarrowArgs& p, int s, const StencilM& M, cudaStream_t st) {
+  if (p.g0)
+    s == 4 ? launch2<4, true>(p, M, st) : launch2<3, true>(p, M, st);
+  else
+    s == 4 ? launch2<4, false>(p, M, st) : launch2<3, false>(p, M, st);
+}
+
+}  // namespace smc

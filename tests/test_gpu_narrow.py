@@ -375,3 +375,27 @@ def test_peer_halo_two_processes_ipc(cuda):
     for p in procs:
         p.join(timeout=60)
     assert all(ok for _, ok, _ in res), res
+
+
+@pytest.mark.parametrize("shape", [(32, 32), (16, 64), (40, 96), (128, 256)])
+@pytest.mark.parametrize("order", [8, 6])
+@pytest.mark.parametrize("src", [False, True])
+def test_heat2d_tiled_kernel_vs_oracle(cuda, shape, order, src):
+    """Shapes with nx % 32 == 0, ny % 8 == 0 take the tiled 2-D kernel
+    (narrow2d_fast.cu); the oracle (pinned to the reference) at 1e-12, with
+    and without the separable source."""
+    ny, nx = shape
+    rng = np.random.default_rng(nx + ny + order)
+    a = rng.uniform(0.5, 2.0, shape)
+    b = rng.uniform(0.5, 2.0, shape)
+    g0 = rng.standard_normal(shape) if src else None
+    u = rng.standard_normal(shape)
+    params = SMC if order == 8 else (P.DEFAULT_M36,)
+    choice = P.StencilChoice.narrow8(*SMC) if order == 8 else P.StencilChoice.narrow6(
+        P.DEFAULT_M36)
+    m, s = O.build_narrow(order, params)
+    dx, dy = 2 * math.pi / nx, 2 * math.pi / ny
+    gt = math.exp(-0.3)
+    ref = O.heat2d_rhs(0 if order == 8 else 1, m, s, a, b, g0, gt if src else 0.0, u, dx, dy)
+    op = P.HeatOperator(nx, ny, choice, a, b, g0, (lambda t: math.exp(-t)) if src else None)
+    assert rel_err(op(0.3, u), ref) <= TOL
