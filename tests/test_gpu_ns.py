@@ -32,8 +32,11 @@ def test_conserved_from_primitives(cuda):
 
 
 @pytest.mark.parametrize("part", [P.NS_FULL, P.NS_ADVDIFF, P.NS_CHEM])
-@pytest.mark.parametrize("n,kw", [(16, {}), (24, {"hot_spot": True})])
+@pytest.mark.parametrize("n,kw", [(16, {}), (24, {"hot_spot": True}), (32, {}),
+                                  (64, {"hot_spot": True})])
 def test_ns_rhs_vs_oracle(cuda, part, n, kw):
+    """n = 32 is configs[0] (single full RHS, 32^3 periodic, the configs[0]
+    state generator); n = 64 runs whole tiles in every direction."""
     U, _ = _state(n, **kw)
     ref = O.ns_rhs(U, DX, part)
     op = P.NsOperator(n, n, n, DX)
