@@ -54,8 +54,11 @@ def _cb(n, part):
     return O.RHS_CB(f)
 
 
-def test_sdc_ten_steps_vs_oracle(cuda, golden):
-    n, steps = 12, 10
+@pytest.mark.parametrize("n", [12, 32])
+def test_sdc_ten_steps_vs_oracle(cuda, golden, n):
+    """configs[2] (10 SDC steps at CFL 0.5 of the configs[0] state) at 12^3 and
+    32^3 (81 oracle RHS evaluations of the 32^3 box: ~20 s on the host)."""
+    steps = 10
     U0, prims = _state(n)  # configs[2]: the configs[0] generator (T = 1200 +- 300 K)
     dt = acoustic_dt(prims, DX)
     t1 = steps * dt
