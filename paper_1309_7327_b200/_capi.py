@@ -8,7 +8,9 @@ import os
 import re
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libsmc_b200.so")
+# SMC_LIB_PATH points at another build of the same library (A/B timing of two
+# builds on one box); the default is the in-tree build.
+LIB_PATH = os.environ.get("SMC_LIB_PATH") or os.path.join(HERE, "libsmc_b200.so")
 HEADER = os.path.join(HERE, "..", "include", "smc_b200.h")
 
 OK, EINVAL, EINTEGRATION, ECUDA = 0, 1, 2, 3

@@ -53,6 +53,12 @@ inline void require(bool ok, const std::string& what) {
 // bank; DFMA reads them as c[0x0][...] operands at no issue cost).
 struct StencilM {
   double m[8][8];
+  // Symmetric / antisymmetric halves of the upper rows (filled by
+  // make_stencil): p[r][j] = (m[r][j] + m[r][L-j]) / 2,
+  // q[r][j] = (m[r][j] - m[r][L-j]) / 2, r, j < S, L = 2S - 1; p[r][S-1] is
+  // implied by the zero row sum and not read.
+  double p[4][4];
+  double q[4][4];
 };
 
 // Structural nonzeros of row r (PAPER.md:263-300 / :320-345): rows of the
@@ -73,84 +79,110 @@ __host__ __device__ inline int wrap(int i, int n) {
 }
 
 #ifdef __CUDACC__
-// H_{i+1/2} = sum_mm a_{i+mm} (sum_nn M[mm][nn] u_{i+nn}) for one interface.
-// a[w], u[w] hold offsets w - (S - 1), w = 0 .. 2S-1.  Order fixed as in
-// stencil_kernel.hpp:13-25 (mm ascending outer, nn ascending inner); explicit
-// fma so the instruction sequence (and hence the bits) is the same no matter
-// which thread or tiling computes the interface.
+// H_{i+1/2} = sum_mm a_{i+mm} (sum_nn M[mm][nn] u_{i+nn}) for one interface
+// (stencil_kernel.hpp:13-25).  a[w], u[w] hold offsets w - (S - 1),
+// w = 0 .. 2S-1.
 //
-// Only the upper half of M is read: the lower rows are taken through the
-// central antisymmetry M[r][c] = -M[2S-1-r][2S-1-c], so a
-// kernel needs 26 (S = 4) distinct constants, which fit the uniform register
-// file, instead of 52.  The products and their order are unchanged.
+// Evaluated through the central antisymmetry M[L-r][L-c] = -M[r][c]
+// (L = 2S - 1): with the window's symmetric and
+// antisymmetric parts s_j = u_j + u_{L-j}, d_j = u_j - u_{L-j} (j < S),
+//   v_r     = sum_c M[r][c] u_c   = P_r + Q_r,
+//   v_{L-r} = -sum_c M[r][c] u_{L-c} = Q_r - P_r,   r < S,
+// with P_r = sum_j p[r][j] s_j and Q_r = sum_j q[r][j] d_j (StencilM::p, q).
+// Each row of M sums to zero (constants are annihilated), so do the rows of
+// p and P_r = sum_{j<S-1} p[r][j] (s_j - s_{S-1}).  That is 3S - 1 adds,
+// S(2S - 1) multiply-adds and 2S adds for the 2S values v_r (47 FP64
+// instructions for S = 4, 28 constants) instead of the 52 structural
+// nonzeros, and the dot with a stays 2S: 55 per interface instead of 60.  The rounding
+// differs from the reference's row order by a few ulps of the interface sum
+// (~1e-13 of the field, inside the 1e-12 single-RHS bar the tests hold);
+// the sequence is fixed, so every thread, tiling and kernel that forms an
+// interface gets the same bits.
+// s'_j = s_j - s_{S-1} (j < S-1; the rows of p sum to zero, so P_r needs
+// only these) and d_j (j < S) of a window.
 template <int S>
-__device__ __forceinline__ double mcoef(const StencilM& M, int r, int c) {
-  return M.m[r][c];
+__device__ __forceinline__ void sd_parts(const double* u, double* sj, double* dj) {
+  constexpr int L = 2 * S - 1;
+  const double sl = __dadd_rn(u[S - 1], u[S]);
+#pragma unroll
+  for (int j = 0; j < S - 1; ++j) sj[j] = __dsub_rn(__dadd_rn(u[j], u[L - j]), sl);
+#pragma unroll
+  for (int j = 0; j < S; ++j) dj[j] = __dsub_rn(u[j], u[L - j]);
 }
+template <int S>
+__device__ __forceinline__ void narrow_vsd(const double* u, const StencilM& M, double* v) {
+  constexpr int L = 2 * S - 1;
+  double sj[S], dj[S];
+  sd_parts<S>(u, sj, dj);
+#pragma unroll
+  for (int r = 0; r < S; ++r) {
+    double pr = __dmul_rn(M.p[r][0], sj[0]), qr = __dmul_rn(M.q[r][0], dj[0]);
+#pragma unroll
+    for (int j = 1; j < S - 1; ++j) pr = __fma_rn(M.p[r][j], sj[j], pr);
+#pragma unroll
+    for (int j = 1; j < S; ++j) qr = __fma_rn(M.q[r][j], dj[j], qr);
+    v[r] = __dadd_rn(qr, pr);
+    v[L - r] = __dsub_rn(qr, pr);
+  }
+}
+template <int S>
+__device__ __forceinline__ double narrow_adot(const double* a, const double* v) {
+  double acc = __dmul_rn(a[0], v[0]);
+#pragma unroll
+  for (int r = 1; r < 2 * S; ++r) acc = __fma_rn(a[r], v[r], acc);
+  return acc;
+}
+// Interface sum with the dot taken in row-pair order r, L-r (r < S), so each
+// pair (P_r, Q_r) is consumed as soon as it is formed.
 template <int S>
 __device__ __forceinline__ double narrow_iface(const double* a, const double* u,
                                                const StencilM& M) {
+  constexpr int L = 2 * S - 1;
+  double sj[S], dj[S];
+  sd_parts<S>(u, sj, dj);
   double acc;
 #pragma unroll
-  for (int r = 0; r < 2 * S; ++r) {
-    constexpr int L = 2 * S - 1;
-    const int lo = row_lo<S>(r), hi = row_hi<S>(r);
-    double v;
-    if (r < S) {
-      v = M.m[r][lo] * u[lo];
+  for (int r = 0; r < S; ++r) {
+    double pr = __dmul_rn(M.p[r][0], sj[0]), qr = __dmul_rn(M.q[r][0], dj[0]);
 #pragma unroll
-      for (int c = lo + 1; c <= hi; ++c) v = __fma_rn(M.m[r][c], u[c], v);
-      acc = (r == 0) ? a[0] * v : __fma_rn(a[r], v, acc);
-    } else {
-      // v_r = sum_c M[r][c] u_c = -sum_c M[L-r][L-c] u_c
-      v = M.m[L - r][L - lo] * u[lo];
+    for (int j = 1; j < S - 1; ++j) pr = __fma_rn(M.p[r][j], sj[j], pr);
 #pragma unroll
-      for (int c = lo + 1; c <= hi; ++c) v = __fma_rn(M.m[L - r][L - c], u[c], v);
-      acc = __fma_rn(-a[r], v, acc);
-    }
+    for (int j = 1; j < S; ++j) qr = __fma_rn(M.q[r][j], dj[j], qr);
+    acc = r == 0 ? __dmul_rn(a[0], __dadd_rn(qr, pr)) : __fma_rn(a[r], __dadd_rn(qr, pr), acc);
+    acc = __fma_rn(a[L - r], __dsub_rn(qr, pr), acc);
   }
   return acc;
 }
 
 // Two independent interfaces in lockstep (same arithmetic as narrow_iface for
-// each): every M entry is used by two adjacent, independent FMAs, which
-// doubles the instruction-level parallelism of the dependent row chains.
+// each): every constant is used by two adjacent, independent instructions,
+// which doubles the instruction-level parallelism of the chains.
 template <int S>
 __device__ __forceinline__ void narrow_iface2(const double* a0, const double* u0, const double* a1,
                                               const double* u1, const StencilM& M, double& h0,
                                               double& h1) {
+  constexpr int L = 2 * S - 1;
+  double s0[S], d0[S], s1[S], d1[S];
+  sd_parts<S>(u0, s0, d0);
+  sd_parts<S>(u1, s1, d1);
   double acc0, acc1;
 #pragma unroll
-  for (int r = 0; r < 2 * S; ++r) {
-    constexpr int L = 2 * S - 1;
-    const int lo = row_lo<S>(r), hi = row_hi<S>(r);
-    double v0, v1;
-    if (r < S) {
-      v0 = M.m[r][lo] * u0[lo];
-      v1 = M.m[r][lo] * u1[lo];
+  for (int r = 0; r < S; ++r) {
+    double p0 = __dmul_rn(M.p[r][0], s0[0]), q0 = __dmul_rn(M.q[r][0], d0[0]);
+    double p1 = __dmul_rn(M.p[r][0], s1[0]), q1 = __dmul_rn(M.q[r][0], d1[0]);
 #pragma unroll
-      for (int c = lo + 1; c <= hi; ++c) {
-        v0 = __fma_rn(M.m[r][c], u0[c], v0);
-        v1 = __fma_rn(M.m[r][c], u1[c], v1);
-      }
-      if (r == 0) {
-        acc0 = a0[0] * v0;
-        acc1 = a1[0] * v1;
-      } else {
-        acc0 = __fma_rn(a0[r], v0, acc0);
-        acc1 = __fma_rn(a1[r], v1, acc1);
-      }
+    for (int j = 1; j < S - 1; ++j) p0 = __fma_rn(M.p[r][j], s0[j], p0), p1 = __fma_rn(M.p[r][j], s1[j], p1);
+#pragma unroll
+    for (int j = 1; j < S; ++j) q0 = __fma_rn(M.q[r][j], d0[j], q0), q1 = __fma_rn(M.q[r][j], d1[j], q1);
+    if (r == 0) {
+      acc0 = __dmul_rn(a0[0], __dadd_rn(q0, p0));
+      acc1 = __dmul_rn(a1[0], __dadd_rn(q1, p1));
     } else {
-      v0 = M.m[L - r][L - lo] * u0[lo];
-      v1 = M.m[L - r][L - lo] * u1[lo];
-#pragma unroll
-      for (int c = lo + 1; c <= hi; ++c) {
-        v0 = __fma_rn(M.m[L - r][L - c], u0[c], v0);
-        v1 = __fma_rn(M.m[L - r][L - c], u1[c], v1);
-      }
-      acc0 = __fma_rn(-a0[r], v0, acc0);
-      acc1 = __fma_rn(-a1[r], v1, acc1);
+      acc0 = __fma_rn(a0[r], __dadd_rn(q0, p0), acc0);
+      acc1 = __fma_rn(a1[r], __dadd_rn(q1, p1), acc1);
     }
+    acc0 = __fma_rn(a0[L - r], __dsub_rn(q0, p0), acc0);
+    acc1 = __fma_rn(a1[L - r], __dsub_rn(q1, p1), acc1);
   }
   h0 = acc0;
   h1 = acc1;

@@ -46,7 +46,7 @@ __device__ __forceinline__ double2 lds2_2(const double* p) {
 }
 
 template <int S, bool SRC>
-__global__ void __launch_bounds__(FT2) narrow2d_fast(const NarrowArgs p, const StencilM M) {
+__global__ void __launch_bounds__(FT2, S == 4 ? 8 : 6) narrow2d_fast(const NarrowArgs p, const StencilM M) {
   constexpr int WIN = 2 * S;
   __shared__ __align__(16) Smem2 sm;
   const int tiles_x = p.nx / TX2;

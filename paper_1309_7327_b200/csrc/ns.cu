@@ -218,33 +218,15 @@ __global__ void __launch_bounds__(256) hyp_kernel(const double* __restrict__ U,
 }
 
 // ------------------------------------------------------------ narrow
-// v'_r of the interface whose window starts at u[0] (antisymmetric form of
-// narrow_iface: rows r >= S carry the sign flip, see common.cuh).
+// v'_r of the interface whose window starts at u[0]: v_r with the sign of
+// rows r >= S folded in (narrow_vsd, common.cuh), so the dot is plain.
 template <int S>
 __device__ __forceinline__ void narrow_v(const double* u, const StencilM& M, double* v) {
-  constexpr int L = 2 * S - 1;
-#pragma unroll
-  for (int r = 0; r < 2 * S; ++r) {
-    const int lo = row_lo<S>(r), hi = row_hi<S>(r);
-    double acc;
-    if (r < S) {
-      acc = M.m[r][lo] * u[lo];
-#pragma unroll
-      for (int c = lo + 1; c <= hi; ++c) acc = __fma_rn(M.m[r][c], u[c], acc);
-    } else {
-      acc = M.m[L - r][L - lo] * u[lo];
-#pragma unroll
-      for (int c = lo + 1; c <= hi; ++c) acc = __fma_rn(M.m[L - r][L - c], u[c], acc);
-    }
-    v[r] = acc;
-  }
+  narrow_vsd<S>(u, M, v);
 }
 template <int S>
 __device__ __forceinline__ double narrow_dot(const double* a, const double* v) {
-  double acc = a[0] * v[0];
-#pragma unroll
-  for (int r = 1; r < 2 * S; ++r) acc = __fma_rn(r < S ? a[r] : -a[r], v[r], acc);
-  return acc;
+  return narrow_adot<S>(a, v);
 }
 
 // All same-direction second-derivative terms of one cell (PAPER.md:150-156,

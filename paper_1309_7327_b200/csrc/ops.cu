@@ -55,6 +55,11 @@ StencilM make_stencil(int order, const double* params, int nparams, int* s_out) 
       M.m[i][j] = v;
       M.m[2 * s - 1 - i][2 * s - 1 - j] = -v;
     }
+  for (int r = 0; r < s; ++r)
+    for (int j = 0; j < s; ++j) {
+      M.p[r][j] = 0.5 * (M.m[r][j] + M.m[r][2 * s - 1 - j]);
+      M.q[r][j] = 0.5 * (M.m[r][j] - M.m[r][2 * s - 1 - j]);
+    }
   if (s_out) *s_out = s;
   return M;
 }
