@@ -5,8 +5,10 @@
 #include <algorithm>
 #include <cfloat>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <string>
+#include <utility>
 
 #include "stiff.hpp"
 
@@ -177,20 +179,25 @@ __global__ void __launch_bounds__(128) lu_solve_update_kernel(const double* jac,
 // matrix staged in shared memory laid out [entry][thread] (conflict-free),
 // factored and solved there: the Jacobian is read once and nothing but the
 // solution is written back (the global-memory factor + solve pair above
-// re-reads and re-writes every entry O(block) times).  Measured on the NS
-// chemistry at 128^3 (block 14): 7.8 ms per factor-and-solve against about
-// 9 ms for the global pair; a warp-per-block variant (rows in registers,
-// shuffles) was slower than both.  delta is
-// replaced by the Newton update; w is updated by a separate kernel once the
-// host has seen that no block was singular (stiff.cpp:66 breaks before it).
+// re-reads and re-writes every entry O(block) times).  B is a template
+// parameter so every loop is unrolled at its exact trip count: a row's
+// loads are issued together instead of one dependent shared-memory round
+// trip per entry.  delta is replaced by the Newton update; w is updated by a
+// separate kernel once the host has seen that no block was singular
+// (stiff.cpp:66 breaks before it).
+//
+// Kept as the fallback (SMC_LU_LANES=0).  Measured on the NS chemistry at
+// 128^3 (block 14): 7.8 ms per factor-and-solve with run-time B, 7.3 ms
+// unrolled; the global pair about 9 ms.  It holds four warps per SM (54 KB
+// of shared memory per warp).  lu_lane_kernel below takes 4.9 ms.
 constexpr int kLuThreads = 32;
 constexpr int kLuMaxB = 16;
 
+template <int B>
 __global__ void __launch_bounds__(kLuThreads) lu_smem_kernel(const double* jac, double* delta,
                                                              double beta, BlockMap bm,
                                                              unsigned long long* flag) {
   extern __shared__ double sh[];
-  const int B = static_cast<int>(bm.B);
   const long long nb = bm.nb;
   const int t = threadIdx.x;
   const long long b = blockIdx.x * static_cast<long long>(kLuThreads) + t;
@@ -199,15 +206,20 @@ __global__ void __launch_bounds__(kLuThreads) lu_smem_kernel(const double* jac, 
   auto m = [&](int r, int c) -> double& { return mat[(r * B + c) * kLuThreads + t]; };
   auto xv = [&](int r) -> double& { return x[r * kLuThreads + t]; };
   if (b >= nb) return;
+#pragma unroll
   for (int r = 0; r < B; ++r)
+#pragma unroll
     for (int c = 0; c < B; ++c)
       m(r, c) = __dsub_rn(r == c ? 1.0 : 0.0,
                           __dmul_rn(beta, jac[(static_cast<long long>(r) * B + c) * nb + b]));
+#pragma unroll
   for (int r = 0; r < B; ++r) xv(r) = delta[bm.at(b, r)];
-  int piv[kLuMaxB];
+  unsigned long long piv = 0;  // 4 bits per column
+#pragma unroll 1
   for (int col = 0; col < B; ++col) {
     int best = col;
     double best_mag = fabs(m(col, col));
+#pragma unroll 1
     for (int r = col + 1; r < B; ++r) {
       const double mag = fabs(m(r, col));
       if (mag > best_mag) {
@@ -215,44 +227,242 @@ __global__ void __launch_bounds__(kLuThreads) lu_smem_kernel(const double* jac, 
         best_mag = mag;
       }
     }
-    piv[col] = best;
+    piv |= static_cast<unsigned long long>(best) << (4 * col);
     if (best_mag == 0.0) {
       atomicMax(flag, 1ull);
       return;
     }
-    if (best != col)
+    double* rc = mat + (col * B) * kLuThreads + t;
+    if (best != col) {
+      double* rb = mat + (best * B) * kLuThreads + t;
+#pragma unroll
       for (int c = 0; c < B; ++c) {
-        const double tmp = m(col, c);
-        m(col, c) = m(best, c);
-        m(best, c) = tmp;
+        const double tmp = rc[c * kLuThreads];
+        rc[c * kLuThreads] = rb[c * kLuThreads];
+        rb[c * kLuThreads] = tmp;
       }
-    const double inv = 1.0 / m(col, col);
+    }
+    // the pivot row in registers (entries left of col are not used)
+    double prow[B];
+#pragma unroll
+    for (int c = 0; c < B; ++c) prow[c] = c >= col ? rc[c * kLuThreads] : 0.0;
+    double inv = 0.0;
+#pragma unroll
+    for (int c = 0; c < B; ++c)
+      if (c == col) inv = 1.0 / prow[c];
+#pragma unroll 1
     for (int r = col + 1; r < B; ++r) {
-      const double l = __dmul_rn(m(r, col), inv);
-      m(r, col) = l;
-      for (int c = col + 1; c < B; ++c) m(r, c) = __dsub_rn(m(r, c), __dmul_rn(l, m(col, c)));
+      double* rr = mat + (r * B) * kLuThreads + t;
+      double row[B];
+#pragma unroll
+      for (int c = 0; c < B; ++c) row[c] = c >= col ? rr[c * kLuThreads] : 0.0;
+      double l = 0.0;
+#pragma unroll
+      for (int c = 0; c < B; ++c)
+        if (c == col) l = __dmul_rn(row[c], inv);
+#pragma unroll
+      for (int c = 0; c < B; ++c) {
+        if (c == col) rr[c * kLuThreads] = l;
+        if (c > col) rr[c * kLuThreads] = __dsub_rn(row[c], __dmul_rn(l, prow[c]));
+      }
     }
   }
-  // lu_solve (matrix.cpp:35-51)
+  // lu_solve (matrix.cpp:35-51), x in registers
+  double xr[B];
+#pragma unroll
+  for (int i = 0; i < B; ++i) xr[i] = xv(i);
+#pragma unroll
   for (int i = 0; i < B; ++i) {
-    const int p = piv[i];
-    if (p != i) {
-      const double tmp = xv(i);
-      xv(i) = xv(p);
-      xv(p) = tmp;
+    const int p = static_cast<int>((piv >> (4 * i)) & 15u);
+    if (p != i) {  // x_i <-> x_p, p > i (a select chain keeps xr in registers)
+      const double xi = xr[i];
+      double xp = xi;
+#pragma unroll
+      for (int q = i + 1; q < B; ++q) xp = p == q ? xr[q] : xp;
+#pragma unroll
+      for (int q = i + 1; q < B; ++q) xr[q] = p == q ? xi : xr[q];
+      xr[i] = xp;
     }
   }
+#pragma unroll
   for (int i = 1; i < B; ++i) {
-    double s = xv(i);
-    for (int j = 0; j < i; ++j) s = __dsub_rn(s, __dmul_rn(m(i, j), xv(j)));
-    xv(i) = s;
+    double s = xr[i];
+#pragma unroll
+    for (int j = 0; j < i; ++j) s = __dsub_rn(s, __dmul_rn(m(i, j), xr[j]));
+    xr[i] = s;
   }
+#pragma unroll
   for (int i = B - 1; i >= 0; --i) {
-    double s = xv(i);
-    for (int j = i + 1; j < B; ++j) s = __dsub_rn(s, __dmul_rn(m(i, j), xv(j)));
-    xv(i) = s / m(i, i);
+    double s = xr[i];
+#pragma unroll
+    for (int j = i + 1; j < B; ++j) s = __dsub_rn(s, __dmul_rn(m(i, j), xr[j]));
+    xr[i] = s / m(i, i);
   }
-  for (int r = 0; r < B; ++r) delta[bm.at(b, r)] = xv(r);
+#pragma unroll
+  for (int r = 0; r < B; ++r) delta[bm.at(b, r)] = xr[r];
+}
+
+// 16 lanes per block, one row of the iteration matrix per lane in registers,
+// 16 blocks per 256-thread CTA.
+//   * The CTA stages its 16 blocks' Jacobian entries through shared memory
+//     (each entry's 16 consecutive blocks are one 128-byte read).
+//   * Rows never move: each lane tracks the position of its row in the
+//     current order (a swap exchanges two positions).
+//   * Pivot search (matrix.cpp:13-20): a 4-round shuffle max of the 64-bit
+//     pattern of |m(., col)| (monotonic for non-negative doubles; NaN and
+//     positions above col excluded), then a 4-round min of the position
+//     among the rows holding it: the first maximum, as the reference's
+//     strict '>' scan finds; a NaN diagonal keeps col.
+//   * The pivot row goes through a shared-memory slot; every row below
+//     eliminates itself against it: the reference's operations on the same
+//     operands (matrix.cpp:21-31).
+//   * lu_solve (matrix.cpp:35-51): the swaps of x are the row swaps, so the
+//     lane of original row r starts from delta_r; forward and backward
+//     substitution broadcast each finished x_j by shuffle and every row
+//     subtracts in ascending j as the reference does.
+constexpr int kLuCells = 16;
+template <int B>
+__global__ void __launch_bounds__(256) lu_lane_kernel(const double* jac, double* delta,
+                                                      double beta, BlockMap bm,
+                                                      unsigned long long* flag) {
+  __shared__ double stage[B * B][kLuCells + 1];
+  __shared__ __align__(16) double slot[8][2][16];  // [warp][group][entry]
+  const long long nb = bm.nb;
+  const long long b0 = blockIdx.x * static_cast<long long>(kLuCells);
+  const int ncell = static_cast<int>(nb - b0 < kLuCells ? nb - b0 : kLuCells);
+  {
+    constexpr int NE = B * B * kLuCells;
+    double v[(NE + 255) / 256];
+#pragma unroll
+    for (int q = 0; q < (NE + 255) / 256; ++q) {
+      const int e = threadIdx.x + 256 * q;
+      const int rc = e / kLuCells, cc = e - rc * kLuCells;
+      v[q] = e < NE && cc < ncell ? jac[rc * nb + b0 + cc] : 0.0;
+    }
+#pragma unroll
+    for (int q = 0; q < (NE + 255) / 256; ++q) {
+      const int e = threadIdx.x + 256 * q;
+      const int rc = e / kLuCells, cc = e - rc * kLuCells;
+      if (e < NE) stage[rc][cc] = v[q];
+    }
+  }
+  __syncthreads();
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int gw = lane >> 4, gl = gw * 16;
+  const int g = warp * 2 + gw;
+  const int r = lane & 15;
+  const bool live = g < ncell;
+  const long long b = b0 + g;
+  double m[B];
+#pragma unroll
+  for (int c = 0; c < B; ++c)
+    m[c] = r < B ? __dsub_rn(r == c ? 1.0 : 0.0, __dmul_rn(beta, stage[r * B + c][g])) : 0.0;
+  double x = live && r < B ? delta[bm.at(b, r)] : 0.0;
+  int pos = r < B ? r : 16;  // padding lanes never take part
+  bool dead = !live;
+  double* ps = slot[warp][gw];
+  auto lane_of = [&](int p) {
+    const unsigned bits = (__ballot_sync(0xffffffffu, pos == p) >> gl) & 0xffffu;
+    return gl + __ffs(static_cast<int>(bits)) - 1;
+  };
+#pragma unroll
+  for (int col = 0; col < B; ++col) {
+    const double mg = fabs(m[col]);
+    const bool cand = pos >= col && pos < B;
+    const unsigned long long key =
+        cand && !isnan(mg) ? static_cast<unsigned long long>(__double_as_longlong(mg)) + 1ull : 0ull;
+    unsigned long long km = key;
+#pragma unroll
+    for (int o = 8; o > 0; o >>= 1) {
+      const unsigned long long ok = __shfl_xor_sync(0xffffffffu, km, o, 16);
+      km = ok > km ? ok : km;
+    }
+    int kp = cand && key == km ? pos : 16;
+#pragma unroll
+    for (int o = 8; o > 0; o >>= 1) kp = min(kp, __shfl_xor_sync(0xffffffffu, kp, o, 16));
+    const bool nan_diag = ((__ballot_sync(0xffffffffu, pos == col && isnan(mg)) >> gl) & 0xffffu) != 0;
+    const int best = nan_diag ? col : kp;
+    if (!nan_diag && km == 1ull && !dead) {  // best_mag == 0: singular
+      if (r == 0) atomicMax(flag, 1ull);
+      dead = true;
+    }
+    if (pos == best) {
+#pragma unroll
+      for (int c = 0; c < B; ++c)
+        if (c >= col) ps[c] = m[c];
+    }
+    if (pos == col)
+      pos = best;
+    else if (pos == best)
+      pos = col;
+    __syncwarp();
+    double p[B];
+#pragma unroll
+    for (int c = 0; c < B; ++c) p[c] = c >= col ? ps[c] : 0.0;
+    __syncwarp();
+    const double inv = 1.0 / p[col];
+    if (pos > col && pos < B) {
+      const double l = __dmul_rn(m[col], inv);
+      m[col] = l;
+#pragma unroll
+      for (int c = col + 1; c < B; ++c) m[c] = __dsub_rn(m[c], __dmul_rn(l, p[c]));
+    }
+  }
+  // forward substitution with the unit lower factor
+#pragma unroll
+  for (int j = 0; j + 1 < B; ++j) {
+    const double xj = __shfl_sync(0xffffffffu, x, lane_of(j));
+    if (pos > j && pos < B) x = __dsub_rn(x, __dmul_rn(m[j], xj));
+  }
+  // backward substitution (the row at position k needs x_{k+1..B-1})
+  double xs[B];
+#pragma unroll
+  for (int k = B - 1; k >= 0; --k) {
+    double sk = x;
+#pragma unroll
+    for (int j = k + 1; j < B; ++j) sk = __dsub_rn(sk, __dmul_rn(m[j], xs[j]));
+    const double xk = sk / m[k];
+    xs[k] = __shfl_sync(0xffffffffu, xk, lane_of(k));
+    if (pos == k && !dead) delta[bm.at(b, k)] = xk;
+  }
+}
+
+// SMC_LU_LANES=0 selects the thread-per-block shared-memory kernel.
+bool lu_lanes() {
+  static const bool v = [] {
+    const char* e = std::getenv("SMC_LU_LANES");
+    return !(e && std::atoi(e) == 0);
+  }();
+  return v;
+}
+
+template <int B>
+void launch_lu_b(const double* jac, double* delta, double beta, BlockMap bm,
+                 unsigned long long* flag, cudaStream_t st) {
+  const std::size_t shm = sizeof(double) * (B * B + B) * kLuThreads;
+  static bool attr = false;
+  if (!attr) {
+    SMC_CUDA(cudaFuncSetAttribute(lu_smem_kernel<B>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  static_cast<int>(shm)));
+    attr = true;
+  }
+  if (lu_lanes()) {
+    lu_lane_kernel<B><<<static_cast<unsigned>((bm.nb + kLuCells - 1) / kLuCells), 256, 0, st>>>(
+        jac, delta, beta, bm, flag);
+  } else {
+    lu_smem_kernel<B><<<static_cast<unsigned>((bm.nb + kLuThreads - 1) / kLuThreads), kLuThreads,
+                        shm, st>>>(jac, delta, beta, bm, flag);
+  }
+  SMC_CHECK_LAUNCH();
+}
+template <int... Bs>
+void launch_lu_any(int B, const double* jac, double* delta, double beta, BlockMap bm,
+                   unsigned long long* flag, cudaStream_t st, std::integer_sequence<int, Bs...>) {
+  ((B == Bs + 1 ? launch_lu_b<Bs + 1>(jac, delta, beta, bm, flag, st) : void()), ...);
+}
+void launch_lu_smem(int B, const double* jac, double* delta, double beta, BlockMap bm,
+                     unsigned long long* flag, cudaStream_t st) {
+  launch_lu_any(B, jac, delta, beta, bm, flag, st, std::make_integer_sequence<int, kLuMaxB>{});
 }
 
 // w -= delta (stiff.cpp:68)
@@ -389,17 +599,7 @@ void DeviceNewton::solve(RhsOp& f, double t, double beta, const double* c, const
     }
     unsigned long long flag;
     if (B <= kLuMaxB) {
-      const std::size_t shm = sizeof(double) * (B * B + B) * kLuThreads;
-      static bool attr = false;
-      if (!attr) {
-        SMC_CUDA(cudaFuncSetAttribute(
-            lu_smem_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-            static_cast<int>(sizeof(double) * (kLuMaxB * kLuMaxB + kLuMaxB) * kLuThreads)));
-        attr = true;
-      }
-      lu_smem_kernel<<<static_cast<unsigned>((bm.nb + kLuThreads - 1) / kLuThreads), kLuThreads,
-                       shm, st>>>(jac_.get(), delta_.get(), beta, bm, slots + 2);
-      SMC_CHECK_LAUNCH();
+      launch_lu_smem(static_cast<int>(B), jac_.get(), delta_.get(), beta, bm, slots + 2, st);
       read_slots(3);
       std::memcpy(&flag, host_slots_ + 2, sizeof(flag));
       if (flag) break;  // singular iteration matrix (stiff.cpp:66)
