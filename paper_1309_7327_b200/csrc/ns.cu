@@ -480,24 +480,65 @@ __global__ void __launch_bounds__(256) wdot_kernel(const double* __restrict__ U,
 // chemistry part alone (MRSDC f2): ctoprim's temperature + wdot fused, so the
 // 32 chemistry calls of an MRSDC step read the 14 conserved fields and write
 // the RHS without materialising the primitive workspace.
+__device__ __forceinline__ void chem_cell(const double* Uc, double* o) {
+  const double rho = Uc[0];
+  const double ri = 1.0 / rho;
+  double u[3], Y[NSP], w[NSP];
+  for (int i = 0; i < 3; ++i) u[i] = Uc[1 + i] * ri;
+#pragma unroll
+  for (int k = 0; k < NSP; ++k) Y[k] = Uc[5 + k] * ri;
+  const double e = Uc[4] * ri - 0.5 * (u[0] * u[0] + u[1] * u[1] + u[2] * u[2]);
+  wdot_cell(rho, temperature(Y, e), Y, w);
+  for (int v = 0; v < 5; ++v) o[v] = 0.0;
+#pragma unroll
+  for (int s = 0; s < NSP; ++s) o[5 + s] = w[s];
+}
+
 __global__ void __launch_bounds__(256) chem_kernel(const double* __restrict__ U,
                                                    double* __restrict__ out, Geo g) {
   const long long n = g.plane * g.nz;
   const long long c = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
   if (c >= n) return;
   const long long cg = c + g.G * g.plane;
-  const long long fl = g.flen;
-  const double rho = U[cg];
-  const double ri = 1.0 / rho;
-  double u[3], Y[NSP], w[NSP];
-  for (int i = 0; i < 3; ++i) u[i] = U[(1 + i) * fl + cg] * ri;
+  double Uc[NV], o[NV];
 #pragma unroll
-  for (int k = 0; k < NSP; ++k) Y[k] = U[(5 + k) * fl + cg] * ri;
-  const double e = U[4 * fl + cg] * ri - 0.5 * (u[0] * u[0] + u[1] * u[1] + u[2] * u[2]);
-  wdot_cell(rho, temperature(Y, e), Y, w);
-  for (int v = 0; v < 5; ++v) out[v * n + c] = 0.0;
+  for (int v = 0; v < NV; ++v) Uc[v] = U[v * g.flen + cg];
+  chem_cell(Uc, o);
 #pragma unroll
-  for (int s = 0; s < NSP; ++s) out[(5 + s) * n + c] = w[s];
+  for (int v = 0; v < NV; ++v) out[v * n + c] = o[v];
+}
+
+// The chemistry part's FD Jacobian, one cell per thread: column j from the
+// cell's state with component j perturbed, as DeviceNewton's column loop
+// (fd_perturb_kernel, the chemistry evaluation, fd_column_kernel) forms it,
+// without the 14 full-grid passes.  Periodic box (no ghost planes).
+__global__ void __launch_bounds__(128) chem_fd_jacobian_kernel(const double* __restrict__ U,
+                                                               const double* __restrict__ FU,
+                                                               double* __restrict__ jac, long long n,
+                                                               double atol, double root_eps) {
+  const long long c = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
+  if (c >= n) return;
+  double w[NV], fw[NV];
+#pragma unroll
+  for (int v = 0; v < NV; ++v) w[v] = U[v * n + c], fw[v] = FU[v * n + c];
+#pragma unroll 1
+  for (int j = 0; j < NV; ++j) {
+    double wp[NV], fp[NV];
+    double hv = 0.0;
+#pragma unroll
+    for (int v = 0; v < NV; ++v) {
+      wp[v] = w[v];
+      if (v == j) {
+        const double a = fabs(w[v]);
+        hv = __dmul_rn(root_eps, (a < atol) ? atol : a);
+        wp[v] = __dadd_rn(w[v], hv);
+      }
+    }
+    chem_cell(wp, fp);
+    const double inv = 1.0 / hv;
+#pragma unroll
+    for (int r = 0; r < NV; ++r) jac[(r * NV + j) * n + c] = __dmul_rn(__dsub_rn(fp[r], fw[r]), inv);
+  }
 }
 
 __global__ void __launch_bounds__(256) tp_kernel(const double* __restrict__ F, double* T,
@@ -686,6 +727,16 @@ void NsWorkspace::rhs(const double* U, double* out, int part, cudaStream_t st) {
     wdot_kernel<<<blocks(n), 256, 0, st>>>(U, F, out, g);
     SMC_CHECK_LAUNCH();
   }
+}
+
+bool NsWorkspace::chem_fd_jacobian(const double* U, const double* FU, double* jac, double atol,
+                                   double root_eps, cudaStream_t st) {
+  if (box_.G != 0) return false;
+  const long long n = box_.cells();
+  chem_fd_jacobian_kernel<<<static_cast<unsigned>((n + 127) / 128), 128, 0, st>>>(U, FU, jac, n,
+                                                                                  atol, root_eps);
+  SMC_CHECK_LAUNCH();
+  return true;
 }
 
 void NsWorkspace::temperature_pressure(const double* U, double* T, double* p, cudaStream_t st) {

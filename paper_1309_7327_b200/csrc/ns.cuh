@@ -31,6 +31,11 @@ class NsWorkspace {
   // SMC_NVAR fields of box.field_len() each (ghosts filled by the caller
   // when box.G > 0).
   void rhs(const double* U, double* out, int part, cudaStream_t st);
+  // Fused FD Jacobian of the chemistry part (RhsOp::fd_block_jacobian) for
+  // the cell-block layout (block SMC_NVAR, field-major); false when the box
+  // has ghost planes (the state is then not cell-block shaped).
+  bool chem_fd_jacobian(const double* U, const double* FU, double* jac, double atol,
+                        double root_eps, cudaStream_t st);
   // T and p of every interior cell (ctoprim), for tests / diagnostics.
   void temperature_pressure(const double* U, double* T, double* p, cudaStream_t st);
   const NsBox& box() const { return box_; }
@@ -60,6 +65,13 @@ class NsRhsOp final : public RhsOp {
     ++evals_;
   }
   const char* name() const override { return "ns"; }
+  bool fd_block_jacobian(const double* w, const double* fw, double* jac, long long block,
+                         int interleaved, double atol, double root_eps) override {
+    if (part_ != kNsChem || block != SMC_NVAR || !interleaved) return false;
+    if (!ws_->chem_fd_jacobian(w, fw, jac, atol, root_eps, stream_)) return false;
+    evals_ += block;
+    return true;
+  }
   NsWorkspace& workspace() { return *ws_; }
   int part() const { return part_; }
 

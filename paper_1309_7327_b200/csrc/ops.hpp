@@ -69,6 +69,18 @@ class RhsOp {
   void set_stream(cudaStream_t s) { stream_ = s; }
   long long evals() const { return evals_; }
 
+  // Optional fused finite-difference block Jacobian for DeviceNewton
+  // (stiff.cpp:16-30 per block): jac[(r * block + j) * nb + b] =
+  // (f(w + h e_j)_r - fw_r) * (1 / h), h = root_eps * max(|w_j|, atol), for
+  // every block b of a block-local f, the same bits as perturbing column j of
+  // every block and evaluating f.  Returns false when the operator has no
+  // fused form for this layout (the caller then runs the column loop).
+  virtual bool fd_block_jacobian(const double* /*w*/, const double* /*fw*/, double* /*jac*/,
+                                 long long /*block*/, int /*interleaved*/, double /*atol*/,
+                                 double /*root_eps*/) {
+    return false;
+  }
+
  protected:
   cudaStream_t stream_ = nullptr;
   long long evals_ = 0;

@@ -586,16 +586,21 @@ void DeviceNewton::solve(RhsOp& f, double t, double beta, const double* c, const
       rep.converged = true;
       break;
     }
-    SMC_CUDA(cudaMemcpyAsync(wp_.get(), w, dim * sizeof(double), cudaMemcpyDeviceToDevice, st));
-    for (long long j = 0; j < B; ++j) {
-      fd_perturb_kernel<<<grid_for(bm.nb), 256, 0, st>>>(w, wp_.get(), h_.get(), j, bm, o.atol,
-                                                        root_eps);
-      SMC_CHECK_LAUNCH();
-      f.eval_device(t, wp_.get(), fp_.get());
-      ++rep.f_evals;
-      fd_column_kernel<<<grid_for(B * bm.nb), 256, 0, st>>>(fp_.get(), fw_.get(), w, wp_.get(),
-                                                           h_.get(), jac_.get(), j, bm);
-      SMC_CHECK_LAUNCH();
+    if (o.block > 0 &&
+        f.fd_block_jacobian(w, fw_.get(), jac_.get(), B, bm.inter, o.atol, root_eps)) {
+      rep.f_evals += static_cast<int>(B);
+    } else {
+      SMC_CUDA(cudaMemcpyAsync(wp_.get(), w, dim * sizeof(double), cudaMemcpyDeviceToDevice, st));
+      for (long long j = 0; j < B; ++j) {
+        fd_perturb_kernel<<<grid_for(bm.nb), 256, 0, st>>>(w, wp_.get(), h_.get(), j, bm, o.atol,
+                                                          root_eps);
+        SMC_CHECK_LAUNCH();
+        f.eval_device(t, wp_.get(), fp_.get());
+        ++rep.f_evals;
+        fd_column_kernel<<<grid_for(B * bm.nb), 256, 0, st>>>(fp_.get(), fw_.get(), w, wp_.get(),
+                                                             h_.get(), jac_.get(), j, bm);
+        SMC_CHECK_LAUNCH();
+      }
     }
     unsigned long long flag;
     if (B <= kLuMaxB) {
