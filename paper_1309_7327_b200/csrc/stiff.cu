@@ -427,6 +427,16 @@ __global__ void __launch_bounds__(256) lu_lane_kernel(const double* jac, double*
   }
 }
 
+// SMC_FD_FUSED=0 forces DeviceNewton's column loop even when f offers a
+// fused block Jacobian (the two must agree bit for bit; see the tests).
+bool fd_fused() {
+  static const bool v = [] {
+    const char* e = std::getenv("SMC_FD_FUSED");
+    return !(e && std::atoi(e) == 0);
+  }();
+  return v;
+}
+
 // SMC_LU_LANES=0 selects the thread-per-block shared-memory kernel.
 bool lu_lanes() {
   static const bool v = [] {
@@ -586,7 +596,7 @@ void DeviceNewton::solve(RhsOp& f, double t, double beta, const double* c, const
       rep.converged = true;
       break;
     }
-    if (o.block > 0 &&
+    if (o.block > 0 && fd_fused() &&
         f.fd_block_jacobian(w, fw_.get(), jac_.get(), B, bm.inter, o.atol, root_eps)) {
       rep.f_evals += static_cast<int>(B);
     } else {
