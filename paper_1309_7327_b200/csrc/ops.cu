@@ -211,29 +211,52 @@ void Narrow3DOp::eval_host(double t, const double* u, double* out) {
   // [lo(c) - S, lo(c+1) - S) have their whole stencil (the last range runs to
   // nz and wraps onto chunk 0), so the stencil lags the copy by S planes and
   // the device->host copy of each range starts as soon as it is computed.
-  h2d(nz_ - s_, nz_);
-  for (int c = 0; c < nchunk; ++c) {
-    h2d(lo(c), c == nchunk - 1 ? nz_ - s_ : lo(c + 1));
-    SMC_CUDA(cudaEventRecord(ev_in_[c], h2d_));
-  }
+  // Enqueue order: per chunk in pipeline order (copy in, stencil, copy out
+  // of the previous chunk) by default.  SMC_E2E_ORDER=0 enqueues all copies
+  // in, then all stencils, then all copies out: the same dependencies, but in
+  // some processes the two copy directions then stopped overlapping (4.5-4.8
+  // ms per call instead of 3.4; measured in 2 of 3 fresh processes at 64-plane
+  // chunks); the pipeline order ran 3.35-3.38 ms in 9 of 9.
+  static const int order = [] {
+    const char* e = std::getenv("SMC_E2E_ORDER");
+    return e ? std::atoi(e) : 1;
+  }();
   auto range = [&](int c, int& k0, int& k1) {
     k0 = c == 0 ? 0 : lo(c) - s_;
     k1 = c == nchunk - 1 ? nz_ : lo(c + 1) - s_;
   };
-  for (int c = 0; c < nchunk; ++c) {
+  auto in = [&](int c) {
+    h2d(lo(c), c == nchunk - 1 ? nz_ - s_ : lo(c + 1));
+    SMC_CUDA(cudaEventRecord(ev_in_[c], h2d_));
+  };
+  auto compute = [&](int c) {
     int k0, k1;
     range(c, k0, k1);
     SMC_CUDA(cudaStreamWaitEvent(stream_, ev_in_[c], 0));
     eval_planes(stage_u_.get(), stage_out_.get(), k0, k1);
     SMC_CUDA(cudaEventRecord(ev_done_[c], stream_));
-  }
-  for (int c = 0; c < nchunk; ++c) {
+  };
+  auto outc = [&](int c) {
     int k0, k1;
     range(c, k0, k1);
     SMC_CUDA(cudaStreamWaitEvent(d2h_, ev_done_[c], 0));
     const std::size_t off = plane * k0, cnt = plane * (k1 - k0);
     SMC_CUDA(cudaMemcpyAsync(out + off, stage_out_.get() + off, cnt * sizeof(double),
                              cudaMemcpyDeviceToHost, d2h_));
+  };
+  h2d(nz_ - s_, nz_);
+  if (order == 1) {
+    // per chunk, in pipeline order
+    for (int c = 0; c < nchunk; ++c) {
+      in(c);
+      compute(c);
+      if (c > 0) outc(c - 1);
+    }
+    outc(nchunk - 1);
+  } else {
+    for (int c = 0; c < nchunk; ++c) in(c);
+    for (int c = 0; c < nchunk; ++c) compute(c);
+    for (int c = 0; c < nchunk; ++c) outc(c);
   }
   SMC_CUDA(cudaStreamSynchronize(d2h_));
   ++evals_;
