@@ -645,11 +645,11 @@ void rhs_v2(const Geo& g, const double* U, const double* F, double* A, double* G
   double* hy1 = SC + 13 * n;
   double* na2 = SC + 27 * n;
   double* hy2 = SC + 40 * n;
-  ns_phase_a<0, S><<<dir_grid<0>(g, allp), DT_THREADS, sm, st>>>(U, F, A, A, GR, out, g, M, -g.G);
+  ns_phase_a<0, S><<<dir_grid<0, NR_A>(g, allp), Tile<0, NR_A>::THREADS, sm, st>>>(U, F, A, A, GR, out, g, M, -g.G);
   SMC_CHECK_LAUNCH();
-  ns_phase_a<1, S><<<dir_grid<1>(g, allp), DT_THREADS, sm, st>>>(U, F, na1, A, GR, hy1, g, M, -g.G);
+  ns_phase_a<1, S><<<dir_grid<1, NR_A>(g, allp), Tile<0, NR_A>::THREADS, sm, st>>>(U, F, na1, A, GR, hy1, g, M, -g.G);
   SMC_CHECK_LAUNCH();
-  ns_phase_a<2, S><<<dir_grid<2>(g, allp), DT_THREADS, sm, st>>>(U, F, na2, A, GR, hy2, g, M, 0);
+  ns_phase_a<2, S><<<dir_grid<2, NR_A>(g, allp), Tile<0, NR_A>::THREADS, sm, st>>>(U, F, na2, A, GR, hy2, g, M, 0);
   SMC_CHECK_LAUNCH();
   ns_mixed_fields<<<blocks(g.plane * allp), 256, 0, st>>>(F, GR, A, MX, g);
   SMC_CHECK_LAUNCH();
@@ -669,6 +669,7 @@ NsWorkspace::NsWorkspace(const NsBox& box, double dx, double dy, double dz, cons
                          int s)
     : box_(box), M_(M), s_(s) {
   require(box.nx >= 9 && box.ny >= 9, "ns: need at least 9 cells in x and y");
+  require(box.nx % 2 == 0, "ns: nx must be even (16-byte staging of x-contiguous pairs)");
   require(box.G == 0 ? box.nz >= 9 : (box.G >= 4 && box.nz >= 1),
           "ns: need nz >= 9 (periodic) or >= 4 ghost planes (slab)");
   require(s == 4 || s == 3, "ns: narrow half width must be 3 or 4");
