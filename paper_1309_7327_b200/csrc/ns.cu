@@ -653,11 +653,11 @@ void rhs_v2(const Geo& g, const double* U, const double* F, double* A, double* G
   SMC_CHECK_LAUNCH();
   ns_mixed_fields<<<blocks(g.plane * allp), 256, 0, st>>>(F, GR, A, MX, g);
   SMC_CHECK_LAUNCH();
-  ns_phase_b<0><<<dir_grid<0>(g, g.nz), DT_THREADS, sizeof(PBSmem), st>>>(F, A, MX, SC + 54 * n, g);
+  ns_phase_b<0><<<dir_grid<0>(g, g.nz), DT_THREADS, sizeof(PBSmem), st>>>(MX, SC + 54 * n, g);
   SMC_CHECK_LAUNCH();
-  ns_phase_b<1><<<dir_grid<1>(g, g.nz), DT_THREADS, sizeof(PBSmem), st>>>(F, A, MX, SC + 67 * n, g);
+  ns_phase_b<1><<<dir_grid<1>(g, g.nz), DT_THREADS, sizeof(PBSmem), st>>>(MX, SC + 67 * n, g);
   SMC_CHECK_LAUNCH();
-  ns_phase_b<2><<<dir_grid<2>(g, g.nz), DT_THREADS, sizeof(PBSmem), st>>>(F, A, MX, SC + 80 * n, g);
+  ns_phase_b<2><<<dir_grid<2>(g, g.nz), DT_THREADS, sizeof(PBSmem), st>>>(MX, SC + 80 * n, g);
   SMC_CHECK_LAUNCH();
   ns_assemble2<<<blocks(n), 256, 0, st>>>(F, A, SC, U, out, g, chem);
   SMC_CHECK_LAUNCH();
