@@ -12,7 +12,10 @@
 //   * ~18 KB of shared memory and no z window: several CTAs per SM.
 // Same interface sums and differencing order as the general kernel
 // (narrow.cu); requires nx % 32 == 0, ny % 8 == 0 and 16-byte aligned fields.
+#include <algorithm>
 #include <cstdint>
+#include <cstdlib>
+#include <string>
 
 #include "common.cuh"
 #include "narrow.cuh"
@@ -152,6 +155,190 @@ void launch2(const NarrowArgs& p, const StencilM& M, cudaStream_t st) {
   SMC_CHECK_LAUNCH();
 }
 
+
+// ---------------------------------------------------------------- y-march
+// The heat RHS as the 3-D kernel's z-march with y as the march axis (no
+// in-plane y): a CTA owns a segment of MW = 256 columns (128 threads, two
+// adjacent cells each) and a chunk of rows.  Per row it stages u and a with
+// a 4-cell x halo (16-byte cp.async, two rows ahead, triple buffer) for the
+// x interfaces; the y window (2S rows of u and b for the thread's two
+// columns) lives in registers, its leading row prefetched two rows ahead.
+// Each interface is formed once: x neighbours' by shuffle, across warps
+// through shared memory, the segment's x0 - 1/2 by warp 0 lane 0; the y
+// interface below the chunk once per chunk.  Same interface sums and
+// differencing order as the tiled kernel (pde.cpp:118-124).
+constexpr int MW = 256;
+constexpr int MT = MW / 2;               // 128 threads
+constexpr int MSW = MW + 2 * HALO2;      // staged row width
+constexpr int MCH = MSW / 2;             // 16-byte chunks per field per row
+constexpr int MCPT = (MCH + MT - 1) / MT;
+
+struct MarchSmem {
+  double row[3][2][MSW];  // u, a
+  double xs[2][MT / 32];  // last x interface of each warp
+  double hxe[2];          // x0 - 1/2
+};
+
+template <int S, bool SRC>
+__global__ void __launch_bounds__(MT, 3) narrow2d_march(const NarrowArgs p, const StencilM M) {
+  constexpr int WIN = 2 * S;
+  __shared__ __align__(16) MarchSmem sm;
+  const int segs = p.nx / MW;
+  const int x0 = (blockIdx.x % segs) * MW;
+  const int k0 = static_cast<int>(blockIdx.x / segs) * p.kc;
+  const int k1 = min(k0 + p.kc, p.ny);
+  const int cp = threadIdx.x, lane = cp & 31, wid = cp >> 5;
+  const int nx = p.nx, ny = p.ny;
+  auto roff = [&](int k) { return static_cast<long long>(wrap(k, ny)) * nx; };
+
+  int soff[MCPT];
+#pragma unroll
+  for (int i = 0; i < MCPT; ++i) {
+    const int c = cp + i * MT;
+    soff[i] = c < MCH ? wrap(x0 - HALO2 + 2 * c, nx) : 0;
+  }
+  auto stage = [&](int buf, int k) {
+    const long long ro = roff(k);
+#pragma unroll
+    for (int i = 0; i < MCPT; ++i) {
+      const int c = cp + i * MT;
+      if (i + 1 < MCPT || c < MCH) {
+        cp16_2(&sm.row[buf][0][2 * c], p.u + ro + soff[i]);
+        cp16_2(&sm.row[buf][1][2 * c], p.cx + ro + soff[i]);
+      }
+    }
+    asm volatile("cp.async.commit_group;\n" ::);
+  };
+  const int col = x0 + 2 * cp;
+  auto ld2 = [&](const double* base, int k) {
+    return __ldg(reinterpret_cast<const double2*>(base + roff(k) + col));
+  };
+
+  // y window: slot j holds row k - S + 1 + j at step k
+  double2 wu[WIN], wb[WIN], pf_u[2], pf_b[2];
+#pragma unroll
+  for (int j = 0; j < WIN; ++j) wu[j] = ld2(p.u, k0 - S + j), wb[j] = ld2(p.cy, k0 - S + j);
+#pragma unroll
+  for (int j = 0; j < 2; ++j)
+    if (k0 + j < k1) pf_u[j] = ld2(p.u, k0 + S + j), pf_b[j] = ld2(p.cy, k0 + S + j);
+  stage(0, k0);
+  if (k0 + 1 < k1)
+    stage(1, k0 + 1);
+  else
+    asm volatile("cp.async.commit_group;\n" ::);
+  // y interface k0 - 1/2
+  double hyp0, hyp1;
+  {
+    double b0[WIN], u0[WIN], b1[WIN], u1[WIN];
+#pragma unroll
+    for (int j = 0; j < WIN; ++j) b0[j] = wb[j].x, u0[j] = wu[j].x, b1[j] = wb[j].y, u1[j] = wu[j].y;
+    hyp0 = narrow_iface<S>(b0, u0, M);
+    hyp1 = narrow_iface<S>(b1, u1, M);
+  }
+  asm volatile("cp.async.wait_group 1;\n" ::: "memory");
+  __syncthreads();
+  const double idx2 = p.idx2, idy2 = p.idy2;
+
+#pragma unroll 1
+  for (int k = k0; k < k1; ++k) {
+    const int t = k - k0, buf = t % 3, hb = t & 1;
+#pragma unroll
+    for (int j = 0; j + 1 < WIN; ++j) wu[j] = wu[j + 1], wb[j] = wb[j + 1];
+    wu[WIN - 1] = pf_u[0];
+    wb[WIN - 1] = pf_b[0];
+    pf_u[0] = pf_u[1];
+    pf_b[0] = pf_b[1];
+    if (k + 2 < k1) pf_u[1] = ld2(p.u, k + 2 + S), pf_b[1] = ld2(p.cy, k + 2 + S);
+    // ---- y interfaces k + 1/2 of my two columns
+    double hy0, hy1;
+    {
+      double b0[WIN], u0[WIN], b1[WIN], u1[WIN];
+#pragma unroll
+      for (int j = 0; j < WIN; ++j) b0[j] = wb[j].x, u0[j] = wu[j].x, b1[j] = wb[j].y, u1[j] = wu[j].y;
+      narrow_iface2<S>(b0, u0, b1, u1, M, hy0, hy1);
+    }
+    // ---- x interfaces x+1/2 of my two cells (staged row k)
+    const double* tu = sm.row[buf][0];
+    const double* ta = sm.row[buf][1];
+    double hx0, hx1;
+    {
+      constexpr int NV = WIN + 2;
+      constexpr int BASE = HALO2 - S + 1 - ((HALO2 - S + 1) & 1);
+      constexpr int OFF = (HALO2 - S + 1) - BASE;
+      double ua[NV], aa[NV];
+      const double* ru = tu + 2 * cp + BASE;
+      const double* ra = ta + 2 * cp + BASE;
+#pragma unroll
+      for (int j = 0; j < NV / 2; ++j) {
+        const double2 vu = lds2_2(ru + 2 * j), va = lds2_2(ra + 2 * j);
+        ua[2 * j] = vu.x, ua[2 * j + 1] = vu.y;
+        aa[2 * j] = va.x, aa[2 * j + 1] = va.y;
+      }
+      narrow_iface2<S>(aa + OFF, ua + OFF, aa + OFF + 1, ua + OFF + 1, M, hx0, hx1);
+    }
+    if (lane == 31) sm.xs[hb][wid] = hx1;
+    if (cp == 0) {  // x0 - 1/2
+      double uu[WIN], aa[WIN];
+#pragma unroll
+      for (int j = 0; j < WIN; ++j) uu[j] = tu[HALO2 - S + j], aa[j] = ta[HALO2 - S + j];
+      sm.hxe[hb] = narrow_iface<S>(aa, uu, M);
+    }
+    if (k + 2 < k1)
+      stage((t + 2) % 3, k + 2);
+    else
+      asm volatile("cp.async.commit_group;\n" ::);
+    asm volatile("cp.async.wait_group 1;\n" ::: "memory");
+    __syncthreads();
+    // ---- (dHx)/dx^2 + (dHy)/dy^2 (+ g0 g(t)), pde.cpp:118-124
+    double hxl = __shfl_up_sync(0xffffffffu, hx1, 1);
+    if (lane == 0) hxl = wid == 0 ? sm.hxe[hb] : sm.xs[hb][wid - 1];
+    double o0 = __dmul_rn(__dsub_rn(hx0, hxl), idx2);
+    double o1 = __dmul_rn(__dsub_rn(hx1, hx0), idx2);
+    o0 = __dadd_rn(o0, __dmul_rn(__dsub_rn(hy0, hyp0), idy2));
+    o1 = __dadd_rn(o1, __dmul_rn(__dsub_rn(hy1, hyp1), idy2));
+    const long long oo = static_cast<long long>(k) * nx + col;
+    if constexpr (SRC) {
+      const double2 g = __ldg(reinterpret_cast<const double2*>(p.g0 + oo));
+      o0 = __dadd_rn(o0, __dmul_rn(g.x, p.gt));
+      o1 = __dadd_rn(o1, __dmul_rn(g.y, p.gt));
+    }
+    *reinterpret_cast<double2*>(p.out + oo) = make_double2(o0, o1);
+    hyp0 = hy0;
+    hyp1 = hy1;
+  }
+  asm volatile("cp.async.wait_group 0;\n" ::: "memory");
+}
+
+template <int S, bool SRC>
+void launch_march(NarrowArgs p, const StencilM& M, cudaStream_t st) {
+  // equal row chunks of about 32 rows, more and shorter (>= 8 rows) while
+  // the grid is under two waves of three CTAs per SM
+  int dev = 0, sms = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const long long segs = p.nx / MW;
+  long long chunks = std::max(1LL, (p.ny + 16LL) / 32);
+  while (segs * chunks < 2LL * 3 * sms && (p.ny + chunks) / (chunks + 1) >= 8) ++chunks;
+  p.kc = static_cast<int>((p.ny + chunks - 1) / chunks);
+  if (const char* e = std::getenv("SMC_HEAT2D_KC")) p.kc = std::max(1, std::atoi(e));
+  const long long grid = segs * ((p.ny + p.kc - 1) / p.kc);
+  narrow2d_march<S, SRC><<<static_cast<unsigned>(grid), MT, 0, st>>>(p, M);
+  SMC_CHECK_LAUNCH();
+}
+
+// SMC_HEAT2D=march selects the y-march where it applies (nx % 256 == 0).  It
+// gives the same bits as the tiled kernel but measured 0.199 against 0.197 ms
+// at 4096^2 (FP64 pipe 58 % at 2.8 warps per scheduler, against 64 % at 7.5
+// for the tiles; row chunks of 16 / 32 / 64 / 128: 0.201 / 0.199 / 0.207 /
+// 0.253 ms; four CTAs per SM spill), so the tiled kernel is the default.
+bool march_enabled() {
+  static bool m = [] {
+    const char* e = std::getenv("SMC_HEAT2D");
+    return e && std::string(e) == "march";
+  }();
+  return m;
+}
+
 }  // namespace
 
 bool narrow2d_fast_applicable(const NarrowArgs& p) {
@@ -161,6 +348,13 @@ bool narrow2d_fast_applicable(const NarrowArgs& p) {
 }
 
 void launch_narrow2d_fast(const NarrowArgs& p, int s, const StencilM& M, cudaStream_t st) {
+  if (p.nx % MW == 0 && p.ny >= 2 * s && march_enabled()) {
+    if (p.g0)
+      s == 4 ? launch_march<4, true>(p, M, st) : launch_march<3, true>(p, M, st);
+    else
+      s == 4 ? launch_march<4, false>(p, M, st) : launch_march<3, false>(p, M, st);
+    return;
+  }
   if (p.g0)
     s == 4 ? launch2<4, true>(p, M, st) : launch2<3, true>(p, M, st);
   else

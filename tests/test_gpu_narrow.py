@@ -382,8 +382,8 @@ def test_peer_halo_two_processes_ipc(cuda):
 @pytest.mark.parametrize("src", [False, True])
 def test_heat2d_tiled_kernel_vs_oracle(cuda, shape, order, src):
     """Shapes with nx % 32 == 0, ny % 8 == 0 take the tiled 2-D kernel
-    (narrow2d_fast.cu); the oracle (pinned to the reference) at 1e-12, with
-    and without the separable source."""
+    (narrow2d_fast.cu), others the general one; the oracle (pinned to the
+    reference) at 1e-12, with and without the separable source."""
     ny, nx = shape
     rng = np.random.default_rng(nx + ny + order)
     a = rng.uniform(0.5, 2.0, shape)
@@ -399,3 +399,72 @@ def test_heat2d_tiled_kernel_vs_oracle(cuda, shape, order, src):
     ref = O.heat2d_rhs(0 if order == 8 else 1, m, s, a, b, g0, gt if src else 0.0, u, dx, dy)
     op = P.HeatOperator(nx, ny, choice, a, b, g0, (lambda t: math.exp(-t)) if src else None)
     assert rel_err(op(0.3, u), ref) <= TOL
+
+
+_TILE_SCRIPT = """
+import sys, numpy as np
+sys.path.insert(0, {root!r})
+import paper_1309_7327_b200 as P
+d = np.load({inp!r})
+op = P.HeatOperator(d['u'].shape[1], d['u'].shape[0], P.StencilChoice.narrow8(*{smc!r}), d['a'], d['b'])
+np.save({out!r}, op(0.0, d['u']))
+"""
+
+
+def test_heat2d_march_equals_tiled_bitwise(cuda, tmp_path):
+    """The y-march (SMC_HEAT2D=march, a child process) and the one-shot tiled
+    kernel (the default) form every interface with the same operation
+    sequence, so the heat RHS is bitwise identical."""
+    import os
+    import subprocess
+    import sys
+    ny, nx = 72, 512
+    rng = np.random.default_rng(5)
+    a, b = rng.uniform(0.5, 2.0, (ny, nx)), rng.uniform(0.5, 2.0, (ny, nx))
+    u = rng.standard_normal((ny, nx))
+    op = P.HeatOperator(nx, ny, P.StencilChoice.narrow8(*SMC), a, b)
+    got = op(0.0, u)
+    inp, out = str(tmp_path / "in.npz"), str(tmp_path / "out.npy")
+    np.savez(inp, u=u, a=a, b=b)
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, SMC_HEAT2D="march")
+    subprocess.run([sys.executable, "-c", _TILE_SCRIPT.format(root=root, inp=inp, out=out,
+                                                             smc=tuple(SMC))],
+                   env=env, check=True, timeout=300)
+    assert np.array_equal(got, np.load(out))
+
+
+@pytest.mark.parametrize("shape", [(9, 256), (75, 512), (300, 256)])
+@pytest.mark.parametrize("src", [False, True])
+def test_heat2d_march_vs_oracle(cuda, tmp_path, shape, src):
+    """The y-march (SMC_HEAT2D=march, in a child process) against the oracle at
+    1e-12: one and several row chunks, ny not a multiple of the chunk."""
+    import os
+    import subprocess
+    import sys
+    ny, nx = shape
+    rng = np.random.default_rng(nx + ny)
+    a, b = rng.uniform(0.5, 2.0, shape), rng.uniform(0.5, 2.0, shape)
+    g0 = rng.standard_normal(shape) if src else np.zeros(shape)
+    u = rng.standard_normal(shape)
+    m, s = O.build_narrow(8, SMC)
+    gt = math.exp(-0.3)
+    ref = O.heat2d_rhs(0, m, s, a, b, g0 if src else None, gt if src else 0.0, u,
+                       2 * math.pi / nx, 2 * math.pi / ny)
+    inp, out = str(tmp_path / "in.npz"), str(tmp_path / "out.npy")
+    np.savez(inp, u=u, a=a, b=b, g0=g0)
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    script = f"""
+import sys, math, numpy as np
+sys.path.insert(0, {root!r})
+import paper_1309_7327_b200 as P
+d = np.load({inp!r})
+ny, nx = d['u'].shape
+g0 = d['g0'] if {src!r} else None
+op = P.HeatOperator(nx, ny, P.StencilChoice.narrow8(*{tuple(SMC)!r}), d['a'], d['b'], g0,
+                    (lambda t: math.exp(-t)) if {src!r} else None)
+np.save({out!r}, op(0.3, d['u']))
+"""
+    subprocess.run([sys.executable, "-c", script], env=dict(os.environ, SMC_HEAT2D="march"),
+                   check=True, timeout=300)
+    assert rel_err(np.load(out), ref) <= TOL
