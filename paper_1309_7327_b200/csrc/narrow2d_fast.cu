@@ -1,7 +1,8 @@
 // 2-D heat operator RHS (HeatOperator::rhs, proj/core/src/pde.cpp:85-129:
 // (a u_x)_x + (b u_y)_y + g0 g(t) on the periodic grid), FP64-issue-optimised
 // like narrow3d_fast.cu's per-plane step, without the z march:
-//   * a CTA owns a 32 x 8 tile (128 threads, 2 adjacent x cells per thread),
+//   * a CTA owns a 32 x 16 tile (256 threads; 32 x 8 when ny % 16 != 0), 2
+//     adjacent x cells per thread,
 //     stages u, a and b with a 4-cell halo by 16-byte cp.async;
 //   * x interfaces of a thread's two cells from 5 LDS.128 per field, y
 //     interfaces of its two columns from 8 LDS.128 per field, each pair
@@ -9,7 +10,8 @@
 //   * the tile-edge interfaces (x0 - 1/2 of each row, y0 - 1/2 of each
 //     column) are packed into warps 1-3, neighbours' interfaces come by
 //     shuffle (x) and through shared memory (y);
-//   * ~18 KB of shared memory and no z window: several CTAs per SM.
+//   * 27.5 KB (17.7 KB) of shared memory and no z window: four (eight) CTAs
+//     per SM.
 // Same interface sums and differencing order as the general kernel
 // (narrow.cu); requires nx % 32 == 0, ny % 8 == 0 and 16-byte aligned fields.
 #include <algorithm>
@@ -24,19 +26,29 @@ namespace smc {
 namespace {
 
 constexpr int TX2 = 32;
-constexpr int TY2 = 8;
 constexpr int LPR2 = TX2 / 2;          // threads per tile row
-constexpr int FT2 = LPR2 * TY2;        // 128 threads
 constexpr int HALO2 = 4;
 constexpr int SW2 = TX2 + 2 * HALO2;   // 40
-constexpr int SH2 = TY2 + 2 * HALO2;   // 16
-constexpr int CH2 = SH2 * SW2 / 2;     // 16-byte chunks per field (320)
-constexpr int CPT2 = (CH2 + FT2 - 1) / FT2;
 
+// Tile of 32 x TY rows: TY = 16 (256 threads, four CTAs per SM) when ny %
+// 16 == 0, else 8 (128 threads, eight CTAs per SM).  The extra interfaces
+// per tile (x0 - 1/2 of each row, y0 - 1/2 of each column) are 40 per 256
+// cells for TY = 8, 48 per 512 for TY = 16.  At 4096^2: TY = 8 0.197 ms,
+// 16 0.192 ms, 32 (two CTAs of 16 warps per SM) 0.216 ms.
+template <int TY>
+struct T2 {
+  static constexpr int FT = LPR2 * TY;              // threads
+  static constexpr int SH = TY + 2 * HALO2;
+  static constexpr int CH = SH * SW2 / 2;           // 16-byte chunks per field
+  static constexpr int CPT = (CH + FT - 1) / FT;
+  static constexpr int OCC = 64 / TY;
+};
+
+template <int TY>
 struct Smem2 {
-  double t[3][SH2 * SW2];  // u, a (x sweep), b (y sweep)
-  double hy[TY2 + 1][TX2];
-  double hxe[TY2];
+  double t[3][T2<TY>::SH * SW2];  // u, a (x sweep), b (y sweep)
+  double hy[TY + 1][TX2];
+  double hxe[TY];
 };
 
 __device__ __forceinline__ void cp16_2(void* dst, const void* src) {
@@ -48,10 +60,12 @@ __device__ __forceinline__ double2 lds2_2(const double* p) {
   return *reinterpret_cast<const double2*>(p);
 }
 
-template <int S, bool SRC>
-__global__ void __launch_bounds__(FT2, S == 4 ? 8 : 6) narrow2d_fast(const NarrowArgs p, const StencilM M) {
+template <int S, bool SRC, int TY>
+__global__ void __launch_bounds__(T2<TY>::FT, S == 4 ? T2<TY>::OCC : T2<TY>::OCC * 3 / 4)
+    narrow2d_fast(const NarrowArgs p, const StencilM M) {
   constexpr int WIN = 2 * S;
-  __shared__ __align__(16) Smem2 sm;
+  constexpr int TY2 = TY, FT2 = T2<TY>::FT, CH2 = T2<TY>::CH, CPT2 = T2<TY>::CPT;
+  __shared__ __align__(16) Smem2<TY> sm;
   const int tiles_x = p.nx / TX2;
   const int x0 = (blockIdx.x % tiles_x) * TX2;
   const int y0 = (blockIdx.x / tiles_x) * TY2;
@@ -150,8 +164,11 @@ __global__ void __launch_bounds__(FT2, S == 4 ? 8 : 6) narrow2d_fast(const Narro
 
 template <int S, bool SRC>
 void launch2(const NarrowArgs& p, const StencilM& M, cudaStream_t st) {
-  const int tiles = (p.nx / TX2) * (p.ny / TY2);
-  narrow2d_fast<S, SRC><<<tiles, FT2, 0, st>>>(p, M);
+  if (p.ny % 16 == 0) {
+    narrow2d_fast<S, SRC, 16><<<(p.nx / TX2) * (p.ny / 16), T2<16>::FT, 0, st>>>(p, M);
+  } else {
+    narrow2d_fast<S, SRC, 8><<<(p.nx / TX2) * (p.ny / 8), T2<8>::FT, 0, st>>>(p, M);
+  }
   SMC_CHECK_LAUNCH();
 }
 
@@ -343,7 +360,7 @@ bool march_enabled() {
 
 bool narrow2d_fast_applicable(const NarrowArgs& p) {
   const auto al = [](const void* q) { return (reinterpret_cast<std::uintptr_t>(q) & 15) == 0; };
-  return p.dims == 2 && p.nx % TX2 == 0 && p.ny % TY2 == 0 && p.nx >= TX2 && p.ny >= TY2 &&
+  return p.dims == 2 && p.nx % TX2 == 0 && p.ny % 8 == 0 && p.nx >= TX2 && p.ny >= 8 &&
          al(p.u) && al(p.cx) && al(p.cy) && al(p.out) && (p.g0 == nullptr || al(p.g0));
 }
 
