@@ -169,6 +169,131 @@ __global__ void __launch_bounds__(256) residual_kernel(const ResidualP p) {
   }
 }
 
+// integrals_fixed_kernel fused with the residual of the previous sweep
+// (MRSDC): both read the same node values F, so one pass serves the next
+// sweep's node integrals and the last sweep's residual.  The per-element
+// residual arithmetic and the block reduction are residual_kernel's.
+template <int ROWS, int NG>
+__global__ void __launch_bounds__(256) integrals_residual_kernel(const IntegralP p,
+                                                                 const ResidualP rp) {
+  const long long n2 = p.n / 2;
+  const long long stride = static_cast<long long>(gridDim.x) * blockDim.x;
+  double r = 0.0;
+  unsigned long long bad = 0;
+  auto res1 = [&](double acc, double u0, double um) {
+    const double v = fabs(__dsub_rn(__fma_rn(rp.dt, acc, u0), um));
+    if (!isfinite(v)) bad = 1;
+    if (v > r) r = v;
+  };
+  for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < n2;
+       i += stride) {
+    double2 gv[NG];
+#pragma unroll
+    for (int j = 0; j < NG; ++j) gv[j] = __ldg(reinterpret_cast<const double2*>(p.g[j]) + i);
+    const double2 u0 = __ldg(reinterpret_cast<const double2*>(rp.u0) + i);
+    const double2 um = __ldg(reinterpret_cast<const double2*>(rp.um) + i);
+#pragma unroll
+    for (int rr = 0; rr < ROWS; ++rr) {
+      double a0 = p.w[rr][0] * gv[0].x, a1 = p.w[rr][0] * gv[0].y;
+#pragma unroll
+      for (int j = 1; j < NG; ++j) a0 = __fma_rn(p.w[rr][j], gv[j].x, a0), a1 = __fma_rn(p.w[rr][j], gv[j].y, a1);
+      reinterpret_cast<double2*>(p.out[rr])[i] = make_double2(__dmul_rn(p.dt, a0), __dmul_rn(p.dt, a1));
+    }
+    double q0 = rp.q[0] * gv[0].x, q1 = rp.q[0] * gv[0].y;
+#pragma unroll
+    for (int j = 1; j < NG; ++j) q0 = __fma_rn(rp.q[j], gv[j].x, q0), q1 = __fma_rn(rp.q[j], gv[j].y, q1);
+    res1(q0, u0.x, um.x);
+    res1(q1, u0.y, um.y);
+  }
+  if ((p.n & 1) && blockIdx.x == 0 && threadIdx.x == 0) {  // odd tail element
+    const long long i = p.n - 1;
+#pragma unroll
+    for (int rr = 0; rr < ROWS; ++rr) {
+      double acc = p.w[rr][0] * p.g[0][i];
+#pragma unroll
+      for (int j = 1; j < NG; ++j) acc = __fma_rn(p.w[rr][j], p.g[j][i], acc);
+      p.out[rr][i] = __dmul_rn(p.dt, acc);
+    }
+    double acc = rp.q[0] * p.g[0][i];
+#pragma unroll
+    for (int j = 1; j < NG; ++j) acc = __fma_rn(rp.q[j], p.g[j][i], acc);
+    res1(acc, rp.u0[i], rp.um[i]);
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    r = fmax(r, __shfl_xor_sync(0xffffffffu, r, o));
+    bad |= __shfl_xor_sync(0xffffffffu, bad, o);
+  }
+  __shared__ double wr[8];
+  __shared__ unsigned long long wb[8];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  if (lane == 0) {
+    wr[warp] = r;
+    wb[warp] = bad;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int w = 1; w < static_cast<int>(blockDim.x >> 5); ++w) {
+      r = fmax(r, wr[w]);
+      bad |= wb[w];
+    }
+    if (isinf(r)) bad = 1;
+    atomicMax(rp.slot, static_cast<unsigned long long>(__double_as_longlong(r)));
+    if (bad) atomicMax(rp.slot + 1, 1ull);
+  }
+}
+
+// SDC: the first node update of sweep k (no F difference, sdc.cpp:74) fused
+// with the residual of sweep k - 1: both read u0 and the same node values F.
+// Per element the update is sweep_update_kernel<0, NG>'s and the residual
+// residual_kernel's; the block reduction is residual_kernel's.  um must not
+// alias next (the caller falls back to two launches for one-interval nodes).
+template <int NG>
+__global__ void __launch_bounds__(256) update_residual_kernel(const UpdateP p, const ResidualP rp) {
+  double r = 0.0;
+  unsigned long long bad = 0;
+  const long long stride = static_cast<long long>(gridDim.x) * blockDim.x;
+  for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < p.n;
+       i += stride) {
+    double gv[NG];
+#pragma unroll
+    for (int j = 0; j < NG; ++j) gv[j] = p.g[j][i];
+    const double cur = p.cur[i];
+    double acc = p.w[0] * gv[0];
+#pragma unroll
+    for (int j = 1; j < NG; ++j) acc = __fma_rn(p.w[j], gv[j], acc);
+    p.next[i] = __dadd_rn(cur, __dmul_rn(p.dt, acc));
+    double q = rp.q[0] * gv[0];
+#pragma unroll
+    for (int j = 1; j < NG; ++j) q = __fma_rn(rp.q[j], gv[j], q);
+    const double v = fabs(__dsub_rn(__fma_rn(rp.dt, q, cur), rp.um[i]));
+    if (!isfinite(v)) bad = 1;
+    if (v > r) r = v;
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    r = fmax(r, __shfl_xor_sync(0xffffffffu, r, o));
+    bad |= __shfl_xor_sync(0xffffffffu, bad, o);
+  }
+  __shared__ double wr[8];
+  __shared__ unsigned long long wb[8];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  if (lane == 0) {
+    wr[warp] = r;
+    wb[warp] = bad;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int w = 1; w < static_cast<int>(blockDim.x >> 5); ++w) {
+      r = fmax(r, wr[w]);
+      bad |= wb[w];
+    }
+    if (isinf(r)) bad = 1;
+    atomicMax(rp.slot, static_cast<unsigned long long>(__double_as_longlong(r)));
+    if (bad) atomicMax(rp.slot + 1, 1ull);
+  }
+}
+
 struct BeRhsP {
   double* c;
   const double* u;
@@ -281,6 +406,60 @@ void launch_residual(const double* u0, const double* um, int ng, const double* c
   SMC_CHECK_LAUNCH();
 }
 
+void launch_integrals_residual(int rows, double* const* out, int ng, const double* const* g,
+                               const double* w, double dt, const double* u0, const double* um,
+                               const double* q, long long n, double* slot, cudaStream_t st) {
+  bool aligned = (reinterpret_cast<std::uintptr_t>(u0) & 15) == 0 &&
+                 (reinterpret_cast<std::uintptr_t>(um) & 15) == 0;
+  for (int j = 0; j < ng; ++j) aligned = aligned && (reinterpret_cast<std::uintptr_t>(g[j]) & 15) == 0;
+  for (int r = 0; r < rows; ++r)
+    aligned = aligned && (reinterpret_cast<std::uintptr_t>(out[r]) & 15) == 0;
+  if (!(aligned && rows == 8 && ng == 12)) {
+    launch_residual(u0, um, ng, g, q, dt, n, slot, st);
+    launch_integrals(rows, out, ng, g, w, dt, n, st);
+    return;
+  }
+  IntegralP p{};
+  p.rows = rows, p.ng = ng, p.dt = dt, p.n = n;
+  for (int r = 0; r < rows; ++r) {
+    p.out[r] = out[r];
+    for (int j = 0; j < ng; ++j) p.w[r][j] = w[r * ng + j];
+  }
+  ResidualP rp{};
+  rp.u0 = u0, rp.um = um, rp.dt = dt, rp.n = n, rp.ng = ng;
+  rp.slot = reinterpret_cast<unsigned long long*>(slot);
+  for (int j = 0; j < ng; ++j) p.g[j] = g[j], rp.g[j] = g[j], rp.q[j] = q[j];
+  const int fb = static_cast<int>(std::max(
+      1LL, std::min((n / 2 + 255) / 256, static_cast<long long>(num_sms()) * 16)));
+  integrals_residual_kernel<8, 12><<<fb, 256, 0, st>>>(p, rp);
+  SMC_CHECK_LAUNCH();
+}
+
+void launch_update_residual(double* next, const double* u0, const double* um, int ng,
+                            const double* const* g, const double* w, const double* q, double dt,
+                            long long n, double* slot, cudaStream_t st) {
+  require(um != next, "update_residual: the residual's end state is the updated node");
+  if (ng < 2 || ng > 5) {
+    launch_residual(u0, um, ng, g, q, dt, n, slot, st);
+    launch_sweep_update(next, u0, 0, nullptr, nullptr, nullptr, ng, g, w, dt, nullptr, n, st);
+    return;
+  }
+  UpdateP p{};
+  p.next = next, p.cur = u0, p.dt = dt, p.n = n, p.ng = ng;
+  ResidualP rp{};
+  rp.u0 = u0, rp.um = um, rp.dt = dt, rp.n = n, rp.ng = ng;
+  rp.slot = reinterpret_cast<unsigned long long*>(slot);
+  for (int j = 0; j < ng; ++j) p.g[j] = g[j], p.w[j] = w[j], rp.g[j] = g[j], rp.q[j] = q[j];
+  const int blocks = blocks_for(n);
+  switch (ng) {
+    case 2: update_residual_kernel<2><<<blocks, 256, 0, st>>>(p, rp); break;
+    case 3: update_residual_kernel<3><<<blocks, 256, 0, st>>>(p, rp); break;
+    case 4: update_residual_kernel<4><<<blocks, 256, 0, st>>>(p, rp); break;
+    default: update_residual_kernel<5><<<blocks, 256, 0, st>>>(p, rp); break;
+  }
+  SMC_CHECK_LAUNCH();
+}
+
 void SweepDiag::add(const SweepDiag& o) {
   residuals.insert(residuals.end(), o.residuals.begin(), o.residuals.end());
   sweeps += o.sweeps;
@@ -367,9 +546,24 @@ void DeviceSdc::run(RhsOp& f, double t_n, double dt, bool have_f0, SweepDiag& d)
   }
   std::vector<const double*> fold(m + 1, f0_), fnew(m + 1, f0_);
   SMC_CUDA(cudaMemsetAsync(res_.get(), 0, res_.size() * sizeof(double), st));
-  std::vector<double> hist;
-  int collected = 0;
-  for (int k = 1; k <= iterations_; ++k) {
+  const double* qrow = &tab_.q.a[static_cast<std::size_t>(m - 1) * (m + 1)];
+  int collected = 0, formed = 0;
+  // the residual of sweep k was formed: read it back when early stopping is
+  // on; false when the step ends there (sdc.cpp:84-91)
+  auto check = [&](int k) {
+    formed = k;
+    if (cutoff_ <= 0.0) return true;
+    collect(res_, k - 1, 1, st, reduce_, d);
+    collected = k;
+    if (!stalled(d.residuals, cutoff_)) return true;
+    d.early_stop = true;
+    return false;
+  };
+  // one-interval nodes: u_[m] is node 1's buffer, so the residual is formed
+  // at the end of its own sweep
+  const bool fuse = m > 1;
+  bool stop = false;
+  for (int k = 1; k <= iterations_ && !stop; ++k) {
     std::vector<double*>& set = (k % 2) ? fa_ : fb_;
     for (int j = 1; j <= m; ++j) fnew[j] = set[j - 1];
     for (int r = 0; r < m; ++r) {
@@ -378,24 +572,35 @@ void DeviceSdc::run(RhsOp& f, double t_n, double dt, bool have_f0, SweepDiag& d)
       const double* db[1] = {fold[r]};
       const double dc[1] = {dtm};
       const int nd = (r == 0 || fnew[r] == fold[r]) ? 0 : 1;  // m == 0 branch, sdc.cpp:74
-      launch_sweep_update(u_[r + 1], u_[r], nd, da, db, dc, m + 1, fold.data(),
-                          &tab_.s.a[static_cast<std::size_t>(r) * (m + 1)], dt, nullptr, n, st);
+      const double* srow = &tab_.s.a[static_cast<std::size_t>(r) * (m + 1)];
+      if (fuse && r == 0 && k > 1) {
+        // node 1 of sweep k with the residual of sweep k - 1 (same u0 and F;
+        // u_[m] is not written here for m > 1, so a stop leaves sweep k - 1's
+        // end state)
+        launch_update_residual(u_[1], u_[0], u_[m], m + 1, fold.data(), srow, qrow, dt, n,
+                               res_.get() + 2 * (k - 2), st);
+        if (!check(k - 1)) {
+          stop = true;
+          break;
+        }
+      } else {
+        launch_sweep_update(u_[r + 1], u_[r], nd, da, db, dc, m + 1, fold.data(), srow, dt,
+                            nullptr, n, st);
+      }
       f.eval_device(t_n + tau[r + 1] * dt, u_[r + 1], set[r]);
       ++d.fresh_evals;
     }
-    launch_residual(u_[0], u_[m], m + 1, fnew.data(),
-                    &tab_.q.a[static_cast<std::size_t>(m - 1) * (m + 1)], dt, n, res_.get() + 2 * (k - 1),
-                    st);
+    if (stop) break;
     d.sweeps = k;
     fold = fnew;
-    if (cutoff_ > 0.0) {
-      collect(res_, k - 1, 1, st, reduce_, d);
-      collected = k;
-      if (stalled(d.residuals, cutoff_)) {
-        d.early_stop = true;
-        break;
-      }
+    if (!fuse) {
+      launch_residual(u_[0], u_[m], m + 1, fold.data(), qrow, dt, n, res_.get() + 2 * (k - 1), st);
+      if (!check(k)) break;
     }
+  }
+  if (formed < d.sweeps) {
+    launch_residual(u_[0], u_[m], m + 1, fold.data(), qrow, dt, n, res_.get() + 2 * (d.sweeps - 1), st);
+    check(d.sweeps);
   }
   if (collected < d.sweeps) collect(res_, collected, d.sweeps - collected, st, reduce_, d);
   f_last_ = const_cast<double*>(fold[m]);
@@ -467,6 +672,59 @@ void DeviceMrsdc::ensure(long long dim) {
 }
 
 // MrsdcStepper::step_mode1 (mrsdc.cpp:84-135) on the internal buffers.
+// The node integrals at the start of sweep k and the residual of sweep k - 1
+// read the same node values, so they are formed in one pass
+// (launch_integrals_residual).  With early stopping the residual of sweep
+// k - 1 is read back there and a stall ends the step before sweep k changes
+// any state, as mrsdc.cpp:120-131 stops after sweep k - 1.
+struct DeviceMrsdc::SweepResiduals {
+  DeviceMrsdc& m;
+  SweepDiag& d;
+  cudaStream_t st;
+  int m2, ng;
+  const std::vector<double>& w;
+  const std::vector<double>& qrow;
+  double dt;
+  long long n;
+  int formed = 0, collected = 0;
+
+  static std::vector<const double*> cat(const std::vector<const double*>& a,
+                                        const std::vector<const double*>& b) {
+    std::vector<const double*> g(a.begin(), a.end());
+    g.insert(g.end(), b.begin(), b.end());
+    return g;
+  }
+  // the residual of sweep k was formed: false when early stopping ends here
+  bool check(int k) {
+    formed = k;
+    if (m.cutoff_ <= 0.0) return true;
+    collect(m.res_, k - 1, 1, st, m.reduce_, d);
+    collected = k;
+    if (!stalled(d.residuals, m.cutoff_)) return true;
+    d.early_stop = true;
+    return false;
+  }
+  bool begin(int k, const std::vector<const double*>& o1, const std::vector<const double*>& o2) {
+    const std::vector<const double*> g = cat(o1, o2);
+    if (k == 1) {
+      launch_integrals(m2, m.so_.data(), ng, g.data(), w.data(), dt, n, st);
+      return true;
+    }
+    launch_integrals_residual(m2, m.so_.data(), ng, g.data(), w.data(), dt, m.u_[0], m.u_[m2],
+                              qrow.data(), n, m.res_.get() + 2 * (k - 2), st);
+    return check(k - 1);
+  }
+  void end(const std::vector<const double*>& o1, const std::vector<const double*>& o2) {
+    if (formed < d.sweeps) {
+      const std::vector<const double*> g = cat(o1, o2);
+      launch_residual(m.u_[0], m.u_[m2], ng, g.data(), qrow.data(), dt, n,
+                      m.res_.get() + 2 * (d.sweeps - 1), st);
+      check(d.sweeps);
+    }
+    if (collected < d.sweeps) collect(m.res_, collected, d.sweeps - collected, st, m.reduce_, d);
+  }
+};
+
 void DeviceMrsdc::run(RhsOp& f1, RhsOp& f2, double t_n, double dt, bool have1, bool have2,
                       SweepDiag& d) {
   const int m1 = h_.coarse.intervals(), m2 = h_.fine.intervals();
@@ -498,14 +756,13 @@ void DeviceMrsdc::run(RhsOp& f1, RhsOp& f2, double t_n, double dt, bool have1, b
   for (int j = 0; j <= m1; ++j) qrow[j] = h_.q21(m2 - 1, j);
   for (int j = 0; j <= m2; ++j) qrow[m1 + 1 + j] = h_.q22(m2 - 1, j);
   SMC_CUDA(cudaMemsetAsync(res_.get(), 0, res_.size() * sizeof(double), st));
-  int collected = 0;
+  SweepResiduals rs{*this, d, st, m2, ng, w, qrow, dt, n};
   for (int k = 1; k <= iterations_; ++k) {
     std::vector<double*>& s1 = (k % 2) ? f1a_ : f1b_;
     std::vector<double*>& s2 = (k % 2) ? f2a_ : f2b_;
     // accumulate_node_terms (mrsdc.cpp:69-82) from the previous sweep's values
-    std::vector<const double*> g(o1.begin(), o1.end());
-    g.insert(g.end(), o2.begin(), o2.end());
-    launch_integrals(m2, so_.data(), ng, g.data(), w.data(), dt, n, st);
+    // (with the previous sweep's residual, mrsdc.cpp:23-35, in the same pass)
+    if (!rs.begin(k, o1, o2)) break;
     for (int p = 1; p <= m1; ++p) n1[p] = o1[p];  // refreshed when the sweep reaches node p
     for (int q = 0; q < m2; ++q) {
       const double dtq = (t2[q + 1] - t2[q]) * dt;
@@ -527,22 +784,11 @@ void DeviceMrsdc::run(RhsOp& f1, RhsOp& f2, double t_n, double dt, bool have1, b
         ++d.f1_evals;
       }
     }
-    std::vector<const double*> gn(n1.begin(), n1.end());
-    gn.insert(gn.end(), n2.begin(), n2.end());
-    launch_residual(u_[0], u_[m2], ng, gn.data(), qrow.data(), dt, n, res_.get() + 2 * (k - 1), st);
     d.sweeps = k;
     o1 = n1;
     o2 = n2;
-    if (cutoff_ > 0.0) {
-      collect(res_, k - 1, 1, st, reduce_, d);
-      collected = k;
-      if (stalled(d.residuals, cutoff_)) {
-        d.early_stop = true;
-        break;
-      }
-    }
   }
-  if (collected < d.sweeps) collect(res_, collected, d.sweeps - collected, st, reduce_, d);
+  rs.end(o1, o2);
   f1_last_ = const_cast<double*>(o1[m1]);
   f2_last_ = const_cast<double*>(o2[m2]);
 }
@@ -598,13 +844,11 @@ void DeviceMrsdc::run2(RhsOp& f1, RhsOp& f2, double t_n, double dt, bool have1, 
   for (int j = 0; j <= m1; ++j) qrow[j] = h_.q21(m2 - 1, j);
   for (int j = 0; j <= m2; ++j) qrow[m1 + 1 + j] = h_.q22(m2 - 1, j);
   SMC_CUDA(cudaMemsetAsync(res_.get(), 0, res_.size() * sizeof(double), st));
-  int collected = 0;
+  SweepResiduals rs{*this, d, st, m2, ng, w, qrow, dt, n};
   for (int k = 1; k <= iterations_; ++k) {
     std::vector<double*>& s1 = (k % 2) ? f1a_ : f1b_;
     std::vector<double*>& s2 = (k % 2) ? f2a_ : f2b_;
-    std::vector<const double*> g(o1.begin(), o1.end());
-    g.insert(g.end(), o2.begin(), o2.end());
-    launch_integrals(m2, so_.data(), ng, g.data(), w.data(), dt, n, st);
+    if (!rs.begin(k, o1, o2)) break;
     for (int p = 0; p < m1; ++p) {
       const int q0 = h_.fine_of_coarse[p], q1 = h_.fine_of_coarse[p + 1];
       const double dt1 = (t1[p + 1] - t1[p]) * dt;
@@ -637,22 +881,11 @@ void DeviceMrsdc::run2(RhsOp& f1, RhsOp& f2, double t_n, double dt, bool have1, 
         ++d.f2_evals;
       }
     }
-    std::vector<const double*> gn(n1.begin(), n1.end());
-    gn.insert(gn.end(), n2.begin(), n2.end());
-    launch_residual(u_[0], u_[m2], ng, gn.data(), qrow.data(), dt, n, res_.get() + 2 * (k - 1), st);
     d.sweeps = k;
     o1 = n1;
     o2 = n2;
-    if (cutoff_ > 0.0) {
-      collect(res_, k - 1, 1, st, reduce_, d);
-      collected = k;
-      if (stalled(d.residuals, cutoff_)) {
-        d.early_stop = true;
-        break;
-      }
-    }
   }
-  if (collected < d.sweeps) collect(res_, collected, d.sweeps - collected, st, reduce_, d);
+  rs.end(o1, o2);
   f1_last_ = const_cast<double*>(o1[m1]);
   f2_last_ = const_cast<double*>(o2[m2]);
 }

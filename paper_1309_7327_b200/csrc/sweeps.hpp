@@ -78,6 +78,7 @@ class DeviceMrsdc {
   const Hierarchy& hierarchy() const { return h_; }
 
  private:
+  struct SweepResiduals;  // node integrals + per-sweep residuals (sweeps.cu)
   void ensure(long long dim);
   void run(RhsOp& f1, RhsOp& f2, double t_n, double dt, bool have_f01, bool have_f02,
            SweepDiag& d);
@@ -120,5 +121,11 @@ void launch_be_rhs(double* c, const double* u, int nso, const double* const* so,
 // *slot = max_i |u0 + dt sum_j q_j g_j - um|  (slot must be zeroed; NaN -> +inf)
 void launch_residual(const double* u0, const double* um, int ng, const double* const* g,
                      const double* q, double dt, long long n, double* slot, cudaStream_t st);
+// launch_integrals for the next sweep fused with launch_residual of the last
+// one (they read the same node values); two launches where the fused
+// fixed-shape kernel does not apply.
+void launch_integrals_residual(int rows, double* const* out, int ng, const double* const* g,
+                               const double* w, double dt, const double* u0, const double* um,
+                               const double* q, long long n, double* slot, cudaStream_t st);
 
 }  // namespace smc
