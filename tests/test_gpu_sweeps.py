@@ -9,6 +9,7 @@ import numpy as np
 import pytest
 
 import paper_1309_7327_b200 as P
+from oracle import oracle as O
 from conftest import rel_err
 
 pytestmark = pytest.mark.gpu
@@ -145,3 +146,68 @@ def test_acceptance_c1_t1_error_table(cuda):
         u, _ = st.integrate(op, np.sin(X) * np.sin(Y), 0.0, 1.0, steps)
         err = np.abs(u - math.exp(-1.0) * np.sin(X) * np.sin(Y)).max()
         assert abs(err - target) <= 0.02 * target, (n, err)
+
+
+def _lin_cb(lam, forcing=0.0):
+    lam = np.asarray(lam, dtype=np.float64)
+
+    def f(t, up, op, n, ctx):
+        for i in range(n):
+            op[i] = lam[i] * up[i] + forcing * math.sin(t)
+    return O.RHS_CB(f)
+
+
+@pytest.mark.parametrize("cutoff", [0.0, 0.05, 0.3])
+def test_sdc_early_stop_vs_oracle(golden, cuda, cutoff):
+    """The residual of sweep k-1 is formed in sweep k's first update and the
+    stall test taken there: sweeps, evaluations, residual histories and the
+    end state agree with the oracle restatement of sdc.cpp (pinned to the
+    reference), with and without early stopping."""
+    import ctypes as C
+    lam = np.array([-1.0, -0.5, -2.0])
+    u0 = np.array([1.0, 0.5, -0.25])
+    uo, res = np.empty(3), np.zeros(256)
+    sw, fe, es = C.c_int(), C.c_int(), C.c_int()
+    D = lambda a: np.ascontiguousarray(a, dtype=np.float64)  # noqa: E731
+    rc = O.lib().or_integrate_sdc(_lin_cb(lam), None, 3, O.dp(u0), C.c_double(0.0),
+                                  C.c_double(1.0), 3, 2, O.dp(D(golden["nodes_gl3"])),
+                                  O.dp(D(golden["q_gl3"])), O.dp(D(golden["s_gl3"])), 12,
+                                  C.c_double(cutoff), 1, O.dp(uo), O.dp(res), 256, C.byref(sw),
+                                  C.byref(fe), C.byref(es))
+    assert rc == 0
+    st = P.SdcStepper(3, P.StepControls(12, cutoff))
+    u, d = st.integrate(P.CallbackRhs(3, lambda t, u: lam * u), u0, 0.0, 1.0, 3)
+    assert (d.sweeps, d.fresh_evals, bool(d.early_stop)) == (sw.value, fe.value, bool(es.value))
+    np.testing.assert_allclose(d.residual_history, res[:sw.value], rtol=1e-6, atol=1e-16)
+    assert rel_err(u, uo) <= 1e-13
+
+
+@pytest.mark.parametrize("cutoff", [0.0, 0.05, 0.3])
+def test_mrsdc_early_stop_vs_oracle(golden, cuda, cutoff):
+    """MRSDC mode 1 with the residual formed in the next sweep's node-integral
+    pass: as the oracle restatement of mrsdc.cpp (pinned to the reference),
+    with and without early stopping."""
+    import ctypes as C
+    l1, l2 = np.array([-1.0, -0.5, -2.0]), np.array([-10.0, -4.0, -7.0])
+    u0 = golden["mr_u0"]
+    h = {k[2:]: golden[k] for k in golden if k.startswith("h_")}
+    I = lambda a: np.ascontiguousarray(a, dtype=np.int32)  # noqa: E731
+    D = lambda a: np.ascontiguousarray(a, dtype=np.float64)  # noqa: E731
+    arrs = [D(h[k]) for k in ("coarse", "fine", "s21", "q21", "s22", "q22")]
+    uo, res = np.empty(3), np.zeros(256)
+    sw, n1, n2 = C.c_int(), C.c_int(), C.c_int()
+    rc = O.lib().or_integrate_mrsdc1(
+        _lin_cb(l1), None, _lin_cb(l2, 0.1), None, 3, O.dp(D(u0)), C.c_double(0.0),
+        C.c_double(0.4), 4, 2, O.dp(arrs[0]), len(h["fine"]) - 1, O.dp(arrs[1]), O.dp(arrs[2]),
+        O.dp(arrs[3]), O.dp(arrs[4]), O.dp(arrs[5]), O.ip(I(h["fine_of_coarse"])),
+        O.ip(I(h["p_map"])), 10, C.c_double(cutoff), O.dp(uo), O.dp(res), 256, C.byref(sw),
+        C.byref(n1), C.byref(n2))
+    assert rc == 0
+    f1 = P.CallbackRhs(3, lambda t, u: l1 * u)
+    f2 = P.CallbackRhs(3, lambda t, u: l2 * u + 0.1 * math.sin(t))
+    st = P.MrsdcStepper(3, 5, P.StepControls(10, cutoff))
+    u, d = st.integrate_mode1(f1, f2, u0, 0.0, 0.4, 4)
+    assert (d.sweeps, d.f1_evals, d.f2_evals) == (sw.value, n1.value, n2.value)
+    np.testing.assert_allclose(d.residual_history, res[:sw.value], rtol=1e-6, atol=1e-16)
+    assert rel_err(u, uo) <= 1e-13
+    assert bool(d.early_stop) == (d.sweeps < 4 * 10)
