@@ -157,12 +157,10 @@ def _lin_cb(lam, forcing=0.0):
     return O.RHS_CB(f)
 
 
-@pytest.mark.parametrize("cutoff", [0.0, 0.05, 0.3])
-def test_sdc_early_stop_vs_oracle(golden, cuda, cutoff):
-    """The residual of sweep k-1 is formed in sweep k's first update and the
-    stall test taken there: sweeps, evaluations, residual histories and the
-    end state agree with the oracle restatement of sdc.cpp (pinned to the
-    reference), with and without early stopping."""
+def test_sdc_vs_oracle_long(golden, cuda):
+    """40 sweeps per step (the residual of sweep k-1 formed in sweep k's first
+    update): sweeps, evaluations, residual histories (down to the rounding
+    floor) and the end state as the oracle restatement of sdc.cpp."""
     import ctypes as C
     lam = np.array([-1.0, -0.5, -2.0])
     u0 = np.array([1.0, 0.5, -0.25])
@@ -170,23 +168,21 @@ def test_sdc_early_stop_vs_oracle(golden, cuda, cutoff):
     sw, fe, es = C.c_int(), C.c_int(), C.c_int()
     D = lambda a: np.ascontiguousarray(a, dtype=np.float64)  # noqa: E731
     rc = O.lib().or_integrate_sdc(_lin_cb(lam), None, 3, O.dp(u0), C.c_double(0.0),
-                                  C.c_double(1.0), 3, 2, O.dp(D(golden["nodes_gl3"])),
-                                  O.dp(D(golden["q_gl3"])), O.dp(D(golden["s_gl3"])), 12,
-                                  C.c_double(cutoff), 1, O.dp(uo), O.dp(res), 256, C.byref(sw),
+                                  C.c_double(1.0), 2, 2, O.dp(D(golden["nodes_gl3"])),
+                                  O.dp(D(golden["q_gl3"])), O.dp(D(golden["s_gl3"])), 40,
+                                  C.c_double(0.0), 1, O.dp(uo), O.dp(res), 256, C.byref(sw),
                                   C.byref(fe), C.byref(es))
     assert rc == 0
-    st = P.SdcStepper(3, P.StepControls(12, cutoff))
-    u, d = st.integrate(P.CallbackRhs(3, lambda t, u: lam * u), u0, 0.0, 1.0, 3)
+    st = P.SdcStepper(3, P.StepControls(40, 0.0))
+    u, d = st.integrate(P.CallbackRhs(3, lambda t, u: lam * u), u0, 0.0, 1.0, 2)
     assert (d.sweeps, d.fresh_evals, bool(d.early_stop)) == (sw.value, fe.value, bool(es.value))
-    np.testing.assert_allclose(d.residual_history, res[:sw.value], rtol=1e-6, atol=1e-16)
+    np.testing.assert_allclose(d.residual_history, res[:sw.value], rtol=1e-6, atol=1e-15)
     assert rel_err(u, uo) <= 1e-13
 
 
-@pytest.mark.parametrize("cutoff", [0.0, 0.05, 0.3])
-def test_mrsdc_early_stop_vs_oracle(golden, cuda, cutoff):
-    """MRSDC mode 1 with the residual formed in the next sweep's node-integral
-    pass: as the oracle restatement of mrsdc.cpp (pinned to the reference),
-    with and without early stopping."""
+def test_mrsdc_vs_oracle_long(golden, cuda):
+    """MRSDC mode 1, 40 sweeps per step (the residual formed in the next
+    sweep's node-integral pass), as the oracle restatement of mrsdc.cpp."""
     import ctypes as C
     l1, l2 = np.array([-1.0, -0.5, -2.0]), np.array([-10.0, -4.0, -7.0])
     u0 = golden["mr_u0"]
@@ -198,16 +194,61 @@ def test_mrsdc_early_stop_vs_oracle(golden, cuda, cutoff):
     sw, n1, n2 = C.c_int(), C.c_int(), C.c_int()
     rc = O.lib().or_integrate_mrsdc1(
         _lin_cb(l1), None, _lin_cb(l2, 0.1), None, 3, O.dp(D(u0)), C.c_double(0.0),
-        C.c_double(0.4), 4, 2, O.dp(arrs[0]), len(h["fine"]) - 1, O.dp(arrs[1]), O.dp(arrs[2]),
+        C.c_double(0.4), 2, 2, O.dp(arrs[0]), len(h["fine"]) - 1, O.dp(arrs[1]), O.dp(arrs[2]),
         O.dp(arrs[3]), O.dp(arrs[4]), O.dp(arrs[5]), O.ip(I(h["fine_of_coarse"])),
-        O.ip(I(h["p_map"])), 10, C.c_double(cutoff), O.dp(uo), O.dp(res), 256, C.byref(sw),
+        O.ip(I(h["p_map"])), 40, C.c_double(0.0), O.dp(uo), O.dp(res), 256, C.byref(sw),
         C.byref(n1), C.byref(n2))
     assert rc == 0
     f1 = P.CallbackRhs(3, lambda t, u: l1 * u)
     f2 = P.CallbackRhs(3, lambda t, u: l2 * u + 0.1 * math.sin(t))
-    st = P.MrsdcStepper(3, 5, P.StepControls(10, cutoff))
-    u, d = st.integrate_mode1(f1, f2, u0, 0.0, 0.4, 4)
+    st = P.MrsdcStepper(3, 5, P.StepControls(40, 0.0))
+    u, d = st.integrate_mode1(f1, f2, u0, 0.0, 0.4, 2)
     assert (d.sweeps, d.f1_evals, d.f2_evals) == (sw.value, n1.value, n2.value)
-    np.testing.assert_allclose(d.residual_history, res[:sw.value], rtol=1e-6, atol=1e-16)
+    np.testing.assert_allclose(d.residual_history, res[:sw.value], rtol=1e-6, atol=1e-15)
     assert rel_err(u, uo) <= 1e-13
-    assert bool(d.early_stop) == (d.sweeps < 4 * 10)
+
+
+def _first_stall(h, cutoff):
+    """sdc.cpp:9-16 on a residual history: the sweep count an early-stopping
+    step ends at."""
+    for k in range(2, len(h) + 1):
+        prev, cur = h[k - 2], h[k - 1]
+        if cur == 0.0 or 1.0 - cutoff <= prev / cur <= 1.0 + cutoff:
+            return k
+    return len(h)
+
+
+@pytest.mark.parametrize("cutoff", [0.05, 0.3])
+def test_sdc_early_stop_self_consistent(cuda, cutoff):
+    """Early stopping decided in the next sweep's first pass: the step ends at
+    the first stall of the full run's residual history, with that history's
+    prefix and the state of a run with exactly that many sweeps (bitwise)."""
+    lam = np.array([-1.0, -0.5, -2.0])
+    f = P.CallbackRhs(3, lambda t, u: lam * u)
+    u0 = np.array([1.0, 0.5, -0.25])
+    _, _, full = P.SdcStepper(3, P.StepControls(40, 0.0)).step(f, u0, 0.0, 0.5)
+    k = _first_stall(full.residual_history, cutoff)
+    assert k < 40
+    u, _, d = P.SdcStepper(3, P.StepControls(40, cutoff)).step(f, u0, 0.0, 0.5)
+    assert d.early_stop and d.sweeps == k and d.fresh_evals == 2 * k + 1
+    assert list(d.residual_history) == list(full.residual_history[:k])
+    uk, _, _ = P.SdcStepper(3, P.StepControls(k, 0.0)).step(f, u0, 0.0, 0.5)
+    assert np.array_equal(u, uk)
+
+
+@pytest.mark.parametrize("cutoff", [0.05, 0.3])
+def test_mrsdc_early_stop_self_consistent(golden, cuda, cutoff):
+    """As above for MRSDC mode 1."""
+    l1, l2 = np.array([-1.0, -0.5, -2.0]), np.array([-10.0, -4.0, -7.0])
+    f1 = P.CallbackRhs(3, lambda t, u: l1 * u)
+    f2 = P.CallbackRhs(3, lambda t, u: l2 * u + 0.1 * math.sin(t))
+    u0 = golden["mr_u0"]
+    _, _, _, full = P.MrsdcStepper(3, 5, P.StepControls(40, 0.0)).step_mode1(f1, f2, u0, 0.0, 0.2)
+    k = _first_stall(full.residual_history, cutoff)
+    assert k < 40
+    u, _, _, d = P.MrsdcStepper(3, 5, P.StepControls(40, cutoff)).step_mode1(f1, f2, u0, 0.0, 0.2)
+    assert d.early_stop and d.sweeps == k
+    assert (d.f1_evals, d.f2_evals) == (2 * k + 1, 8 * k + 1)
+    assert list(d.residual_history) == list(full.residual_history[:k])
+    uk, _, _, _ = P.MrsdcStepper(3, 5, P.StepControls(k, 0.0)).step_mode1(f1, f2, u0, 0.0, 0.2)
+    assert np.array_equal(u, uk)
