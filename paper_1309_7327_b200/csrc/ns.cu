@@ -25,6 +25,10 @@ enum : int {
   F_U = 0, F_T = 3, F_P, F_ETA, F_ETA43, F_LAM2, F_LAM, F_DHP, F_HYS, F_Y,
   F_X = F_Y + NSP, F_D = F_X + NSP, F_DH = F_D + NSP, F_DP = F_DH + NSP, F_COUNT = F_DP + NSP
 };
+// v2 keeps the transport factor s (rhoD_k = rhoD0_k s) in the first rhoD slot
+// and forms rhoD_k and eta43 = (4/3 + xi/eta) eta in the stencil kernels; the
+// v1 debug path reads all nine rhoD_k and eta43 (prim_kernel's all_fields).
+constexpr int F_S = F_D;
 // acc_ field indices (interior)
 enum : int { A_DM = 0, A_DE = 3, A_DY = 4, A_VC = A_DY + NSP, A_HEAT = A_VC + 3, A_COUNT };
 // mixed_ fields (all planes): M_ij = eta d_i u_j for (i, j), i != j; L_i
@@ -93,7 +97,7 @@ __device__ double temperature(const double* Y, double e) {
 
 // ---------------------------------------------------------------- prim
 __global__ void __launch_bounds__(256) prim_kernel(const double* __restrict__ U,
-                                                   double* __restrict__ F, Geo g) {
+                                                   double* __restrict__ F, Geo g, int all_fields) {
   const long long n = g.flen;  // all planes incl. ghosts
   const long long c = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
   if (c >= n) return;
@@ -126,7 +130,7 @@ __global__ void __launch_bounds__(256) prim_kernel(const double* __restrict__ U,
   F[F_T * n + c] = T;
   F[F_P * n + c] = p;
   F[F_ETA * n + c] = eta;
-  F[F_ETA43 * n + c] = 4.0 / 3.0 * eta + xi;
+  if (all_fields) F[F_ETA43 * n + c] = 4.0 / 3.0 * eta + xi;
   F[F_LAM2 * n + c] = xi - 2.0 / 3.0 * eta;
   F[F_LAM * n + c] = lam;
 #pragma unroll
@@ -135,7 +139,7 @@ __global__ void __launch_bounds__(256) prim_kernel(const double* __restrict__ U,
     const double rd = cT.rhoD0[k] * s;
     F[(F_Y + k) * n + c] = Y[k];
     F[(F_X + k) * n + c] = X[k];
-    F[(F_D + k) * n + c] = rd;
+    if (all_fields) F[(F_D + k) * n + c] = rd;
     F[(F_DH + k) * n + c] = rd * h;
     F[(F_DP + k) * n + c] = rd * (X[k] - Y[k]) * pinv;
     dhp += rd * h * (X[k] - Y[k]) * pinv;
@@ -143,6 +147,7 @@ __global__ void __launch_bounds__(256) prim_kernel(const double* __restrict__ U,
   }
   F[F_DHP * n + c] = dhp;
   F[F_HYS * n + c] = hys;
+  if (!all_fields) F[F_S * n + c] = s;
 }
 
 __device__ __forceinline__ void cell_ijk(long long c, const Geo& g, int& i, int& j, int& k) {
@@ -702,7 +707,7 @@ void NsWorkspace::rhs(const double* U, double* out, int part, cudaStream_t st) {
     SMC_CHECK_LAUNCH();
     return;
   }
-  prim_kernel<<<blocks(g.flen), 256, 0, st>>>(U, F, g);
+  prim_kernel<<<blocks(g.flen), 256, 0, st>>>(U, F, g, ns_v1() ? 1 : 0);
   SMC_CHECK_LAUNCH();
   if (part != kNsChem && !ns_v1()) {
     if (s_ == 4)
@@ -742,7 +747,7 @@ bool NsWorkspace::chem_fd_jacobian(const double* U, const double* FU, double* ja
 
 void NsWorkspace::temperature_pressure(const double* U, double* T, double* p, cudaStream_t st) {
   const Geo g = make_geo(box_, dx_);
-  prim_kernel<<<blocks(g.flen), 256, 0, st>>>(U, prim_.get(), g);
+  prim_kernel<<<blocks(g.flen), 256, 0, st>>>(U, prim_.get(), g, 0);
   SMC_CHECK_LAUNCH();
   tp_kernel<<<blocks(box_.cells()), 256, 0, st>>>(prim_.get(), T, p, g);
   SMC_CHECK_LAUNCH();
