@@ -26,8 +26,9 @@ enum : int {
   F_X = F_Y + NSP, F_D = F_X + NSP, F_DH = F_D + NSP, F_DP = F_DH + NSP, F_COUNT = F_DP + NSP
 };
 // v2 keeps the transport factor s (rhoD_k = rhoD0_k s) in the first rhoD slot
-// and forms rhoD_k and eta43 = (4/3 + xi/eta) eta in the stencil kernels; the
-// v1 debug path reads all nine rhoD_k and eta43 (prim_kernel's all_fields).
+// and forms rhoD_k, eta43 = (4/3 + xi/eta) eta and lam2 = (xi/eta - 2/3) eta
+// where they are used; the v1 debug path reads all nine rhoD_k, eta43 and
+// lam2 (prim_kernel's all_fields).
 constexpr int F_S = F_D;
 // acc_ field indices (interior)
 enum : int { A_DM = 0, A_DE = 3, A_DY = 4, A_VC = A_DY + NSP, A_HEAT = A_VC + 3, A_COUNT };
@@ -131,7 +132,7 @@ __global__ void __launch_bounds__(256) prim_kernel(const double* __restrict__ U,
   F[F_P * n + c] = p;
   F[F_ETA * n + c] = eta;
   if (all_fields) F[F_ETA43 * n + c] = 4.0 / 3.0 * eta + xi;
-  F[F_LAM2 * n + c] = xi - 2.0 / 3.0 * eta;
+  if (all_fields) F[F_LAM2 * n + c] = xi - 2.0 / 3.0 * eta;
   F[F_LAM * n + c] = lam;
 #pragma unroll
   for (int k = 0; k < NSP; ++k) {
