@@ -74,21 +74,30 @@ __device__ __forceinline__ double spec_h(int k, double T) {
   const double* c = cT.hc[k];
   return cT.R[k] * (c[3] + T * (c[0] + T * (c[1] + T * c[2])));
 }
-__device__ __forceinline__ double spec_cv(int k, double T) {
-  const double* a = cT.th[k];
-  return cT.R[k] * ((a[0] - 1.0) + T * (a[1] + T * a[2]));
-}
 
-// T from e by Newton, same start and stopping rule as the oracle.
+// T from e by Newton, same start and stopping rule as the oracle.  The
+// mixture's e(T) = sum_k Y_k e_k(T) is one cubic, E0 + T (E1 + T (E2 + T E3)),
+// and cv = de/dT = E1 + T (2 E2 + 3 E3 T) (the cv_k polynomials are the e_k
+// derivatives), so its coefficients are summed once per cell and an
+// iteration costs two Horner evaluations instead of 2 x 9 (the oracle sums
+// per species per iteration: the iterates agree to rounding).
 __device__ double temperature(const double* Y, double e) {
+  double E0 = 0.0, E1 = 0.0, E2 = 0.0, E3 = 0.0;
+#pragma unroll
+  for (int k = 0; k < NSP; ++k) {
+    const double yr = Y[k] * cT.R[k];
+    const double* c = cT.hc[k];
+    E0 += yr * c[3];
+    E1 += yr * (c[0] - 1.0);
+    E2 += yr * c[1];
+    E3 += yr * c[2];
+  }
+  E0 -= e;
+  const double D2 = 2.0 * E2, D3 = 3.0 * E3;
   double T = 1000.0;
   for (int it = 0; it < 50; ++it) {
-    double f = -e, df = 0.0;
-#pragma unroll
-    for (int k = 0; k < NSP; ++k) {
-      f += Y[k] * spec_e(k, T);
-      df += Y[k] * spec_cv(k, T);
-    }
+    const double f = E0 + T * (E1 + T * (E2 + T * E3));
+    const double df = E1 + T * (D2 + T * D3);
     const double dT = f / df;
     T -= dT;
     if (fabs(dT) <= 1e-9 * T) break;
