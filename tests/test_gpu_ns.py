@@ -120,3 +120,14 @@ def test_ns_slab_matches_periodic_anisotropic(cuda):
     slab.rhs_ghosted(Ug, out)
     torch.cuda.synchronize()
     assert max(_percomp(out.cpu().numpy(), full[:, z0:z0 + nzl])) <= 1e-13
+
+
+def test_ns_rejects_odd_nx(cuda):
+    """The direction kernels stage x-contiguous element pairs (16-byte copies),
+    so nx must be even; other shape errors as before (std::invalid_argument ->
+    SmcInvalidArgument, a ValueError)."""
+    with pytest.raises(ValueError, match="nx must be even"):
+        P.NsOperator(15, 16, 16, DX)
+    with pytest.raises(ValueError):
+        P.NsOperator(8, 16, 16, DX)
+    P.NsOperator(10, 9, 9, DX)  # smallest even / odd extents that are allowed
