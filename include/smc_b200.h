@@ -189,7 +189,9 @@ int smc_narrow3d_set_kc(smc_rhs* op, int kc);
  * advection-diffusion part (MRSDC f1: hypterm + diffterm) and the chemistry
  * part (MRSDC f2: wdot) — the split of PAPER.md:732-735.  Any view pointer
  * may be NULL.  zghost = 0: periodic box (interior-only arrays); zghost >= 4:
- * one z-slab, arrays passed to smc_ns_rhs_ghosted carry the ghost planes. */
+ * one z-slab, arrays passed to smc_ns_rhs_ghosted carry the ghost planes.
+ * nx must be even (the stencil kernels stage x-contiguous 16-byte pairs) and
+ * nx, ny >= 9; otherwise SMC_EINVAL. */
 int smc_ns_create(int nx, int ny, int nz, int zghost, double dx, double dy, double dz, int order,
                   const double* params, int nparams, smc_rhs** full, smc_rhs** advdiff,
                   smc_rhs** chem);
