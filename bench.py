@@ -213,6 +213,10 @@ def run_reference(args):
 # ---------------------------------------------------------- NS secondary
 NS_FLOP_PER_CELL = 8850   # frozen algorithmic count, DESIGN.md "NS RHS flop count"
 NS_BYTES_PER_CELL = 224   # 14 conserved fp64 in + 14 out (fully fused minimum)
+# DRAM bytes per cell-RHS the direction-split design moves (sum over its
+# kernels of ncu dram__bytes_read + write at 128^3, profiles/ncu_ns_r01.json:
+# prim 452, phase A 3 x 632, mixed 138, phase B 3 x 29, assemble2 738)
+NS_DESIGN_BYTES_PER_CELL = 3311
 
 
 def heat2d_measurement(dev, stream, fp64_peak, n=4096, reps=100):
@@ -298,7 +302,12 @@ def ns_rhs_measurement(n, dev, stream, fp64_peak, hbm_peak, steps):
            "roofline": {"bound": "fp64", "achieved": tf, "peak": fp64_peak, "unit": "TFLOP/s",
                         "frac": tf / fp64_peak, "flop_per_cell": NS_FLOP_PER_CELL,
                         "hbm": {"achieved": gbs, "peak": hbm_peak, "frac": gbs / hbm_peak,
-                                "bytes_per_cell": NS_BYTES_PER_CELL}}}
+                                "bytes_per_cell": NS_BYTES_PER_CELL},
+                        # the traffic this design moves at the HBM peak: how close the
+                        # split kernels are to their own memory floor
+                        "hbm_design": {"bytes_per_cell": NS_DESIGN_BYTES_PER_CELL,
+                                       "floor_ms": NS_DESIGN_BYTES_PER_CELL * cells / hbm_peak / 1e6,
+                                       "frac": NS_DESIGN_BYTES_PER_CELL * cells / hbm_peak / 1e6 / ms}}}
     # the oracle (C restatement, 1 thread) on a 24^3 sample of the same generator
     try:
         import time as _t
