@@ -527,7 +527,7 @@ __global__ void __launch_bounds__(256) chem_kernel(const double* __restrict__ U,
 // cell's state with component j perturbed, as DeviceNewton's column loop
 // (fd_perturb_kernel, the chemistry evaluation, fd_column_kernel) forms it,
 // without the 14 full-grid passes.  Periodic box (no ghost planes).
-__global__ void __launch_bounds__(128) chem_fd_jacobian_kernel(const double* __restrict__ U,
+__global__ void __launch_bounds__(128, 4) chem_fd_jacobian_kernel(const double* __restrict__ U,
                                                                const double* __restrict__ FU,
                                                                double* __restrict__ jac, long long n,
                                                                double atol, double root_eps) {

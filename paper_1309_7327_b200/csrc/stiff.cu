@@ -322,7 +322,7 @@ __global__ void __launch_bounds__(kLuThreads) lu_smem_kernel(const double* jac, 
 //     subtracts in ascending j as the reference does.
 constexpr int kLuCells = 16;
 template <int B>
-__global__ void __launch_bounds__(256) lu_lane_kernel(const double* jac, double* delta,
+__global__ void __launch_bounds__(256, 4) lu_lane_kernel(const double* jac, double* delta,
                                                       double beta, BlockMap bm,
                                                       unsigned long long* flag) {
   __shared__ double stage[B * B][kLuCells + 1];
