@@ -106,7 +106,7 @@ __device__ double temperature(const double* Y, double e) {
 }
 
 // ---------------------------------------------------------------- prim
-__global__ void __launch_bounds__(256) prim_kernel(const double* __restrict__ U,
+__global__ void __launch_bounds__(256, 3) prim_kernel(const double* __restrict__ U,
                                                    double* __restrict__ F, Geo g, int all_fields) {
   const long long n = g.flen;  // all planes incl. ghosts
   const long long c = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
