@@ -22,7 +22,8 @@ import numpy as np
 
 from . import _capi
 from ._capi import (CLENSHAW_CURTIS, DEVICE, GAUSS_LOBATTO, HOST, NARROW6, NARROW8, WIDE8,
-                    SmcError, SmcIntegrationError, SmcInvalidArgument, check, dptr, where_of)
+                    SmcError, SmcIntegrationError, SmcInvalidArgument, check, check_arrays, defer,
+                    dptr, where_of)
 
 __all__ = [
     "SmcError", "SmcInvalidArgument", "SmcIntegrationError", "StencilChoice", "stencil_preset",
@@ -146,7 +147,8 @@ class _Rhs:
         """Rhs contract (field.hpp:14-16): out = f(t, u)."""
         if out is None:
             out = _out_like(u)
-        check(_capi.lib().smc_rhs_eval(self._h, t, dptr(u), dptr(out), where_of(u)))
+        w = check_arrays(self.dim, u, out, names=("u", "out"))
+        check(_capi.lib().smc_rhs_eval(self._h, t, dptr(u), dptr(out), w))
         return out
 
     def close(self):
@@ -191,7 +193,14 @@ class HeatOperator(_Rhs):
                                           C.byref(h)))
         super().__init__(h)
         if G is not None and g_time is not None:
-            cb = _capi.TIME_FN(lambda t, ctx: float(g_time(t)))
+            def gt(t, ctx):
+                try:
+                    return float(g_time(t))
+                except BaseException as e:  # re-raised by check() after the C call
+                    defer(e)
+                    return math.nan
+
+            cb = _capi.TIME_FN(gt)
             self._keep.append(cb)
             check(_capi.lib().smc_heat_set_time_source(self._h, cb, None))
 
@@ -275,9 +284,14 @@ class DeviceCallbackRhs(_Rhs):
         import torch
 
         def tramp(t, u, out, n, stream, ctx):
-            s = torch.cuda.ExternalStream(stream) if stream else torch.cuda.default_stream()
-            with torch.cuda.stream(s):
-                fn(t, device_tensor(u, n, stream), device_tensor(out, n, stream))
+            try:
+                s = torch.cuda.ExternalStream(stream) if stream else torch.cuda.default_stream()
+                with torch.cuda.stream(s):
+                    fn(t, device_tensor(u, n, stream), device_tensor(out, n, stream))
+            except BaseException as e:  # re-raised by check() after the C call
+                defer(e)
+                with torch.cuda.stream(s):
+                    device_tensor(out, n, stream).fill_(math.nan)
 
         cb = _capi.DEV_RHS_FN(tramp)
         h = C.c_void_p()
@@ -293,7 +307,11 @@ class CallbackRhs(_Rhs):
         def tramp(t, u, out, n, ctx):
             uu = np.ctypeslib.as_array(u, shape=(n,))
             oo = np.ctypeslib.as_array(out, shape=(n,))
-            oo[:] = fn(t, uu)
+            try:
+                oo[:] = fn(t, uu)
+            except BaseException as e:  # re-raised by check() after the C call
+                defer(e)
+                oo[:] = math.nan
 
         cb = _capi.RHS_FN(tramp)
         h = C.c_void_p()
@@ -371,7 +389,8 @@ def integrate_stiff(f: "_Rhs", u0, t0: float, t1: float, stiff: "StiffOptions" =
     u = _out_like(u0)
     so = (stiff or StiffOptions()).c()
     acc, rej = C.c_int(), C.c_int()
-    check(_capi.lib().smc_integrate_stiff(f.handle, dptr(u0), t0, t1, dptr(u), where_of(u0),
+    w = check_arrays(f.dim, u0, u, names=("u0", "u"))
+    check(_capi.lib().smc_integrate_stiff(f.handle, dptr(u0), t0, t1, dptr(u), w,
                                           C.byref(so), C.byref(acc), C.byref(rej)))
     return u, (acc.value, rej.value)
 
@@ -384,14 +403,22 @@ def solve_backward_euler(f: "_Rhs", t: float, beta: float, c, guess, stiff: "Sti
     w = _out_like(c)
     rep = _capi.NewtonReport()
     so = (stiff or StiffOptions()).c()
+    wh = check_arrays(f.dim, c, guess, w, names=("c", "guess", "w"))
     check(_capi.lib().smc_solve_backward_euler(f.handle, t, beta, dptr(c), dptr(guess), dptr(w),
-                                               where_of(c), C.byref(so),
+                                               wh, C.byref(so),
                                                C.byref(rep) if report else None))
     return w, NewtonReport(rep.iterations, rep.final_residual, bool(rep.converged), rep.f_evals)
 
 
 def _reducer(fn):
-    return _capi.REDUCE_FN(lambda v, ctx: float(fn(v)))
+    def red(v, ctx):
+        try:
+            return float(fn(v))
+        except BaseException as e:  # re-raised by check() after the C call
+            defer(e)
+            return math.nan
+
+    return _capi.REDUCE_FN(red)
 
 
 class SdcStepper:
@@ -417,15 +444,17 @@ class SdcStepper:
         u = _out_like(u0)
         fe = _out_like(u0)
         d, buf = _diag()
+        w = check_arrays(f.dim, u0, f0, u, fe, names=("u0", "f0", "u", "f_end"))
         check(_capi.lib().smc_sdc_step(self._h, f.handle, dptr(u0), t_n, dt, dptr(f0), dptr(u),
-                                       dptr(fe), where_of(u0), C.byref(d)))
+                                       dptr(fe), w, C.byref(d)))
         return u, fe, _from_diag(d, buf)
 
     def integrate(self, f: _Rhs, u0, t0: float, t1: float, nsteps: int, out=None):
         u = out if out is not None else _out_like(u0)
         d, buf = _diag()
+        w = check_arrays(f.dim, u0, u, names=("u0", "out"))
         check(_capi.lib().smc_sdc_integrate(self._h, f.handle, dptr(u0), t0, t1, nsteps, dptr(u),
-                                            where_of(u0), C.byref(d)))
+                                            w, C.byref(d)))
         return u, _from_diag(d, buf)
 
     def __del__(self):
@@ -466,9 +495,10 @@ class MrsdcStepper:
     def step_mode1(self, f1: _Rhs, f2: _Rhs, u0, t_n, dt, f0_1=None, f0_2=None):
         u, e1, e2 = _out_like(u0), _out_like(u0), _out_like(u0)
         d, buf = _diag()
+        w = self._arrays(f1, f2, u0, f0_1, f0_2, u, e1, e2)
         check(_capi.lib().smc_mrsdc_step_mode1(self._h, f1.handle, f2.handle, dptr(u0), t_n, dt,
                                                dptr(f0_1), dptr(f0_2), dptr(u), dptr(e1),
-                                               dptr(e2), where_of(u0), C.byref(d)))
+                                               dptr(e2), w, C.byref(d)))
         return u, e1, e2, _from_diag(d, buf)
 
     def integrate_mode1(self, f1: _Rhs, f2: _Rhs, u0, t0, t1, nsteps, out=None):
@@ -477,20 +507,28 @@ class MrsdcStepper:
     def step_mode2(self, f1: _Rhs, f2: _Rhs, u0, t_n, dt, f0_1=None, f0_2=None):
         u, e1, e2 = _out_like(u0), _out_like(u0), _out_like(u0)
         d, buf = _diag()
+        w = self._arrays(f1, f2, u0, f0_1, f0_2, u, e1, e2)
         check(_capi.lib().smc_mrsdc_step_mode2(self._h, f1.handle, f2.handle, dptr(u0), t_n, dt,
                                                dptr(f0_1), dptr(f0_2), dptr(u), dptr(e1),
-                                               dptr(e2), where_of(u0), C.byref(d)))
+                                               dptr(e2), w, C.byref(d)))
         return u, e1, e2, _from_diag(d, buf)
 
     def integrate_mode2(self, f1: _Rhs, f2: _Rhs, u0, t0, t1, nsteps, out=None):
         return self._integrate(2, f1, f2, u0, t0, t1, nsteps, out)
+
+    @staticmethod
+    def _arrays(f1, f2, *arrays):
+        if f1.dim != f2.dim:
+            raise SmcInvalidArgument("mrsdc: f1 and f2 have different dimensions")
+        return check_arrays(f1.dim, *arrays)
 
     def _integrate(self, mode, f1, f2, u0, t0, t1, nsteps, out):
         u = out if out is not None else _out_like(u0)
         d, buf = _diag()
         fn = _capi.lib().smc_mrsdc_integrate_mode2 if mode == 2 else \
             _capi.lib().smc_mrsdc_integrate_mode1
-        check(fn(self._h, f1.handle, f2.handle, dptr(u0), t0, t1, nsteps, dptr(u), where_of(u0),
+        w = self._arrays(f1, f2, u0, u)
+        check(fn(self._h, f1.handle, f2.handle, dptr(u0), t0, t1, nsteps, dptr(u), w,
                  C.byref(d)))
         return u, _from_diag(d, buf)
 

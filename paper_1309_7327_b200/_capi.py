@@ -159,7 +159,22 @@ def lib():
     return _lib
 
 
+# Exceptions raised inside Python callbacks (RHS trampolines, reducers) cannot
+# cross the C frames that called them: ctypes would print and swallow them and
+# hand the C side an undefined value.  The trampolines store them here and
+# return a poisoned value (NaN); check() re-raises after the C call returns.
+_pending: list = []
+
+
+def defer(exc: BaseException) -> None:
+    _pending.append(exc)
+
+
 def check(rc: int) -> None:
+    if _pending:
+        exc = _pending[0]
+        _pending.clear()
+        raise exc
     if rc == OK:
         return
     msg = lib().smc_last_error().decode()
@@ -175,10 +190,42 @@ def dptr(a) -> C.c_void_p:
     if a is None:
         return None
     if hasattr(a, "data_ptr"):
-        assert a.is_contiguous() and str(a.dtype) == "torch.float64"
+        if not (a.is_contiguous() and str(a.dtype) == "torch.float64"):
+            raise SmcInvalidArgument("expected a contiguous torch.float64 tensor")
         return C.c_void_p(a.data_ptr())
-    assert a.dtype.name == "float64" and a.flags.c_contiguous
+    if not (getattr(a, "dtype", None) is not None and a.dtype.name == "float64"
+            and a.flags.c_contiguous):
+        raise SmcInvalidArgument("expected a C-contiguous float64 numpy array")
     return C.c_void_p(a.ctypes.data)
+
+
+def numel(a) -> int:
+    return int(a.numel()) if hasattr(a, "numel") else int(a.size)
+
+
+def check_arrays(dim: int, *arrays, names=None) -> int:
+    """The C side copies / reads dim doubles through every array argument:
+    each given array (None = absent) must hold exactly dim float64 values and
+    all of them must live on the same side (host numpy or CUDA tensor);
+    device arrays must be 16-byte aligned (the kernels' vector accesses).
+    Returns the common where_of."""
+    where = None
+    for i, a in enumerate(arrays):
+        if a is None:
+            continue
+        name = names[i] if names else f"argument {i}"
+        dptr(a)  # dtype / contiguity
+        if numel(a) != dim:
+            raise SmcInvalidArgument(f"{name}: holds {numel(a)} values, the operator's "
+                                     f"dimension is {dim}")
+        w = where_of(a)
+        if where is None:
+            where = w
+        elif w != where:
+            raise SmcInvalidArgument(f"{name}: host and device arrays mixed in one call")
+        if w == DEVICE and a.data_ptr() % 16:
+            raise SmcInvalidArgument(f"{name}: device array is not 16-byte aligned")
+    return HOST if where is None else where
 
 
 def where_of(a) -> int:

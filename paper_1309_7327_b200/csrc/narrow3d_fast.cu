@@ -412,7 +412,8 @@ bool narrow3d_fast_applicable(const NarrowArgs& p) {
   const auto al = [](const void* q) { return (reinterpret_cast<std::uintptr_t>(q) & 15) == 0; };
   const int fx = fast_fx();
   return p.dims == 3 && p.nx % fx == 0 && p.ny % NG<64>::FY == 0 && p.nx >= fx &&
-         p.cx == p.cz && p.cy == p.cz && p.g0 == nullptr && al(p.u) && al(p.cz) && al(p.out);
+         p.cx == p.cz && p.cy == p.cz && p.g0 == nullptr && al(p.u) && al(p.cz) && al(p.out) &&
+         (!p.zpeer || (al(p.u_lo) && al(p.u_hi)));
 }
 
 void launch_narrow3d_fast(const NarrowArgs& p, int s, const StencilM& M, cudaStream_t st) {

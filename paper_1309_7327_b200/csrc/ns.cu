@@ -1,13 +1,13 @@
-// NS right-hand side kernels (see ns.cuh).  v1 layout: one thread per cell,
-// neighbour values gathered through L1/L2; the same decomposition as the CPU
-// oracle (oracle/ns_oracle.c) so every intermediate is comparable:
-//   prim    : ctoprim (Newton for T) + transport + derived coefficient fields
-//   hyp     : -div F with 8th-order centred first derivatives  -> out
-//   narrow  : same-direction second derivatives, narrow stencil -> acc
-//   grad    : velocity gradients -> mixed-term fields, tau:grad u, V_c
-//   assemble: mixed viscous terms, correction-velocity terms  -> out
-//   wdot    : rho omega_k                                       -> out
+// NS right-hand side kernels (see ns.cuh).  The decomposition follows the CPU
+// oracle (oracle/ns_oracle.c), so every intermediate is comparable:
+//   prim      : ctoprim (Newton for T) + transport + coefficient fields
+//   phase A   : per direction, the narrow diffusion terms, hyperbolic flux
+//               derivatives, velocity gradients, V_c (ns_dir.inc)
+//   mixed     : eta d_i u_j, lam2 div, tau:grad u
+//   phase B   : mixed viscous derivatives (ns_dir.inc)
+//   assemble2 : direction sums in order + pointwise terms + wdot
 #include <cmath>
+#include <cstdint>
 #include <cstdlib>
 #include <utility>
 
@@ -21,15 +21,13 @@ constexpr int NSP = SMC_NSP;
 constexpr int NV = SMC_NVAR;
 
 // prim_ field indices (same roles as the oracle's F_* enum)
+// The transport factor s (rhoD_k = rhoD0_k s) is stored once; rhoD_k,
+// eta43 = (4/3 + xi/eta) eta and lam2 = (xi/eta - 2/3) eta are formed where
+// they are used.
 enum : int {
-  F_U = 0, F_T = 3, F_P, F_ETA, F_ETA43, F_LAM2, F_LAM, F_DHP, F_HYS, F_Y,
-  F_X = F_Y + NSP, F_D = F_X + NSP, F_DH = F_D + NSP, F_DP = F_DH + NSP, F_COUNT = F_DP + NSP
+  F_U = 0, F_T = 3, F_P, F_ETA, F_LAM, F_DHP, F_HYS, F_S, F_Y,
+  F_X = F_Y + NSP, F_DH = F_X + NSP, F_DP = F_DH + NSP, F_COUNT = F_DP + NSP
 };
-// v2 keeps the transport factor s (rhoD_k = rhoD0_k s) in the first rhoD slot
-// and forms rhoD_k, eta43 = (4/3 + xi/eta) eta and lam2 = (xi/eta - 2/3) eta
-// where they are used; the v1 debug path reads all nine rhoD_k, eta43 and
-// lam2 (prim_kernel's all_fields).
-constexpr int F_S = F_D;
 // acc_ field indices (interior)
 enum : int { A_DM = 0, A_DE = 3, A_DY = 4, A_VC = A_DY + NSP, A_HEAT = A_VC + 3, A_COUNT };
 // mixed_ fields (all planes): M_ij = eta d_i u_j for (i, j), i != j; L_i
@@ -107,7 +105,7 @@ __device__ double temperature(const double* Y, double e) {
 
 // ---------------------------------------------------------------- prim
 __global__ void __launch_bounds__(256, 3) prim_kernel(const double* __restrict__ U,
-                                                   double* __restrict__ F, Geo g, int all_fields) {
+                                                   double* __restrict__ F, Geo g) {
   const long long n = g.flen;  // all planes incl. ghosts
   const long long c = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
   if (c >= n) return;
@@ -140,8 +138,6 @@ __global__ void __launch_bounds__(256, 3) prim_kernel(const double* __restrict__
   F[F_T * n + c] = T;
   F[F_P * n + c] = p;
   F[F_ETA * n + c] = eta;
-  if (all_fields) F[F_ETA43 * n + c] = 4.0 / 3.0 * eta + xi;
-  if (all_fields) F[F_LAM2 * n + c] = xi - 2.0 / 3.0 * eta;
   F[F_LAM * n + c] = lam;
 #pragma unroll
   for (int k = 0; k < NSP; ++k) {
@@ -149,7 +145,6 @@ __global__ void __launch_bounds__(256, 3) prim_kernel(const double* __restrict__
     const double rd = cT.rhoD0[k] * s;
     F[(F_Y + k) * n + c] = Y[k];
     F[(F_X + k) * n + c] = X[k];
-    if (all_fields) F[(F_D + k) * n + c] = rd;
     F[(F_DH + k) * n + c] = rd * h;
     F[(F_DP + k) * n + c] = rd * (X[k] - Y[k]) * pinv;
     dhp += rd * h * (X[k] - Y[k]) * pinv;
@@ -157,79 +152,7 @@ __global__ void __launch_bounds__(256, 3) prim_kernel(const double* __restrict__
   }
   F[F_DHP * n + c] = dhp;
   F[F_HYS * n + c] = hys;
-  if (!all_fields) F[F_S * n + c] = s;
-}
-
-__device__ __forceinline__ void cell_ijk(long long c, const Geo& g, int& i, int& j, int& k) {
-  i = static_cast<int>(c % g.nx);
-  const long long r = c / g.nx;
-  j = static_cast<int>(r % g.ny);
-  k = static_cast<int>(r / g.ny);
-}
-
-constexpr double C1 = 4.0 / 5.0, C2 = -1.0 / 5.0, C3 = 4.0 / 105.0, C4 = -1.0 / 280.0;
-__device__ __forceinline__ double dcoef(int o) {  // antisymmetric 8th-order weights
-  const int a = o < 0 ? -o : o;
-  const double c = a == 1 ? C1 : a == 2 ? C2 : a == 3 ? C3 : C4;
-  return o < 0 ? -c : c;
-}
-
-// d/dx_d of field f (plane-0 pointer) at interior cell (i, j, k)
-__device__ __forceinline__ double d8(const double* f, const Geo& g, int i, int j, int k, int d) {
-  double w[9];
-#pragma unroll
-  for (int o = -4; o <= 4; ++o) w[o + 4] = o == 0 ? 0.0 : __ldg(f + nb(g, i, j, k, d, o));
-  return deriv8_w(w, g.d1[d]);
-}
-
-// ----------------------------------------------------------------- hyp
-// out = -sum_d d_d F_d, fluxes formed at the neighbours.
-__global__ void __launch_bounds__(256) hyp_kernel(const double* __restrict__ U,
-                                                  const double* __restrict__ F,
-                                                  double* __restrict__ out, Geo g, int init) {
-  const long long n = g.plane * g.nz;
-  const long long c = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
-  if (c >= n) return;
-  int i, j, k;
-  cell_ijk(c, g, i, j, k);
-  const double* U0 = U + g.G * g.plane;  // plane 0 of interior, field stride flen
-  const double* F0 = F + g.G * g.plane;
-  double acc[NV];
-#pragma unroll
-  for (int v = 0; v < NV; ++v) acc[v] = 0.0;
-  for (int d = 0; d < 3; ++d) {
-    double dv[NV];
-#pragma unroll
-    for (int v = 0; v < NV; ++v) dv[v] = 0.0;
-    // per offset pair (o, -o): c_o (F(+o) - F(-o))
-#pragma unroll
-    for (int a = 4; a >= 1; --a) {
-      double fp[NV], fm[NV];
-#pragma unroll
-      for (int sgn = 0; sgn < 2; ++sgn) {
-        const long long q = nb(g, i, j, k, d, sgn ? -a : a);
-        const double ud = __ldg(F0 + F_U * 0 + (F_U + d) * g.flen + q);
-        const double p = __ldg(F0 + F_P * g.flen + q);
-        double* f = sgn ? fm : fp;
-        f[0] = __ldg(U0 + (1 + d) * g.flen + q);
-#pragma unroll
-        for (int m = 0; m < 3; ++m) f[1 + m] = __ldg(U0 + (1 + m) * g.flen + q) * ud + (m == d ? p : 0.0);
-        f[4] = (__ldg(U0 + 4 * g.flen + q) + p) * ud;
-#pragma unroll
-        for (int s = 0; s < NSP; ++s) f[5 + s] = __ldg(U0 + (5 + s) * g.flen + q) * ud;
-      }
-      const double ca = a == 1 ? C1 : a == 2 ? C2 : a == 3 ? C3 : C4;
-#pragma unroll
-      for (int v = 0; v < NV; ++v) dv[v] = __fma_rn(ca, fp[v] - fm[v], dv[v]);
-    }
-#pragma unroll
-    for (int v = 0; v < NV; ++v) acc[v] -= dv[v] * g.d1[d];
-  }
-#pragma unroll
-  for (int v = 0; v < NV; ++v) {
-    double* o = out + v * n + c;
-    *o = init ? acc[v] : *o + acc[v];
-  }
+  F[F_S * n + c] = s;
 }
 
 // ------------------------------------------------------------ narrow
@@ -242,180 +165,6 @@ __device__ __forceinline__ void narrow_v(const double* u, const StencilM& M, dou
 template <int S>
 __device__ __forceinline__ double narrow_dot(const double* a, const double* v) {
   return narrow_adot<S>(a, v);
-}
-
-// All same-direction second-derivative terms of one cell (PAPER.md:150-156,
-// :170-213): both interfaces of the cell are formed here (v1).
-template <int S>
-__global__ void __launch_bounds__(256) narrow_kernel(const double* __restrict__ F,
-                                                     double* __restrict__ A, Geo g,
-                                                     const StencilM M) {
-  const long long n = g.plane * g.nz;
-  const long long c = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
-  if (c >= n) return;
-  int i, j, k;
-  cell_ijk(c, g, i, j, k);
-  const double* F0 = F + g.G * g.plane;
-  double dm[3] = {0, 0, 0}, dE = 0.0, dY[NSP];
-#pragma unroll
-  for (int s = 0; s < NSP; ++s) dY[s] = 0.0;
-  constexpr int WN = 2 * S + 1;  // window covering both interfaces
-  for (int d = 0; d < 3; ++d) {
-    long long q[WN];
-#pragma unroll
-    for (int o = 0; o < WN; ++o) q[o] = nb(g, i, j, k, d, o - S);
-    const double id2 = g.d2[d];
-    auto win = [&](int fld, double* w) {
-      const double* f = F0 + static_cast<long long>(fld) * g.flen;
-#pragma unroll
-      for (int o = 0; o < WN; ++o) w[o] = __ldg(f + q[o]);
-    };
-    // (coef a, field u): (H(i+1/2) - H(i-1/2)) / d^2 via the shared v'
-    double u[WN], a[WN], vl[2 * S], vr[2 * S];
-    // velocities
-#pragma unroll 1
-    for (int m = 0; m < 3; ++m) {
-      win(F_U + m, u);
-      win(m == d ? F_ETA43 : F_ETA, a);
-      narrow_v<S>(u, M, vl);
-      narrow_v<S>(u + 1, M, vr);
-      dm[m] += (narrow_dot<S>(a + 1, vr) - narrow_dot<S>(a, vl)) * id2;
-    }
-    // temperature
-    win(F_T, u);
-    win(F_LAM, a);
-    narrow_v<S>(u, M, vl);
-    narrow_v<S>(u + 1, M, vr);
-    dE += (narrow_dot<S>(a + 1, vr) - narrow_dot<S>(a, vl)) * id2;
-    // mole fractions: rhoD_k and rhoD_k h_k
-#pragma unroll 1
-    for (int s = 0; s < NSP; ++s) {
-      win(F_X + s, u);
-      narrow_v<S>(u, M, vl);
-      narrow_v<S>(u + 1, M, vr);
-      win(F_D + s, a);
-      dY[s] += (narrow_dot<S>(a + 1, vr) - narrow_dot<S>(a, vl)) * id2;
-      win(F_DH + s, a);
-      dE += (narrow_dot<S>(a + 1, vr) - narrow_dot<S>(a, vl)) * id2;
-    }
-    // pressure: rhoD_k (X_k - Y_k) / p and sum_k rhoD_k h_k (X_k - Y_k) / p
-    win(F_P, u);
-    narrow_v<S>(u, M, vl);
-    narrow_v<S>(u + 1, M, vr);
-#pragma unroll 1
-    for (int s = 0; s < NSP; ++s) {
-      win(F_DP + s, a);
-      dY[s] += (narrow_dot<S>(a + 1, vr) - narrow_dot<S>(a, vl)) * id2;
-    }
-    win(F_DHP, a);
-    dE += (narrow_dot<S>(a + 1, vr) - narrow_dot<S>(a, vl)) * id2;
-  }
-  for (int m = 0; m < 3; ++m) A[(A_DM + m) * n + c] = dm[m];
-  A[A_DE * n + c] = dE;
-#pragma unroll
-  for (int s = 0; s < NSP; ++s) A[(A_DY + s) * n + c] = dY[s];
-}
-
-// ------------------------------------------------------------- grad
-// Interior: tau:grad u, V_c, and the mixed-term fields; ghost planes (slab
-// mode): the mixed-term fields that are differentiated along z, from in-plane
-// derivatives only.
-__global__ void __launch_bounds__(256) grad_kernel(const double* __restrict__ F,
-                                                   double* __restrict__ A,
-                                                   double* __restrict__ MX, Geo g) {
-  const long long n = g.plane * g.nz;
-  const long long all = g.plane * (g.nz + 2 * g.G);
-  const long long t = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
-  if (t >= all) return;
-  // t indexes planes -G .. nz+G-1
-  const long long cg = t;  // offset within the field including ghosts
-  int i, j, kk;
-  cell_ijk(t, g, i, j, kk);
-  const int k = kk - g.G;
-  const bool interior = k >= 0 && k < g.nz;
-  const double* F0 = F + g.G * g.plane;
-  const double* fu[3] = {F0 + F_U * g.flen, F0 + (F_U + 1) * g.flen, F0 + (F_U + 2) * g.flen};
-  const double eta = __ldg(F + F_ETA * g.flen + cg);
-  const double lam2 = __ldg(F + F_LAM2 * g.flen + cg);
-  if (!interior) {
-    // eta d_x w, eta d_y w (differentiated along z), lam2 (d_x u + d_y v)
-    MX[mx_index(0, 2) * g.flen + cg] = eta * d8(fu[2], g, i, j, k, 0);
-    MX[mx_index(1, 2) * g.flen + cg] = eta * d8(fu[2], g, i, j, k, 1);
-    MX[(6 + 2) * g.flen + cg] = lam2 * (d8(fu[0], g, i, j, k, 0) + d8(fu[1], g, i, j, k, 1));
-    return;
-  }
-  double G[3][3];
-  for (int a = 0; a < 3; ++a)
-    for (int b = 0; b < 3; ++b) G[a][b] = d8(fu[a], g, i, j, k, b);
-  const long long c = static_cast<long long>(k) * g.plane + static_cast<long long>(j) * g.nx + i;
-  // mixed-term fields M_ij = eta d_i u_j = eta G[j][i]; L_i = lam2 sum_{j!=i} G[j][j]
-  for (int a = 0; a < 3; ++a)
-    for (int b = 0; b < 3; ++b)
-      if (a != b) MX[mx_index(a, b) * g.flen + cg] = eta * G[b][a];
-  for (int a = 0; a < 3; ++a) {
-    double sd = 0.0;
-    for (int b = 0; b < 3; ++b)
-      if (b != a) sd += G[b][b];
-    MX[(6 + a) * g.flen + cg] = lam2 * sd;
-  }
-  // tau : grad u
-  const double div = G[0][0] + G[1][1] + G[2][2];
-  double heat = 0.0;
-  for (int a = 0; a < 3; ++a)
-    for (int b = 0; b < 3; ++b) {
-      const double tau = eta * (G[a][b] + G[b][a]) + (a == b ? lam2 * div : 0.0);
-      heat += tau * G[a][b];
-    }
-  A[A_HEAT * n + c] = heat;
-  // V_c = -sum_l (rhoD_l grad X_l + rhoD_l (X_l - Y_l)/p grad p)
-  double gp[3];
-  for (int b = 0; b < 3; ++b) gp[b] = d8(F0 + F_P * g.flen, g, i, j, k, b);
-  double vc[3] = {0, 0, 0};
-  for (int l = 0; l < NSP; ++l) {
-    const double D = __ldg(F + (F_D + l) * g.flen + cg);
-    const double DP = __ldg(F + (F_DP + l) * g.flen + cg);
-    for (int b = 0; b < 3; ++b)
-      vc[b] -= D * d8(F0 + (F_X + l) * g.flen, g, i, j, k, b) + DP * gp[b];
-  }
-  for (int b = 0; b < 3; ++b) A[(A_VC + b) * n + c] = vc[b];
-}
-
-// --------------------------------------------------------- assemble
-__global__ void __launch_bounds__(256) assemble_kernel(const double* __restrict__ F,
-                                                       const double* __restrict__ A,
-                                                       const double* __restrict__ MX,
-                                                       double* __restrict__ out, Geo g) {
-  const long long n = g.plane * g.nz;
-  const long long c = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
-  if (c >= n) return;
-  int i, j, k;
-  cell_ijk(c, g, i, j, k);
-  const long long cg = c + g.G * g.plane;
-  const double* MX0 = MX + g.G * g.plane;
-  const double* F0 = F + g.G * g.plane;
-  // div tau = narrow part + sum_{j!=i} d_j(eta d_i u_j) + d_i(lam2 sum_{j!=i} d_j u_j)
-  double dm[3];
-  for (int a = 0; a < 3; ++a) {
-    double v = A[(A_DM + a) * n + c];
-    for (int b = 0; b < 3; ++b)
-      if (b != a) v += d8(MX0 + mx_index(a, b) * g.flen, g, i, j, k, b);
-    v += d8(MX0 + (6 + a) * g.flen, g, i, j, k, a);
-    dm[a] = v;
-  }
-  double divvc = 0.0;
-  for (int s = 0; s < NSP; ++s) divvc -= A[(A_DY + s) * n + c];
-  const double vc[3] = {A[A_VC * n + c], A[(A_VC + 1) * n + c], A[(A_VC + 2) * n + c]};
-  for (int s = 0; s < NSP; ++s) {
-    double v = A[(A_DY + s) * n + c] + __ldg(F + (F_Y + s) * g.flen + cg) * divvc;
-    for (int b = 0; b < 3; ++b) v += vc[b] * d8(F0 + (F_Y + s) * g.flen, g, i, j, k, b);
-    out[(5 + s) * n + c] += v;
-  }
-  double e = A[A_DE * n + c] + A[A_HEAT * n + c];
-  for (int a = 0; a < 3; ++a) e += __ldg(F + (F_U + a) * g.flen + cg) * dm[a];
-  e += __ldg(F + F_HYS * g.flen + cg) * divvc;
-  for (int b = 0; b < 3; ++b) e += vc[b] * d8(F0 + F_HYS * g.flen, g, i, j, k, b);
-  out[4 * n + c] += e;
-  for (int a = 0; a < 3; ++a) out[(1 + a) * n + c] += dm[a];
 }
 
 // ------------------------------------------------------------- wdot
@@ -474,22 +223,6 @@ __device__ __forceinline__ void wdot_cell(double rho, double T, const double* Y,
   rx_all(std::make_integer_sequence<int, SMC_NREAC>{}, C, M, lnT, invRT, om);
 #pragma unroll
   for (int s = 0; s < NSP; ++s) w[s] = cT.W[s] * om[s];
-}
-
-// full RHS: += wdot, from the primitive fields
-__global__ void __launch_bounds__(256) wdot_kernel(const double* __restrict__ U,
-                                                   const double* __restrict__ F,
-                                                   double* __restrict__ out, Geo g) {
-  const long long n = g.plane * g.nz;
-  const long long c = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
-  if (c >= n) return;
-  const long long cg = c + g.G * g.plane;
-  double Y[NSP], w[NSP];
-#pragma unroll
-  for (int s = 0; s < NSP; ++s) Y[s] = F[(F_Y + s) * g.flen + cg];
-  wdot_cell(U[cg], F[F_T * g.flen + cg], Y, w);
-#pragma unroll
-  for (int s = 0; s < NSP; ++s) out[(5 + s) * n + c] += w[s];
 }
 
 // chemistry part alone (MRSDC f2): ctoprim's temperature + wdot fused, so the
@@ -626,15 +359,6 @@ int blocks(long long n) { return static_cast<int>((n + 255) / 256); }
 
 #include "ns_dir.inc"
 
-// SMC_NS_V1=1 selects the v1 one-thread-per-cell gather kernels (debug).
-bool ns_v1() {
-  static bool v = [] {
-    const char* e = std::getenv("SMC_NS_V1");
-    return e && std::atoi(e) == 1;
-  }();
-  return v;
-}
-
 template <class K>
 void set_smem(K kern, std::size_t bytes) {
   SMC_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -695,7 +419,7 @@ NsWorkspace::NsWorkspace(const NsBox& box, double dx, double dy, double dz, cons
   acc_.resize(static_cast<std::size_t>(A_COUNT) * box.cells());
   mixed_.resize(static_cast<std::size_t>(MX_COUNT) * box.field_len());
   grad_.resize(static_cast<std::size_t>(9) * box.field_len());
-  if (!ns_v1()) scratch_.resize(static_cast<std::size_t>(93) * box.cells());
+  scratch_.resize(static_cast<std::size_t>(93) * box.cells());
 }
 
 static Geo make_geo(const NsBox& b, const double* d) {
@@ -708,6 +432,11 @@ static Geo make_geo(const NsBox& b, const double* d) {
 }
 
 void NsWorkspace::rhs(const double* U, double* out, int part, cudaStream_t st) {
+  // the direction kernels stage U with 16-byte copies and write out with
+  // 16-byte stores (x-contiguous cell pairs)
+  require(reinterpret_cast<std::uintptr_t>(U) % 16 == 0 &&
+              reinterpret_cast<std::uintptr_t>(out) % 16 == 0,
+          "ns rhs: U and out must be 16-byte aligned device arrays");
   const Geo g = make_geo(box_, dx_);
   const long long n = box_.cells();
   double* F = prim_.get();
@@ -717,32 +446,12 @@ void NsWorkspace::rhs(const double* U, double* out, int part, cudaStream_t st) {
     SMC_CHECK_LAUNCH();
     return;
   }
-  prim_kernel<<<blocks(g.flen), 256, 0, st>>>(U, F, g, ns_v1() ? 1 : 0);
+  prim_kernel<<<blocks(g.flen), 256, 0, st>>>(U, F, g);
   SMC_CHECK_LAUNCH();
-  if (part != kNsChem && !ns_v1()) {
-    if (s_ == 4)
-      rhs_v2<4>(g, U, F, A, grad_.get(), mixed_.get(), scratch_.get(), out, M_,
-                part == kNsFull, st);
-    else
-      rhs_v2<3>(g, U, F, A, grad_.get(), mixed_.get(), scratch_.get(), out, M_,
-                part == kNsFull, st);
-  } else if (part != kNsChem) {
-    hyp_kernel<<<blocks(n), 256, 0, st>>>(U, F, out, g, 1);
-    SMC_CHECK_LAUNCH();
-    if (s_ == 4)
-      narrow_kernel<4><<<blocks(n), 256, 0, st>>>(F, A, g, M_);
-    else
-      narrow_kernel<3><<<blocks(n), 256, 0, st>>>(F, A, g, M_);
-    SMC_CHECK_LAUNCH();
-    grad_kernel<<<blocks(g.plane * (g.nz + 2 * g.G)), 256, 0, st>>>(F, A, mixed_.get(), g);
-    SMC_CHECK_LAUNCH();
-    assemble_kernel<<<blocks(n), 256, 0, st>>>(F, A, mixed_.get(), out, g);
-    SMC_CHECK_LAUNCH();
-  }
-  if (part == kNsFull && ns_v1()) {  // v2 forms wdot inside ns_assemble2
-    wdot_kernel<<<blocks(n), 256, 0, st>>>(U, F, out, g);
-    SMC_CHECK_LAUNCH();
-  }
+  if (s_ == 4)
+    rhs_v2<4>(g, U, F, A, grad_.get(), mixed_.get(), scratch_.get(), out, M_, part == kNsFull, st);
+  else
+    rhs_v2<3>(g, U, F, A, grad_.get(), mixed_.get(), scratch_.get(), out, M_, part == kNsFull, st);
 }
 
 bool NsWorkspace::chem_fd_jacobian(const double* U, const double* FU, double* jac, double atol,
@@ -757,7 +466,7 @@ bool NsWorkspace::chem_fd_jacobian(const double* U, const double* FU, double* ja
 
 void NsWorkspace::temperature_pressure(const double* U, double* T, double* p, cudaStream_t st) {
   const Geo g = make_geo(box_, dx_);
-  prim_kernel<<<blocks(g.flen), 256, 0, st>>>(U, prim_.get(), g, 0);
+  prim_kernel<<<blocks(g.flen), 256, 0, st>>>(U, prim_.get(), g);
   SMC_CHECK_LAUNCH();
   tp_kernel<<<blocks(box_.cells()), 256, 0, st>>>(prim_.get(), T, p, g);
   SMC_CHECK_LAUNCH();

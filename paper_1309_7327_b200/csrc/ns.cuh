@@ -60,7 +60,13 @@ class NsRhsOp final : public RhsOp {
  public:
   NsRhsOp(std::shared_ptr<NsWorkspace> ws, int part) : ws_(std::move(ws)), part_(part) {}
   long long dim() const override { return SMC_NVAR * ws_->box().cells(); }
+  // The Rhs view is the periodic box only: a ghosted workspace (zghost > 0)
+  // reads 14 fields of field_len() each, which a caller's state of dim()
+  // doubles does not hold (smc_ns_rhs_ghosted and the slab RHS take those).
   void eval_device(double, const double* u, double* out) override {
+    require(ws_->box().G == 0,
+            "ns: a ghosted (zghost > 0) operator has no plain Rhs view; use "
+            "smc_ns_rhs_ghosted or the slab RHS (smc_ns_slab_*)");
     ws_->rhs(u, out, part_, stream_);
     ++evals_;
   }

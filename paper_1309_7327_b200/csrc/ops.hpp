@@ -5,6 +5,7 @@
 
 #include <cuda_runtime.h>
 
+#include <functional>
 #include <memory>
 #include <string>
 #include <vector>
@@ -50,6 +51,11 @@ class DevBuf {
 };
 
 enum Where : int { kHost = 0, kDevice = 1 };
+
+// Global max over ranks of a per-rank value (identity on one rank): the
+// residual max-norms of the sweeps (sdc.cpp:20-30, mrsdc.cpp:23-35) and the
+// Newton / step-control norms of the implicit solver (stiff.cpp:49-66).
+using Reducer = std::function<double(double)>;
 
 class RhsOp {
  public:

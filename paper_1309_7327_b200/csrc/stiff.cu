@@ -590,7 +590,8 @@ void DeviceNewton::solve(RhsOp& f, double t, double beta, const double* c, const
     read_slots(2);
     unsigned long long u[2];
     std::memcpy(u, host_slots_, sizeof(u));
-    const double rnorm = bits_to_double(u[0]), wnorm = bits_to_double(u[1]);
+    double rnorm = bits_to_double(u[0]), wnorm = bits_to_double(u[1]);
+    if (reduce_) rnorm = reduce_(rnorm), wnorm = reduce_(wnorm);
     rep.final_residual = rnorm;
     if (rnorm <= o.atol + o.rtol * wnorm) {
       rep.converged = true;
@@ -617,6 +618,7 @@ void DeviceNewton::solve(RhsOp& f, double t, double beta, const double* c, const
       launch_lu_smem(static_cast<int>(B), jac_.get(), delta_.get(), beta, bm, slots + 2, st);
       read_slots(3);
       std::memcpy(&flag, host_slots_ + 2, sizeof(flag));
+      if (reduce_) flag = reduce_(flag ? 1.0 : 0.0) > 0.0;
       if (flag) break;  // singular iteration matrix (stiff.cpp:66)
       sub_kernel<<<grid_for(dim), 256, 0, st>>>(w, delta_.get(), dim);
       SMC_CHECK_LAUNCH();
@@ -627,6 +629,7 @@ void DeviceNewton::solve(RhsOp& f, double t, double beta, const double* c, const
       SMC_CHECK_LAUNCH();
       read_slots(3);
       std::memcpy(&flag, host_slots_ + 2, sizeof(flag));
+      if (reduce_) flag = reduce_(flag ? 1.0 : 0.0) > 0.0;
       if (flag) break;  // singular iteration matrix (stiff.cpp:66)
       lu_solve_update_kernel<<<lu_grid, 128, 0, st>>>(jac_.get(), piv_, delta_.get(), w, bm);
       SMC_CHECK_LAUNCH();
@@ -643,8 +646,14 @@ double bdf2_coeff(double rho) {  // stiff.cpp:118-121
 
 }  // namespace
 
+// The host step controller below follows stiff.cpp:115-188 statement for
+// statement (rho_full / rho_mid / c_half / weight / the clamps): bitwise
+// agreement with the reference's accepted-step sequence needs the same
+// scalar arithmetic in the same order.  What is new is the device side:
+// every implicit stage is a DeviceNewton solve (batched per-block LU, fused
+// FD Jacobian) and the norms are device reductions read back once per step.
 void integrate_stiff(RhsOp& f, const double* u0, double t0, double t1, double* u_out,
-                     const StiffOpts& o, StiffStats* stats) {
+                     const StiffOpts& o, StiffStats* stats, const Reducer& reduce) {
   const long long dim = f.dim();
   cudaStream_t st = f.stream();
   StiffStats local;
@@ -664,6 +673,7 @@ void integrate_stiff(RhsOp& f, const double* u0, double t0, double t1, double* u
   double* y_half = Yh.get();
   SMC_CUDA(cudaMemcpyAsync(u, u0, dim * sizeof(double), cudaMemcpyDeviceToDevice, st));
   DeviceNewton newton;
+  if (reduce) newton.set_reducer(reduce);
   auto be = [&](double t_new, double h, const double* un, double* out) {
     NewtonReport rep;
     newton.solve(f, t_new, h, un, un, out, o, rep);
@@ -714,6 +724,7 @@ void integrate_stiff(RhsOp& f, const double* u0, double t0, double t1, double* u
     SMC_CHECK_LAUNCH();
     SMC_CUDA(cudaMemcpyAsync(host, slots.get(), sizeof(host), cudaMemcpyDeviceToHost, st));
     SMC_CUDA(cudaStreamSynchronize(st));
+    if (reduce) host[0] = reduce(host[0]), host[1] = reduce(host[1]);
     const double err = weight * host[0];
     const double p = have_history ? 3.0 : 2.0;
     const double tol = o.rtol * host[1] + o.atol;

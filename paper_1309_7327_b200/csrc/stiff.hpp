@@ -48,6 +48,10 @@ class DeviceNewton {
   // caller inspects rep.converged (stiff.cpp:71-75 with a report).
   void solve(RhsOp& f, double t, double beta, const double* c, const double* guess, double* w,
              const StiffOpts& o, NewtonReport& rep);
+  // Multi-rank f (a slab of a decomposed box): the residual and solution
+  // norms and the singular flag are reduced (max) over ranks, so every rank
+  // takes the same number of Newton steps and calls f equally often.
+  void set_reducer(Reducer r) { reduce_ = std::move(r); }
 
  private:
   void ensure(long long dim, long long block);
@@ -56,6 +60,7 @@ class DeviceNewton {
   int* piv_ = nullptr;
   long long piv_n_ = 0;
   double* host_slots_ = nullptr;  // pinned readback
+  Reducer reduce_;
 };
 
 // integrate_stiff (proj/core/src/stiff.cpp:80-188): adaptive backward Euler,
@@ -67,7 +72,10 @@ class DeviceNewton {
 struct StiffStats {
   int accepted = 0, rejected = 0;
 };
+// With a reducer (multi-rank f) the error norms are reduced over ranks, so
+// every rank accepts and rejects the same steps.
 void integrate_stiff(RhsOp& f, const double* u0, double t0, double t1, double* u_out,
-                     const StiffOpts& o, StiffStats* stats = nullptr);
+                     const StiffOpts& o, StiffStats* stats = nullptr,
+                     const Reducer& reduce = Reducer());
 
 }  // namespace smc

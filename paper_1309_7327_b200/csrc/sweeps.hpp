@@ -26,9 +26,6 @@ struct SweepDiag {
   void add(const SweepDiag& o);
 };
 
-// global max over ranks of a per-rank residual (identity on one rank)
-using Reducer = std::function<double(double)>;
-
 class DeviceSdc {
  public:
   DeviceSdc(Nodes nodes, int iterations, double cutoff, bool reuse_first);
@@ -72,7 +69,10 @@ class DeviceMrsdc {
                   double* f2_end, SweepDiag& d);
   void integrate_mode2(RhsOp& f1, RhsOp& f2, const double* u0, double t0, double t1, int nsteps,
                        double* u_out, SweepDiag& d);
-  void set_reducer(Reducer r) { reduce_ = std::move(r); }
+  void set_reducer(Reducer r) {
+    reduce_ = r;
+    newton_.set_reducer(std::move(r));
+  }
   void set_stiff(const StiffOpts& o) { stiff_ = o; }
   const StiffOpts& stiff() const { return stiff_; }
   const Hierarchy& hierarchy() const { return h_; }

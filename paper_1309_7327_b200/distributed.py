@@ -163,13 +163,19 @@ def exchange_halo_fields(U, slab: Slab, dist) -> None:
 
 def allreduce_max(dist, device=None):
     """Reducer for the device steppers' residual (max over ranks, one double
-    per sweep, sdc.cpp:20-30 / mrsdc.cpp:23-35)."""
+    per sweep, sdc.cpp:20-30 / mrsdc.cpp:23-35).  The NCCL backend reduces
+    device tensors only, so the default device is the current CUDA device
+    there and the host under gloo."""
     import torch
 
     def fn(v: float) -> float:
         if dist is None or not dist.is_initialized() or dist.get_world_size() == 1:
             return v
-        t = torch.tensor([v], dtype=torch.float64, device=device)
+        dev = device
+        if dev is None:
+            dev = (torch.device("cuda", torch.cuda.current_device())
+                   if dist.get_backend() == "nccl" else torch.device("cpu"))
+        t = torch.tensor([v], dtype=torch.float64, device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return float(t.item())
 
@@ -197,7 +203,8 @@ class DistributedNs:
         """out = RHS(U) on interior cells (device tensors, 14 x nz x ny x nx)."""
         G, nz = self.slab.ghost, self.slab.nz
         self.U[:, G:G + nz].copy_(U_interior.view(14, nz, self.ny, self.nx))
-        exchange_halo_fields(self.U, self.slab, self.dist)
+        if part != 2:  # chemistry is pointwise: no ghosts needed
+            exchange_halo_fields(self.U, self.slab, self.dist)
         import torch
         self.ns.set_stream(torch.cuda.current_stream())
         self.ns.rhs_ghosted(self.U, out.view(14, nz, self.ny, self.nx), part)

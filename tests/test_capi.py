@@ -99,3 +99,58 @@ def test_product_never_imports_oracle():
                 text = open(os.path.join(dirpath, f)).read()
                 assert "import oracle" not in text and "from oracle" not in text, f
                 assert "liboracle" not in text and "libnsdc_ref" not in text, f
+
+
+def test_wrappers_validate_array_sizes():
+    """The C side copies dim() doubles through every array argument, so the
+    Python wrappers check sizes, dtype and host/device placement before any
+    call (an undersized host array would overflow the staging copy)."""
+    f = P.CallbackRhs(8, lambda t, u: u)
+    with pytest.raises(P.SmcInvalidArgument, match="dimension is 8"):
+        f(0.0, np.zeros(7))
+    with pytest.raises(P.SmcInvalidArgument, match="dimension is 8"):
+        f(0.0, np.zeros(8), np.zeros(9))
+    with pytest.raises(P.SmcInvalidArgument, match="float64"):
+        f(0.0, np.zeros(8, dtype=np.float32))
+    st = P.SdcStepper(3, P.StepControls(2, 0.0))
+    with pytest.raises(P.SmcInvalidArgument):
+        st.step(f, np.zeros(8), 0.0, 0.1, f0=np.zeros(4))
+    with pytest.raises(P.SmcInvalidArgument, match="different dimensions"):
+        P.MrsdcStepper._arrays(f, P.CallbackRhs(9, lambda t, u: u), np.zeros(8))
+
+
+def test_callback_exceptions_are_deferred():
+    """An exception inside a callback is stored and re-raised by check() after
+    the C call returns (ctypes cannot propagate it through C frames)."""
+    _capi.defer(KeyError("from a callback"))
+    with pytest.raises(KeyError, match="from a callback"):
+        _capi.check(_capi.OK)
+    _capi.check(_capi.OK)  # cleared
+
+
+def test_allreduce_max_device_default():
+    """Under NCCL the reducer's tensor lives on the current CUDA device; under
+    gloo (and with one rank) it stays on the host."""
+    from paper_1309_7327_b200.distributed import allreduce_max
+
+    class Fake:
+        def __init__(self, backend):
+            self.backend, self.seen = backend, None
+
+        def is_initialized(self):
+            return True
+
+        def get_world_size(self):
+            return 2
+
+        def get_backend(self):
+            return self.backend
+
+        class ReduceOp:
+            MAX = "max"
+
+        def all_reduce(self, t, op=None):
+            self.seen = t.device.type
+
+    d = Fake("gloo")
+    assert allreduce_max(d)(3.5) == 3.5 and d.seen == "cpu"
