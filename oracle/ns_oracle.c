@@ -1,5 +1,9 @@
 /* TEST INFRASTRUCTURE ONLY — CPU restatement of the NS right-hand side.
- * See ns_oracle.h for the specification sources and the pinning status. */
+ * See ns_oracle.h for the specification sources and the pinning status.
+ * Every cell loop is an OpenMP loop (the reference's threading model is a
+ * static partition over std::threads, parallel.cpp:20-36); each cell's
+ * arithmetic is unchanged, so results are bitwise independent of the thread
+ * count (tests/test_ns_oracle.py). */
 #include "ns_oracle.h"
 
 #include <math.h>
@@ -78,9 +82,43 @@ void or_ns_wdot_cell(double rho, double T, const double* Y, double* wdot) {
   for (int k = 0; k < NSP; ++k) wdot[k] = SMC_W[k] * om[k];
 }
 
+/* Gross production magnitude of every species (test diagnostics): W_k
+ * sum_r |nu_rk| (qf_r + qr_r) with the rates of or_ns_wdot_cell.  Near
+ * equilibrium the net rho omega_k is a small difference of these, so
+ * max gross / max |net| bounds how much rounding the chemistry can lose. */
+static void wdot_gross_cell(double rho, double T, const double* Y, double* g) {
+  double C[NSP], M = 0.0, om[NSP];
+  for (int k = 0; k < NSP; ++k) {
+    C[k] = rho * Y[k] / SMC_W[k];
+    M += C[k];
+    om[k] = 0.0;
+  }
+  const double lnT = log(T), invRT = 1.0 / (SMC_RU * T);
+  for (int r = 0; r < SMC_NREAC; ++r) {
+    const smc_reaction* R = &SMC_REACTIONS[r];
+    double qf = R->fwd[0] * exp(R->fwd[1] * lnT - R->fwd[2] * invRT);
+    double qr = R->rev[0] * exp(R->rev[1] * lnT - R->rev[2] * invRT);
+    for (int j = 0; j < 3; ++j) {
+      if (R->reac[j] >= 0) qf *= C[R->reac[j]];
+      if (R->prod[j] >= 0) qr *= C[R->prod[j]];
+    }
+    if (R->third_body) {
+      qf *= M;
+      qr *= M;
+    }
+    const double q = fabs(qf) + fabs(qr);
+    for (int j = 0; j < 3; ++j) {
+      if (R->reac[j] >= 0) om[R->reac[j]] += q;
+      if (R->prod[j] >= 0) om[R->prod[j]] += q;
+    }
+  }
+  for (int k = 0; k < NSP; ++k) g[k] = SMC_W[k] * om[k];
+}
+
 /* ---------------------------------------------------------- state */
 void or_ns_conserved(const double* T, const double* p, const double* uvw, const double* Y,
                      long long n, double* U) {
+  #pragma omp parallel for schedule(static) if (n > 4096)
   for (long long c = 0; c < n; ++c) {
     double Yc[NSP], rinv = 0.0, e = 0.0;
     for (int k = 0; k < NSP; ++k) {
@@ -136,6 +174,7 @@ static void ctoprim_cell(const double* U, long long n, long long c, cellprim* q)
 }
 
 void or_ns_temperature_pressure(const double* U, long long n, double* T, double* p) {
+  #pragma omp parallel for schedule(static) if (n > 4096)
   for (long long c = 0; c < n; ++c) {
     cellprim q;
     ctoprim_cell(U, n, c, &q);
@@ -159,6 +198,7 @@ int or_ns_rhs(const double* U, int nx, int ny, int nz, double dx, double dy, dou
   double* f = malloc(sizeof(double) * F_COUNT * n);
 #define FLD(i) (f + (long long)(i) * n)
   double* rho = malloc(sizeof(double) * n);
+  #pragma omp parallel for schedule(static) if (n > 4096)
   for (long long c = 0; c < n; ++c) {
     cellprim q;
     ctoprim_cell(U, n, c, &q);
@@ -190,6 +230,7 @@ int or_ns_rhs(const double* U, int nx, int ny, int nz, double dx, double dy, dou
     for (int d = 0; d < 3; ++d) {
       const double* ud = FLD(F_U + d);
       for (int v = 0; v < NV; ++v) {
+        #pragma omp parallel for schedule(static) if (n > 4096)
         for (long long c = 0; c < n; ++c) {
           double fv;
           if (v == 0)
@@ -203,6 +244,7 @@ int or_ns_rhs(const double* U, int nx, int ny, int nz, double dx, double dy, dou
           flux[c] = fv;
         }
         or_deriv8_dir(flux, nx, ny, nz, d, d1[d], tmp);
+        #pragma omp parallel for schedule(static) if (n > 4096)
         for (long long c = 0; c < n; ++c) out[v * n + c] -= tmp[c];
       }
     }
@@ -230,10 +272,13 @@ int or_ns_rhs(const double* U, int nx, int ny, int nz, double dx, double dy, dou
     for (int i = 0; i < 3; ++i) {
       for (int j = 0; j < 3; ++j) {
         if (j == i) continue;
+        #pragma omp parallel for schedule(static) if (n > 4096)
         for (long long c = 0; c < n; ++c) flux[c] = FLD(F_ETA)[c] * G[(3 * j + i) * n + c];
         or_deriv8_dir(flux, nx, ny, nz, j, d1[j], tmp);
+        #pragma omp parallel for schedule(static) if (n > 4096)
         for (long long c = 0; c < n; ++c) dm[i * n + c] += tmp[c];
       }
+      #pragma omp parallel for schedule(static) if (n > 4096)
       for (long long c = 0; c < n; ++c) {
         double sdiv = 0.0;
         for (int j = 0; j < 3; ++j)
@@ -241,6 +286,7 @@ int or_ns_rhs(const double* U, int nx, int ny, int nz, double dx, double dy, dou
         flux[c] = FLD(F_LAM2)[c] * sdiv;
       }
       or_deriv8_dir(flux, nx, ny, nz, i, d1[i], tmp);
+      #pragma omp parallel for schedule(static) if (n > 4096)
       for (long long c = 0; c < n; ++c) dm[i * n + c] += tmp[c];
     }
     /* ---- correction velocity V_c = sum_l Fbar_l */
@@ -250,11 +296,13 @@ int or_ns_rhs(const double* U, int nx, int ny, int nz, double dx, double dy, dou
     for (int l = 0; l < NSP; ++l)
       for (int j = 0; j < 3; ++j) {
         or_deriv8_dir(FLD(F_X + l), nx, ny, nz, j, d1[j], tmp);
+        #pragma omp parallel for schedule(static) if (n > 4096)
         for (long long c = 0; c < n; ++c)
           Vc[j * n + c] -= FLD(F_D + l)[c] * tmp[c] + FLD(F_DP + l)[c] * gp[j * n + c];
       }
     /* div V_c = sum_l div Fbar_l = -sum_l (narrow part of species l) */
     double* divVc = malloc(sizeof(double) * n);
+    #pragma omp parallel for schedule(static) if (n > 4096)
     for (long long c = 0; c < n; ++c) {
       double sdv = 0.0;
       for (int k = 0; k < NSP; ++k) sdv += dY[k * n + c];
@@ -263,14 +311,17 @@ int or_ns_rhs(const double* U, int nx, int ny, int nz, double dx, double dy, dou
     /* species: -div F_k = -div Fbar_k + Y_k div V_c + V_c . grad Y_k */
     for (int k = 0; k < NSP; ++k) {
       double* o = out + (5 + k) * n;
+      #pragma omp parallel for schedule(static) if (n > 4096)
       for (long long c = 0; c < n; ++c) o[c] += dY[k * n + c] + FLD(F_Y + k)[c] * divVc[c];
       for (int j = 0; j < 3; ++j) {
         or_deriv8_dir(FLD(F_Y + k), nx, ny, nz, j, d1[j], tmp);
+        #pragma omp parallel for schedule(static) if (n > 4096)
         for (long long c = 0; c < n; ++c) o[c] += Vc[j * n + c] * tmp[c];
       }
     }
     /* energy: div(lam grad T) + div(tau.u) - div sum F_k h_k */
     double* oE = out + 4 * n;
+    #pragma omp parallel for schedule(static) if (n > 4096)
     for (long long c = 0; c < n; ++c) {
       double g[3][3];
       for (int i = 0; i < 3; ++i)
@@ -292,15 +343,18 @@ int or_ns_rhs(const double* U, int nx, int ny, int nz, double dx, double dy, dou
     for (int k = 0; k < NSP; ++k)
       for (int j = 0; j < 3; ++j) {
         or_deriv8_dir(FLD(F_HY + k), nx, ny, nz, j, d1[j], tmp);
+        #pragma omp parallel for schedule(static) if (n > 4096)
         for (long long c = 0; c < n; ++c) oE[c] += Vc[j * n + c] * tmp[c];
       }
     /* momentum: div tau */
     for (int i = 0; i < 3; ++i)
+      #pragma omp parallel for schedule(static) if (n > 4096)
       for (long long c = 0; c < n; ++c) out[(1 + i) * n + c] += dm[i * n + c];
     free(tmp); free(flux); free(dm); free(dE); free(dY); free(G); free(Vc); free(gp); free(divVc);
   }
   if (part != OR_NS_ADVDIFF) {
     /* wdot: rho omega_k */
+    #pragma omp parallel for schedule(static) if (n > 4096)
     for (long long c = 0; c < n; ++c) {
       double Y[NSP], w[NSP];
       for (int k = 0; k < NSP; ++k) Y[k] = FLD(F_Y + k)[c];
@@ -312,4 +366,15 @@ int or_ns_rhs(const double* U, int nx, int ny, int nz, double dx, double dy, dou
   free(f);
   free(rho);
   return 0;
+}
+
+void or_ns_chem_gross(const double* U, long long n, double* gross) {
+#pragma omp parallel for schedule(static) if (n > 4096)
+  for (long long c = 0; c < n; ++c) {
+    cellprim q;
+    ctoprim_cell(U, n, c, &q);
+    double g[NSP];
+    wdot_gross_cell(q.rho, q.T, q.Y, g);
+    for (int k = 0; k < NSP; ++k) gross[k * n + c] = g[k];
+  }
 }

@@ -37,6 +37,10 @@ int or_ns_rhs(const double* U, int nx, int ny, int nz, double dx, double dy, dou
 /* rho omega_k W_k for one cell (mass production rates, kg/m^3/s). */
 void or_ns_wdot_cell(double rho, double T, const double* Y, double* wdot);
 
+/* Gross chemistry magnitudes W_k sum_r |nu_rk| (qf_r + qr_r) per cell
+ * (gross[k * n + c]); diagnostics for the wdot cancellation (tests). */
+void or_ns_chem_gross(const double* U, long long n, double* gross);
+
 /* Conserved state from (rho-free) primitives: T, p, u, v, w, Y_k per cell. */
 void or_ns_conserved(const double* T, const double* p, const double* uvw, const double* Y,
                      long long n, double* U);

@@ -8,6 +8,9 @@
 #include <math.h>
 #include <stdlib.h>
 #include <string.h>
+#ifdef _OPENMP
+#include <omp.h>
+#endif
 
 /* ------------------------------------------------------------------ M */
 /* Affine entries c + p*m47 + q*m48 of rows 1..s (PAPER.md:263-300 for order
@@ -135,18 +138,23 @@ static inline long long lin(int i, int j, int k, int nx, int ny) {
 void or_narrow_dir(const double* m64, int s, const double* c, const double* u, int nx, int ny,
                    int nz, int dir, double inv_d2, int accumulate, double* out) {
   /* One direction of narrow_rhs_rows<S> (pde.cpp:85-129): interfaces once per
-   * line, then differenced.  Lines along dir are gathered with periodic wrap. */
+   * line, then differenced.  Lines along dir are gathered with periodic wrap;
+   * lines are independent, so they are shared out over OpenMP threads (the
+   * reference's parallel_for over rows, parallel.cpp:20-36) with the same
+   * per-element arithmetic: bitwise independent of the thread count. */
   const int n = dir == 0 ? nx : dir == 1 ? ny : nz;
-  double* cl = malloc(sizeof(double) * n);
-  double* ul = malloc(sizeof(double) * n);
-  double* cb = malloc(sizeof(double) * (n + 2 * s));
-  double* ub = malloc(sizeof(double) * (n + 2 * s));
-  double* h = malloc(sizeof(double) * n);
   const int n1 = dir == 0 ? ny : nx, n2 = dir == 2 ? ny : nz;
-  for (int b2 = 0; b2 < n2; ++b2)
-    for (int b1 = 0; b1 < n1; ++b1) {
-      long long idx[1];
-      (void)idx;
+  const long long lines = (long long)n1 * n2;
+#pragma omp parallel if (lines * n > 4096)
+  {
+    double* cl = malloc(sizeof(double) * n);
+    double* ul = malloc(sizeof(double) * n);
+    double* cb = malloc(sizeof(double) * (n + 2 * s));
+    double* ub = malloc(sizeof(double) * (n + 2 * s));
+    double* h = malloc(sizeof(double) * n);
+#pragma omp for schedule(static)
+    for (long long line = 0; line < lines; ++line) {
+      const int b1 = (int)(line % n1), b2 = (int)(line / n1);
       for (int q = 0; q < n; ++q) {
         int i, j, k;
         if (dir == 0) { i = q; j = b1; k = b2; }
@@ -169,29 +177,37 @@ void or_narrow_dir(const double* m64, int s, const double* c, const double* u, i
         out[o] = accumulate ? out[o] + v : v;
       }
     }
-  free(cl);
-  free(ul);
-  free(cb);
-  free(ub);
-  free(h);
+    free(cl);
+    free(ul);
+    free(cb);
+    free(ub);
+    free(h);
+  }
 }
 
 void or_deriv8_dir(const double* u, int nx, int ny, int nz, int dir, double inv_d, double* out) {
-  /* stencil_kernel.hpp:48-54 along dir with periodic wrap */
+  /* stencil_kernel.hpp:48-54 along dir with periodic wrap.  The wrapped
+   * neighbour offsets come from a table (no modulo per access); the
+   * arithmetic is the reference's expression in its order. */
   const long long st = dir == 0 ? 1 : dir == 1 ? nx : (long long)nx * ny;
   const int n = dir == 0 ? nx : dir == 1 ? ny : nz;
+  long long* wrap = malloc(sizeof(long long) * (n + 8));
+  for (int q = -4; q < n + 4; ++q) wrap[q + 4] = (long long)(((q % n) + n) % n) * st;
+#pragma omp parallel for schedule(static) if ((long long)nx * ny * nz > 4096)
   for (int k = 0; k < nz; ++k)
     for (int j = 0; j < ny; ++j)
       for (int i = 0; i < nx; ++i) {
         const int q = dir == 0 ? i : dir == 1 ? j : k;
         const long long base = lin(i, j, k, nx, ny) - (long long)q * st;
-#define AT(d) u[base + (long long)(((q + (d)) % n + n) % n) * st]
+        const long long* w = wrap + q + 4;
+#define AT(d) u[base + w[d]]
         out[lin(i, j, k, nx, ny)] =
             (C1 * (AT(1) - AT(-1)) + C2 * (AT(2) - AT(-2)) + C3 * (AT(3) - AT(-3)) +
              C4 * (AT(4) - AT(-4))) *
             inv_d;
 #undef AT
       }
+  free(wrap);
 }
 
 int or_narrow3d(const double* m64, int s, const double* a, const double* u, int nx, int ny,
@@ -279,6 +295,7 @@ int or_integrate_sdc(or_rhs_cb f, void* ctx, long long dim, const double* u0, do
     int hl = 0;
     for (int it = 1; it <= iterations; ++it) {
       for (int r = 0; r < m; ++r)
+#pragma omp parallel for schedule(static) if (dim > 4096)
         for (long long i = 0; i < dim; ++i) {
           double acc = 0.0;
           for (int j = 0; j <= m; ++j) acc += smat[r * (m + 1) + j] * F[j * dim + i];
@@ -289,8 +306,10 @@ int or_integrate_sdc(or_rhs_cb f, void* ctx, long long dim, const double* u0, do
         double* next = U + (r + 1) * dim;
         const double* cur = U + r * dim;
         if (r == 0) {
+#pragma omp parallel for schedule(static) if (dim > 4096)
           for (long long i = 0; i < dim; ++i) next[i] = cur[i] + I[i];
         } else {
+#pragma omp parallel for schedule(static) if (dim > 4096)
           for (long long i = 0; i < dim; ++i)
             next[i] = cur[i] + dtm * (F[r * dim + i] - fold[i]) + I[r * dim + i];
         }
@@ -300,6 +319,7 @@ int or_integrate_sdc(or_rhs_cb f, void* ctx, long long dim, const double* u0, do
       }
       /* sdc_residual, sdc.cpp:20-30 */
       double res = 0.0;
+#pragma omp parallel for schedule(static) reduction(max : res) if (dim > 4096)
       for (long long i = 0; i < dim; ++i) {
         double acc = 0.0;
         for (int j = 0; j <= m; ++j) acc += q[(m - 1) * (m + 1) + j] * F[j * dim + i];
@@ -368,6 +388,7 @@ int or_integrate_mrsdc1(or_rhs_cb f1, void* c1, or_rhs_cb f2, void* c2, long lon
     for (int it = 1; it <= iterations; ++it) {
       /* accumulate_node_terms, mrsdc.cpp:69-82 */
       for (int q = 0; q < m2; ++q)
+#pragma omp parallel for schedule(static) if (dim > 4096)
         for (long long i = 0; i < dim; ++i) {
           double acc = 0.0;
           for (int j = 0; j <= m1; ++j) acc += s21[q * (m1 + 1) + j] * F1[j * dim + i];
@@ -382,6 +403,7 @@ int or_integrate_mrsdc1(or_rhs_cb f1, void* c1, or_rhs_cb f2, void* c2, long lon
         const int p = p_map[q];
         double* next = U + (q + 1) * dim;
         const double* cur = U + q * dim;
+#pragma omp parallel for schedule(static) if (dim > 4096)
         for (long long i = 0; i < dim; ++i)
           next[i] = cur[i] + dtq * (F1[p * dim + i] - OF1[p * dim + i]) +
                     dtq * (F2[q * dim + i] - fold[i]) + SO[q * dim + i];
@@ -396,6 +418,7 @@ int or_integrate_mrsdc1(or_rhs_cb f1, void* c1, or_rhs_cb f2, void* c2, long lon
       }
       /* mrsdc_residual, mrsdc.cpp:23-35 */
       double res = 0.0;
+#pragma omp parallel for schedule(static) reduction(max : res) if (dim > 4096)
       for (long long i = 0; i < dim; ++i) {
         double acc = 0.0;
         for (int j = 0; j <= m1; ++j) acc += q21[(m2 - 1) * (m1 + 1) + j] * F1[j * dim + i];
@@ -595,6 +618,7 @@ int or_integrate_mrsdc2(or_rhs_cb f1, void* c1, or_rhs_cb f2, void* c2, long lon
     for (int it = 1; it <= iterations && rc == 0; ++it) {
       /* accumulate_node_terms, mrsdc.cpp:69-82 */
       for (int q = 0; q < m2; ++q)
+#pragma omp parallel for schedule(static) if (dim > 4096)
         for (long long i = 0; i < dim; ++i) {
           double acc = 0.0;
           for (int j = 0; j <= m1; ++j) acc += s21[q * (m1 + 1) + j] * F1[j * dim + i];
@@ -640,6 +664,7 @@ int or_integrate_mrsdc2(or_rhs_cb f1, void* c1, or_rhs_cb f2, void* c2, long lon
       if (rc) break;
       /* mrsdc_residual, mrsdc.cpp:23-35 */
       double res = 0.0;
+#pragma omp parallel for schedule(static) reduction(max : res) if (dim > 4096)
       for (long long i = 0; i < dim; ++i) {
         double acc = 0.0;
         for (int j = 0; j <= m1; ++j) acc += q21[(m2 - 1) * (m1 + 1) + j] * F1[j * dim + i];
@@ -771,4 +796,22 @@ int or_integrate_stiff(or_rhs_cb f, void* ctx, long long dim, const double* u0, 
   memcpy(u_out, u, bytes);
   free(u); free(u_prev); free(y_full); free(y_mid); free(y_half); free(c); free(guess);
   return rc;
+}
+
+/* Thread count of the OpenMP loops (0: the runtime default, i.e. every host
+ * thread or OMP_NUM_THREADS).  Results do not depend on it. */
+void or_set_threads(int n) {
+#ifdef _OPENMP
+  omp_set_num_threads(n > 0 ? n : omp_get_num_procs());
+#else
+  (void)n;
+#endif
+}
+
+int or_get_threads(void) {
+#ifdef _OPENMP
+  return omp_get_max_threads();
+#else
+  return 1;
+#endif
 }

@@ -47,6 +47,11 @@ void or_narrow_dir(const double* m64, int s, const double* c, const double* u, i
 void or_deriv8_dir(const double* u, int nx, int ny, int nz, int dir, double inv_d, double* out);
 
 /* configs[1]: (a U_x)_x + (a U_y)_y + (a U_z)_z, summed x, y, z in that order. */
+/* OpenMP thread count of the oracle's loops (0 = all host threads); results
+ * are bitwise independent of it. */
+void or_set_threads(int n);
+int or_get_threads(void);
+
 int or_narrow3d(const double* m64, int s, const double* a, const double* u, int nx, int ny,
                 int nz, double dx, double dy, double dz, double* out);
 

@@ -194,6 +194,22 @@ def ns_rhs(U, dx, part=0, m64=None, s=4) -> np.ndarray:
     return out
 
 
+def set_threads(n: int = 0) -> int:
+    """OpenMP threads of the oracle's loops (0 = every host thread); results
+    are bitwise independent of it.  Returns the count in effect."""
+    lib().or_set_threads(int(n))
+    lib().or_get_threads.restype = C.c_int
+    return int(lib().or_get_threads())
+
+
+def ns_chem_gross(U) -> np.ndarray:
+    """Per-species gross chemistry magnitude (see ns_oracle.h)."""
+    n = U[0].size
+    g = np.empty((9,) + U.shape[1:])
+    lib().or_ns_chem_gross(dp(U), C.c_longlong(n), dp(g))
+    return g
+
+
 def ns_temperature_pressure(U):
     n = U[0].size
     T, p = np.empty(U.shape[1:]), np.empty(U.shape[1:])

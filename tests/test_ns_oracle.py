@@ -61,3 +61,16 @@ def test_spatial_order_of_accuracy():
         e1 = np.abs(rs[16][v] - rs[64][v][::4, ::4, ::4]).max()
         e2 = np.abs(rs[32][v][::2, ::2, ::2] - rs[64][v][::4, ::4, ::4]).max()
         assert np.log2(e1 / e2) > 6.5, (v, e1, e2)
+
+
+def test_threads_do_not_change_bits():
+    """The OpenMP loops of the oracle keep each cell's arithmetic, so the RHS
+    is bitwise independent of the thread count (as the reference's
+    parallel_for, pde_test.cpp:119-133)."""
+    U, _, _ = _U(20, hot_spot=True)
+    O.set_threads(1)
+    r1 = O.ns_rhs(U, DX, part=0)
+    O.set_threads(4)
+    r4 = O.ns_rhs(U, DX, part=0)
+    O.set_threads(0)
+    assert np.array_equal(r1, r4)
