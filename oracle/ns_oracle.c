@@ -186,6 +186,15 @@ void or_ns_temperature_pressure(const double* U, long long n, double* T, double*
 /* ------------------------------------------------------------- RHS */
 int or_ns_rhs(const double* U, int nx, int ny, int nz, double dx, double dy, double dz,
               const double* m64, int s, int part, double* out) {
+  return or_ns_rhs_terms(U, nx, ny, nz, dx, dy, dz, m64, s, part, OR_T_ALL, out);
+}
+
+/* The RHS restricted to the terms in `terms` (OR_T_* of ns_oracle.h); with
+ * OR_T_ALL every sum is formed in the same order as the full RHS. */
+int or_ns_rhs_terms(const double* U, int nx, int ny, int nz, double dx, double dy, double dz,
+                    const double* m64, int s, int part, int terms, double* out) {
+  const int hyp = terms & OR_T_HYP, visc = terms & OR_T_VISC, heatc = terms & OR_T_HEAT,
+            spec = terms & OR_T_SPEC, enth = terms & OR_T_ENTH;
   const long long n = (long long)nx * ny * nz;
   const double d1[3] = {1.0 / dx, 1.0 / dy, 1.0 / dz};
   const double d2[3] = {1.0 / (dx * dx), 1.0 / (dy * dy), 1.0 / (dz * dz)};
@@ -227,7 +236,7 @@ int or_ns_rhs(const double* U, int nx, int ny, int nz, double dx, double dy, dou
     double* tmp = malloc(sizeof(double) * n);
     double* flux = malloc(sizeof(double) * n);
     /* ---- hypterm: -div F, 8th-order centred first derivatives */
-    for (int d = 0; d < 3; ++d) {
+    for (int d = 0; d < 3 && hyp; ++d) {
       const double* ud = FLD(F_U + d);
       for (int v = 0; v < NV; ++v) {
         #pragma omp parallel for schedule(static) if (n > 4096)
@@ -253,23 +262,26 @@ int or_ns_rhs(const double* U, int nx, int ny, int nz, double dx, double dy, dou
     double* dE = calloc(n, sizeof(double));
     double* dY = calloc(NSP * n, sizeof(double));
     for (int d = 0; d < 3; ++d) {
-      for (int i = 0; i < 3; ++i)
+      for (int i = 0; i < 3 && visc; ++i)
         or_narrow_dir(m64, s, FLD(i == d ? F_ETA43 : F_ETA), FLD(F_U + i), nx, ny, nz, d, d2[d],
                       1, dm + i * n);
-      or_narrow_dir(m64, s, FLD(F_LAM), FLD(F_T), nx, ny, nz, d, d2[d], 1, dE);
+      if (heatc) or_narrow_dir(m64, s, FLD(F_LAM), FLD(F_T), nx, ny, nz, d, d2[d], 1, dE);
       for (int k = 0; k < NSP; ++k) {
-        or_narrow_dir(m64, s, FLD(F_D + k), FLD(F_X + k), nx, ny, nz, d, d2[d], 1, dY + k * n);
-        or_narrow_dir(m64, s, FLD(F_DH + k), FLD(F_X + k), nx, ny, nz, d, d2[d], 1, dE);
-        or_narrow_dir(m64, s, FLD(F_DP + k), FLD(F_P), nx, ny, nz, d, d2[d], 1, dY + k * n);
+        if (spec || enth)
+          or_narrow_dir(m64, s, FLD(F_D + k), FLD(F_X + k), nx, ny, nz, d, d2[d], 1, dY + k * n);
+        if (enth)
+          or_narrow_dir(m64, s, FLD(F_DH + k), FLD(F_X + k), nx, ny, nz, d, d2[d], 1, dE);
+        if (spec || enth)
+          or_narrow_dir(m64, s, FLD(F_DP + k), FLD(F_P), nx, ny, nz, d, d2[d], 1, dY + k * n);
       }
-      or_narrow_dir(m64, s, FLD(F_DHP), FLD(F_P), nx, ny, nz, d, d2[d], 1, dE);
+      if (enth) or_narrow_dir(m64, s, FLD(F_DHP), FLD(F_P), nx, ny, nz, d, d2[d], 1, dE);
     }
     /* ---- velocity gradients G[i][j] = d_j u_i */
     double* G = malloc(sizeof(double) * 9 * n);
     for (int i = 0; i < 3; ++i)
       for (int j = 0; j < 3; ++j) or_deriv8_dir(FLD(F_U + i), nx, ny, nz, j, d1[j], G + (3 * i + j) * n);
     /* ---- mixed viscous terms: sum_{j!=i} d_j(eta d_i u_j) + d_i(lam2 sum_{j!=i} d_j u_j) */
-    for (int i = 0; i < 3; ++i) {
+    for (int i = 0; i < 3 && visc; ++i) {
       for (int j = 0; j < 3; ++j) {
         if (j == i) continue;
         #pragma omp parallel for schedule(static) if (n > 4096)
@@ -309,7 +321,7 @@ int or_ns_rhs(const double* U, int nx, int ny, int nz, double dx, double dy, dou
       divVc[c] = -sdv;
     }
     /* species: -div F_k = -div Fbar_k + Y_k div V_c + V_c . grad Y_k */
-    for (int k = 0; k < NSP; ++k) {
+    for (int k = 0; k < NSP && spec; ++k) {
       double* o = out + (5 + k) * n;
       #pragma omp parallel for schedule(static) if (n > 4096)
       for (long long c = 0; c < n; ++c) o[c] += dY[k * n + c] + FLD(F_Y + k)[c] * divVc[c];
@@ -338,9 +350,9 @@ int or_ns_rhs(const double* U, int nx, int ny, int nz, double dx, double dy, dou
       for (int i = 0; i < 3; ++i) udivtau += FLD(F_U + i)[c] * dm[i * n + c];
       double hyd = 0.0;
       for (int k = 0; k < NSP; ++k) hyd += FLD(F_HY + k)[c] * divVc[c];
-      oE[c] += dE[c] + heat + udivtau + hyd;
+      oE[c] += dE[c] + (visc ? heat : 0.0) + (visc ? udivtau : 0.0) + (enth ? hyd : 0.0);
     }
-    for (int k = 0; k < NSP; ++k)
+    for (int k = 0; k < NSP && enth; ++k)
       for (int j = 0; j < 3; ++j) {
         or_deriv8_dir(FLD(F_HY + k), nx, ny, nz, j, d1[j], tmp);
         #pragma omp parallel for schedule(static) if (n > 4096)
@@ -352,7 +364,7 @@ int or_ns_rhs(const double* U, int nx, int ny, int nz, double dx, double dy, dou
       for (long long c = 0; c < n; ++c) out[(1 + i) * n + c] += dm[i * n + c];
     free(tmp); free(flux); free(dm); free(dE); free(dY); free(G); free(Vc); free(gp); free(divVc);
   }
-  if (part != OR_NS_ADVDIFF) {
+  if (part != OR_NS_ADVDIFF && (terms & OR_T_CHEM)) {
     /* wdot: rho omega_k */
     #pragma omp parallel for schedule(static) if (n > 4096)
     for (long long c = 0; c < n; ++c) {

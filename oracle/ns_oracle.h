@@ -34,6 +34,24 @@ void or_ns_temperature_pressure(const double* U, long long n, double* T, double*
 int or_ns_rhs(const double* U, int nx, int ny, int nz, double dx, double dy, double dz,
               const double* m64, int s, int part, double* out);
 
+/* Term selection for or_ns_rhs_terms (the manufactured-solution tests pin
+ * each physical term separately against the exact calculus):
+ *   HYP   -div of the Euler fluxes (all 14 equations)
+ *   VISC  div tau (momentum) and div(tau . u) (energy)
+ *   HEAT  div(lambda grad T) (energy)
+ *   SPEC  -div F_k = -div Fbar_k + div(Y_k V_c) (species)
+ *   ENTH  -div sum_k F_k h_k (energy)
+ *   CHEM  rho omega_k (species) */
+#define OR_T_HYP 1
+#define OR_T_VISC 2
+#define OR_T_HEAT 4
+#define OR_T_SPEC 8
+#define OR_T_ENTH 16
+#define OR_T_CHEM 32
+#define OR_T_ALL 63
+int or_ns_rhs_terms(const double* U, int nx, int ny, int nz, double dx, double dy, double dz,
+                    const double* m64, int s, int part, int terms, double* out);
+
 /* rho omega_k W_k for one cell (mass production rates, kg/m^3/s). */
 void or_ns_wdot_cell(double rho, double T, const double* Y, double* wdot);
 

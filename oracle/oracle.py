@@ -210,6 +210,18 @@ def ns_chem_gross(U) -> np.ndarray:
     return g
 
 
+def ns_rhs_terms(U, dx, terms, part=0, m64=None, s=4) -> np.ndarray:
+    """or_ns_rhs_terms: the RHS restricted to the OR_T_* terms in `terms`."""
+    _, nz, ny, nx = U.shape
+    if m64 is None:
+        m64, s = build_narrow(8, (3557.0 / 44100.0, -2083.0 / 117600.0))
+    out = np.empty_like(U)
+    rc = lib().or_ns_rhs_terms(dp(U), nx, ny, nz, C.c_double(dx), C.c_double(dx), C.c_double(dx),
+                               dp(m64), s, part, int(terms), dp(out))
+    assert rc == 0
+    return out
+
+
 def ns_temperature_pressure(U):
     n = U[0].size
     T, p = np.empty(U.shape[1:]), np.empty(U.shape[1:])
