@@ -235,9 +235,16 @@ int or_ns_rhs_terms(const double* U, int nx, int ny, int nz, double dx, double d
   if (part != OR_NS_CHEM) {
     double* tmp = malloc(sizeof(double) * n);
     double* flux = malloc(sizeof(double) * n);
-    /* ---- hypterm: -div F, 8th-order centred first derivatives */
+    /* ---- hypterm: -div F, 8th-order centred first derivatives.
+     * The momentum flux rho u_i u_d + delta_id p is differentiated as
+     * d(rho u_i u_d) + d(p): formed as one number, p (~1e5 Pa) would bury
+     * the convective part's low bits, and the rounding of that sum (~eps p
+     * / dx) would dominate a weakly driven momentum RHS (uniform p, fine
+     * grids).  The same split is exact in exact arithmetic. */
+    double* dp = malloc(sizeof(double) * n);
     for (int d = 0; d < 3 && hyp; ++d) {
       const double* ud = FLD(F_U + d);
+      or_deriv8_dir(FLD(F_P), nx, ny, nz, d, d1[d], dp);
       for (int v = 0; v < NV; ++v) {
         #pragma omp parallel for schedule(static) if (n > 4096)
         for (long long c = 0; c < n; ++c) {
@@ -245,7 +252,7 @@ int or_ns_rhs_terms(const double* U, int nx, int ny, int nz, double dx, double d
           if (v == 0)
             fv = U[n + d * n + c];                             /* rho u_d */
           else if (v <= 3)
-            fv = U[v * n + c] * ud[c] + (v - 1 == d ? FLD(F_P)[c] : 0.0);
+            fv = U[v * n + c] * ud[c];                         /* + p: dp below */
           else if (v == 4)
             fv = (U[4 * n + c] + FLD(F_P)[c]) * ud[c];
           else
@@ -253,10 +260,12 @@ int or_ns_rhs_terms(const double* U, int nx, int ny, int nz, double dx, double d
           flux[c] = fv;
         }
         or_deriv8_dir(flux, nx, ny, nz, d, d1[d], tmp);
+        const int with_p = v - 1 == d;
         #pragma omp parallel for schedule(static) if (n > 4096)
-        for (long long c = 0; c < n; ++c) out[v * n + c] -= tmp[c];
+        for (long long c = 0; c < n; ++c) out[v * n + c] -= with_p ? tmp[c] + dp[c] : tmp[c];
       }
     }
+    free(dp);
     /* ---- diffterm, same-direction second derivatives: narrow stencil */
     double* dm = calloc(3 * n, sizeof(double));
     double* dE = calloc(n, sizeof(double));
