@@ -17,7 +17,7 @@
 #define NV SMC_NVAR
 
 /* ---------------------------------------------------------- thermo */
-/* e_k(T) = h_k(T) - R_k T and cv_k = cp_k - R_k, per unit mass. */
+/* e_k(T) = h_k(T) - R_k T, per unit mass. */
 static double spec_e(int k, double T) {
   const double* a = SMC_THERMO[k];
   const double R = SMC_RU / SMC_W[k];
@@ -28,24 +28,35 @@ static double spec_h(int k, double T) {
   const double R = SMC_RU / SMC_W[k];
   return R * (a[0] * T + a[1] * T * T / 2.0 + a[2] * T * T * T / 3.0 + a[3]);
 }
-static double spec_cv(int k, double T) {
-  const double* a = SMC_THERMO[k];
-  const double R = SMC_RU / SMC_W[k];
-  return R * (a[0] + a[1] * T + a[2] * T * T - 1.0);
-}
 
 /* T from the specific internal energy by Newton (ideal gas
- * mixture; e = sum_k Y_k e_k(T)).  Same stopping rule on the GPU. */
+ * mixture; e = sum_k Y_k e_k(T)).  e(T) is a cubic in T (the cp_k/R_k are
+ * quadratics), so the mixture's coefficients
+ *   e(T) = E0 + T (E1 + T (E2 + T E3)),  E0 = sum Y_k R_k b_k,
+ *   E1 = sum Y_k R_k (a0_k - 1), E2 = sum Y_k R_k a1_k / 2, E3 = sum Y_k R_k a2_k / 3
+ * are summed once and Newton iterates on the cubic, cv = de/dT.  Every
+ * operation is written out (fma() where fused), the same sequence as the
+ * GPU kernel, so the two give the same T bits: on fine grids of a nearly
+ * uniform-pressure state the momentum RHS is -grad p plus small terms and a
+ * few-ulp per-cell difference of p would be amplified by 1/dx. */
 static double temperature(const double* Y, double e) {
+  double E0 = 0.0, E1 = 0.0, E2 = 0.0, E3 = 0.0;
+  for (int k = 0; k < NSP; ++k) {
+    const double* a = SMC_THERMO[k];
+    const double yr = Y[k] * (SMC_RU / SMC_W[k]);
+    E0 = fma(yr, a[3], E0);
+    E1 = fma(yr, a[0] - 1.0, E1);
+    E2 = fma(yr, a[1] / 2.0, E2);
+    E3 = fma(yr, a[2] / 3.0, E3);
+  }
+  E0 = E0 - e;
+  const double D2 = 2.0 * E2, D3 = 3.0 * E3;
   double T = 1000.0;
   for (int it = 0; it < 50; ++it) {
-    double f = -e, df = 0.0;
-    for (int k = 0; k < NSP; ++k) {
-      f += Y[k] * spec_e(k, T);
-      df += Y[k] * spec_cv(k, T);
-    }
+    const double f = fma(T, fma(T, fma(T, E3, E2), E1), E0);
+    const double df = fma(T, fma(T, D3, D2), E1);
     const double dT = f / df;
-    T -= dT;
+    T = T - dT;
     if (fabs(dT) <= 1e-9 * T) break;
   }
   return T;
@@ -148,13 +159,14 @@ static void ctoprim_cell(const double* U, long long n, long long c, cellprim* q)
   q->rho = U[c];
   const double ri = 1.0 / q->rho;
   for (int i = 0; i < 3; ++i) q->u[i] = U[(1 + i) * n + c] * ri;
-  double wsum = 0.0;
+  double wsum = 0.0; /* sum_k Y_k / W_k as fma(Y_k, 1 / W_k, .) (the GPU's sequence) */
   for (int k = 0; k < NSP; ++k) {
     q->Y[k] = U[(5 + k) * n + c] * ri;
-    wsum += q->Y[k] / SMC_W[k];
+    wsum = fma(q->Y[k], 1.0 / SMC_W[k], wsum);
   }
-  const double e =
-      U[4 * n + c] * ri - 0.5 * (q->u[0] * q->u[0] + q->u[1] * q->u[1] + q->u[2] * q->u[2]);
+  /* e = rho E / rho - |u|^2 / 2 */
+  const double k2 = fma(q->u[2], q->u[2], fma(q->u[1], q->u[1], q->u[0] * q->u[0]));
+  const double e = fma(-0.5, k2, U[4 * n + c] * ri);
   q->T = temperature(q->Y, e);
   q->p = q->rho * SMC_RU * q->T * wsum;
   for (int k = 0; k < NSP; ++k) {

@@ -38,7 +38,7 @@ struct Tables {
   double W[NSP], th[NSP][4], mu0[NSP], lam0[NSP], rhoD0[NSP];
   // derived on the host: R_k = R_u / W_k, 1 / W_k and the enthalpy
   // polynomial in Horner form {a0, a1/2, a2/3, a3}: no divisions per cell
-  double R[NSP], Winv[NSP], hc[NSP][4];
+  double R[NSP], Winv[NSP], hc[NSP][4], hcm1[NSP];
   double kf[SMC_NREAC][3], kr[SMC_NREAC][3];
   int reac[SMC_NREAC][3], prod[SMC_NREAC][3], tb[SMC_NREAC];
 };
@@ -73,34 +73,47 @@ __device__ __forceinline__ double spec_h(int k, double T) {
   return cT.R[k] * (c[3] + T * (c[0] + T * (c[1] + T * c[2])));
 }
 
-// T from e by Newton, same start and stopping rule as the oracle.  The
-// mixture's e(T) = sum_k Y_k e_k(T) is one cubic, E0 + T (E1 + T (E2 + T E3)),
-// and cv = de/dT = E1 + T (2 E2 + 3 E3 T) (the cv_k polynomials are the e_k
-// derivatives), so its coefficients are summed once per cell and an
-// iteration costs two Horner evaluations instead of 2 x 9 (the oracle sums
-// per species per iteration: the iterates agree to rounding).
+// T from e by Newton on the mixture's energy cubic: e(T) = sum_k Y_k e_k(T)
+// = E0 + T (E1 + T (E2 + T E3)) with cv = de/dT = E1 + T (2 E2 + 3 E3 T), so
+// an iteration costs two Horner evaluations instead of 2 x 9 species sums.
+//
+// The operation sequence is fixed with explicit roundings (_rn intrinsics,
+// fused multiply-adds where written) and restated operation for operation
+// by the oracle (oracle/ns_oracle.c temperature(), with C fma()), so T, and
+// p below, are the same bits on both sides.  That matters: on fine grids of
+// a nearly uniform-pressure state the momentum RHS is -grad p plus small
+// terms, and a per-cell difference of a few ulps of p (~1e5 Pa) becomes
+// eps p / dx ~ 1e-7 after differentiation, ~3e-10 of the momentum RHS at
+// 256^3 (measured), above the single-RHS bar.
 __device__ double temperature(const double* Y, double e) {
   double E0 = 0.0, E1 = 0.0, E2 = 0.0, E3 = 0.0;
 #pragma unroll
   for (int k = 0; k < NSP; ++k) {
-    const double yr = Y[k] * cT.R[k];
+    const double yr = __dmul_rn(Y[k], cT.R[k]);
     const double* c = cT.hc[k];
-    E0 += yr * c[3];
-    E1 += yr * (c[0] - 1.0);
-    E2 += yr * c[1];
-    E3 += yr * c[2];
+    E0 = __fma_rn(yr, c[3], E0);
+    E1 = __fma_rn(yr, cT.hcm1[k], E1);
+    E2 = __fma_rn(yr, c[1], E2);
+    E3 = __fma_rn(yr, c[2], E3);
   }
-  E0 -= e;
-  const double D2 = 2.0 * E2, D3 = 3.0 * E3;
+  E0 = __dsub_rn(E0, e);
+  const double D2 = __dmul_rn(2.0, E2), D3 = __dmul_rn(3.0, E3);
   double T = 1000.0;
   for (int it = 0; it < 50; ++it) {
-    const double f = E0 + T * (E1 + T * (E2 + T * E3));
-    const double df = E1 + T * (D2 + T * D3);
-    const double dT = f / df;
-    T -= dT;
-    if (fabs(dT) <= 1e-9 * T) break;
+    const double f = __fma_rn(T, __fma_rn(T, __fma_rn(T, E3, E2), E1), E0);
+    const double df = __fma_rn(T, __fma_rn(T, D3, D2), E1);
+    const double dT = __ddiv_rn(f, df);
+    T = __dsub_rn(T, dT);
+    if (fabs(dT) <= __dmul_rn(1e-9, T)) break;
   }
   return T;
+}
+
+// Specific internal energy from the conserved state (canonical sequence,
+// shared bit for bit with the oracle): e = rho E / rho - |u|^2 / 2.
+__device__ __forceinline__ double internal_energy(double rhoE, double ri, const double* u) {
+  const double k2 = __fma_rn(u[2], u[2], __fma_rn(u[1], u[1], __dmul_rn(u[0], u[0])));
+  return __fma_rn(-0.5, k2, __dmul_rn(rhoE, ri));
 }
 
 // ---------------------------------------------------------------- prim
@@ -110,18 +123,18 @@ __global__ void __launch_bounds__(256, 3) prim_kernel(const double* __restrict__
   const long long c = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
   if (c >= n) return;
   const double rho = U[c];
-  const double ri = 1.0 / rho;
+  const double ri = __ddiv_rn(1.0, rho);
   double u[3], Y[NSP], X[NSP];
-  for (int i = 0; i < 3; ++i) u[i] = U[(1 + i) * n + c] * ri;
-  double wsum = 0.0;
+  for (int i = 0; i < 3; ++i) u[i] = __dmul_rn(U[(1 + i) * n + c], ri);
+  double wsum = 0.0;  // sum_k Y_k / W_k (canonical sequence, as the oracle)
 #pragma unroll
   for (int k = 0; k < NSP; ++k) {
-    Y[k] = U[(5 + k) * n + c] * ri;
-    wsum += Y[k] * cT.Winv[k];
+    Y[k] = __dmul_rn(U[(5 + k) * n + c], ri);
+    wsum = __fma_rn(Y[k], cT.Winv[k], wsum);
   }
-  const double e = U[4 * n + c] * ri - 0.5 * (u[0] * u[0] + u[1] * u[1] + u[2] * u[2]);
+  const double e = internal_energy(U[4 * n + c], ri, u);
   const double T = temperature(Y, e);
-  const double p = rho * SMC_RU * T * wsum;
+  const double p = __dmul_rn(__dmul_rn(__dmul_rn(rho, SMC_RU), T), wsum);
   const double s = pow(T / SMC_T_REF, SMC_TRANSPORT_EXP);
   double eta = 0.0, lam = 0.0, dhp = 0.0, hys = 0.0;
   const double pinv = 1.0 / p, wsinv = 1.0 / wsum;
@@ -230,13 +243,12 @@ __device__ __forceinline__ void wdot_cell(double rho, double T, const double* Y,
 // the RHS without materialising the primitive workspace.
 __device__ __forceinline__ void chem_cell(const double* Uc, double* o) {
   const double rho = Uc[0];
-  const double ri = 1.0 / rho;
+  const double ri = __ddiv_rn(1.0, rho);
   double u[3], Y[NSP], w[NSP];
-  for (int i = 0; i < 3; ++i) u[i] = Uc[1 + i] * ri;
+  for (int i = 0; i < 3; ++i) u[i] = __dmul_rn(Uc[1 + i], ri);
 #pragma unroll
-  for (int k = 0; k < NSP; ++k) Y[k] = Uc[5 + k] * ri;
-  const double e = Uc[4] * ri - 0.5 * (u[0] * u[0] + u[1] * u[1] + u[2] * u[2]);
-  wdot_cell(rho, temperature(Y, e), Y, w);
+  for (int k = 0; k < NSP; ++k) Y[k] = __dmul_rn(Uc[5 + k], ri);
+  wdot_cell(rho, temperature(Y, internal_energy(Uc[4], ri, u)), Y, w);
   for (int v = 0; v < 5; ++v) o[v] = 0.0;
 #pragma unroll
   for (int s = 0; s < NSP; ++s) o[5 + s] = w[s];
@@ -341,6 +353,7 @@ void upload_tables() {
     t.hc[s][1] = SMC_THERMO[s][1] / 2.0;
     t.hc[s][2] = SMC_THERMO[s][2] / 3.0;
     t.hc[s][3] = SMC_THERMO[s][3];
+    t.hcm1[s] = SMC_THERMO[s][0] - 1.0;
   }
   for (int r = 0; r < SMC_NREAC; ++r) {
     for (int q = 0; q < 3; ++q) {
