@@ -25,7 +25,7 @@ constexpr int NV = SMC_NVAR;
 // eta43 = (4/3 + xi/eta) eta and lam2 = (xi/eta - 2/3) eta are formed where
 // they are used.
 enum : int {
-  F_U = 0, F_T = 3, F_P, F_ETA, F_LAM, F_DHP, F_HYS, F_S, F_Y,
+  F_U = 0, F_T = 3, F_P, F_ETA, F_LAM, F_DHP, F_HYS, F_S, F_RHO, F_Y,
   F_X = F_Y + NSP, F_DH = F_X + NSP, F_DP = F_DH + NSP, F_COUNT = F_DP + NSP
 };
 // acc_ field indices (interior)
@@ -48,6 +48,22 @@ struct Geo {
   int nx, ny, nz, G;
   long long plane, flen;
   double d1[3], d2[3];
+};
+
+// Device view of the conserved state (NsStateView): the three blocks as
+// base pointers rebased so that block b's element of in-interior offset o
+// (plane-0 relative, ghost planes negative) is p_b + o + v * fs_b.  Scalar
+// members and selects: an indexed array would live in local memory.
+struct UV {
+  const double *p0, *p1, *p2;
+  long long fs0, fs1, fs2;
+  long long lim1;  // offset of plane nz (block 0 ends at offset 0)
+  // address of field 0 of the cell at offset o, and that block's field stride
+  __device__ __forceinline__ const double* at(long long o, long long& fs) const {
+    const bool lo = o < 0, hi = o >= lim1;
+    fs = lo ? fs0 : hi ? fs2 : fs1;
+    return (lo ? p0 : hi ? p2 : p1) + o;
+  }
 };
 
 __device__ __forceinline__ long long zo(const Geo& g, int k) {
@@ -117,22 +133,27 @@ __device__ __forceinline__ double internal_energy(double rhoE, double ri, const 
 }
 
 // ---------------------------------------------------------------- prim
-__global__ void __launch_bounds__(256, 3) prim_kernel(const double* __restrict__ U,
-                                                   double* __restrict__ F, Geo g) {
-  const long long n = g.flen;  // all planes incl. ghosts
-  const long long c = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
-  if (c >= n) return;
-  const double rho = U[c];
+// planes [k0, k1) of the ghosted workspace (k in [-G, nz + G))
+__global__ void __launch_bounds__(256, 3) prim_kernel(const UV U, double* __restrict__ F, Geo g,
+                                                   int k0, int k1) {
+  const long long n = g.flen;  // F: all planes incl. ghosts
+  const long long r = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
+  if (r >= (k1 - k0) * g.plane) return;
+  const long long o = r + k0 * g.plane;  // offset relative to interior plane 0
+  const long long c = o + g.G * g.plane;
+  long long fs;
+  const double* uc = U.at(o, fs);
+  const double rho = uc[0];
   const double ri = __ddiv_rn(1.0, rho);
   double u[3], Y[NSP], X[NSP];
-  for (int i = 0; i < 3; ++i) u[i] = __dmul_rn(U[(1 + i) * n + c], ri);
+  for (int i = 0; i < 3; ++i) u[i] = __dmul_rn(uc[(1 + i) * fs], ri);
   double wsum = 0.0;  // sum_k Y_k / W_k (canonical sequence, as the oracle)
 #pragma unroll
   for (int k = 0; k < NSP; ++k) {
-    Y[k] = __dmul_rn(U[(5 + k) * n + c], ri);
+    Y[k] = __dmul_rn(uc[(5 + k) * fs], ri);
     wsum = __fma_rn(Y[k], cT.Winv[k], wsum);
   }
-  const double e = internal_energy(U[4 * n + c], ri, u);
+  const double e = internal_energy(uc[4 * fs], ri, u);
   const double T = temperature(Y, e);
   const double p = __dmul_rn(__dmul_rn(__dmul_rn(rho, SMC_RU), T), wsum);
   const double s = pow(T / SMC_T_REF, SMC_TRANSPORT_EXP);
@@ -149,6 +170,7 @@ __global__ void __launch_bounds__(256, 3) prim_kernel(const double* __restrict__
   const double xi = SMC_XI_OVER_ETA * eta;
   for (int i = 0; i < 3; ++i) F[(F_U + i) * n + c] = u[i];
   F[F_T * n + c] = T;
+  F[F_RHO * n + c] = rho;
   F[F_P * n + c] = p;
   F[F_ETA * n + c] = eta;
   F[F_LAM * n + c] = lam;
@@ -254,18 +276,18 @@ __device__ __forceinline__ void chem_cell(const double* Uc, double* o) {
   for (int s = 0; s < NSP; ++s) o[5 + s] = w[s];
 }
 
-__global__ void __launch_bounds__(256) chem_kernel(const double* __restrict__ U,
-                                                   double* __restrict__ out, Geo g) {
+__global__ void __launch_bounds__(256) chem_kernel(const UV U, double* __restrict__ out,
+                                                   long long out_fs, Geo g) {
   const long long n = g.plane * g.nz;
   const long long c = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
   if (c >= n) return;
-  const long long cg = c + g.G * g.plane;
+  const double* uc = U.p1 + c;  // interior block
   double Uc[NV], o[NV];
 #pragma unroll
-  for (int v = 0; v < NV; ++v) Uc[v] = U[v * g.flen + cg];
+  for (int v = 0; v < NV; ++v) Uc[v] = uc[v * U.fs1];
   chem_cell(Uc, o);
 #pragma unroll
-  for (int v = 0; v < NV; ++v) out[v * n + c] = o[v];
+  for (int v = 0; v < NV; ++v) out[v * out_fs + c] = o[v];
 }
 
 // The chemistry part's FD Jacobian, one cell per thread: column j from the
@@ -378,9 +400,13 @@ void set_smem(K kern, std::size_t bytes) {
                                 static_cast<int>(bytes)));
 }
 
+// The direction-split evaluation; `phase` selects the part that needs no
+// ghost plane (kNsInterior: ctoprim and the x / y passes on the interior
+// planes), the rest (kNsBoundary) or both (kNsAll).
 template <int S>
-void rhs_v2(const Geo& g, const double* U, const double* F, double* A, double* GR, double* MX,
-            double* SC, double* out, const StencilM& M, int chem, cudaStream_t st) {
+void rhs_v2(const Geo& g, const UV& U, const double* F, double* A, double* GR, double* MX,
+            double* SC, double* out, long long ofs, const StencilM& M, int chem, int phase,
+            cudaStream_t st) {
   static bool configured = false;
   const std::size_t sm = sizeof(DirSmem);
   if (!configured) {
@@ -397,11 +423,26 @@ void rhs_v2(const Geo& g, const double* U, const double* F, double* A, double* G
   double* hy1 = SC + 13 * n;
   double* na2 = SC + 27 * n;
   double* hy2 = SC + 40 * n;
-  ns_phase_a<0, S><<<dir_grid<0, NR_A>(g, allp), Tile<0, NR_A>::THREADS, sm, st>>>(U, F, A, A, GR, out, g, M, -g.G);
-  SMC_CHECK_LAUNCH();
-  ns_phase_a<1, S><<<dir_grid<1, NR_A>(g, allp), Tile<0, NR_A>::THREADS, sm, st>>>(U, F, na1, A, GR, hy1, g, M, -g.G);
-  SMC_CHECK_LAUNCH();
-  ns_phase_a<2, S><<<dir_grid<2, NR_A>(g, allp), Tile<0, NR_A>::THREADS, sm, st>>>(U, F, na2, A, GR, hy2, g, M, 0);
+  constexpr int NT = Tile<0, NR_A>::THREADS;
+  // ctoprim + the x / y passes over planes [k0, k0 + np)
+  auto planes = [&](int k0, int np) {
+    if (np <= 0) return;
+    prim_kernel<<<blocks(np * g.plane), 256, 0, st>>>(U, const_cast<double*>(F), g, k0, k0 + np);
+    SMC_CHECK_LAUNCH();
+    dim3 g0 = dir_grid<0, NR_A>(g, np), g1 = dir_grid<1, NR_A>(g, np);
+    ns_phase_a<0, S><<<g0, NT, sm, st>>>(F, A, A, GR, out, ofs, g, M, k0);
+    SMC_CHECK_LAUNCH();
+    ns_phase_a<1, S><<<g1, NT, sm, st>>>(F, na1, A, GR, hy1, n, g, M, k0);
+    SMC_CHECK_LAUNCH();
+  };
+  if (phase == kNsAll) planes(-g.G, allp);
+  if (phase == kNsInterior) planes(0, g.nz);
+  if (phase == kNsInterior) return;
+  if (phase == kNsBoundary) {
+    planes(-g.G, g.G);
+    planes(g.nz, g.G);
+  }
+  ns_phase_a<2, S><<<dir_grid<2, NR_A>(g, allp), NT, sm, st>>>(F, na2, A, GR, hy2, n, g, M, 0);
   SMC_CHECK_LAUNCH();
   ns_mixed_fields<<<blocks(g.plane * allp), 256, 0, st>>>(F, GR, A, MX, g);
   SMC_CHECK_LAUNCH();
@@ -411,7 +452,7 @@ void rhs_v2(const Geo& g, const double* U, const double* F, double* A, double* G
   SMC_CHECK_LAUNCH();
   ns_phase_b<2><<<dir_grid<2>(g, g.nz), DT_THREADS, sizeof(PBSmem), st>>>(MX, SC + 80 * n, g);
   SMC_CHECK_LAUNCH();
-  ns_assemble2<<<blocks(n), 256, 0, st>>>(F, A, SC, U, out, g, chem);
+  ns_assemble2<<<blocks(n), 256, 0, st>>>(F, A, SC, out, ofs, g, chem);
   SMC_CHECK_LAUNCH();
 }
 
@@ -444,27 +485,54 @@ static Geo make_geo(const NsBox& b, const double* d) {
   return g;
 }
 
+static UV make_uv(const NsStateView& v, const NsBox& b) {
+  UV u;
+  const long long plane = b.plane(), n = b.cells();
+  u.p1 = v.mid, u.fs1 = v.mid_fs;
+  if (b.G == 0) {
+    u.p0 = u.p2 = v.mid, u.fs0 = u.fs2 = v.mid_fs;
+  } else {
+    // rebase each block so that p + (plane-0 relative offset) addresses it
+    u.p0 = v.lo + b.G * plane, u.fs0 = v.lo_fs;
+    u.p2 = v.hi - n, u.fs2 = v.hi_fs;
+  }
+  u.lim1 = n;
+  return u;
+}
+
 void NsWorkspace::rhs(const double* U, double* out, int part, cudaStream_t st) {
+  rhs(NsStateView::ghosted(U, box_), out, box_.cells(), part, st, kNsAll);
+}
+
+void NsWorkspace::rhs(const NsStateView& U, double* out, long long out_fs, int part,
+                      cudaStream_t st, int phase) {
   // the direction kernels stage U with 16-byte copies and write out with
   // 16-byte stores (x-contiguous cell pairs)
-  require(reinterpret_cast<std::uintptr_t>(U) % 16 == 0 &&
-              reinterpret_cast<std::uintptr_t>(out) % 16 == 0,
+  auto al16 = [](const void* p) { return reinterpret_cast<std::uintptr_t>(p) % 16 == 0; };
+  const bool ghosts = box_.G > 0;
+  require(U.mid && (!ghosts || (U.lo && U.hi)), "ns rhs: missing state block");
+  require(al16(U.mid) && al16(out) && (!ghosts || (al16(U.lo) && al16(U.hi))) &&
+              U.mid_fs % 2 == 0 && (!ghosts || (U.lo_fs % 2 == 0 && U.hi_fs % 2 == 0)) &&
+              out_fs % 2 == 0,
           "ns rhs: U and out must be 16-byte aligned device arrays");
+  require(out_fs >= box_.cells() && U.mid_fs >= box_.cells(), "ns rhs: field stride too small");
   const Geo g = make_geo(box_, dx_);
+  const UV uv = make_uv(U, box_);
   const long long n = box_.cells();
-  double* F = prim_.get();
-  double* A = acc_.get();
   if (part == kNsChem) {
-    chem_kernel<<<blocks(n), 256, 0, st>>>(U, out, g);
+    if (phase == kNsBoundary) return;  // pointwise: all of it is interior work
+    chem_kernel<<<blocks(n), 256, 0, st>>>(uv, out, out_fs, g);
     SMC_CHECK_LAUNCH();
     return;
   }
-  prim_kernel<<<blocks(g.flen), 256, 0, st>>>(U, F, g);
-  SMC_CHECK_LAUNCH();
+  double* F = prim_.get();
+  double* A = acc_.get();
   if (s_ == 4)
-    rhs_v2<4>(g, U, F, A, grad_.get(), mixed_.get(), scratch_.get(), out, M_, part == kNsFull, st);
+    rhs_v2<4>(g, uv, F, A, grad_.get(), mixed_.get(), scratch_.get(), out, out_fs, M_,
+              part == kNsFull, phase, st);
   else
-    rhs_v2<3>(g, U, F, A, grad_.get(), mixed_.get(), scratch_.get(), out, M_, part == kNsFull, st);
+    rhs_v2<3>(g, uv, F, A, grad_.get(), mixed_.get(), scratch_.get(), out, out_fs, M_,
+              part == kNsFull, phase, st);
 }
 
 bool NsWorkspace::chem_fd_jacobian(const double* U, const double* FU, double* jac, double atol,
@@ -479,7 +547,8 @@ bool NsWorkspace::chem_fd_jacobian(const double* U, const double* FU, double* ja
 
 void NsWorkspace::temperature_pressure(const double* U, double* T, double* p, cudaStream_t st) {
   const Geo g = make_geo(box_, dx_);
-  prim_kernel<<<blocks(g.flen), 256, 0, st>>>(U, prim_.get(), g);
+  prim_kernel<<<blocks(g.flen), 256, 0, st>>>(make_uv(NsStateView::ghosted(U, box_), box_),
+                                              prim_.get(), g, -g.G, g.nz + g.G);
   SMC_CHECK_LAUNCH();
   tp_kernel<<<blocks(box_.cells()), 256, 0, st>>>(prim_.get(), T, p, g);
   SMC_CHECK_LAUNCH();

@@ -23,6 +23,34 @@ struct NsBox {
 
 enum NsPart : int { kNsFull = 0, kNsAdvDiff = 1, kNsChem = 2 };
 
+// Where the conserved state of a box with G ghost planes lives: planes
+// [-G, 0) (lower halo), [0, nz) (interior) and [nz, nz + G) (upper halo) are
+// three field-major blocks, each with its own base pointer (its first plane)
+// and field stride.  They may be one ghosted array (field stride
+// field_len()), an interior array plus two separate halo buffers (a rank's
+// state and the planes received from its neighbours: no ghost copy of the
+// state), or three windows of one larger array (z-chunks of a box).  The
+// periodic box (G = 0) uses the interior block only and wraps z.
+struct NsStateView {
+  const double* lo = nullptr;
+  long long lo_fs = 0;
+  const double* mid = nullptr;
+  long long mid_fs = 0;
+  const double* hi = nullptr;
+  long long hi_fs = 0;
+  // one contiguous array of nz + 2G planes per field
+  static NsStateView ghosted(const double* U, const NsBox& b) {
+    const long long fl = b.field_len();
+    return {U, fl, U + b.G * b.plane(), fl, U + (b.G + b.nz) * b.plane(), fl};
+  }
+};
+
+// Plane range of the RHS evaluation (for the overlap of a halo exchange
+// with the interior work).  kAll: the whole evaluation; kInterior: the work
+// that needs no ghost plane (ctoprim and the x / y direction passes of the
+// interior planes); kBoundary: the rest, after the ghosts have arrived.
+enum NsPhase : int { kNsAll = 0, kNsInterior = 1, kNsBoundary = 2 };
+
 // Device workspace shared by the three RHS views (full / f1 / f2).
 class NsWorkspace {
  public:
@@ -31,6 +59,10 @@ class NsWorkspace {
   // SMC_NVAR fields of box.field_len() each (ghosts filled by the caller
   // when box.G > 0).
   void rhs(const double* U, double* out, int part, cudaStream_t st);
+  // The general form: U through a state view, out with field stride out_fs
+  // (>= cells()), optionally one phase of the evaluation.
+  void rhs(const NsStateView& U, double* out, long long out_fs, int part, cudaStream_t st,
+           int phase = kNsAll);
   // Fused FD Jacobian of the chemistry part (RhsOp::fd_block_jacobian) for
   // the cell-block layout (block SMC_NVAR, field-major); false when the box
   // has ghost planes (the state is then not cell-block shaped).

@@ -109,7 +109,9 @@ def test_configs2_sdc_ten_steps_128(cuda, golden):
             oracle_threads=threads, oracle_s=t_oracle)
     assert d.sweeps == sw.value and d.fresh_evals == fe.value == 81
     assert max(errs) <= 1e-9, errs
-    np.testing.assert_allclose(d.residual_history, res[: sw.value], rtol=1e-5, atol=1e-300)
+    # the residual is a max-norm of a difference of nearly equal states (~1e-11
+    # of the field): its low digits are rounding, so only 1e-3 relative
+    np.testing.assert_allclose(d.residual_history, res[: sw.value], rtol=1e-3, atol=1e-300)
 
 
 def test_configs4_mrsdc_mode1_128(cuda, golden):
