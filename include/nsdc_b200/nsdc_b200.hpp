@@ -392,6 +392,77 @@ class NsOperator {
   detail::RhsHandle full_, adv_, chem_;
 };
 
+// ------------------------------------------------ multi-GPU (z-slab) NS
+// One rank of an NCCL communicator (smc_comm_*): the unique id is created on
+// one rank (unique_id()) and shared by the host program (MPI, a file, a
+// socket), then every rank constructs Communicator(id, size, rank) on its
+// own GPU.  A C++ host replaces the reference's single-process
+// parallel_for (parallel.cpp:20-36) by one process per GPU.
+class Communicator {
+ public:
+  static std::string unique_id() {
+    std::string id(128, '\0');
+    detail::check(smc_comm_unique_id(id.data()));
+    return id;
+  }
+  Communicator(const std::string& id, int size, int rank) {
+    if (id.size() != 128) throw std::invalid_argument("Communicator: the id holds 128 bytes");
+    smc_comm* c = nullptr;
+    detail::check(smc_comm_init(id.data(), size, rank, &c));
+    c_.reset(c);
+  }
+  int rank() const {
+    int r = 0, s = 0;
+    detail::check(smc_comm_rank(c_.get(), &r, &s));
+    return r;
+  }
+  int size() const {
+    int r = 0, s = 0;
+    detail::check(smc_comm_rank(c_.get(), &r, &s));
+    return s;
+  }
+  double allreduce_max(double v) {
+    detail::check(smc_comm_allreduce_max(c_.get(), &v));
+    return v;
+  }
+  smc_comm* handle() const { return c_.get(); }
+
+ private:
+  struct Del {
+    void operator()(smc_comm* c) const { smc_comm_destroy(c); }
+  };
+  std::unique_ptr<smc_comm, Del> c_;
+};
+
+// This rank's z-slab (nz planes) of the periodic nx x ny x (nz * size) NS
+// box: the same Rhs / SplitRHS views as NsOperator over the rank's interior
+// state; the 4-plane halo is exchanged inside every evaluation.
+class NsSlabOperator {
+ public:
+  NsSlabOperator(Communicator& comm, int nx, int ny, int nz, double dx,
+                 const StencilChoice& c = StencilChoice::narrow8(kSmcM47, kSmcM48)) {
+    smc_rhs *f = nullptr, *a = nullptr, *ch = nullptr;
+    const int order = c.kind == StencilChoice::Kind::Narrow6 ? 6 : 8;
+    detail::check(smc_ns_slab_create(comm.handle(), nx, ny, nz, dx, dx, dx, order,
+                                     c.params.data(), order == 8 ? 2 : 1, &f, &a, &ch));
+    full_.reset(f), adv_.reset(a), chem_.reset(ch);
+  }
+  Rhs as_rhs() const { return wrap(full_.get()); }
+  SplitRHS as_split() const { return SplitRHS{wrap(adv_.get()), wrap(chem_.get())}; }
+  smc_rhs* full() const { return full_.get(); }
+  smc_rhs* advdiff() const { return adv_.get(); }
+  smc_rhs* chem() const { return chem_.get(); }
+
+ private:
+  static Rhs wrap(smc_rhs* h) {
+    return [h](double t, const Field& u, Field& out) {
+      out.resize(u.size());
+      detail::check(smc_rhs_eval(h, t, u.data(), out.data(), SMC_HOST));
+    };
+  }
+  detail::RhsHandle full_, adv_, chem_;
+};
+
 // ----------------------------------------------------------------- sdc.hpp
 struct StepControls {
   int num_iterations = 4;
@@ -517,6 +588,8 @@ class SdcStepper {
     return {std::move(u), {db.history(), db.d.sweeps, db.d.fresh_evals, db.d.early_stop != 0}};
   }
   const NodeSet& nodes() const { return nodes_; }
+  // residual reduced over the ranks of a slab decomposition
+  void set_communicator(const Communicator& c) { detail::check(smc_sdc_set_comm(s_.get(), c.handle())); }
 
  private:
   NodeSet nodes_;
@@ -576,6 +649,10 @@ class MrsdcStepper {
     Field u, f1_end, f2_end;
     MrsdcDiagnostics diag;
   };
+  // residual and implicit-solver norms reduced over a slab decomposition
+  void set_communicator(const Communicator& c) {
+    detail::check(smc_mrsdc_set_comm(m_.get(), c.handle()));
+  }
   Result step_mode1(smc_rhs* f1, smc_rhs* f2, const Field& u0, double t_n, double dt,
                     const Field* f01 = nullptr, const Field* f02 = nullptr) {
     return step(smc_mrsdc_step_mode1, f1, f2, u0, t_n, dt, f01, f02);

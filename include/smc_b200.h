@@ -50,6 +50,7 @@ extern "C" {
 typedef struct smc_rhs smc_rhs;     /* a right-hand side f(t, u) on the device */
 typedef struct smc_sdc smc_sdc;     /* device-resident single-rate SDC stepper */
 typedef struct smc_mrsdc smc_mrsdc; /* device-resident multirate SDC stepper */
+typedef struct smc_comm smc_comm;   /* one rank of a z-slab decomposition (NCCL or local) */
 
 typedef void (*smc_rhs_fn)(double t, const double* u, double* out, long long n, void* ctx);
 typedef double (*smc_time_fn)(double t, void* ctx);
@@ -202,6 +203,45 @@ int smc_ns_temperature_pressure(smc_rhs* ns, const double* U, double* T, double*
 /* Conserved state from T, p, velocity (3 fields), Y (9 fields); n cells. */
 int smc_ns_conserved(const double* T, const double* p, const double* uvw, const double* Y,
                      long long n, double* U, int where);
+
+/* ---- multi-GPU: z-slab decomposition of the NS box ----
+ * The reference is single-process (parallel_for over rows, parallel.cpp:20-36);
+ * the paper decomposes the box into boxes with 4 ghost cells and recomputes
+ * the coefficients on the ghosts.  A rank owns
+ * nz interior planes of an nx x ny x (nz * size) periodic box; its RHS is an
+ * smc_rhs of dim 14 nx ny nz that the device steppers advance unchanged (the
+ * drop-in nsdc::Rhs contract, field.hpp:14-16), exchanging 4 ghost planes
+ * of the conserved state with its two neighbours per evaluation (NCCL
+ * send/recv on a communication stream, overlapped with ctoprim and the x / y
+ * passes of the interior planes).  Results are bitwise independent of the
+ * number of ranks. */
+/* NCCL unique id (128 bytes) for smc_comm_init; created on one rank and
+ * shared with the others by the caller.  SMC_ECUDA if libnccl is absent. */
+int smc_comm_unique_id(char* id128);
+/* This process's rank of an NCCL communicator of nranks on the current device. */
+int smc_comm_init(const char* id128, int nranks, int rank, smc_comm** out);
+/* nranks ranks of one in-process group on the current device (device copies
+ * instead of NCCL): out[0..nranks).  For testing several slabs on one GPU;
+ * each rank's state must be published (smc_ns_slab_publish) before a
+ * neighbour evaluates. */
+int smc_comm_init_local(int nranks, smc_comm** out);
+int smc_comm_rank(const smc_comm* c, int* rank, int* size);
+/* *v = max over ranks of *v (synchronous). */
+int smc_comm_allreduce_max(smc_comm* c, double* v);
+int smc_comm_destroy(smc_comm* c);
+/* This rank's slab RHS views (full / advection-diffusion / chemistry, as
+ * smc_ns_create) of the nx x ny x (nz * size) periodic box. */
+int smc_ns_slab_create(smc_comm* c, int nx, int ny, int nz, double dx, double dy, double dz,
+                       int order, const double* params, int nparams, smc_rhs** full,
+                       smc_rhs** advdiff, smc_rhs** chem);
+/* In-process groups: the device state u the neighbours read in their next
+ * evaluation (an evaluation publishes its own input too).  No-op for NCCL. */
+int smc_ns_slab_publish(smc_rhs* slab, const double* u);
+/* The steppers' residual max-norm (sdc.cpp:20-30, mrsdc.cpp:23-35) and the
+ * implicit solver's norms reduced over the communicator's ranks, so every
+ * rank takes the same sweeps and Newton steps. */
+int smc_sdc_set_comm(smc_sdc* s, smc_comm* c);
+int smc_mrsdc_set_comm(smc_mrsdc* m, smc_comm* c);
 
 /* Any host callback as an operator (nsdc::Rhs, core/include/nsdc/field.hpp:14-16). */
 int smc_rhs_from_callback(long long dim, smc_rhs_fn f, void* ctx, smc_rhs** out);

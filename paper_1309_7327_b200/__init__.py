@@ -440,6 +440,11 @@ class SdcStepper:
         self._keep.append(cb)
         check(_capi.lib().smc_sdc_set_reducer(self._h, cb, None))
 
+    def set_comm(self, comm) -> None:
+        """Reduce the residual over a distributed.Comm's ranks (in the library)."""
+        self._keep.append(comm)
+        check(_capi.lib().smc_sdc_set_comm(self._h, comm.handle))
+
     def step(self, f: _Rhs, u0, t_n: float, dt: float, f0=None):
         u = _out_like(u0)
         fe = _out_like(u0)
@@ -491,6 +496,12 @@ class MrsdcStepper:
         cb = _reducer(fn)
         self._keep.append(cb)
         check(_capi.lib().smc_mrsdc_set_reducer(self._h, cb, None))
+
+    def set_comm(self, comm) -> None:
+        """Reduce the residual and the implicit solver's norms over a
+        distributed.Comm's ranks (in the library)."""
+        self._keep.append(comm)
+        check(_capi.lib().smc_mrsdc_set_comm(self._h, comm.handle))
 
     def step_mode1(self, f1: _Rhs, f2: _Rhs, u0, t_n, dt, f0_1=None, f0_2=None):
         u, e1, e2 = _out_like(u0), _out_like(u0), _out_like(u0)

@@ -133,6 +133,18 @@ _SIG = {
     "smc_integrate_stiff": (C.c_int, [_VP, _VP, C.c_double, C.c_double, _VP, C.c_int,
                                       C.POINTER(Stiff), _I, _I]),
     "smc_mrsdc_set_reducer": (C.c_int, [_VP, REDUCE_FN, _VP]),
+    "smc_comm_unique_id": (C.c_int, [C.c_char_p]),
+    "smc_comm_init": (C.c_int, [C.c_char_p, C.c_int, C.c_int, C.POINTER(_VP)]),
+    "smc_comm_init_local": (C.c_int, [C.c_int, C.POINTER(_VP)]),
+    "smc_comm_rank": (C.c_int, [_VP, _I, _I]),
+    "smc_comm_allreduce_max": (C.c_int, [_VP, _D]),
+    "smc_comm_destroy": (C.c_int, [_VP]),
+    "smc_ns_slab_create": (C.c_int, [_VP, C.c_int, C.c_int, C.c_int, C.c_double, C.c_double,
+                                     C.c_double, C.c_int, _D, C.c_int, C.POINTER(_VP),
+                                     C.POINTER(_VP), C.POINTER(_VP)]),
+    "smc_ns_slab_publish": (C.c_int, [_VP, _VP]),
+    "smc_sdc_set_comm": (C.c_int, [_VP, _VP]),
+    "smc_mrsdc_set_comm": (C.c_int, [_VP, _VP]),
     "smc_mrsdc_destroy": (C.c_int, [_VP]),
 }
 

@@ -5,6 +5,7 @@
 #include <vector>
 
 #include "../../include/smc_b200.h"
+#include "dist.hpp"
 #include "narrow.cuh"
 #include "ns.cuh"
 #include "ops.hpp"
@@ -13,6 +14,9 @@
 
 struct smc_rhs {
   std::unique_ptr<smc::RhsOp> op;
+};
+struct smc_comm {
+  std::shared_ptr<smc::HaloTransport> t;
 };
 struct smc_sdc {
   std::unique_ptr<smc::DeviceSdc> s;
@@ -361,6 +365,84 @@ int smc_ns_create(int nx, int ny, int nz, int zghost, double dx, double dy, doub
   });
 }
 
+int smc_comm_unique_id(char* id128) {
+  return guarded([&] {
+    need(id128, "id");
+    smc::nccl_unique_id(id128);
+  });
+}
+
+int smc_comm_init(const char* id128, int nranks, int rank, smc_comm** out) {
+  return guarded([&] {
+    need(id128, "id"), need(out, "out");
+    *out = nullptr;
+    auto c = std::make_unique<smc_comm>();
+    c->t = smc::make_nccl_transport(id128, nranks, rank);
+    *out = c.release();
+  });
+}
+
+int smc_comm_init_local(int nranks, smc_comm** out) {
+  return guarded([&] {
+    need(out, "out");
+    auto group = smc::make_local_group(nranks);
+    for (int r = 0; r < nranks; ++r) {
+      auto c = std::make_unique<smc_comm>();
+      c->t = group[r];
+      out[r] = c.release();
+    }
+  });
+}
+
+int smc_comm_rank(const smc_comm* c, int* rank, int* size) {
+  return guarded([&] {
+    need(c, "comm"), need(rank, "rank"), need(size, "size");
+    *rank = c->t->rank();
+    *size = c->t->size();
+  });
+}
+
+int smc_comm_allreduce_max(smc_comm* c, double* v) {
+  return guarded([&] {
+    need(c, "comm"), need(v, "v");
+    *v = c->t->allreduce_max(*v, nullptr);
+  });
+}
+
+int smc_comm_destroy(smc_comm* c) {
+  delete c;
+  return SMC_OK;
+}
+
+int smc_ns_slab_create(smc_comm* c, int nx, int ny, int nz, double dx, double dy, double dz,
+                       int order, const double* params, int nparams, smc_rhs** full,
+                       smc_rhs** advdiff, smc_rhs** chem) {
+  return guarded([&] {
+    need(c, "comm"), need(params, "params");
+    int s = 0;
+    smc::StencilM M = smc::make_stencil(order, params, nparams, &s);
+    smc::NsBox box;
+    box.nx = nx, box.ny = ny, box.nz = nz, box.G = 4;
+    auto ws = std::make_shared<smc::NsWorkspace>(box, dx, dy, dz, M, s);
+    smc_rhs** outs[3] = {full, advdiff, chem};
+    for (int part = 0; part < 3; ++part) {
+      if (!outs[part]) continue;
+      auto h = std::make_unique<smc_rhs>();
+      h->op = std::make_unique<smc::NsSlabOp>(c->t, ws, part);
+      *outs[part] = h.release();
+    }
+  });
+}
+
+int smc_ns_slab_publish(smc_rhs* h, const double* u) {
+  return guarded([&] {
+    need(u, "u");
+    auto* op = dynamic_cast<smc::NsSlabOp*>(&op_of(h));
+    if (!op) throw smc::InvalidArgument("not an NS slab operator");
+    op->publish(u);
+  });
+}
+
 static smc::NsRhsOp& ns_of(smc_rhs* h) {
   auto* op = dynamic_cast<smc::NsRhsOp*>(&op_of(h));
   if (!op) throw smc::InvalidArgument("not an NS operator");
@@ -512,6 +594,22 @@ int smc_mrsdc_create(int coarse_family, int coarse_nodes, int inner_family, int 
                              smc::make_nodes(inner_family, inner_nodes), repeats),
         iterations, cutoff, reuse_first != 0);
     *out = m.release();
+  });
+}
+
+int smc_sdc_set_comm(smc_sdc* s, smc_comm* c) {
+  return guarded([&] {
+    need(s, "sdc handle"), need(c, "comm");
+    std::shared_ptr<smc::HaloTransport> t = c->t;
+    s->s->set_reducer([t](double v) { return t->allreduce_max(v, nullptr); });
+  });
+}
+
+int smc_mrsdc_set_comm(smc_mrsdc* m, smc_comm* c) {
+  return guarded([&] {
+    need(m, "mrsdc handle"), need(c, "comm");
+    std::shared_ptr<smc::HaloTransport> t = c->t;
+    m->m->set_reducer([t](double v) { return t->allreduce_max(v, nullptr); });
   });
 }
 

@@ -1,6 +1,17 @@
 """Block decomposition of the periodic box into z-slabs, one per GPU, with a
-4-plane halo exchanged over NCCL (torch.distributed send/recv over NVLink /
-NVSwitch), optionally overlapped with the interior compute.
+4-plane halo exchanged over NCCL, overlapped with the interior compute
+(SURVEY.md §8(e)).
+
+The reacting-NS slab RHS lives in the library (csrc/dist.cu): `Comm` is one
+rank of an NCCL communicator (unique id shared over torch.distributed) or of
+an in-process group on one device, `NsSlab` this rank's RHS views.  The
+exchange runs on the library's communication stream while ctoprim and the
+x / y passes work on the interior planes; the kernels read the two halo
+blocks in place, so the state is never copied into a ghosted array.  The
+torch.distributed classes below (narrow operator slabs, the peer halo, and
+DistributedNs, the NS RHS as a device callback with a Python-side exchange)
+are the earlier host-orchestrated paths, kept for the narrow operator and as
+the gloo-tested statement of the message order the library follows.
 
 Why z-slabs: with 256^3 cells per GPU a slab has 2 halo faces (vs 6 for a 3-D
 block), the ghost planes are contiguous in memory (no pack/unpack kernels:
@@ -316,3 +327,109 @@ class PeerNarrow3D:
         for p in self._raw:
             _capi.lib().smc_device_free(C.c_void_p(p))
         self._raw = []
+
+
+# ------------------------------------------------- library slab NS RHS
+class Comm:
+    """One rank of a z-slab decomposition, owned by the library (smc_comm)."""
+
+    def __init__(self, handle):
+        self._h = handle
+
+    @property
+    def handle(self):
+        return self._h
+
+    @staticmethod
+    def nccl(dist=None, device=None) -> "Comm":
+        """NCCL communicator over the torch.distributed world (one rank per
+        GPU, current device); rank 0 creates the unique id and broadcasts it."""
+        import ctypes as C
+        from . import _capi, check
+        world = dist.get_world_size() if dist is not None and dist.is_initialized() else 1
+        rank = dist.get_rank() if world > 1 else 0
+        uid = [None]
+        if rank == 0:
+            buf = C.create_string_buffer(128)
+            check(_capi.lib().smc_comm_unique_id(buf))
+            uid[0] = buf.raw
+        if world > 1:
+            dist.broadcast_object_list(uid, src=0, device=device)
+        h = C.c_void_p()
+        check(_capi.lib().smc_comm_init(uid[0], world, rank, C.byref(h)))
+        return Comm(h)
+
+    @staticmethod
+    def local_group(n: int) -> list:
+        """n ranks of one in-process group on the current device."""
+        import ctypes as C
+        from . import _capi, check
+        hs = (C.c_void_p * n)()
+        check(_capi.lib().smc_comm_init_local(n, hs))
+        return [Comm(C.c_void_p(h)) for h in hs]
+
+    @property
+    def rank(self) -> int:
+        import ctypes as C
+        from . import _capi, check
+        r, s = C.c_int(), C.c_int()
+        check(_capi.lib().smc_comm_rank(self._h, C.byref(r), C.byref(s)))
+        return r.value
+
+    @property
+    def size(self) -> int:
+        import ctypes as C
+        from . import _capi, check
+        r, s = C.c_int(), C.c_int()
+        check(_capi.lib().smc_comm_rank(self._h, C.byref(r), C.byref(s)))
+        return s.value
+
+    def allreduce_max(self, v: float) -> float:
+        import ctypes as C
+        from . import _capi, check
+        d = C.c_double(v)
+        check(_capi.lib().smc_comm_allreduce_max(self._h, C.byref(d)))
+        return d.value
+
+    def close(self) -> None:
+        if self._h:
+            from . import _capi
+            _capi.lib().smc_comm_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+class NsSlab:
+    """This rank's z-slab (nz planes) of the periodic nx x ny x (nz * size)
+    NS box: .full, .advdiff (MRSDC f1), .chem (f2) are Rhs views of dim
+    14 nx ny nz over the rank's interior state (device tensors)."""
+
+    def __init__(self, comm: Comm, nx: int, ny: int, nz: int, dx: float, dy=None, dz=None,
+                 choice=None):
+        import ctypes as C
+        from . import _Rhs, StencilChoice, _capi, _params, check
+        choice = choice or StencilChoice()
+        dy = dy or dx
+        dz = dz or dx
+        self.comm = comm
+        self.shape = (nz, ny, nx)
+        hs = [C.c_void_p() for _ in range(3)]
+        pp, keep = _params(choice.params)
+        check(_capi.lib().smc_ns_slab_create(comm.handle, nx, ny, nz, dx, dy, dz, choice.order,
+                                             pp, len(choice.params), C.byref(hs[0]),
+                                             C.byref(hs[1]), C.byref(hs[2])))
+        self.full, self.advdiff, self.chem = (_Rhs(h) for h in hs)
+
+    def set_stream(self, stream) -> None:
+        for r in (self.full, self.advdiff, self.chem):
+            r.set_stream(stream)
+
+    def publish(self, u) -> None:
+        """In-process groups: the state the neighbours read next (device)."""
+        from . import _capi, check, dptr
+        check(_capi.lib().smc_ns_slab_publish(self.full.handle, dptr(u)))
