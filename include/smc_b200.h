@@ -117,6 +117,10 @@ int smc_measure_fp64_peak(int iters, double* tflops);
 /* FP64 tensor path (mma.sync m8n8k4 f64) throughput; mode 1 mixes DMMA and
  * DFMA warps.  Diagnostic only. */
 int smc_measure_dmma_peak(int iters, int mode, double* tflops);
+/* TFLOP/s of up to n DFMA probe variants (chains per thread, operand
+ * placement, warps per SM): the best of them and of the DMMA probe is the
+ * FP64 roofline denominator (bench.py reports them all). */
+int smc_measure_fp64_variants(int iters, double* tflops, int n);
 
 /* ------------------------------------------------------------- stencil */
 /* nsdc::build_narrow — core/src/stencil.cpp:117-132.  m64: 8x8 row-major. */
@@ -198,6 +202,11 @@ int smc_ns_create(int nx, int ny, int nz, int zghost, double dx, double dy, doub
                   smc_rhs** chem);
 /* Slab mode: out (interior) = RHS of U (SMC_NVAR ghosted fields), device. */
 int smc_ns_rhs_ghosted(smc_rhs* ns, const double* U, double* out);
+/* One evaluation of a periodic NS view on device buffers with an event after
+ * every kernel: ms[i] / names[i] (static strings) of the first cap kernels in
+ * launch order, *count = kernels launched.  For bench.py's per-kernel table. */
+int smc_ns_profile(smc_rhs* ns, const double* U, double* out, double* ms, const char** names,
+                   int cap, int* count);
 /* ctoprim: temperature and pressure of every interior cell. */
 int smc_ns_temperature_pressure(smc_rhs* ns, const double* U, double* T, double* p, int where);
 /* Conserved state from T, p, velocity (3 fields), Y (9 fields); n cells. */

@@ -618,6 +618,17 @@ class NsOperator:
         h = (self.full, self.advdiff, self.chem)[part].handle
         check(_capi.lib().smc_ns_rhs_ghosted(h, dptr(U), dptr(out)))
 
+    def profile(self, U, out, part: int = NS_FULL):
+        """One evaluation on device tensors with an event after every kernel:
+        [(kernel, ms)] in launch order."""
+        h = (self.full, self.advdiff, self.chem)[part].handle
+        cap = 64
+        ms = (C.c_double * cap)()
+        names = (C.c_char_p * cap)()
+        cnt = C.c_int()
+        check(_capi.lib().smc_ns_profile(h, dptr(U), dptr(out), ms, names, cap, C.byref(cnt)))
+        return [(names[i].decode(), ms[i]) for i in range(min(cnt.value, cap))]
+
     def temperature_pressure(self, U):
         nz, ny, nx = self.shape
         if hasattr(U, "is_cuda"):

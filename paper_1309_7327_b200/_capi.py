@@ -71,6 +71,7 @@ _SIG = {
     "smc_synchronize": (C.c_int, []),
     "smc_measure_fp64_peak": (C.c_int, [C.c_int, _D]),
     "smc_measure_dmma_peak": (C.c_int, [C.c_int, C.c_int, _D]),
+    "smc_measure_fp64_variants": (C.c_int, [C.c_int, _D, C.c_int]),
     "smc_build_narrow": (C.c_int, [C.c_int, _D, C.c_int, _D, _I]),
     "smc_apply_narrow": (C.c_int, [C.c_int, _D, C.c_int, _VP, _VP, C.c_int, C.c_double, _VP,
                                    C.c_int]),
@@ -98,6 +99,7 @@ _SIG = {
                                 C.POINTER(_VP)]),
     "smc_ns_rhs_ghosted": (C.c_int, [_VP, _VP, _VP]),
     "smc_ns_temperature_pressure": (C.c_int, [_VP, _VP, _VP, _VP, C.c_int]),
+    "smc_ns_profile": (C.c_int, [_VP, _VP, _VP, _D, C.POINTER(C.c_char_p), C.c_int, _I]),
     "smc_ns_conserved": (C.c_int, [_VP, _VP, _VP, _VP, C.c_longlong, _VP, C.c_int]),
     "smc_rhs_from_callback": (C.c_int, [C.c_longlong, RHS_FN, _VP, C.POINTER(_VP)]),
     "smc_rhs_from_device_callback": (C.c_int, [C.c_longlong, DEV_RHS_FN, _VP, C.POINTER(_VP)]),

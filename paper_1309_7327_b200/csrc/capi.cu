@@ -457,6 +457,36 @@ int smc_ns_rhs_ghosted(smc_rhs* h, const double* U, double* out) {
   });
 }
 
+int smc_ns_profile(smc_rhs* h, const double* U, double* out, double* ms, const char** names,
+                   int cap, int* count) {
+  return guarded([&] {
+    need(U, "U"), need(out, "out"), need(count, "count");
+    smc::NsRhsOp& op = ns_of(h);
+    cudaStream_t st = op.stream();
+    smc::KernelMarks marks;
+    SMC_CUDA(cudaEventCreate(&marks.start));
+    SMC_CUDA(cudaEventRecord(marks.start, st));
+    op.workspace().set_marks(&marks);
+    try {
+      op.eval_device(0.0, U, out);
+    } catch (...) {
+      op.workspace().set_marks(nullptr);
+      throw;
+    }
+    op.workspace().set_marks(nullptr);
+    SMC_CUDA(cudaStreamSynchronize(st));
+    *count = static_cast<int>(marks.ev.size());
+    cudaEvent_t prev = marks.start;
+    for (int i = 0; i < *count && i < cap; ++i) {
+      float t = 0.0f;
+      SMC_CUDA(cudaEventElapsedTime(&t, prev, marks.ev[i].second));
+      if (ms) ms[i] = t;
+      if (names) names[i] = marks.ev[i].first;
+      prev = marks.ev[i].second;
+    }
+  });
+}
+
 int smc_ns_temperature_pressure(smc_rhs* h, const double* U, double* T, double* p, int where) {
   return guarded([&] {
     need(U, "U"), need(T, "T"), need(p, "p");

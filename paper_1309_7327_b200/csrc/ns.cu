@@ -406,7 +406,10 @@ void set_smem(K kern, std::size_t bytes) {
 template <int S>
 void rhs_v2(const Geo& g, const UV& U, const double* F, double* A, double* GR, double* MX,
             double* SC, double* out, long long ofs, const StencilM& M, int chem, int phase,
-            cudaStream_t st) {
+            cudaStream_t st, KernelMarks* marks) {
+  auto mark = [&](const char* name) {
+    if (marks) marks->mark(name, st);
+  };
   static bool configured = false;
   const std::size_t sm = sizeof(DirSmem);
   if (!configured) {
@@ -429,11 +432,14 @@ void rhs_v2(const Geo& g, const UV& U, const double* F, double* A, double* GR, d
     if (np <= 0) return;
     prim_kernel<<<blocks(np * g.plane), 256, 0, st>>>(U, const_cast<double*>(F), g, k0, k0 + np);
     SMC_CHECK_LAUNCH();
+    mark("prim");
     dim3 g0 = dir_grid<0, NR_A>(g, np), g1 = dir_grid<1, NR_A>(g, np);
     ns_phase_a<0, S><<<g0, NT, sm, st>>>(F, A, A, GR, out, ofs, g, M, k0);
     SMC_CHECK_LAUNCH();
+    mark("phase_a_x");
     ns_phase_a<1, S><<<g1, NT, sm, st>>>(F, na1, A, GR, hy1, n, g, M, k0);
     SMC_CHECK_LAUNCH();
+    mark("phase_a_y");
   };
   if (phase == kNsAll) planes(-g.G, allp);
   if (phase == kNsInterior) planes(0, g.nz);
@@ -444,19 +450,37 @@ void rhs_v2(const Geo& g, const UV& U, const double* F, double* A, double* GR, d
   }
   ns_phase_a<2, S><<<dir_grid<2, NR_A>(g, allp), NT, sm, st>>>(F, na2, A, GR, hy2, n, g, M, 0);
   SMC_CHECK_LAUNCH();
+  mark("phase_a_z");
   ns_mixed_fields<<<blocks(g.plane * allp), 256, 0, st>>>(F, GR, A, MX, g);
   SMC_CHECK_LAUNCH();
+  mark("mixed_fields");
   ns_phase_b<0><<<dir_grid<0>(g, g.nz), DT_THREADS, sizeof(PBSmem), st>>>(MX, SC + 54 * n, g);
   SMC_CHECK_LAUNCH();
+  mark("phase_b_x");
   ns_phase_b<1><<<dir_grid<1>(g, g.nz), DT_THREADS, sizeof(PBSmem), st>>>(MX, SC + 67 * n, g);
   SMC_CHECK_LAUNCH();
+  mark("phase_b_y");
   ns_phase_b<2><<<dir_grid<2>(g, g.nz), DT_THREADS, sizeof(PBSmem), st>>>(MX, SC + 80 * n, g);
   SMC_CHECK_LAUNCH();
+  mark("phase_b_z");
   ns_assemble2<<<blocks(n), 256, 0, st>>>(F, A, SC, out, ofs, g, chem);
   SMC_CHECK_LAUNCH();
+  mark(chem ? "assemble_wdot" : "assemble");
 }
 
 }  // namespace
+
+void KernelMarks::mark(const char* name, cudaStream_t st) {
+  cudaEvent_t e;
+  SMC_CUDA(cudaEventCreate(&e));
+  SMC_CUDA(cudaEventRecord(e, st));
+  ev.emplace_back(name, e);
+}
+
+KernelMarks::~KernelMarks() {
+  for (auto& p : ev) cudaEventDestroy(p.second);
+  if (start) cudaEventDestroy(start);
+}
 
 NsWorkspace::NsWorkspace(const NsBox& box, double dx, double dy, double dz, const StencilM& M,
                          int s)
@@ -523,16 +547,17 @@ void NsWorkspace::rhs(const NsStateView& U, double* out, long long out_fs, int p
     if (phase == kNsBoundary) return;  // pointwise: all of it is interior work
     chem_kernel<<<blocks(n), 256, 0, st>>>(uv, out, out_fs, g);
     SMC_CHECK_LAUNCH();
+    if (marks_) marks_->mark("chem", st);
     return;
   }
   double* F = prim_.get();
   double* A = acc_.get();
   if (s_ == 4)
     rhs_v2<4>(g, uv, F, A, grad_.get(), mixed_.get(), scratch_.get(), out, out_fs, M_,
-              part == kNsFull, phase, st);
+              part == kNsFull, phase, st, marks_);
   else
     rhs_v2<3>(g, uv, F, A, grad_.get(), mixed_.get(), scratch_.get(), out, out_fs, M_,
-              part == kNsFull, phase, st);
+              part == kNsFull, phase, st, marks_);
 }
 
 bool NsWorkspace::chem_fd_jacobian(const double* U, const double* FU, double* jac, double atol,

@@ -10,6 +10,9 @@
 #include "common.cuh"
 #include "ops.hpp"
 
+#include <utility>
+#include <vector>
+
 namespace smc {
 
 // Periodic box or one z-slab with G ghost planes per field (multi-GPU).
@@ -51,6 +54,15 @@ struct NsStateView {
 // interior planes); kBoundary: the rest, after the ghosts have arrived.
 enum NsPhase : int { kNsAll = 0, kNsInterior = 1, kNsBoundary = 2 };
 
+// Optional per-kernel timing of one evaluation (smc_ns_profile): an event is
+// recorded after every kernel, named by the kernel.
+struct KernelMarks {
+  std::vector<std::pair<const char*, cudaEvent_t>> ev;
+  cudaEvent_t start = nullptr;
+  void mark(const char* name, cudaStream_t st);
+  ~KernelMarks();
+};
+
 // Device workspace shared by the three RHS views (full / f1 / f2).
 class NsWorkspace {
  public:
@@ -71,8 +83,10 @@ class NsWorkspace {
   // T and p of every interior cell (ctoprim), for tests / diagnostics.
   void temperature_pressure(const double* U, double* T, double* p, cudaStream_t st);
   const NsBox& box() const { return box_; }
+  void set_marks(KernelMarks* m) { marks_ = m; }
 
  private:
+  KernelMarks* marks_ = nullptr;
   NsBox box_;
   double dx_[3];
   StencilM M_;
