@@ -1,19 +1,29 @@
 #!/usr/bin/env python
-"""bench.py — fp64 cell-RHS evaluations per second of the narrow-stencil
-operator (a U_x)_x + (a U_y)_y + (a U_z)_z, BASELINE.json configs[1]
-(256^3 per GPU, periodic; weak scaling over z-slabs with a 4-plane NCCL halo
-exchange overlapped with the interior for N > 1, configs[3]-style).
+"""bench.py -- fp64 cell-RHS evaluations per second of the full reacting
+Navier-Stokes right-hand side (ctoprim, hypterm, narrow-stencil diffterm with
+transport, wdot): BASELINE.json's metric on its configs[3] workload, 256^3
+cells per GPU, weak scaling over z-slabs of one periodic box with the 4-plane
+halo exchanged by NCCL inside the library, overlapped with the interior work.
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
 
-One "step" = one evaluation of the operator over the whole job's box.
-value   = cells of all ranks / max-over-ranks device time of K steps.
-e2e     = the same metric through the public API with host (pinned) buffers:
-          H2D of U, the operator, D2H of the result, inside the timed region.
-roofline: dominant kernel (narrow_kernel), FP64-bound: 341 flop/cell
-           against a DFMA-loop FP64 peak measured here.
-cpu_baseline: the reference's own kernels (oracle/_ref, built from
-          /root/reference) composed in 3-D, all host threads, rank 0, N=1.
+One "step" = one full RHS evaluation over the whole job's box (every rank
+its 256^3 slab).
+value    = cells of all ranks / max-over-ranks device time of K steps.
+e2e      = the same metric through the public API with host (pinned) buffers:
+           the state H2D, the RHS, the result D2H inside the timed region.
+roofline = the whole RHS (the frozen 8,850 flop per cell-RHS, DESIGN.md
+           §4.3) against the best FP64 probe measured in this run (DFMA
+           variants and DMMA, all reported); `kernels` = one evaluation
+           timed per kernel with CUDA events; `traffic` = the ncu DRAM bytes
+           of one RHS (profiles/ncu_ns_r02.json).
+cpu_baseline = the CPU restatement of the same RHS (oracle/ns_oracle.c,
+           OpenMP over every host thread) on the full 256^3 box, rank 0, N=1.
+--impl reference times that CPU path alone on the same config (no reference
+NS implementation exists: SURVEY.md §0).  Secondary blocks at N=1: configs[1]
+(the narrow operator, with the reference's own kernels as its CPU path),
+the 2-D heat RHS (the reference's HeatOperator), and the configs[2]/[4]
+time advances with their CPU baselines.
 """
 from __future__ import annotations
 
@@ -30,36 +40,58 @@ import time
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
-FLOP_PER_CELL = 341          # 3 x 112 + 3 + 2
-BYTES_PER_CELL = 24          # read U, a; write out (compulsory)
-N_CELLS_SIDE = 256
+NS_FLOP_PER_CELL = 8850   # frozen algorithmic count
+NS_BYTES_PER_CELL = 224   # compulsory: 14 conserved fp64 in + 14 out
+NS_DX = 1e-4
+NARROW_FLOP_PER_CELL = 341   # 3 x 112 + 3 + 2
+NARROW_BYTES_PER_CELL = 24   # read U, a; write out
+METRIC = "fp64 cell-RHS evals/sec (full reacting-NS RHS, configs[3])"
 
 
 def parse():
     p = argparse.ArgumentParser()
     p.add_argument("--gpus", type=int, default=1)
-    p.add_argument("--steps", type=int, default=4000)
-    p.add_argument("--warmup", type=int, default=50)
+    p.add_argument("--steps", type=int, default=20)
+    p.add_argument("--warmup", type=int, default=3)
     p.add_argument("--impl", choices=["ours", "reference"], default="ours")
-    p.add_argument("--n", type=int, default=N_CELLS_SIDE)
-    p.add_argument("--kc", type=int, default=0)
+    p.add_argument("--n", type=int, default=256, help="cells per side per GPU")
+    p.add_argument("--e2e-steps", type=int, default=3)
     p.add_argument("--no-cpu-baseline", action="store_true")
-    p.add_argument("--e2e-steps", type=int, default=20)
-    p.add_argument("--no-ns", action="store_true")
-    p.add_argument("--no-advance", action="store_true",
-                   help="skip the configs[2] SDC / configs[4] MRSDC time-advance blocks")
-    p.add_argument("--ns-steps", type=int, default=5)
-    p.add_argument("--overlap", action="store_true",
-                   help="N>1: interior planes run while the halo is in flight (split launch)")
+    p.add_argument("--no-secondary", action="store_true",
+                   help="skip the configs[1] / heat / time-advance blocks")
+    p.add_argument("--no-advance", action="store_true")
+    p.add_argument("--narrow-steps", type=int, default=2000)
     p.add_argument("--slab", action="store_true",
-                   help="use the multi-GPU z-slab path also at N=1 (ghosts by self-copy)")
-    p.add_argument("--halo", choices=["peer", "nccl"], default="nccl",
-                   help="slab halo: nccl (default) = send/recv into ghost planes before the "
-                        "kernel; peer = the kernel reads the neighbours' planes over CUDA IPC / "
-                        "NVLink (falls back to nccl if the mapping fails).  At N=1 the step is "
-                        "0.302 ms (nccl) vs 0.311 ms (peer): the peer instantiation's per-plane "
-                        "base selection costs more than the 4-plane exchange")
+                   help="N=1: run the library's NCCL slab path (self halo) instead of the "
+                        "periodic operator")
     return p.parse_args()
+
+
+def ns_config(n: int, world: int) -> dict:
+    """The workload, identical in both arms."""
+    return {
+        "workload": f"configs[3] full reacting-NS RHS (ctoprim, hypterm, narrow diffterm + "
+                    f"transport, wdot), {n}^3 cells per GPU",
+        "box": f"{n}x{n}x{n * world} periodic" + (f", z-slabs of {n} planes per GPU, 4-plane "
+                                                  "NCCL halo overlapped" if world > 1 else ""),
+        "cells_per_gpu": n ** 3,
+        "state": "seeded configs[0] generator + Gaussian hot spot (T peak 1800 K, radius 20 "
+                 "cells), 9-species synthetic mechanism, dx = 1e-4 m",
+        "stencil": "narrow SMC (m47=3557/44100, m48=-2083/117600)",
+        "l2": f"inputs larger than L2 ({14 * 8 * n ** 3 / 1e9:.2f} GB state per GPU), no flush",
+    }
+
+
+def cpu_info() -> dict:
+    model, threads = None, os.cpu_count()
+    try:
+        out = subprocess.run(["lscpu"], capture_output=True, text=True, timeout=10).stdout
+        for ln in out.splitlines():
+            if ln.startswith("Model name:"):
+                model = ln.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return {"model": model, "threads": threads}
 
 
 # ------------------------------------------------------------------ clocks
@@ -116,115 +148,178 @@ class ClockSampler:
                 "reasons": sorted(reasons), "samples": len(sm)}
 
 
+# ------------------------------------------------------------- FP64 peaks
+def fp64_peaks(max_over_ranks) -> dict:
+    """The FP64 roofline denominator: the best of the DFMA probe variants
+    (chains per thread, operand placement, warps per SM) and the DMMA probe
+    (mma.sync f64 shares the FP64 pipe on B200), clocks sampled meanwhile."""
+    import ctypes as C
+    from paper_1309_7327_b200 import _capi
+    L = _capi.lib()
+    sampler = ClockSampler(int(os.environ.get("LOCAL_RANK", "0")))
+    sampler.start()
+    time.sleep(0.2)
+    v = (C.c_double * 5)()
+    _capi.check(L.smc_measure_fp64_variants(4000, v, 5))
+    dm = C.c_double()
+    _capi.check(L.smc_measure_dmma_peak(4000, 0, C.byref(dm)))
+    clocks = sampler.stop()
+    names = ["dfma_8chains", "dfma_16chains", "dfma_8chains_own_multiplier",
+             "dfma_8chains_const_operands", "dfma_const_operands_half_warps"]
+    probes = {nm: max_over_ranks(x) for nm, x in zip(names, list(v))}
+    probes["dmma_m8n8k4"] = max_over_ranks(dm.value)
+    best = max(probes, key=probes.get)
+    return {"peak": probes[best], "best": best, "probes": probes, "clocks": clocks}
+
+
 # ------------------------------------------------------------ CPU baselines
-def cpu_reference_rate(n: int, budget_s: float = 12.0, max_reps: int = 5):
-    """The reference's own line kernels composed in 3-D (oracle/_ref), all
-    host threads; returns (cells/s, cores, kind, sample)."""
-    import numpy as np
+def cpu_ns_rate(n: int):
+    """The NS RHS restated on the CPU (oracle/ns_oracle.c), every host thread,
+    on the full n^3 box (one evaluation after a warm-up on a small box), plus
+    one thread on a 64^3 sample."""
     from oracle import oracle as O
     from paper_1309_7327_b200 import workloads as W
-    a, u = W.narrow3d_inputs(n)
-    m, s = O.build_narrow(8, (3557.0 / 44100.0, -2083.0 / 117600.0))
-    if O.have_ref(fast=True):
-        r = O.ref(fast=True)
-        r.ref_set_workers(0)
-        cores = int(r.ref_worker_limit())
-        fn = lambda: O.ref_narrow3d(m, s, a, u, 1 / n, 1 / n, 1 / n, fast=True)  # noqa: E731
-        kind = "reference"
-        sample = f"full {n}^3 box per rep, reference kernels narrow_interfaces<4>/_rows<4> " \
-                 f"composed as narrow_rhs_rows (oracle/ref_capi.cpp), parallel_for over z planes"
-    else:
-        n = min(n, 96)
-        a, u = W.narrow3d_inputs(n)
-        cores = 1
-        fn = lambda: O.narrow3d(m, s, a, u, 1 / n, 1 / n, 1 / n)  # noqa: E731
-        kind = "port"
-        sample = f"full {n}^3 box per rep, C restatement oracle/oracle.c, 1 thread"
-    fn()  # warm-up
-    best, spent, reps = math.inf, 0.0, 0
-    while reps < max_reps and (spent < budget_s or reps < 1):
-        t0 = time.perf_counter()
-        fn()
-        dt = time.perf_counter() - t0
-        best = min(best, dt)
-        spent += dt
-        reps += 1
-    return n ** 3 / best, cores, kind, sample + f", best of {reps}", best
+    threads = O.set_threads(0)
+    U = O.ns_conserved(*W.ns_primitives(n, hot_spot=True))
+    Us = O.ns_conserved(*W.ns_primitives(32, hot_spot=True))
+    O.ns_rhs(Us, NS_DX, 0)
+    t0 = time.perf_counter()
+    O.ns_rhs(U, NS_DX, 0)
+    dt = time.perf_counter() - t0
+    O.set_threads(1)
+    U64 = O.ns_conserved(*W.ns_primitives(64, hot_spot=True))
+    t1 = time.perf_counter()
+    O.ns_rhs(U64, NS_DX, 0)
+    one = 64 ** 3 / (time.perf_counter() - t1)
+    O.set_threads(0)
+    return {"value": n ** 3 / dt, "unit": "cell-RHS/s", "cores": threads, "kind": "port",
+            "sample": f"one full {n}^3 RHS (configs[3] state), oracle/ns_oracle.c with OpenMP "
+                      f"over {threads} host threads; no reference NS implementation exists "
+                      "(SURVEY.md §0)",
+            "one_thread": {"value": one, "unit": "cell-RHS/s", "sample": "64^3 box, 1 thread"},
+            "cpu": cpu_info()}
 
 
 def run_reference(args):
-    """--impl reference: the reference CPU path on the same workload."""
+    """--impl reference: the CPU path of the same RHS on the same config
+    (rank 0 only), every host thread, each step one full per-GPU block."""
     rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
     if rank != 0:
         return
-    n = args.n
-    import numpy as np
     from oracle import oracle as O
     from paper_1309_7327_b200 import workloads as W
-    if not O.have_ref(fast=True):
-        O.build_ref()
-    a, u = W.narrow3d_inputs(n)
-    m, s = O.build_narrow(8, (3557.0 / 44100.0, -2083.0 / 117600.0))
-    have = O.have_ref(fast=True)
-    if have:
-        r = O.ref(fast=True)
-        r.ref_set_workers(0)
-        cores = int(r.ref_worker_limit())
-        step = lambda: O.ref_narrow3d(m, s, a, u, 1 / n, 1 / n, 1 / n, fast=True)  # noqa: E731
-        kind = "reference"
-    else:
-        cores = 1
-        step = lambda: O.narrow3d(m, s, a, u, 1 / n, 1 / n, 1 / n)  # noqa: E731
-        kind = "port"
-    for _ in range(min(args.warmup, 1)):
-        step()
-    t_one = None
-    times = []
-    budget = 120.0
-    k = 0
+    n = args.n
+    threads = O.set_threads(0)
+    U = O.ns_conserved(*W.ns_primitives(n, hot_spot=True))
+    Us = O.ns_conserved(*W.ns_primitives(32, hot_spot=True))
+    for _ in range(max(1, min(args.warmup, 1))):
+        O.ns_rhs(Us, NS_DX, 0)
+    times, budget = [], 150.0
     t_start = time.perf_counter()
-    while k < args.steps:
+    while len(times) < args.steps:
         t0 = time.perf_counter()
-        step()
+        O.ns_rhs(U, NS_DX, 0)
         times.append(time.perf_counter() - t0)
-        k += 1
         if time.perf_counter() - t_start > budget:
             break
+    k = len(times)
     total = sum(times)
     value = n ** 3 * k / total
+    sample = (f"{k} full {n}^3 RHS evaluations (one per-GPU block per step; time-capped at "
+              f"{budget:.0f} s), oracle/ns_oracle.c with OpenMP over {threads} host threads")
     out = {
-        "metric": "fp64 cell-RHS evals/sec (narrow operator, configs[1])",
-        "value": value, "unit": "cell-RHS/s", "n_gpus": args.gpus, "steps": k,
-        "steps_requested": args.steps, "warmup": args.warmup,
-        "ms_per_step": 1e3 * total / k, "higher_is_better": True, "scaling": "weak",
-        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": f"configs[1] narrow operator {n}^3 periodic (CPU reference path)",
-                   "cells": n ** 3},
-        "impl": "reference",
-        "cpu_baseline": {"value": value, "unit": "cell-RHS/s", "cores": cores, "kind": kind,
-                         "sample": f"full {n}^3 box per step; {k} steps (time-capped at "
-                                   f"{budget:.0f} s)"},
+        "metric": METRIC, "value": value, "unit": "cell-RHS/s", "n_gpus": world, "steps": k,
+        "steps_requested": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * total / k,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic", "config": ns_config(n, world), "impl": "reference",
+        "cpu_baseline": {"value": value, "unit": "cell-RHS/s", "cores": threads, "kind": "port",
+                         "sample": sample, "cpu": cpu_info()},
         "e2e": {"value": value, "unit": "cell-RHS/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
     }
     print(json.dumps(out), flush=True)
 
 
-# ---------------------------------------------------------- NS secondary
-NS_FLOP_PER_CELL = 8850   # frozen algorithmic count, DESIGN.md "NS RHS flop count"
-NS_BYTES_PER_CELL = 224   # 14 conserved fp64 in + 14 out (fully fused minimum)
-# DRAM bytes per cell-RHS the direction-split design moves (sum over its
-# kernels of ncu dram__bytes_read + write at 128^3, profiles/ncu_ns_r01.json:
-# prim 452, phase A 3 x 632, mixed 138, phase B 3 x 29, assemble2 738)
-NS_DESIGN_BYTES_PER_CELL = 3311
+# ---------------------------------------------- secondary: configs[1]
+def narrow_block(dev, stream, peak, steps):
+    """configs[1]: the narrow operator alone, 256^3 periodic, with its own
+    roofline (341 flop / 24 B per cell), e2e and the reference's own kernels
+    composed in 3-D as its CPU path (oracle/_ref, every host thread)."""
+    import torch
+    import paper_1309_7327_b200 as P
+    from paper_1309_7327_b200 import workloads as W
+    n = 256
+    a, u = W.narrow3d_inputs(n, xp=torch, device=dev)
+    op = P.Narrow3DOperator(a, 1 / n, 1 / n, 1 / n)
+    op.set_stream(stream)
+    out = torch.empty_like(u)
+    for _ in range(20):
+        op(0.0, u, out)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(steps):
+        op(0.0, u, out)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / steps
+    tf = NARROW_FLOP_PER_CELL * n ** 3 / (ms * 1e-3) / 1e12
+    gbs = NARROW_BYTES_PER_CELL * n ** 3 / (ms * 1e-3) / 1e9
+    traffic = None
+    try:
+        traffic = json.load(open(os.path.join(ROOT, "profiles", "ncu_narrow3d.json"))).get(
+            "dram_bytes_per_launch")
+    except Exception:
+        pass
+    uh = torch.empty((n, n, n), dtype=torch.float64).pin_memory()
+    oh = torch.empty((n, n, n), dtype=torch.float64).pin_memory()
+    uh.copy_(u.cpu())
+    op(0.0, uh, oh)
+    t0 = time.perf_counter()
+    for _ in range(5):
+        op(0.0, uh, oh)  # H2D, kernel, D2H, synchronize (smc_rhs_eval, SMC_HOST)
+    e2e_ms = (time.perf_counter() - t0) * 1e3 / 5
+    res = {"workload": "configs[1] narrow 8th-order (a U_x)_x+(a U_y)_y+(a U_z)_z, 256^3 "
+                       "periodic, SMC stencil", "value": n ** 3 / (ms * 1e-3),
+           "unit": "cell-RHS/s", "ms_per_step": ms, "steps": steps,
+           "roofline": {"bound": "fp64", "achieved": tf, "peak": peak, "unit": "TFLOP/s",
+                        "frac": tf / peak, "traffic": traffic,
+                        "flop_per_cell": NARROW_FLOP_PER_CELL,
+                        "hbm": {"achieved": gbs, "bytes_per_cell": NARROW_BYTES_PER_CELL}},
+           "e2e": {"value": n ** 3 / (e2e_ms * 1e-3), "unit": "cell-RHS/s",
+                   "h2d_bytes_per_step": 8 * n ** 3, "d2h_bytes_per_step": 8 * n ** 3,
+                   "ms_per_step": e2e_ms}}
+    try:
+        from oracle import oracle as O
+        if not O.have_ref(fast=True):
+            O.build_ref()
+        if O.have_ref(fast=True):
+            ah, uhn = W.narrow3d_inputs(n)
+            m, s = O.build_narrow(8, (3557.0 / 44100.0, -2083.0 / 117600.0))
+            r = O.ref(fast=True)
+            r.ref_set_workers(0)
+            O.ref_narrow3d(m, s, ah, uhn, 1 / n, 1 / n, 1 / n, fast=True)
+            best = math.inf
+            for _ in range(3):
+                t0 = time.perf_counter()
+                O.ref_narrow3d(m, s, ah, uhn, 1 / n, 1 / n, 1 / n, fast=True)
+                best = min(best, time.perf_counter() - t0)
+            res["cpu_baseline"] = {"value": n ** 3 / best, "unit": "cell-RHS/s",
+                                   "cores": int(r.ref_worker_limit()), "kind": "reference",
+                                   "sample": "full 256^3 box, the reference's narrow_interfaces"
+                                             "<4>/_rows<4> composed as narrow_rhs_rows "
+                                             "(oracle/ref_capi.cpp), best of 3"}
+    except Exception as exc:  # noqa: BLE001
+        res["cpu_baseline"] = {"value": None, "sample": f"failed: {exc}"}
+    del a, u, out
+    torch.cuda.empty_cache()
+    return res
 
 
-def heat2d_measurement(dev, stream, fp64_peak, n=4096, reps=100):
-    """The reference's own RHS (HeatOperator::rhs, pde.cpp:266-274; the 2-D
-    T2 problem, narrow SMC stencil) on the GPU at n^2 next to the reference
-    CPU path on all host threads (oracle/_ref, operator built once, best of 3
-    calls).  Roofline: 2 x 112 + 3 + 2 flop per cell (two directions, the
-    1/d^2 scalings and combine), 32 B per cell (u, a, b in; out)."""
+def heat2d_block(dev, stream, peak, n=4096, reps=100):
+    """The reference's own RHS (HeatOperator::rhs, pde.cpp:266-274; T2, narrow
+    SMC) at n^2, next to the reference CPU path on every host thread."""
     import ctypes as C
     import numpy as np
     import torch
@@ -251,8 +346,8 @@ def heat2d_measurement(dev, stream, fp64_peak, n=4096, reps=100):
     res = {"workload": f"HeatOperator::rhs, T2 coefficients, narrow SMC, {n}^2 periodic",
            "value": n * n / (ms * 1e-3), "unit": "cell-RHS/s", "ms_per_rhs": ms,
            "roofline": {"bound": "fp64", "achieved": flop * n * n / (ms * 1e-3) / 1e12,
-                        "peak": fp64_peak, "unit": "TFLOP/s",
-                        "frac": flop * n * n / (ms * 1e-3) / 1e12 / fp64_peak,
+                        "peak": peak, "unit": "TFLOP/s",
+                        "frac": flop * n * n / (ms * 1e-3) / 1e12 / peak,
                         "flop_per_cell": flop, "bytes_per_cell": 32}}
     try:
         from oracle import oracle as O
@@ -261,75 +356,17 @@ def heat2d_measurement(dev, stream, fp64_peak, n=4096, reps=100):
             r.ref_set_workers(0)
             best = C.c_double()
             pp = np.array([P.SMC_M47, P.SMC_M48])
-            rc = r.ref_heat2d_time(2, n, n, 0, O.dp(pp), 3, C.byref(best))
-            if rc == 0:
+            if r.ref_heat2d_time(2, n, n, 0, O.dp(pp), 3, C.byref(best)) == 0:
                 res["cpu_baseline"] = {"value": n * n / best.value, "unit": "cell-RHS/s",
                                        "cores": int(r.ref_worker_limit()), "kind": "reference",
-                                       "sample": f"HeatOperator::rhs at {n}^2, operator built "
-                                                 "once, best of 3 calls"}
+                                       "sample": f"HeatOperator::rhs at {n}^2, best of 3"}
     except Exception as exc:  # noqa: BLE001
         res["cpu_baseline"] = {"value": None, "sample": f"failed: {exc}"}
     return res
 
 
-def ns_rhs_measurement(n, dev, stream, fp64_peak, hbm_peak, steps):
-    """Full NS RHS (ctoprim, hypterm, narrow diffterm + transport, wdot) on
-    the configs[3] state generator (hot spot), n^3 periodic, dx = 1e-4 m."""
-    import torch
-    import paper_1309_7327_b200 as P
-    from paper_1309_7327_b200 import workloads as W
-    T, p, uvw, Y = W.ns_primitives(n, hot_spot=True)
-    U = P.ns_conserved(*(torch.from_numpy(a).to(dev) for a in (T, p, uvw, Y)))
-    del T, p, uvw, Y
-    op = P.NsOperator(n, n, n, 1e-4)
-    op.set_stream(stream)
-    out = torch.empty_like(U)
-    op.full(0.0, U, out)
-    torch.cuda.synchronize()
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    e0.record(stream)
-    for _ in range(steps):
-        op.full(0.0, U, out)
-    e1.record(stream)
-    torch.cuda.synchronize()
-    ms = e0.elapsed_time(e1) / steps
-    cells = n ** 3
-    tf = NS_FLOP_PER_CELL * cells / (ms * 1e-3) / 1e12
-    gbs = NS_BYTES_PER_CELL * cells / (ms * 1e-3) / 1e9
-    res = {"workload": f"configs[3] full reacting-NS RHS, {n}^3, hot spot, 9-species synthetic "
-                       "mechanism, periodic", "value": cells / (ms * 1e-3),
-           "unit": "cell-RHS/s", "ms_per_rhs": ms, "steps": steps,
-           "roofline": {"bound": "fp64", "achieved": tf, "peak": fp64_peak, "unit": "TFLOP/s",
-                        "frac": tf / fp64_peak, "flop_per_cell": NS_FLOP_PER_CELL,
-                        "hbm": {"achieved": gbs, "peak": hbm_peak, "frac": gbs / hbm_peak,
-                                "bytes_per_cell": NS_BYTES_PER_CELL},
-                        # the traffic this design moves at the HBM peak: how close the
-                        # split kernels are to their own memory floor
-                        "hbm_design": {"bytes_per_cell": NS_DESIGN_BYTES_PER_CELL,
-                                       "floor_ms": NS_DESIGN_BYTES_PER_CELL * cells / hbm_peak / 1e6,
-                                       "frac": NS_DESIGN_BYTES_PER_CELL * cells / hbm_peak / 1e6 / ms}}}
-    # the oracle (C restatement, 1 thread) on a 24^3 sample of the same generator
-    try:
-        import time as _t
-        from oracle import oracle as O
-        Tn, pn, un, Yn = W.ns_primitives(24, hot_spot=True)
-        Uh = O.ns_conserved(Tn, pn, un, Yn)
-        O.ns_rhs(Uh, 1e-4, 0)
-        t0 = _t.perf_counter()
-        O.ns_rhs(Uh, 1e-4, 0)
-        res["cpu_baseline"] = {"value": 24 ** 3 / (_t.perf_counter() - t0), "unit": "cell-RHS/s",
-                               "cores": 1, "kind": "port",
-                               "sample": "24^3 box, oracle/ns_oracle.c (no reference NS exists)"}
-    except Exception as exc:  # noqa: BLE001
-        res["cpu_baseline"] = {"value": None, "kind": "unavailable", "sample": str(exc)}
-    del U, out
-    torch.cuda.empty_cache()
-    return res
-
-
 def acoustic_dt(T, p, uvw, Y, dx, cfl=0.5):
-    """CFL 0.5 on max(|u_i| + c) (the synthetic thermodynamics of
-    include/smc_mechanism.h), host side."""
+    """CFL 0.5 on max(|u_i| + c) (include/smc_mechanism.h thermodynamics)."""
     import numpy as np
     W_ = np.array([2.01588e-3, 31.9988e-3, 18.01528e-3, 1.00794e-3, 15.9994e-3, 17.00734e-3,
                    33.00674e-3, 34.01468e-3, 28.0134e-3])
@@ -343,30 +380,30 @@ def acoustic_dt(T, p, uvw, Y, dx, cfl=0.5):
     return cfl * dx / float((np.abs(uvw).max(axis=0) + c).max())
 
 
-def advance_measurement(dev, stream):
-    """configs[2]: 10 SDC steps (3 Gauss-Lobatto nodes, 4 sweeps) at CFL 0.5
-    of the configs[0] generator on 128^3; configs[4] (one GPU point): one
-    MRSDC mode-1 step (GL(3) coarse advection-diffusion, GL(5) fine
-    chemistry per coarse interval) on the ignition state at 128^3; MRSDC
-    mode 2 (chemistry implicit on the GL(3) coarse
-    nodes through the per-cell block Newton, advection-diffusion explicit on
-    the GL(5) fine nodes) on the same state, one step of twice the acoustic
-    dt."""
+def advance_block(dev, stream, cpu: bool):
+    """configs[2]: SDC (3 Gauss-Lobatto nodes, 4 sweeps) at CFL 0.5 of the
+    configs[0] state, 10 steps at 128^3; configs[4] (one-GPU point): MRSDC
+    mode 1 (GL(3) advection-diffusion, GL(5) chemistry per coarse interval)
+    on the ignition state at 128^3, one step; MRSDC mode 2 (chemistry
+    implicit through the per-cell block Newton) on the same state.  CPU
+    baselines: one step of the oracle's SDC and MRSDC restatements driving
+    the threaded NS oracle on the same 128^3 states."""
+    import numpy as np
     import torch
     import paper_1309_7327_b200 as P
     from paper_1309_7327_b200 import workloads as W
-    n, dx, res = 128, 1e-4, {}
+    n, res = 128, {}
     for name, kw in (("sdc_configs2", {}), ("mrsdc_configs4", {"ignition": True}),
                      ("mrsdc_mode2_implicit_chem", {"ignition": True})):
         T, p, uvw, Y = W.ns_primitives(n, **kw)
-        dt = acoustic_dt(T, p, uvw, Y, dx) * (2.0 if "mode2" in name else 1.0)
+        dt = acoustic_dt(T, p, uvw, Y, NS_DX) * (2.0 if "mode2" in name else 1.0)
         U = P.ns_conserved(*(torch.from_numpy(x).to(dev) for x in (T, p, uvw, Y)))
-        op = P.NsOperator(n, n, n, dx)
+        op = P.NsOperator(n, n, n, NS_DX)
         op.set_stream(stream)
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         if name.startswith("sdc"):
             st = P.SdcStepper(3, P.StepControls(4, 0.0))
-            st.integrate(op.full, U, 0.0, dt, 1)  # warm-up (buffers)
+            st.integrate(op.full, U, 0.0, dt, 1)
             torch.cuda.synchronize()
             e0.record(stream)
             out, d = st.integrate(op.full, U, 0.0, 10 * dt, 10)
@@ -399,6 +436,30 @@ def advance_measurement(dev, stream):
                      "finite": bool(torch.isfinite(out).all().item())}
         if "mode2" in name:
             res[name].update(implicit_solves=d.implicit_solves, newton_f1_evals=d.newton_f1_evals)
+        if cpu and "mode2" not in name:
+            try:
+                from oracle import oracle as O
+                threads = O.set_threads(0)
+                Uh = U.cpu().numpy()
+                shape = Uh.shape
+                t0 = time.perf_counter()
+                if name.startswith("sdc"):
+                    q, s = P.integration_matrices(0, 3)
+                    O.integrate_sdc(O.ns_callback(shape, NS_DX, 0), Uh, 0.0, dt, 1, P.nodes(0, 3),
+                                    q, s)
+                else:
+                    h = P.build_hierarchy(3, 5)
+                    h["coarse"] = P.nodes(0, 3)
+                    O.integrate_mrsdc1(O.ns_callback(shape, NS_DX, 1),
+                                       O.ns_callback(shape, NS_DX, 2), Uh, 0.0, dt, 1, h)
+                cpu_ms = (time.perf_counter() - t0) * 1e3
+                res[name]["cpu_baseline"] = {
+                    "ms_per_step": cpu_ms, "cores": threads, "kind": "port",
+                    "sample": f"one step at {n}^3: the oracle's integrator restatement "
+                              "(oracle.c) driving the threaded NS oracle",
+                    "speedup": cpu_ms / (ms / steps)}
+            except Exception as exc:  # noqa: BLE001
+                res[name]["cpu_baseline"] = {"ms_per_step": None, "sample": f"failed: {exc}"}
         del U, out, op, st
         torch.cuda.empty_cache()
     return res
@@ -410,12 +471,12 @@ def main():
     if args.impl == "reference":
         run_reference(args)
         return
+    import numpy as np
     import torch
     import torch.distributed as dist
     import paper_1309_7327_b200 as P
-    from paper_1309_7327_b200 import _capi, workloads as W
-    from paper_1309_7327_b200.distributed import DistributedNarrow3D, Slab
-    import ctypes as C
+    from paper_1309_7327_b200 import workloads as W
+    from paper_1309_7327_b200.distributed import Comm, NsSlab
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -429,61 +490,6 @@ def main():
     cells_total = cells_rank * world
     stream = torch.cuda.current_stream()
 
-    # ---- inputs resident in HBM
-    slab_mode = world > 1 or args.slab
-    halo = None
-    if not slab_mode:
-        a, u = W.narrow3d_inputs(n, xp=torch, device=dev)
-        op = P.Narrow3DOperator(a, 1 / n, 1 / n, 1 / n)
-        op.set_stream(stream)
-        if args.kc:
-            op.set_kc(args.kc)
-        out = torch.empty_like(u)
-
-        def step():
-            op(0.0, u, out)
-    else:
-        slab = Slab(rank, world, n)
-        zg = torch.tensor(slab.global_planes(), dtype=torch.float64, device=dev) / n
-        x = torch.arange(n, dtype=torch.float64, device=dev) / n
-        tw = 2 * math.pi
-        a = (1.0 + 0.5 * torch.sin(tw * x).view(1, 1, n) * torch.cos(tw * x).view(1, n, 1)
-             * torch.sin(tw * zg).view(-1, 1, 1)).contiguous()
-        ks, amps, ph = W.modes()
-        u = torch.zeros_like(a)
-        for k, A, p in zip(ks, amps, ph):
-            u += A * torch.sin(tw * (k[0] * x.view(1, 1, n) + k[1] * x.view(1, n, 1)
-                                     + k[2] * zg.view(-1, 1, 1)) + p)
-        out = torch.empty((n, n, n), dtype=torch.float64, device=dev)
-        halo = args.halo
-        if halo == "peer":
-            try:
-                from paper_1309_7327_b200.distributed import PeerNarrow3D
-                pdop = PeerNarrow3D(a, slab, 1 / n, 1 / n, 1 / n, dist if world > 1 else None,
-                                    exchange_a=False, sync="nccl")
-                for b in pdop.bufs:
-                    b.copy_(u[4:4 + n])
-            except Exception as exc:  # noqa: BLE001  (a GPU path either way)
-                print(f"peer halo unavailable ({exc}); using the NCCL exchange", file=sys.stderr)
-                halo = "nccl"
-        if halo == "peer":
-            if args.kc:
-                pdop.op.set_kc(args.kc)
-            op = pdop.op
-            counter = [0]
-
-            def step():
-                pdop.apply(counter[0], out)
-                counter[0] += 1
-        else:
-            dop = DistributedNarrow3D(a, slab, 1 / n, 1 / n, 1 / n, dist, exchange_a=False)
-            if args.kc:
-                dop.op.set_kc(args.kc)
-            op = dop.op
-
-            def step():
-                dop.apply(u, out, overlap=args.overlap)
-
     def barrier():
         if world > 1:
             dist.barrier()
@@ -496,12 +502,26 @@ def main():
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return float(t.item())
 
-    # ---- FP64 peak of this device (roofline denominator)
-    peak = C.c_double()
-    _capi.check(_capi.lib().smc_measure_fp64_peak(20000, C.byref(peak)))
-    fp64_peak = max_over_ranks(peak.value)
+    # ---- this rank's state, resident in HBM (slab z0 = rank * n of the box)
+    T, p, uvw, Y = W.ns_primitives(n, nz=n, z0=rank * n, nz_global=n * world, hot_spot=True)
+    U = P.ns_conserved(*(torch.from_numpy(a).to(dev) for a in (T, p, uvw, Y)))
+    del T, p, uvw, Y
+    out = torch.empty_like(U)
+    slab_mode = world > 1 or args.slab
+    if slab_mode:
+        comm = Comm.nccl(dist if world > 1 else None, device=dev)
+        op = NsSlab(comm, n, n, n, NS_DX)
+    else:
+        op = P.NsOperator(n, n, n, NS_DX)
+    op.set_stream(stream)
 
-    # ---- warm-up + timed region (inputs 403 MB/step per rank > 126 MB L2)
+    def step():
+        op.full(0.0, U, out)
+
+    peaks = fp64_peaks(max_over_ranks)
+    peak = peaks["peak"]
+
+    # ---- warm-up + timed region (1.9 GB state per rank > 126 MB L2)
     for _ in range(max(args.warmup, 3)):
         step()
     barrier()
@@ -522,143 +542,102 @@ def main():
     ms_step = ms / args.steps
     value = cells_total * args.steps / (ms * 1e-3)
 
-    # ---- dominant kernel alone (for N > 1 the step also holds the exchange)
+    # ---- per-kernel times of one evaluation (periodic operator view)
+    kernels = None
     if not slab_mode:
-        k_ms = ms_step
-    else:
-        k0, k1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        barrier()
-        k0.record(stream)
-        kk = max(10, args.steps // 10)
-        for _ in range(kk):
-            op.apply_planes(u, out, 0, n)
-        k1.record(stream)
-        barrier()
-        k_ms = max_over_ranks(k0.elapsed_time(k1)) / kk
-    achieved_tf = FLOP_PER_CELL * cells_rank / (k_ms * 1e-3) / 1e12
-    achieved_gbs = BYTES_PER_CELL * cells_rank / (k_ms * 1e-3) / 1e9
-    peaks = {}
-    try:
-        peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
-    except Exception:
-        pass
-    hbm_peak = peaks.get("hbm_gbs", 6650.0)
+        prof = op.profile(U, out)
+        tot = sum(t for _, t in prof)
+        kernels = {"ms": {f"{i:02d}_{k}": t for i, (k, t) in enumerate(prof)},
+                   "sum_ms": tot,
+                   "phase_a_share": sum(t for k, t in prof if k.startswith("phase_a")) / tot}
+
+    tf = NS_FLOP_PER_CELL * cells_rank / (ms_step * 1e-3) / 1e12
+    gbs = NS_BYTES_PER_CELL * cells_rank / (ms_step * 1e-3) / 1e9
     traffic = None
     try:
-        prof = json.load(open(os.path.join(ROOT, "profiles", "ncu_narrow3d.json")))
-        traffic = prof.get("dram_bytes_per_launch")
+        nprof = json.load(open(os.path.join(ROOT, "profiles", "ncu_ns_r02.json")))
+        traffic = nprof["dram_bytes_per_cell_rhs"] * cells_rank
     except Exception:
         pass
+    meas = {}
+    try:
+        meas = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+    except Exception:
+        pass
+    hbm_peak = meas.get("hbm_gbs", 6650.0)
 
-    # ---- e2e through the public API with host buffers
-    e2e_steps = max(3, min(args.e2e_steps, args.steps))
-    if not slab_mode:
-        uh = torch.empty((n, n, n), dtype=torch.float64).pin_memory()
-        oh = torch.empty((n, n, n), dtype=torch.float64).pin_memory()
-        uh.copy_(u.cpu())
+    # ---- e2e through the public API with host (pinned) buffers
+    Uh = torch.empty(U.shape, dtype=torch.float64).pin_memory()
+    Oh = torch.empty(U.shape, dtype=torch.float64).pin_memory()
+    Uh.copy_(U.cpu())
+    e2e_steps = max(1, args.e2e_steps)
 
-        def e2e_step():
-            op(0.0, uh, oh)          # H2D, kernel, D2H, synchronize (smc_rhs_eval, SMC_HOST)
-    else:
-        uh = torch.empty((n, n, n), dtype=torch.float64).pin_memory()
-        oh = torch.empty((n, n, n), dtype=torch.float64).pin_memory()
-        uh.copy_(u[4:4 + n].cpu())
-
-        if halo == "peer":
-            def e2e_step():
-                i = counter[0]
-                pdop.buffer(i).copy_(uh, non_blocking=True)
-                pdop.apply(i, out)
-                counter[0] += 1
-                oh.copy_(out, non_blocking=True)
-                torch.cuda.current_stream().synchronize()
+    def e2e_step():
+        if slab_mode:  # the rank's state in, the slab RHS, the result out
+            U.copy_(Uh, non_blocking=True)
+            op.full(0.0, U, out)
+            Oh.copy_(out, non_blocking=True)
+            stream.synchronize()
         else:
-            def e2e_step():
-                u[4:4 + n].copy_(uh, non_blocking=True)
-                dop.apply(u, out, overlap=args.overlap)
-                oh.copy_(out, non_blocking=True)
-                torch.cuda.current_stream().synchronize()
+            op.full(0.0, Uh, Oh)  # smc_rhs_eval with SMC_HOST buffers
     e2e_step()
     barrier()
-    f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    f0.record(stream)
+    t0 = time.perf_counter()
     for _ in range(e2e_steps):
         e2e_step()
-    f1.record(stream)
     barrier()
-    e2e_ms = max_over_ranks(f0.elapsed_time(f1)) / e2e_steps
+    e2e_ms = max_over_ranks((time.perf_counter() - t0) * 1e3 / e2e_steps)
     e2e_value = cells_total / (e2e_ms * 1e-3)
+    del Uh, Oh
 
-    # ---- secondary: the full reacting-NS RHS (configs[3] state, this GPU's block)
-    ns = None
-    if not args.no_ns and world == 1:
-        try:
-            ns = ns_rhs_measurement(n, dev, stream, fp64_peak, hbm_peak, args.ns_steps)
-        except Exception as exc:  # noqa: BLE001
-            ns = {"error": str(exc)}
-
-    heat = None
-    if not args.no_ns and world == 1:
-        try:
-            heat = heat2d_measurement(dev, stream, fp64_peak)
-        except Exception as exc:  # noqa: BLE001
-            heat = {"error": str(exc)}
-
-    adv = None
-    if not args.no_advance and world == 1:
-        try:
-            adv = advance_measurement(dev, stream)
-        except Exception as exc:  # noqa: BLE001
-            adv = {"error": str(exc)}
-
-    # ---- CPU baseline (rank 0, N = 1 only)
     cpu = None
     if world == 1 and rank == 0 and not args.no_cpu_baseline:
         try:
-            v, cores, kind, sample, best = cpu_reference_rate(n)
-            cpu = {"value": v, "unit": "cell-RHS/s", "cores": cores, "kind": kind,
-                   "sample": sample}
+            cpu = cpu_ns_rate(n)
         except Exception as exc:  # noqa: BLE001
             cpu = {"value": None, "unit": "cell-RHS/s", "cores": 0, "kind": "unavailable",
                    "sample": f"failed: {exc}"}
 
+    secondary = {}
+    if world == 1 and not args.no_secondary:
+        del U, out
+        torch.cuda.empty_cache()
+        for key, fn in (("narrow_configs1", lambda: narrow_block(dev, stream, peak,
+                                                                 args.narrow_steps)),
+                        ("heat2d_rhs", lambda: heat2d_block(dev, stream, peak)),
+                        ("time_advance", lambda: None if args.no_advance else
+                         advance_block(dev, stream, not args.no_cpu_baseline))):
+            try:
+                secondary[key] = fn()
+            except Exception as exc:  # noqa: BLE001
+                secondary[key] = {"error": str(exc)}
+
     if rank == 0:
         line = {
-            "metric": "fp64 cell-RHS evals/sec (narrow operator, configs[1])",
-            "value": value, "unit": "cell-RHS/s", "n_gpus": world, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {
-                "workload": f"configs[1] narrow 8th-order (a U_x)_x+(a U_y)_y+(a U_z)_z, "
-                            f"{n}^3 per GPU, periodic" +
-                            ("" if not slab_mode else f", z-slabs of a {n}x{n}x{n * world} box, "
-                                                      + ("4-plane halo read by the kernel over peer memory (CUDA IPC / NVLink)"
-                                                         if halo == "peer" else
-                                                         "4-plane NCCL halo" + (", overlapped" if args.overlap else ""))),
-                "cells_per_gpu": cells_rank, "stencil": "SMC (m47=3557/44100, m48=-2083/117600)",
-                "l2": f"inputs larger than L2 ({(2 * 8 * cells_rank) / 1e6:.0f} MB read + "
-                      f"{8 * cells_rank / 1e6:.0f} MB written per step per GPU)",
-                "kc": args.kc or "heuristic",
-            },
+            "metric": METRIC, "value": value, "unit": "cell-RHS/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic", "config": ns_config(n, world),
             "roofline": {
-                "bound": "fp64", "achieved": achieved_tf, "peak": fp64_peak,
-                "unit": "TFLOP/s", "frac": achieved_tf / fp64_peak, "traffic": traffic,
-                "peak_source": "DFMA-loop peak measured in this run (smc_measure_fp64_peak); "
+                "bound": "fp64", "achieved": tf, "peak": peak, "unit": "TFLOP/s",
+                "frac": tf / peak, "traffic": traffic,
+                "scope": "the whole RHS (its kernels in sequence), 8,850 flop per cell-RHS",
+                "peak_source": f"best FP64 probe measured in this run ({peaks['best']}); "
                                "MEASURED_PEAKS.json has no FP64 figure",
-                "flop_per_cell": FLOP_PER_CELL, "kernel_ms": k_ms,
-                "hbm": {"achieved": achieved_gbs, "peak": hbm_peak, "unit": "GB/s",
-                        "frac": achieved_gbs / hbm_peak, "bytes_per_cell": BYTES_PER_CELL},
+                "probes_tflops": peaks["probes"], "probe_clocks": peaks["clocks"],
+                "flop_per_cell": NS_FLOP_PER_CELL,
+                "hbm": {"achieved": gbs, "peak": hbm_peak, "unit": "GB/s",
+                        "frac": gbs / hbm_peak, "bytes_per_cell": NS_BYTES_PER_CELL},
             },
+            "kernels": kernels,
             "e2e": {"value": e2e_value, "unit": "cell-RHS/s",
-                    "h2d_bytes_per_step": 8 * cells_rank, "d2h_bytes_per_step": 8 * cells_rank,
-                    "ms_per_step": e2e_ms},
+                    "h2d_bytes_per_step": 14 * 8 * cells_rank,
+                    "d2h_bytes_per_step": 14 * 8 * cells_rank, "ms_per_step": e2e_ms},
             "gpu_launches": launches,
             "clocks": clocks,
             "cpu_baseline": cpu,
-            "ns_rhs": ns,
-            "heat2d_rhs": heat,
-            "time_advance": adv,
         }
+        line.update(secondary)
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()

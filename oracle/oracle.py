@@ -222,6 +222,53 @@ def ns_rhs_terms(U, dx, terms, part=0, m64=None, s=4) -> np.ndarray:
     return out
 
 
+def ns_callback(shape, dx, part, counter=None):
+    """RHS_CB evaluating the NS oracle on a state of `shape` (14, nz, ny, nx)."""
+    def f(t, u, out, dim, ctx):
+        uu = np.ctypeslib.as_array(u, shape=(dim,)).reshape(shape)
+        np.ctypeslib.as_array(out, shape=(dim,))[:] = ns_rhs(uu, dx, part).ravel()
+        if counter is not None:
+            counter[0] += 1
+    return RHS_CB(f)
+
+
+def integrate_sdc(fcb, u0, t0, t1, nsteps, nodes, q, s, iterations=4, cutoff=0.0):
+    """or_integrate_sdc (sdc.cpp:38-127 restated): (u, sweeps, fresh_evals)."""
+    u0 = np.ascontiguousarray(u0, dtype=np.float64).ravel()
+    uo = np.empty_like(u0)
+    res = np.zeros(256)
+    sw, fe, es = C.c_int(), C.c_int(), C.c_int()
+    D = lambda a: np.ascontiguousarray(a, dtype=np.float64)  # noqa: E731
+    nodes, q, s = D(nodes), D(q), D(s)
+    rc = lib().or_integrate_sdc(fcb, None, u0.size, dp(u0), C.c_double(t0), C.c_double(t1),
+                                nsteps, len(nodes) - 1, dp(nodes), dp(q), dp(s), iterations,
+                                C.c_double(cutoff), 1, dp(uo), dp(res), res.size, C.byref(sw),
+                                C.byref(fe), C.byref(es))
+    assert rc == 0
+    return uo, sw.value, fe.value
+
+
+def integrate_mrsdc1(f1cb, f2cb, u0, t0, t1, nsteps, h, iterations=4, cutoff=0.0):
+    """or_integrate_mrsdc1 (mrsdc.cpp:43-135, :227-259 restated) with the
+    hierarchy dict h (coarse, fine, s21, q21, s22, q22, fine_of_coarse,
+    p_map): (u, sweeps, f1_evals, f2_evals)."""
+    u0 = np.ascontiguousarray(u0, dtype=np.float64).ravel()
+    uo = np.empty_like(u0)
+    res = np.zeros(256)
+    sw, n1, n2 = C.c_int(), C.c_int(), C.c_int()
+    D = lambda a: np.ascontiguousarray(a, dtype=np.float64)  # noqa: E731
+    I = lambda a: np.ascontiguousarray(a, dtype=np.int32)  # noqa: E731
+    arrs = [D(h[k]) for k in ("coarse", "fine", "s21", "q21", "s22", "q22")]
+    foc, pm = I(h["fine_of_coarse"]), I(h["p_map"])
+    rc = lib().or_integrate_mrsdc1(
+        f1cb, None, f2cb, None, u0.size, dp(u0), C.c_double(t0), C.c_double(t1), nsteps,
+        len(arrs[0]) - 1, dp(arrs[0]), len(arrs[1]) - 1, dp(arrs[1]), dp(arrs[2]), dp(arrs[3]),
+        dp(arrs[4]), dp(arrs[5]), ip(foc), ip(pm), iterations, C.c_double(cutoff), dp(uo),
+        dp(res), res.size, C.byref(sw), C.byref(n1), C.byref(n2))
+    assert rc == 0
+    return uo, sw.value, n1.value, n2.value
+
+
 def ns_temperature_pressure(U):
     n = U[0].size
     T, p = np.empty(U.shape[1:]), np.empty(U.shape[1:])
