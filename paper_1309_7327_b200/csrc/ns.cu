@@ -560,6 +560,83 @@ void NsWorkspace::rhs(const NsStateView& U, double* out, long long out_fs, int p
               part == kNsFull, phase, st, marks_);
 }
 
+std::shared_ptr<NsWorkspace> NsWorkspace::chunk_workspace(int nz_chunk) const {
+  NsBox b = box_;
+  b.nz = nz_chunk;
+  b.G = 4;
+  return std::make_shared<NsWorkspace>(b, dx_[0], dx_[1], dx_[2], M_, s_);
+}
+
+NsRhsOp::~NsRhsOp() {
+  for (cudaEvent_t e : ev_in_) cudaEventDestroy(e);
+  for (cudaEvent_t e : ev_done_) cudaEventDestroy(e);
+  if (ev_halo_) cudaEventDestroy(ev_halo_);
+  if (h2d_) cudaStreamDestroy(h2d_);
+  if (d2h_) cudaStreamDestroy(d2h_);
+}
+
+void NsRhsOp::eval_host(double t, const double* u, double* out) {
+  const NsBox& b = ws_->box();
+  static const int kc = [] {  // planes per chunk (SMC_NS_E2E_CHUNK, default 32)
+    const char* e = std::getenv("SMC_NS_E2E_CHUNK");
+    return e ? std::max(4, std::atoi(e)) : 32;
+  }();
+  if (b.G != 0 || b.nz % kc != 0 || b.nz / kc < 2) {
+    RhsOp::eval_host(t, u, out);
+    return;
+  }
+  require(b.G == 0, "ns: a ghosted (zghost > 0) operator has no plain Rhs view");
+  const int nch = b.nz / kc, G = 4;
+  const long long n = b.cells(), plane = b.plane();
+  stage_u_.resize(static_cast<std::size_t>(SMC_NVAR) * n);
+  stage_out_.resize(static_cast<std::size_t>(SMC_NVAR) * n);
+  if (!chunk_ws_ || chunk_ws_->box().nz != kc) chunk_ws_ = ws_->chunk_workspace(kc);
+  if (!h2d_) {
+    SMC_CUDA(cudaStreamCreateWithFlags(&h2d_, cudaStreamNonBlocking));
+    SMC_CUDA(cudaStreamCreateWithFlags(&d2h_, cudaStreamNonBlocking));
+    SMC_CUDA(cudaEventCreateWithFlags(&ev_halo_, cudaEventDisableTiming));
+  }
+  while (static_cast<int>(ev_in_.size()) < nch) {
+    cudaEvent_t a, c;
+    SMC_CUDA(cudaEventCreateWithFlags(&a, cudaEventDisableTiming));
+    SMC_CUDA(cudaEventCreateWithFlags(&c, cudaEventDisableTiming));
+    ev_in_.push_back(a);
+    ev_done_.push_back(c);
+  }
+  double* dU = stage_u_.get();
+  double* dO = stage_out_.get();
+  auto copy = [&](double* dst, const double* src, int k0, int k1, cudaMemcpyKind kind,
+                  cudaStream_t st) {
+    for (int v = 0; v < SMC_NVAR; ++v)
+      SMC_CUDA(cudaMemcpyAsync(dst + v * n + k0 * plane, src + v * n + k0 * plane,
+                               sizeof(double) * (k1 - k0) * plane, kind, st));
+  };
+  // the previous call's reads of the staging buffers precede this call's writes
+  SMC_CUDA(cudaEventRecord(ev_halo_, stream_));
+  SMC_CUDA(cudaStreamWaitEvent(h2d_, ev_halo_, 0));
+  copy(dU, u, b.nz - G, b.nz, cudaMemcpyHostToDevice, h2d_);  // chunk 0's lower halo
+  SMC_CUDA(cudaEventRecord(ev_halo_, h2d_));
+  for (int c = 0; c < nch; ++c) {
+    const int k0 = c * kc, k1 = c + 1 == nch ? b.nz - G : k0 + kc;
+    copy(dU, u, k0, k1, cudaMemcpyHostToDevice, h2d_);
+    SMC_CUDA(cudaEventRecord(ev_in_[c], h2d_));
+  }
+  for (int c = 0; c < nch; ++c) {
+    const int k0 = c * kc, k1 = k0 + kc;
+    if (c == 0) SMC_CUDA(cudaStreamWaitEvent(stream_, ev_halo_, 0));
+    SMC_CUDA(cudaStreamWaitEvent(stream_, ev_in_[c], 0));
+    if (c + 1 < nch) SMC_CUDA(cudaStreamWaitEvent(stream_, ev_in_[c + 1], 0));
+    const NsStateView view{dU + ((k0 - G + b.nz) % b.nz) * plane, n, dU + k0 * plane, n,
+                           dU + (k1 % b.nz) * plane, n};
+    chunk_ws_->rhs(view, dO + k0 * plane, n, part_, stream_, kNsAll);
+    SMC_CUDA(cudaEventRecord(ev_done_[c], stream_));
+    SMC_CUDA(cudaStreamWaitEvent(d2h_, ev_done_[c], 0));
+    copy(out, dO, k0, k1, cudaMemcpyDeviceToHost, d2h_);
+  }
+  SMC_CUDA(cudaStreamSynchronize(d2h_));
+  ++evals_;
+}
+
 bool NsWorkspace::chem_fd_jacobian(const double* U, const double* FU, double* jac, double atol,
                                    double root_eps, cudaStream_t st) {
   if (box_.G != 0) return false;

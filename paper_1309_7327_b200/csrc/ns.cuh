@@ -84,6 +84,9 @@ class NsWorkspace {
   void temperature_pressure(const double* U, double* T, double* p, cudaStream_t st);
   const NsBox& box() const { return box_; }
   void set_marks(KernelMarks* m) { marks_ = m; }
+  // A workspace for nz_chunk-plane z-chunks of this box (4 ghost planes,
+  // same spacings and stencil): the host-buffer pipeline evaluates chunks.
+  std::shared_ptr<NsWorkspace> chunk_workspace(int nz_chunk) const;
 
  private:
   KernelMarks* marks_ = nullptr;
@@ -126,10 +129,22 @@ class NsRhsOp final : public RhsOp {
   }
   NsWorkspace& workspace() { return *ws_; }
   int part() const { return part_; }
+  // Host buffers (smc_rhs_eval with SMC_HOST): a z-chunk pipeline.  The
+  // state goes H2D chunk by chunk (the box's top 4 planes first: the first
+  // chunk's lower halo); each chunk's RHS runs as soon as it and the next
+  // chunk's first planes have landed, reading its halo in place from the
+  // neighbouring chunks (NsStateView), and its result goes D2H while later
+  // chunks are still arriving (the link is full duplex).
+  void eval_host(double t, const double* u, double* out) override;
+  ~NsRhsOp() override;
 
  private:
   std::shared_ptr<NsWorkspace> ws_;
   int part_;
+  std::shared_ptr<NsWorkspace> chunk_ws_;
+  cudaStream_t h2d_ = nullptr, d2h_ = nullptr;
+  std::vector<cudaEvent_t> ev_in_, ev_done_;
+  cudaEvent_t ev_halo_ = nullptr;
 };
 
 }  // namespace smc
