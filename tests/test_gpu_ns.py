@@ -146,7 +146,7 @@ def test_ns_host_pipeline_matches_device_path(cuda, part, n):
     f = (op.full, op.advdiff, op.chem)[part]
     dev = f(0.0, U).cpu().numpy()
     Uh = U.cpu().pin_memory()
-    host = f(0.0, Uh)
+    host = f(0.0, Uh).numpy()
     errs = [float(np.abs(host[v] - dev[v]).max() / max(np.abs(dev[v]).max(), 1e-300))
             for v in range(14)]
     assert max(errs) <= 1e-13, errs
