@@ -29,7 +29,16 @@ enum : int {
   F_X = F_Y + NSP, F_DH = F_X + NSP, F_DP = F_DH + NSP, F_COUNT = F_DP + NSP
 };
 // acc_ field indices (interior)
-enum : int { A_DM = 0, A_DE = 3, A_DY = 4, A_VC = A_DY + NSP, A_HEAT = A_VC + 3, A_COUNT };
+// acc_ fields (interior): the narrow momentum results of direction x, the
+// direction's sum over species of the narrow species results (for div V_c)
+// and tau : grad u.  Phase A of y and z and phase B write the same layout
+// (first 4 / first 3 entries) into the scratch blocks below.
+enum : int { A_DM = 0, A_DY = 3, A_HEAT = 4, A_COUNT };
+// scratch_ blocks (interior arrays): NA_1 | HY_1 | NA_2 | HY_2 | PB_0 | PB_1 | PB_2
+enum : int {
+  SC_NA1 = 0, SC_HY1 = SC_NA1 + 4, SC_NA2 = SC_HY1 + SMC_NVAR, SC_HY2 = SC_NA2 + 4,
+  SC_PB0 = SC_HY2 + SMC_NVAR, SC_PB1 = SC_PB0 + 3, SC_PB2 = SC_PB1 + 3, SC_COUNT = SC_PB2 + 3
+};
 // mixed_ fields (all planes): M_ij = eta d_i u_j for (i, j), i != j; L_i
 constexpr int MX_COUNT = 9;
 __host__ __device__ constexpr int mx_index(int i, int j) { return 3 * i + j - (j > i) - i; }
@@ -420,12 +429,12 @@ void rhs_v2(const Geo& g, const UV& U, const double* F, double* A, double* GR, d
   }
   const int allp = g.nz + 2 * g.G;
   const long long n = g.plane * g.nz;
-  // scratch SC (93 arrays of n): phase A of directions 1, 2 -> [NA | HY] x 2
-  // (54), phase B of the three directions (3 x 13); ns_assemble2 adds them in
-  double* na1 = SC;
-  double* hy1 = SC + 13 * n;
-  double* na2 = SC + 27 * n;
-  double* hy2 = SC + 40 * n;
+  // scratch SC (SC_COUNT arrays of n): phase A of directions 1, 2 -> [NA |
+  // HY] x 2, phase B of the three directions; ns_assemble2 adds them in
+  double* na1 = SC + SC_NA1 * n;
+  double* hy1 = SC + SC_HY1 * n;
+  double* na2 = SC + SC_NA2 * n;
+  double* hy2 = SC + SC_HY2 * n;
   constexpr int NT = Tile<0, NR_A>::THREADS;
   // ctoprim + the x / y passes over planes [k0, k0 + np)
   auto planes = [&](int k0, int np) {
@@ -454,13 +463,13 @@ void rhs_v2(const Geo& g, const UV& U, const double* F, double* A, double* GR, d
   ns_mixed_fields<<<blocks(g.plane * allp), 256, 0, st>>>(F, GR, A, MX, g);
   SMC_CHECK_LAUNCH();
   mark("mixed_fields");
-  ns_phase_b<0><<<dir_grid<0>(g, g.nz), DT_THREADS, sizeof(PBSmem), st>>>(MX, SC + 54 * n, g);
+  ns_phase_b<0><<<dir_grid<0>(g, g.nz), DT_THREADS, sizeof(PBSmem), st>>>(MX, SC + SC_PB0 * n, g);
   SMC_CHECK_LAUNCH();
   mark("phase_b_x");
-  ns_phase_b<1><<<dir_grid<1>(g, g.nz), DT_THREADS, sizeof(PBSmem), st>>>(MX, SC + 67 * n, g);
+  ns_phase_b<1><<<dir_grid<1>(g, g.nz), DT_THREADS, sizeof(PBSmem), st>>>(MX, SC + SC_PB1 * n, g);
   SMC_CHECK_LAUNCH();
   mark("phase_b_y");
-  ns_phase_b<2><<<dir_grid<2>(g, g.nz), DT_THREADS, sizeof(PBSmem), st>>>(MX, SC + 80 * n, g);
+  ns_phase_b<2><<<dir_grid<2>(g, g.nz), DT_THREADS, sizeof(PBSmem), st>>>(MX, SC + SC_PB2 * n, g);
   SMC_CHECK_LAUNCH();
   mark("phase_b_z");
   ns_assemble2<<<blocks(n), 256, 0, st>>>(F, A, SC, out, ofs, g, chem);
@@ -497,7 +506,7 @@ NsWorkspace::NsWorkspace(const NsBox& box, double dx, double dy, double dz, cons
   acc_.resize(static_cast<std::size_t>(A_COUNT) * box.cells());
   mixed_.resize(static_cast<std::size_t>(MX_COUNT) * box.field_len());
   grad_.resize(static_cast<std::size_t>(9) * box.field_len());
-  scratch_.resize(static_cast<std::size_t>(93) * box.cells());
+  scratch_.resize(static_cast<std::size_t>(SC_COUNT) * box.cells());
 }
 
 static Geo make_geo(const NsBox& b, const double* d) {
