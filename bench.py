@@ -87,6 +87,22 @@ def ns_config(n: int, world: int) -> dict:
     }
 
 
+class stdout_to_stderr:
+    """NCCL may print its version banner on stdout at communicator creation;
+    rank 0's stdout carries exactly one JSON line, so route fd 1 to fd 2
+    meanwhile."""
+
+    def __enter__(self):
+        sys.stdout.flush()
+        self.saved = os.dup(1)
+        os.dup2(2, 1)
+
+    def __exit__(self, *exc):
+        sys.stdout.flush()
+        os.dup2(self.saved, 1)
+        os.close(self.saved)
+
+
 def cpu_info() -> dict:
     model, threads = None, os.cpu_count()
     try:
@@ -520,7 +536,8 @@ def run_mrsdc(args):
         dt = float(t.item())
     U = P.ns_conserved(*(torch.from_numpy(a).to(dev) for a in (T, p, uvw, Y)))
     del T, p, uvw, Y
-    comm = Comm.nccl(dist if world > 1 else None, device=dev)
+    with stdout_to_stderr():
+        comm = Comm.nccl(dist if world > 1 else None, device=dev)
     slab = NsSlab(comm, ng, ng, nz, NS_DX)
     stream = torch.cuda.current_stream()
     slab.set_stream(stream)
@@ -601,7 +618,8 @@ def main():
     out = torch.empty_like(U)
     slab_mode = world > 1 or args.slab
     if slab_mode:
-        comm = Comm.nccl(dist if world > 1 else None, device=dev)
+        with stdout_to_stderr():
+            comm = Comm.nccl(dist if world > 1 else None, device=dev)
         op = NsSlab(comm, n, n, n, NS_DX)
     else:
         op = P.NsOperator(n, n, n, NS_DX)
