@@ -20,6 +20,9 @@
 // The work is FP64-bound (341 flop / 24 B per cell); there
 // is nothing GEMM-shaped here, so no tensor cores.
 #include "common.cuh"
+#include <cstdlib>
+#include <string>
+
 #include "narrow.cuh"
 
 namespace smc {
@@ -374,12 +377,96 @@ int grid_for(long long n) {
   return static_cast<int>(b > 148 * 64 ? 148 * 64 : (b < 1 ? 1 : b));
 }
 
+// Single-pass wide route: a CTA owns a WX x WY tile, stages u with an 8-cell
+// halo (w1 = a D_x u is needed 4 cells past the tile in x, and D_x of u 4
+// further), a (x halo 4) and b (y halo 4), forms w1 / w2 on the tile's
+// extended rows / columns in shared memory and differences them: one read
+// of u, a, b and one write per point (32 B) instead of two passes with two
+// temporaries (the reference's wide_pass1 / wide_pass2, pde.cpp:131-194,
+// whose arithmetic and order it keeps, so the results are the same bits).
+constexpr int WX = 32, WY = 16, WH = 4;
+struct WideSmem {
+  double u[WY + 4 * WH][WX + 4 * WH];  // u over [x0-8, x0+40) x [y0-8, y0+24)
+  double a[WY][WX + 2 * WH];           // a over [x0-4, x0+36) x tile rows
+  double b[WY + 2 * WH][WX];           // b over tile columns x [y0-4, y0+20)
+  double w1[WY][WX + 2 * WH];
+  double w2[WY + 2 * WH][WX];
+};
+
+__device__ __forceinline__ double d8_at(const double* p, int stride, double inv_d) {
+  double w[9];
+#pragma unroll
+  for (int d = -4; d <= 4; ++d) w[d + 4] = d == 0 ? 0.0 : p[d * stride];
+  return deriv8_w(w, inv_d);
+}
+
+__global__ void __launch_bounds__(256) wide_tiled(const double* __restrict__ u,
+                                                  const double* __restrict__ a,
+                                                  const double* __restrict__ b,
+                                                  const double* __restrict__ g0, double gt,
+                                                  double* __restrict__ out, int nx, int ny,
+                                                  double inv_dx, double inv_dy) {
+  __shared__ WideSmem sm;
+  const int x0 = blockIdx.x * WX, y0 = blockIdx.y * WY;
+  const int tid = threadIdx.x;
+  auto gidx = [&](int x, int y) {
+    return static_cast<long long>(wrap(y, ny)) * nx + wrap(x, nx);
+  };
+  constexpr int UW = WX + 4 * WH, UH = WY + 4 * WH;
+  for (int e = tid; e < UW * UH; e += 256) {
+    const int r = e / UW, c = e % UW;
+    sm.u[r][c] = __ldg(u + gidx(x0 - 2 * WH + c, y0 - 2 * WH + r));
+  }
+  for (int e = tid; e < WY * (WX + 2 * WH); e += 256) {
+    const int r = e / (WX + 2 * WH), c = e % (WX + 2 * WH);
+    sm.a[r][c] = __ldg(a + gidx(x0 - WH + c, y0 + r));
+  }
+  for (int e = tid; e < (WY + 2 * WH) * WX; e += 256) {
+    const int r = e / WX, c = e % WX;
+    sm.b[r][c] = __ldg(b + gidx(x0 + c, y0 - WH + r));
+  }
+  __syncthreads();
+  // w1 = a D_x u on the tile rows, x in [x0-4, x0+36); w2 = b D_y u on the
+  // tile columns, y in [y0-4, y0+20)
+  for (int e = tid; e < WY * (WX + 2 * WH); e += 256) {
+    const int r = e / (WX + 2 * WH), c = e % (WX + 2 * WH);
+    sm.w1[r][c] = sm.a[r][c] * d8_at(&sm.u[r + 2 * WH][c + WH], 1, inv_dx);
+  }
+  for (int e = tid; e < (WY + 2 * WH) * WX; e += 256) {
+    const int r = e / WX, c = e % WX;
+    sm.w2[r][c] = sm.b[r][c] * d8_at(&sm.u[r + WH][c + 2 * WH], UW, inv_dy);
+  }
+  __syncthreads();
+  for (int e = tid; e < WX * WY; e += 256) {
+    const int r = e / WX, c = e % WX;
+    double o = d8_at(&sm.w1[r][c + WH], 1, inv_dx);
+    o = __dadd_rn(o, d8_at(&sm.w2[r + WH][c], WX, inv_dy));
+    const long long gi = static_cast<long long>(y0 + r) * nx + x0 + c;
+    if (g0) o = __dadd_rn(o, __dmul_rn(g0[gi], gt));
+    out[gi] = o;
+  }
+}
+
+bool wide_tiled_on() {
+  static const bool on = [] {
+    const char* e = std::getenv("SMC_WIDE");
+    return !(e && std::string(e) == "2pass");
+  }();
+  return on;
+}
+
 }  // namespace
 
 void launch_wide2d(const double* u, const double* a, const double* b, const double* g0, double gt,
                    double* w1, double* w2, double* out, int nx, int ny, double dx, double dy,
                    cudaStream_t st) {
   const long long n = static_cast<long long>(nx) * ny;
+  if (b && nx % WX == 0 && ny % WY == 0 && wide_tiled_on()) {
+    wide_tiled<<<dim3(nx / WX, ny / WY), 256, 0, st>>>(u, a, b, g0, gt, out, nx, ny, 1.0 / dx,
+                                                        1.0 / dy);
+    SMC_CHECK_LAUNCH();
+    return;
+  }
   wide_pass1<<<grid_for(n), 256, 0, st>>>(u, a, b, w1, w2, nx, ny, 1.0 / dx, 1.0 / dy);
   SMC_CHECK_LAUNCH();
   wide_pass2<<<grid_for(n), 256, 0, st>>>(w1, w2, g0, gt, out, nx, ny, 1.0 / dx, 1.0 / dy);

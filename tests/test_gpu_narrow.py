@@ -468,3 +468,36 @@ np.save({out!r}, op(0.3, d['u']))
     subprocess.run([sys.executable, "-c", script], env=dict(os.environ, SMC_HEAT2D="march"),
                    check=True, timeout=300)
     assert rel_err(np.load(out), ref) <= TOL
+
+
+_WIDE_SCRIPT = """
+import sys, numpy as np
+sys.path.insert(0, {root!r})
+import paper_1309_7327_b200 as P
+d = np.load({inp!r})
+op = P.HeatOperator(d['u'].shape[1], d['u'].shape[0], P.StencilChoice.wide8(), d['a'], d['b'],
+                    d['g'], lambda t: 0.75)
+np.save({out!r}, op(0.3, d['u']))
+"""
+
+
+@pytest.mark.parametrize("shape", [(48, 64), (256, 512)])
+def test_wide_tiled_equals_two_pass_bitwise(cuda, tmp_path, shape):
+    """The single-pass tiled wide route (default on 32 x 16 multiples) keeps
+    wide_pass1 / wide_pass2's arithmetic (pde.cpp:131-194): the same bits as
+    the two-pass kernels (SMC_WIDE=2pass, a child process)."""
+    import os
+    import subprocess
+    import sys
+    ny, nx = shape
+    rng = np.random.default_rng(9)
+    a, b = rng.uniform(0.5, 2.0, (ny, nx)), rng.uniform(0.5, 2.0, (ny, nx))
+    g, u = rng.standard_normal((ny, nx)), rng.standard_normal((ny, nx))
+    got = P.HeatOperator(nx, ny, P.StencilChoice.wide8(), a, b, g, lambda t: 0.75)(0.3, u)
+    inp, out = str(tmp_path / "in.npz"), str(tmp_path / "out.npy")
+    np.savez(inp, u=u, a=a, b=b, g=g)
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, SMC_WIDE="2pass")
+    subprocess.run([sys.executable, "-c", _WIDE_SCRIPT.format(root=root, inp=inp, out=out)],
+                   env=env, check=True, timeout=300)
+    assert np.array_equal(got, np.load(out))

@@ -47,9 +47,11 @@ def main():
         res[name] = {"s_per_rhs": t, "ns_per_point": t / (n * n) * 1e9}
     import ctypes as C
     from paper_1309_7327_b200 import _capi
-    pk = C.c_double()
-    _capi.check(_capi.lib().smc_measure_fp64_peak(20000, C.byref(pk)))
-    peak = pk.value
+    v = (C.c_double * 5)()
+    _capi.check(_capi.lib().smc_measure_fp64_variants(4000, v, 5))
+    dm = C.c_double()
+    _capi.check(_capi.lib().smc_measure_dmma_peak(4000, 0, C.byref(dm)))
+    peak = max(list(v) + [dm.value])
     bw = 6531.9e9
     try:
         bw = json.load(open(os.path.join(os.path.dirname(__file__), "..",
@@ -66,6 +68,10 @@ def main():
                     "crossover_bandwidth_GBs": 64.0 * flops / (narrow_f - wide_f) / 1e9}
     res["measured_delta_ns_per_point"] = (res["narrow8"]["ns_per_point"] -
                                           res["wide8"]["ns_per_point"])
+    # the single-pass wide kernel's HBM floor: u, a, b in, out written
+    res["wide8"]["hbm_floor_s"] = 32.0 * n * n / bw
+    res["wide8"]["hbm_frac"] = res["wide8"]["hbm_floor_s"] / res["wide8"]["s_per_rhs"]
+    res["narrow8"]["fp64_frac"] = (2 * 112 + 3 + 2) * n * n / flops / res["narrow8"]["s_per_rhs"]
     print(json.dumps(res, indent=1))
 
 
