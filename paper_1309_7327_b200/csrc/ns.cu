@@ -6,6 +6,7 @@
 //   mixed     : eta d_i u_j, lam2 div, tau:grad u
 //   phase B   : mixed viscous derivatives (ns_dir.inc)
 //   assemble2 : direction sums in order + pointwise terms + wdot
+#include <algorithm>
 #include <cmath>
 #include <cstdint>
 #include <cstdlib>
@@ -584,22 +585,50 @@ NsRhsOp::~NsRhsOp() {
   if (d2h_) cudaStreamDestroy(d2h_);
 }
 
+// Chunk boundaries of the host pipeline: short chunks at both ends (the
+// pipeline's fill and drain), SMC_NS_E2E_CHUNK planes (default 32) in the
+// middle; every chunk holds >= 8 planes (2 x the halo).  Empty when the box
+// is too short to pipeline.
+static std::vector<int> e2e_bounds(int nz) {
+  static const int mid = [] {
+    const char* e = std::getenv("SMC_NS_E2E_CHUNK");
+    return e ? std::max(8, std::atoi(e)) : 32;
+  }();
+  std::vector<int> b{0};
+  if (nz < 2 * mid) return {};
+  int lo = 0, hi = nz;
+  std::vector<int> tail;
+  for (int w : {8, 8, 16}) {  // ramp: 8, 8, 16 planes at each end
+    if (hi - lo < 2 * w + mid) break;
+    lo += w, b.push_back(lo);
+    hi -= w, tail.push_back(hi);
+  }
+  const int nm = std::max(1, (hi - lo + mid - 1) / mid);
+  for (int q = 1; q < nm; ++q) b.push_back(lo + static_cast<int>(1LL * (hi - lo) * q / nm));
+  b.push_back(hi);
+  for (auto it = tail.rbegin(); it != tail.rend(); ++it) b.push_back(*it == hi ? -1 : *it);
+  b.erase(std::remove(b.begin(), b.end(), -1), b.end());
+  if (b.back() != nz) b.push_back(nz);
+  return b;
+}
+
 void NsRhsOp::eval_host(double t, const double* u, double* out) {
   const NsBox& b = ws_->box();
-  static const int kc = [] {  // planes per chunk (SMC_NS_E2E_CHUNK, default 32)
-    const char* e = std::getenv("SMC_NS_E2E_CHUNK");
-    return e ? std::max(4, std::atoi(e)) : 32;
-  }();
-  if (b.G != 0 || b.nz % kc != 0 || b.nz / kc < 2) {
+  const std::vector<int> bnd = b.G == 0 ? e2e_bounds(b.nz) : std::vector<int>{};
+  if (bnd.size() < 3) {
     RhsOp::eval_host(t, u, out);
     return;
   }
-  require(b.G == 0, "ns: a ghosted (zghost > 0) operator has no plain Rhs view");
-  const int nch = b.nz / kc, G = 4;
+  const int nch = static_cast<int>(bnd.size()) - 1, G = 4;
   const long long n = b.cells(), plane = b.plane();
   stage_u_.resize(static_cast<std::size_t>(SMC_NVAR) * n);
   stage_out_.resize(static_cast<std::size_t>(SMC_NVAR) * n);
-  if (!chunk_ws_ || chunk_ws_->box().nz != kc) chunk_ws_ = ws_->chunk_workspace(kc);
+  auto ws_for = [&](int kc) -> NsWorkspace& {
+    for (auto& w : chunk_ws_)
+      if (w->box().nz == kc) return *w;
+    chunk_ws_.push_back(ws_->chunk_workspace(kc));
+    return *chunk_ws_.back();
+  };
   if (!h2d_) {
     SMC_CUDA(cudaStreamCreateWithFlags(&h2d_, cudaStreamNonBlocking));
     SMC_CUDA(cudaStreamCreateWithFlags(&d2h_, cudaStreamNonBlocking));
@@ -626,18 +655,18 @@ void NsRhsOp::eval_host(double t, const double* u, double* out) {
   copy(dU, u, b.nz - G, b.nz, cudaMemcpyHostToDevice, h2d_);  // chunk 0's lower halo
   SMC_CUDA(cudaEventRecord(ev_halo_, h2d_));
   for (int c = 0; c < nch; ++c) {
-    const int k0 = c * kc, k1 = c + 1 == nch ? b.nz - G : k0 + kc;
+    const int k0 = bnd[c], k1 = c + 1 == nch ? b.nz - G : bnd[c + 1];
     copy(dU, u, k0, k1, cudaMemcpyHostToDevice, h2d_);
     SMC_CUDA(cudaEventRecord(ev_in_[c], h2d_));
   }
   for (int c = 0; c < nch; ++c) {
-    const int k0 = c * kc, k1 = k0 + kc;
+    const int k0 = bnd[c], k1 = bnd[c + 1];
     if (c == 0) SMC_CUDA(cudaStreamWaitEvent(stream_, ev_halo_, 0));
     SMC_CUDA(cudaStreamWaitEvent(stream_, ev_in_[c], 0));
     if (c + 1 < nch) SMC_CUDA(cudaStreamWaitEvent(stream_, ev_in_[c + 1], 0));
     const NsStateView view{dU + ((k0 - G + b.nz) % b.nz) * plane, n, dU + k0 * plane, n,
                            dU + (k1 % b.nz) * plane, n};
-    chunk_ws_->rhs(view, dO + k0 * plane, n, part_, stream_, kNsAll);
+    ws_for(k1 - k0).rhs(view, dO + k0 * plane, n, part_, stream_, kNsAll);
     SMC_CUDA(cudaEventRecord(ev_done_[c], stream_));
     SMC_CUDA(cudaStreamWaitEvent(d2h_, ev_done_[c], 0));
     copy(out, dO, k0, k1, cudaMemcpyDeviceToHost, d2h_);

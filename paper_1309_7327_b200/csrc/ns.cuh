@@ -141,7 +141,7 @@ class NsRhsOp final : public RhsOp {
  private:
   std::shared_ptr<NsWorkspace> ws_;
   int part_;
-  std::shared_ptr<NsWorkspace> chunk_ws_;
+  std::vector<std::shared_ptr<NsWorkspace>> chunk_ws_;  // one per chunk size
   cudaStream_t h2d_ = nullptr, d2h_ = nullptr;
   std::vector<cudaEvent_t> ev_in_, ev_done_;
   cudaEvent_t ev_halo_ = nullptr;
