@@ -55,7 +55,7 @@ def parse():
     p.add_argument("--warmup", type=int, default=3)
     p.add_argument("--impl", choices=["ours", "reference"], default="ours")
     p.add_argument("--n", type=int, default=256, help="cells per side per GPU")
-    p.add_argument("--e2e-steps", type=int, default=3)
+    p.add_argument("--e2e-steps", type=int, default=5)
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-secondary", action="store_true",
                    help="skip the configs[1] / heat / time-advance blocks")
@@ -494,9 +494,11 @@ def run_mrsdc(args):
     n_global^3 periodic box split into z-slabs over the ranks, 20 steps at
     CFL 0.5.  Strong scaling: the box is fixed.  The device stepper advances
     each rank's slab with the library's slab RHS (NCCL halo) and reduces the
-    residual over the ranks in the library.  A 512^3 box needs about 1.3 KB of
-    device memory per cell (NS workspace + 43 stepper arrays), ~174 GB: the
-    series starts at 2 GPUs."""
+    residual over the ranks in the library.  Device memory per cell: the
+    MRSDC mode-1 stepper holds 43 states of 14 fields (9 fine-node values,
+    F1 and F2 double-buffered, 8 node integrals, carries) plus the state and
+    the result, the NS workspace ~116 fields: ~6.0 KB per cell, ~800 GB for
+    512^3, so the 512^3 series starts at 8 GPUs."""
     import torch
     import torch.distributed as dist
     import paper_1309_7327_b200 as P
@@ -512,7 +514,7 @@ def run_mrsdc(args):
     ng = args.n_global
     nz = ng // world
     cells_local = ng * ng * nz
-    need = 1.35e3 * cells_local
+    need = 8.0 * (14 * (43 + 2) + 116) * cells_local
     free, _ = torch.cuda.mem_get_info(dev)
     base = {"metric": f"configs[4] MRSDC mode-1 cell-steps/sec ({ng}^3, strong scaling)",
             "unit": "cell-steps/s", "n_gpus": world, "higher_is_better": True,
