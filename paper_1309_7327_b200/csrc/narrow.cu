@@ -384,11 +384,12 @@ int grid_for(long long n) {
 // of u, a, b and one write per point (32 B) instead of two passes with two
 // temporaries (the reference's wide_pass1 / wide_pass2, pde.cpp:131-194,
 // whose arithmetic and order it keeps, so the results are the same bits).
-constexpr int WX = 32, WY = 16, WH = 4;
+constexpr int WX = 32, WY = 32, WH = 4, WT = 256;
+constexpr int UW = WX + 4 * WH, UH = WY + 4 * WH;  // u over [x0-8, x0+40) x [y0-8, y0+40)
 struct WideSmem {
-  double u[WY + 4 * WH][WX + 4 * WH];  // u over [x0-8, x0+40) x [y0-8, y0+24)
-  double a[WY][WX + 2 * WH];           // a over [x0-4, x0+36) x tile rows
-  double b[WY + 2 * WH][WX];           // b over tile columns x [y0-4, y0+20)
+  double u[UH][UW];
+  double a[WY][WX + 2 * WH];  // a over [x0-4, x0+36) x tile rows
+  double b[WY + 2 * WH][WX];  // b over tile columns x [y0-4, y0+36)
   double w1[WY][WX + 2 * WH];
   double w2[WY + 2 * WH][WX];
 };
@@ -400,44 +401,54 @@ __device__ __forceinline__ double d8_at(const double* p, int stride, double inv_
   return deriv8_w(w, inv_d);
 }
 
-__global__ void __launch_bounds__(256) wide_tiled(const double* __restrict__ u,
-                                                  const double* __restrict__ a,
-                                                  const double* __restrict__ b,
-                                                  const double* __restrict__ g0, double gt,
-                                                  double* __restrict__ out, int nx, int ny,
-                                                  double inv_dx, double inv_dy) {
-  __shared__ WideSmem sm;
+// rows [r0, r0 + nr) x columns [c0, c0 + nc) of field f (periodic) into the
+// shared block dst (pitch nc): 16-byte loads when the rows do not wrap in x
+// (every interior tile; x0 and the offsets are even), element loads else.
+template <int NC>
+__device__ __forceinline__ void stage(double* dst, const double* __restrict__ f, int r0, int nr,
+                                      int c0, int nx, int ny) {
+  const bool inside = c0 >= 0 && c0 + NC <= nx;
+  if (inside) {
+    for (int e = threadIdx.x; e < nr * (NC / 2); e += WT) {
+      const int r = e / (NC / 2), c = 2 * (e % (NC / 2));
+      const double2 v = __ldg(reinterpret_cast<const double2*>(
+          f + static_cast<long long>(wrap(r0 + r, ny)) * nx + c0 + c));
+      dst[r * NC + c] = v.x, dst[r * NC + c + 1] = v.y;
+    }
+  } else {
+    for (int e = threadIdx.x; e < nr * NC; e += WT) {
+      const int r = e / NC, c = e % NC;
+      dst[e] = __ldg(f + static_cast<long long>(wrap(r0 + r, ny)) * nx + wrap(c0 + c, nx));
+    }
+  }
+}
+
+__global__ void __launch_bounds__(WT) wide_tiled(const double* __restrict__ u,
+                                                 const double* __restrict__ a,
+                                                 const double* __restrict__ b,
+                                                 const double* __restrict__ g0, double gt,
+                                                 double* __restrict__ out, int nx, int ny,
+                                                 double inv_dx, double inv_dy) {
+  extern __shared__ __align__(16) unsigned char wide_raw[];
+  WideSmem& sm = *reinterpret_cast<WideSmem*>(wide_raw);
   const int x0 = blockIdx.x * WX, y0 = blockIdx.y * WY;
   const int tid = threadIdx.x;
-  auto gidx = [&](int x, int y) {
-    return static_cast<long long>(wrap(y, ny)) * nx + wrap(x, nx);
-  };
-  constexpr int UW = WX + 4 * WH, UH = WY + 4 * WH;
-  for (int e = tid; e < UW * UH; e += 256) {
-    const int r = e / UW, c = e % UW;
-    sm.u[r][c] = __ldg(u + gidx(x0 - 2 * WH + c, y0 - 2 * WH + r));
-  }
-  for (int e = tid; e < WY * (WX + 2 * WH); e += 256) {
-    const int r = e / (WX + 2 * WH), c = e % (WX + 2 * WH);
-    sm.a[r][c] = __ldg(a + gidx(x0 - WH + c, y0 + r));
-  }
-  for (int e = tid; e < (WY + 2 * WH) * WX; e += 256) {
-    const int r = e / WX, c = e % WX;
-    sm.b[r][c] = __ldg(b + gidx(x0 + c, y0 - WH + r));
-  }
+  stage<UW>(&sm.u[0][0], u, y0 - 2 * WH, UH, x0 - 2 * WH, nx, ny);
+  stage<WX + 2 * WH>(&sm.a[0][0], a, y0, WY, x0 - WH, nx, ny);
+  stage<WX>(&sm.b[0][0], b, y0 - WH, WY + 2 * WH, x0, nx, ny);
   __syncthreads();
   // w1 = a D_x u on the tile rows, x in [x0-4, x0+36); w2 = b D_y u on the
-  // tile columns, y in [y0-4, y0+20)
-  for (int e = tid; e < WY * (WX + 2 * WH); e += 256) {
+  // tile columns, y in [y0-4, y0+36)
+  for (int e = tid; e < WY * (WX + 2 * WH); e += WT) {
     const int r = e / (WX + 2 * WH), c = e % (WX + 2 * WH);
     sm.w1[r][c] = sm.a[r][c] * d8_at(&sm.u[r + 2 * WH][c + WH], 1, inv_dx);
   }
-  for (int e = tid; e < (WY + 2 * WH) * WX; e += 256) {
+  for (int e = tid; e < (WY + 2 * WH) * WX; e += WT) {
     const int r = e / WX, c = e % WX;
     sm.w2[r][c] = sm.b[r][c] * d8_at(&sm.u[r + WH][c + 2 * WH], UW, inv_dy);
   }
   __syncthreads();
-  for (int e = tid; e < WX * WY; e += 256) {
+  for (int e = tid; e < WX * WY; e += WT) {
     const int r = e / WX, c = e % WX;
     double o = d8_at(&sm.w1[r][c + WH], 1, inv_dx);
     o = __dadd_rn(o, d8_at(&sm.w2[r + WH][c], WX, inv_dy));
@@ -461,9 +472,15 @@ void launch_wide2d(const double* u, const double* a, const double* b, const doub
                    double* w1, double* w2, double* out, int nx, int ny, double dx, double dy,
                    cudaStream_t st) {
   const long long n = static_cast<long long>(nx) * ny;
-  if (b && nx % WX == 0 && ny % WY == 0 && wide_tiled_on()) {
-    wide_tiled<<<dim3(nx / WX, ny / WY), 256, 0, st>>>(u, a, b, g0, gt, out, nx, ny, 1.0 / dx,
-                                                        1.0 / dy);
+  if (b && nx % WX == 0 && ny % WY == 0 && nx >= UW && wide_tiled_on()) {
+    static bool configured = false;
+    if (!configured) {
+      SMC_CUDA(cudaFuncSetAttribute(wide_tiled, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    static_cast<int>(sizeof(WideSmem))));
+      configured = true;
+    }
+    wide_tiled<<<dim3(nx / WX, ny / WY), WT, sizeof(WideSmem), st>>>(u, a, b, g0, gt, out, nx,
+                                                                     ny, 1.0 / dx, 1.0 / dy);
     SMC_CHECK_LAUNCH();
     return;
   }

@@ -481,7 +481,7 @@ np.save({out!r}, op(0.3, d['u']))
 """
 
 
-@pytest.mark.parametrize("shape", [(48, 64), (256, 512)])
+@pytest.mark.parametrize("shape", [(48, 64), (64, 64), (256, 512), (96, 128)])
 def test_wide_tiled_equals_two_pass_bitwise(cuda, tmp_path, shape):
     """The single-pass tiled wide route (default on 32 x 16 multiples) keeps
     wide_pass1 / wide_pass2's arithmetic (pde.cpp:131-194): the same bits as
