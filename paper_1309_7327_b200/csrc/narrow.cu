@@ -384,14 +384,12 @@ int grid_for(long long n) {
 // of u, a, b and one write per point (32 B) instead of two passes with two
 // temporaries (the reference's wide_pass1 / wide_pass2, pde.cpp:131-194,
 // whose arithmetic and order it keeps, so the results are the same bits).
-constexpr int WX = 32, WY = 32, WH = 4, WT = 256;
+constexpr int WX = 32, WY = 32, WH = 4, WT = 512;
 constexpr int UW = WX + 4 * WH, UH = WY + 4 * WH;  // u over [x0-8, x0+40) x [y0-8, y0+40)
-struct WideSmem {
+struct WideSmem {  // a and b are read once each, straight from global memory
   double u[UH][UW];
-  double a[WY][WX + 2 * WH];  // a over [x0-4, x0+36) x tile rows
-  double b[WY + 2 * WH][WX];  // b over tile columns x [y0-4, y0+36)
-  double w1[WY][WX + 2 * WH];
-  double w2[WY + 2 * WH][WX];
+  double w1[WY][WX + 2 * WH];  // x in [x0-4, x0+36), tile rows
+  double w2[WY + 2 * WH][WX];  // tile columns, y in [y0-4, y0+36)
 };
 
 __device__ __forceinline__ double d8_at(const double* p, int stride, double inv_d) {
@@ -434,18 +432,18 @@ __global__ void __launch_bounds__(WT) wide_tiled(const double* __restrict__ u,
   const int x0 = blockIdx.x * WX, y0 = blockIdx.y * WY;
   const int tid = threadIdx.x;
   stage<UW>(&sm.u[0][0], u, y0 - 2 * WH, UH, x0 - 2 * WH, nx, ny);
-  stage<WX + 2 * WH>(&sm.a[0][0], a, y0, WY, x0 - WH, nx, ny);
-  stage<WX>(&sm.b[0][0], b, y0 - WH, WY + 2 * WH, x0, nx, ny);
   __syncthreads();
   // w1 = a D_x u on the tile rows, x in [x0-4, x0+36); w2 = b D_y u on the
   // tile columns, y in [y0-4, y0+36)
   for (int e = tid; e < WY * (WX + 2 * WH); e += WT) {
     const int r = e / (WX + 2 * WH), c = e % (WX + 2 * WH);
-    sm.w1[r][c] = sm.a[r][c] * d8_at(&sm.u[r + 2 * WH][c + WH], 1, inv_dx);
+    const double ac = __ldg(a + static_cast<long long>(y0 + r) * nx + wrap(x0 - WH + c, nx));
+    sm.w1[r][c] = ac * d8_at(&sm.u[r + 2 * WH][c + WH], 1, inv_dx);
   }
   for (int e = tid; e < (WY + 2 * WH) * WX; e += WT) {
     const int r = e / WX, c = e % WX;
-    sm.w2[r][c] = sm.b[r][c] * d8_at(&sm.u[r + WH][c + 2 * WH], UW, inv_dy);
+    const double bc = __ldg(b + static_cast<long long>(wrap(y0 - WH + r, ny)) * nx + x0 + c);
+    sm.w2[r][c] = bc * d8_at(&sm.u[r + WH][c + 2 * WH], UW, inv_dy);
   }
   __syncthreads();
   for (int e = tid; e < WX * WY; e += WT) {
