@@ -2,6 +2,7 @@
 // (see dist.hpp).
 #include <dlfcn.h>
 
+#include <algorithm>
 #include <cstring>
 #include <mutex>
 #include <string>
@@ -158,6 +159,7 @@ class LocalTransport final : public HaloTransport {
     }
   }
   double allreduce_max(double v, cudaStream_t) override { return v; }
+  bool remote() const override { return false; }
 
  private:
   std::shared_ptr<LocalGroup> g_;
@@ -205,7 +207,86 @@ NsSlabOp::NsSlabOp(std::shared_ptr<HaloTransport> tr, std::shared_ptr<NsWorkspac
 NsSlabOp::~NsSlabOp() {
   if (ev_in_) cudaEventDestroy(ev_in_);
   if (ev_halo_) cudaEventDestroy(ev_halo_);
+  if (ev_bnd_) cudaEventDestroy(ev_bnd_);
+  if (ev_prev_) cudaEventDestroy(ev_prev_);
+  for (cudaEvent_t e : ev_chunk_) cudaEventDestroy(e);
+  for (cudaEvent_t e : ev_done_) cudaEventDestroy(e);
+  if (h2d_) cudaStreamDestroy(h2d_);
+  if (d2h_) cudaStreamDestroy(d2h_);
   if (comm_) cudaStreamDestroy(comm_);
+}
+
+void NsSlabOp::eval_host(double t, const double* u, double* out) {
+  const NsBox& b = ws_->box();
+  const std::vector<int> bnd = ns_e2e_bounds(b.nz);
+  if (!tr_->remote() || part_ == kNsChem || bnd.size() < 3) {
+    RhsOp::eval_host(t, u, out);
+    return;
+  }
+  const int nch = static_cast<int>(bnd.size()) - 1, G = b.G;
+  const long long n = b.cells(), plane = b.plane();
+  stage_u_.resize(static_cast<std::size_t>(SMC_NVAR) * n);
+  stage_out_.resize(static_cast<std::size_t>(SMC_NVAR) * n);
+  auto ws_for = [&](int kc) -> NsWorkspace& {
+    for (auto& w : chunk_ws_)
+      if (w->box().nz == kc) return *w;
+    chunk_ws_.push_back(ws_->chunk_workspace(kc));
+    return *chunk_ws_.back();
+  };
+  if (!h2d_) {
+    SMC_CUDA(cudaStreamCreateWithFlags(&h2d_, cudaStreamNonBlocking));
+    SMC_CUDA(cudaStreamCreateWithFlags(&d2h_, cudaStreamNonBlocking));
+    SMC_CUDA(cudaEventCreateWithFlags(&ev_bnd_, cudaEventDisableTiming));
+    SMC_CUDA(cudaEventCreateWithFlags(&ev_prev_, cudaEventDisableTiming));
+  }
+  while (static_cast<int>(ev_chunk_.size()) < nch) {
+    cudaEvent_t a, c;
+    SMC_CUDA(cudaEventCreateWithFlags(&a, cudaEventDisableTiming));
+    SMC_CUDA(cudaEventCreateWithFlags(&c, cudaEventDisableTiming));
+    ev_chunk_.push_back(a);
+    ev_done_.push_back(c);
+  }
+  double* dU = stage_u_.get();
+  double* dO = stage_out_.get();
+  auto copy = [&](double* dst, const double* src, int k0, int k1, cudaMemcpyKind kind,
+                  cudaStream_t st) {
+    if (k1 <= k0) return;
+    for (int v = 0; v < SMC_NVAR; ++v)
+      SMC_CUDA(cudaMemcpyAsync(dst + v * n + k0 * plane, src + v * n + k0 * plane,
+                               sizeof(double) * (k1 - k0) * plane, kind, st));
+  };
+  // the previous evaluation's reads of the staging and halo buffers come first
+  SMC_CUDA(cudaEventRecord(ev_prev_, stream_));
+  SMC_CUDA(cudaStreamWaitEvent(h2d_, ev_prev_, 0));
+  SMC_CUDA(cudaStreamWaitEvent(comm_, ev_prev_, 0));
+  copy(dU, u, 0, G, cudaMemcpyHostToDevice, h2d_);           // the planes the
+  copy(dU, u, b.nz - G, b.nz, cudaMemcpyHostToDevice, h2d_);  // neighbours need
+  SMC_CUDA(cudaEventRecord(ev_bnd_, h2d_));
+  SMC_CUDA(cudaStreamWaitEvent(comm_, ev_bnd_, 0));
+  tr_->exchange(dU, n, lo_.get(), hi_.get(), plane, G, b.nz, SMC_NVAR, comm_);
+  SMC_CUDA(cudaEventRecord(ev_halo_, comm_));
+  for (int c = 0; c < nch; ++c) {
+    const int k0 = std::max(bnd[c], G), k1 = std::min(bnd[c + 1], b.nz - G);
+    copy(dU, u, k0, k1, cudaMemcpyHostToDevice, h2d_);
+    SMC_CUDA(cudaEventRecord(ev_chunk_[c], h2d_));
+  }
+  SMC_CUDA(cudaStreamWaitEvent(stream_, ev_bnd_, 0));
+  for (int c = 0; c < nch; ++c) {
+    const int k0 = bnd[c], k1 = bnd[c + 1];
+    SMC_CUDA(cudaStreamWaitEvent(stream_, ev_chunk_[c], 0));
+    if (c + 1 < nch) SMC_CUDA(cudaStreamWaitEvent(stream_, ev_chunk_[c + 1], 0));
+    if (c == 0 || c + 1 == nch) SMC_CUDA(cudaStreamWaitEvent(stream_, ev_halo_, 0));
+    const long long hs = G * plane;
+    const NsStateView view{c == 0 ? lo_.get() : dU + (k0 - G) * plane, c == 0 ? hs : n,
+                           dU + k0 * plane, n,
+                           c + 1 == nch ? hi_.get() : dU + k1 * plane, c + 1 == nch ? hs : n};
+    ws_for(k1 - k0).rhs(view, dO + k0 * plane, n, part_, stream_, kNsAll);
+    SMC_CUDA(cudaEventRecord(ev_done_[c], stream_));
+    SMC_CUDA(cudaStreamWaitEvent(d2h_, ev_done_[c], 0));
+    copy(out, dO, k0, k1, cudaMemcpyDeviceToHost, d2h_);
+  }
+  SMC_CUDA(cudaStreamSynchronize(d2h_));
+  ++evals_;
 }
 
 void NsSlabOp::eval_device(double, const double* u, double* out) {

@@ -44,6 +44,9 @@ class HaloTransport {
   // In-process groups: the state this rank's neighbours read in their next
   // exchange (the NCCL transport sends instead and ignores it).
   virtual void publish(const double* /*u*/, long long /*ufs*/) {}
+  // true when the neighbours' halo arrives by messages (NCCL), false for an
+  // in-process group reading published device states
+  virtual bool remote() const { return true; }
 };
 
 // NCCL: `id` is NCCL_UNIQUE_ID_BYTES (128) bytes from nccl_unique_id() on one
@@ -65,8 +68,19 @@ class NsSlabOp final : public RhsOp {
   const char* name() const override { return "ns_slab"; }
   HaloTransport& transport() { return *tr_; }
   void publish(const double* u) { tr_->publish(u, ws_->box().cells()); }
+  // Host buffers: the rank's 4 bottom and 4 top planes go H2D first and to
+  // the neighbours while the rest of the state streams in chunk by chunk;
+  // each chunk's RHS (halo read in place: the neighbouring chunks, or the
+  // received blocks at the slab's ends) runs as soon as its planes landed,
+  // and its result goes D2H meanwhile (NsRhsOp::eval_host's pipeline with
+  // the exchange folded in).  In-process groups take the plain path.
+  void eval_host(double t, const double* u, double* out) override;
 
  private:
+  std::vector<std::shared_ptr<NsWorkspace>> chunk_ws_;
+  cudaStream_t h2d_ = nullptr, d2h_ = nullptr;
+  std::vector<cudaEvent_t> ev_chunk_, ev_done_;
+  cudaEvent_t ev_bnd_ = nullptr, ev_prev_ = nullptr;
   std::shared_ptr<HaloTransport> tr_;
   std::shared_ptr<NsWorkspace> ws_;
   int part_;

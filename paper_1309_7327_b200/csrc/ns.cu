@@ -589,7 +589,7 @@ NsRhsOp::~NsRhsOp() {
 // pipeline's fill and drain), SMC_NS_E2E_CHUNK planes (default 32) in the
 // middle; every chunk holds >= 8 planes (2 x the halo).  Empty when the box
 // is too short to pipeline.
-static std::vector<int> e2e_bounds(int nz) {
+std::vector<int> ns_e2e_bounds(int nz) {
   static const int mid = [] {
     const char* e = std::getenv("SMC_NS_E2E_CHUNK");
     return e ? std::max(8, std::atoi(e)) : 32;
@@ -614,7 +614,7 @@ static std::vector<int> e2e_bounds(int nz) {
 
 void NsRhsOp::eval_host(double t, const double* u, double* out) {
   const NsBox& b = ws_->box();
-  const std::vector<int> bnd = b.G == 0 ? e2e_bounds(b.nz) : std::vector<int>{};
+  const std::vector<int> bnd = b.G == 0 ? ns_e2e_bounds(b.nz) : std::vector<int>{};
   if (bnd.size() < 3) {
     RhsOp::eval_host(t, u, out);
     return;

@@ -101,6 +101,11 @@ class NsWorkspace {
   DevBuf scratch_;  // v2: per-direction results (93 interior arrays), summed in order
 };
 
+// Chunk boundaries of the host-buffer pipelines (0 = b[0] < ... < b.back() =
+// nz): 8, 8, 16-plane chunks at both ends, ~32 in the middle; empty when nz
+// is too short to pipeline.
+std::vector<int> ns_e2e_bounds(int nz);
+
 // Conserved state from primitives (T, p, u, v, w, Y_k), n cells, device ptrs.
 void ns_conserved_from_primitives(const double* T, const double* p, const double* uvw,
                                   const double* Y, long long n, double* U, cudaStream_t st);

@@ -106,3 +106,24 @@ def test_slab_rejects_thin_slabs(cuda):
     comms = Comm.local_group(2)
     with pytest.raises(ValueError):
         NsSlab(comms[0], 32, 32, 2, DX)  # fewer planes than the halo is deep
+
+
+@pytest.mark.parametrize("part", [P.NS_FULL, P.NS_ADVDIFF, P.NS_CHEM])
+def test_nccl_slab_host_pipeline_matches_device_path(cuda, part):
+    """Host buffers on an NCCL slab: boundary planes first, the halo
+    exchange folded into the chunk pipeline; the same RHS as the device
+    path."""
+    import torch
+    from paper_1309_7327_b200 import _capi
+    n = 64
+    T, p, uvw, Y = W.ns_primitives(n, hot_spot=True)
+    U = O.ns_conserved(T, p, uvw, Y)
+    try:
+        comm = Comm.nccl()
+    except _capi.SmcError as exc:
+        pytest.skip(f"NCCL unavailable: {exc}")
+    slab = NsSlab(comm, n, n, n, DX)
+    f = (slab.full, slab.advdiff, slab.chem)[part]
+    dev = f(0.0, torch.from_numpy(U).to(cuda)).cpu().numpy()
+    host = f(0.0, torch.from_numpy(U).pin_memory()).numpy()
+    assert _percomp(host, dev) <= 1e-13
