@@ -1,7 +1,20 @@
+# The round's measurement commands (run under gpurun from the repo root; each
+# ncu command only after the same command exited 0 without ncu).
 set -x
-python bench.py > gpurun_out/bench_r01c.log 2>&1; tail -1 gpurun_out/bench_r01c.log | head -c 600; echo
-ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file gpurun_out/launches_r01c.csv python bench.py --steps 20 --warmup 3 --no-cpu-baseline --no-ns --no-advance --e2e-steps 3 > gpurun_out/ncu_l.log 2>&1
-ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/ns256_launches_r01c.csv python tools/ns_bench.py 256 1 > gpurun_out/ncu_ns.log 2>&1
-ncu --set full --import-source on --clock-control none -k regex:narrow3d_fast -s 3 -c 1 -o gpurun_out/prof_narrow_r01c python bench.py --steps 5 --warmup 3 --no-cpu-baseline --no-ns --no-advance --e2e-steps 3 > gpurun_out/ncu_n.log 2>&1
-ncu --set full --import-source on --clock-control none -k "regex:ns_phase|prim_kernel|ns_assemble2|wdot_kernel|chem_kernel|ns_mixed" -c 12 -o gpurun_out/prof_ns_r01c python tools/ns_bench.py 128 1 > gpurun_out/ncu_ns2.log 2>&1
+python bench.py > gpurun_out/bench.json 2> gpurun_out/bench.err; tail -c 600 gpurun_out/bench.json; echo
+python bench.py --impl reference --steps 3 --warmup 1 > gpurun_out/bench_ref.json 2>&1
+# launch list + DRAM bytes of the NS RHS (full, advection-diffusion, chemistry)
+python tools/ns_bench.py 256 1 > gpurun_out/nsb.log 2>&1 && \
+ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none \
+    --csv --log-file gpurun_out/ns256_launches.csv python tools/ns_bench.py 256 1 > gpurun_out/ncu_l.log 2>&1
+# full sections of one NS RHS (its 9 kernels) and of the configs[1] kernel
+ncu --set full --import-source on --clock-control none -k 'regex:ns_phase|prim_kernel|ns_assemble2|ns_mixed' \
+    -c 9 -o gpurun_out/prof_ns python tools/ns_bench.py 256 1 > gpurun_out/ncu_ns.log 2>&1
+python tools/narrow_time.py 256 50 > gpurun_out/nt.log 2>&1 && \
+ncu --set full --import-source on --clock-control none -k regex:narrow3d_fast -s 3 -c 1 \
+    -o gpurun_out/prof_narrow python tools/narrow_time.py 256 50 > gpurun_out/ncu_n.log 2>&1
+# one SDC and one MRSDC step at 128^3: shares and DRAM bytes per launch
+python tools/advance_launches.py 128 mrsdc > gpurun_out/adv.log 2>&1 && \
+ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none \
+    --csv --log-file gpurun_out/adv_mrsdc.csv python tools/advance_launches.py 128 mrsdc > gpurun_out/ncu_a.log 2>&1
 ls -la gpurun_out
