@@ -183,12 +183,14 @@ def ns_conserved(T, p, uvw, Y) -> np.ndarray:
     return U
 
 
-def ns_rhs(U, dx, part=0, m64=None, s=4) -> np.ndarray:
+def ns_rhs(U, dx, part=0, m64=None, s=4, dy=None, dz=None) -> np.ndarray:
     _, nz, ny, nx = U.shape
     if m64 is None:
         m64, s = build_narrow(8, (3557.0 / 44100.0, -2083.0 / 117600.0))
     out = np.empty_like(U)
-    rc = lib().or_ns_rhs(dp(U), nx, ny, nz, C.c_double(dx), C.c_double(dx), C.c_double(dx),
+    dy = dx if dy is None else dy
+    dz = dx if dz is None else dz
+    rc = lib().or_ns_rhs(dp(U), nx, ny, nz, C.c_double(dx), C.c_double(dy), C.c_double(dz),
                          dp(m64), s, part, dp(out))
     assert rc == 0
     return out
