@@ -105,6 +105,23 @@ inline Field first_derivative8(const Field& u, double dx) {
                                       SMC_HOST));
   return out;
 }
+// Non-periodic lines with the paper's boundary closure (smc_b200.h
+// smc_apply_narrow_bounded): one line of u.size() cells.
+inline Field apply_narrow_bounded(const Field& a, const Field& u, double dx,
+                                  const std::vector<double>& params = {}) {
+  if (a.size() != u.size()) throw std::invalid_argument("apply_narrow_bounded: size mismatch");
+  Field out(u.size());
+  detail::check(smc_apply_narrow_bounded(params.data(), static_cast<int>(params.size()), a.data(),
+                                         u.data(), static_cast<int>(u.size()), 1, dx, out.data(),
+                                         SMC_HOST));
+  return out;
+}
+inline Field first_derivative_bounded(const Field& u, double dx) {
+  Field out(u.size());
+  detail::check(smc_first_derivative_bounded(u.data(), static_cast<int>(u.size()), 1, dx,
+                                             out.data(), SMC_HOST));
+  return out;
+}
 inline Field apply_wide(const Field& a, const Field& u, double dx) {
   if (a.size() != u.size()) throw std::invalid_argument("apply_wide: size mismatch");
   Field out(u.size());

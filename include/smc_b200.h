@@ -130,6 +130,21 @@ int smc_apply_narrow(int order, const double* params, int nparams, const double*
                      const double* u, int n, double dx, double* out, int where);
 /* nsdc::first_derivative8 — core/src/stencil.cpp:157-169. */
 int smc_first_derivative8(const double* u, int n, double dx, double* out, int where);
+/* Non-periodic lines (no reference counterpart: the reference's operators
+ * are periodic; this is the physical-boundary closure of PAPER.md:449-461):
+ * nlines contiguous lines of n >= 8 cells.  Diffusion (a u_x)_x: 8th-order
+ * narrow stencils from the fifth cell in, 6th / 4th-order centred narrow
+ * stencils at the fourth / third cells, centred 2nd order at the second and
+ * completely biased 2nd order at the boundary cell.  params = {} (SMC
+ * defaults), {m47, m48} or {m47, m48, m36} (the 6th-order matrix of the
+ * fourth cells; default 281/3600, stencil.hpp:33). */
+int smc_apply_narrow_bounded(const double* params, int nparams, const double* a, const double* u,
+                             int n, int nlines, double dx, double* out, int where);
+/* First derivative with the same closure: 8th / 6th / 4th-order centred,
+ * biased 3rd order at the second cell and completely biased 3rd order at
+ * the boundary cell. */
+int smc_first_derivative_bounded(const double* u, int n, int nlines, double dx, double* out,
+                                 int where);
 /* nsdc::apply_wide — core/src/stencil.cpp:171-176. */
 int smc_apply_wide(const double* a, const double* u, int n, double dx, double* out, int where);
 

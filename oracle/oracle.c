@@ -815,3 +815,91 @@ int or_get_threads(void) {
   return 1;
 #endif
 }
+
+/* ------------------------------------------- physical boundaries (§8(f) 4)
+ * Non-periodic lines with the closure of PAPER.md:449-461: 8th-order stencils
+ * from the fifth cell on, 6th and 4th-order centred stencils at the fourth
+ * and third cells, centred 2nd order (diffusion) / biased 3rd order
+ * (advection) at the second cell, completely biased 2nd (diffusion) / 3rd
+ * (advection) order at the boundary cell; mirrored at the far end.  The
+ * paper gives the orders, not the coefficients: the centred narrow
+ * interfaces of order 6 use the reference's 6th-order matrix at its default
+ * parameter (stencil.hpp:33, m36 = 281/3600), order 4 the narrow matrix of
+ * the 2-parameter 4th-order family with zero corners (m33 = 0, m32 = -1/12:
+ * for a = 1 the classic (-1, 16, -30, 16, -1)/12), order 2
+ * H = (a_i + a_{i+1})/2 (u_{i+1} - u_i); the biased formulas are the
+ * classical one-sided ones. */
+static const double M4B[4][4] = {{0.0, 1.0 / 12.0, -1.0 / 12.0, 0.0},
+                                 {1.0 / 12.0, -3.0 / 4.0, 2.0 / 3.0, 0.0},
+                                 {0.0, -2.0 / 3.0, 3.0 / 4.0, -1.0 / 12.0},
+                                 {0.0, 1.0 / 12.0, -1.0 / 12.0, 0.0}};
+
+/* one narrow interface i+1/2 of half width s from an 8x8 (or smaller) matrix */
+static double iface(int s, const double* mat, int pitch, const double* a, const double* u, int i) {
+  double acc = 0.0;
+  for (int mm = -s + 1; mm <= s; ++mm) {
+    double v = 0.0;
+    for (int nn = -s + 1; nn <= s; ++nn) v += mat[(mm + s - 1) * pitch + nn + s - 1] * u[i + nn];
+    acc += a[i + mm] * v;
+  }
+  return acc;
+}
+
+/* interface i+1/2 at the order of cell `cell` (the cell it is differenced for) */
+static double iface_bounded(const double* m8, const double* m6, const double* a, const double* u,
+                            int n, int cell, int i) {
+  const int d = cell < n - 1 - cell ? cell : n - 1 - cell; /* distance to the boundary */
+  if (d >= 4) return iface(4, m8, 8, a, u, i);
+  if (d == 3) return iface(3, m6, 8, a, u, i);
+  if (d == 2) return iface(2, &M4B[0][0], 4, a, u, i);
+  return 0.5 * (a[i] + a[i + 1]) * (u[i + 1] - u[i]); /* d == 1 */
+}
+
+/* (a u_x)_x with one-sided 2nd-order formulas at a boundary cell; dir = +1
+ * at the left end (cells 0, 1, 2, 3), -1 at the right end (mirrored) */
+static double diff_biased(const double* a, const double* u, int i, int dir, double dx) {
+  const double* ua = u + i;
+  const double* aa = a + i;
+  const double ux = dir * (-3.0 * ua[0] + 4.0 * ua[dir] - ua[2 * dir]) / (2.0 * dx);
+  const double ax = dir * (-3.0 * aa[0] + 4.0 * aa[dir] - aa[2 * dir]) / (2.0 * dx);
+  const double uxx = (2.0 * ua[0] - 5.0 * ua[dir] + 4.0 * ua[2 * dir] - ua[3 * dir]) / (dx * dx);
+  return aa[0] * uxx + ax * ux;
+}
+
+int or_apply_narrow_bounded(const double* m8, const double* m6, const double* a, const double* u,
+                            int n, double dx, double* out) {
+  if (n < 8 || !(dx > 0.0)) return 1;
+  const double id2 = 1.0 / (dx * dx);
+  for (int i = 0; i < n; ++i) {
+    if (i == 0 || i == n - 1) {
+      out[i] = diff_biased(a, u, i, i == 0 ? 1 : -1, dx);
+      continue;
+    }
+    const double hr = iface_bounded(m8, m6, a, u, n, i, i);
+    const double hl = iface_bounded(m8, m6, a, u, n, i, i - 1);
+    out[i] = (hr - hl) * id2;
+  }
+  return 0;
+}
+
+int or_first_derivative_bounded(const double* u, int n, double dx, double* out) {
+  if (n < 8 || !(dx > 0.0)) return 1;
+  for (int i = 0; i < n; ++i) {
+    const int d = i < n - 1 - i ? i : n - 1 - i;
+    const int dir = i < n - 1 - i ? 1 : -1;
+    const double* w = u + i;
+    double v;
+    if (d >= 4)
+      v = C1 * (w[1] - w[-1]) + C2 * (w[2] - w[-2]) + C3 * (w[3] - w[-3]) + C4 * (w[4] - w[-4]);
+    else if (d == 3)
+      v = 0.75 * (w[1] - w[-1]) - 0.15 * (w[2] - w[-2]) + (1.0 / 60.0) * (w[3] - w[-3]);
+    else if (d == 2)
+      v = (2.0 / 3.0) * (w[1] - w[-1]) - (1.0 / 12.0) * (w[2] - w[-2]);
+    else if (d == 1) /* biased 3rd order: (-2 u_{i-1} - 3 u_i + 6 u_{i+1} - u_{i+2}) / 6 */
+      v = dir * (-2.0 * w[-dir] - 3.0 * w[0] + 6.0 * w[dir] - w[2 * dir]) / 6.0;
+    else /* completely biased 3rd order: (-11 u_0 + 18 u_1 - 9 u_2 + 2 u_3) / 6 */
+      v = dir * (-11.0 * w[0] + 18.0 * w[dir] - 9.0 * w[2 * dir] + 2.0 * w[3 * dir]) / 6.0;
+    out[i] = v / dx;
+  }
+  return 0;
+}

@@ -34,6 +34,13 @@ int or_apply_narrow(const double* m64, int s, const double* a, const double* u, 
 
 /* stencil.cpp:157-169 / stencil_kernel.hpp:48-54 (periodic 8th-order D). */
 int or_first_derivative8(const double* u, int n, double dx, double* out);
+
+/* Non-periodic lines with the boundary closure of PAPER.md:449-461 (see
+ * oracle.c): m8 = the 8th-order matrix (or_build_narrow(8, ...)), m6 = the
+ * 6th-order one for the fourth cells; n >= 8. */
+int or_apply_narrow_bounded(const double* m8, const double* m6, const double* a, const double* u,
+                            int n, double dx, double* out);
+int or_first_derivative_bounded(const double* u, int n, double dx, double* out);
 /* stencil.cpp:171-176 */
 int or_apply_wide(const double* a, const double* u, int n, double dx, double* out);
 

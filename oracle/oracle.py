@@ -91,6 +91,37 @@ def build_narrow(order: int, params) -> tuple[np.ndarray, int]:
     return m, s.value
 
 
+def apply_narrow_bounded(params8, a, u, dx, m36=281.0 / 3600.0) -> np.ndarray:
+    """or_apply_narrow_bounded on one non-periodic line."""
+    m8, _ = build_narrow(8, params8)
+    m6, _ = build_narrow(6, (m36,))
+    a = np.ascontiguousarray(a, dtype=np.float64)
+    u = np.ascontiguousarray(u, dtype=np.float64)
+    out = np.empty_like(u)
+    rc = lib().or_apply_narrow_bounded(dp(m8), dp(m6), dp(a), dp(u), len(u), C.c_double(dx),
+                                       dp(out))
+    if rc:
+        raise ValueError("or_apply_narrow_bounded: bad args")
+    return out
+
+
+def first_derivative_bounded(u, dx) -> np.ndarray:
+    u = np.ascontiguousarray(u, dtype=np.float64)
+    out = np.empty_like(u)
+    rc = lib().or_first_derivative_bounded(dp(u), len(u), C.c_double(dx), dp(out))
+    if rc:
+        raise ValueError("or_first_derivative_bounded: bad args")
+    return out
+
+
+def first_derivative8(u, dx) -> np.ndarray:
+    """or_first_derivative8 (periodic)."""
+    u = np.ascontiguousarray(u, dtype=np.float64)
+    out = np.empty_like(u)
+    assert lib().or_first_derivative8(dp(u), len(u), C.c_double(dx), dp(out)) == 0
+    return out
+
+
 def narrow3d(m64, s, a, u, dx, dy, dz) -> np.ndarray:
     nz, ny, nx = u.shape
     out = np.empty_like(u)

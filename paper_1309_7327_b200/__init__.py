@@ -27,7 +27,8 @@ from ._capi import (CLENSHAW_CURTIS, DEVICE, GAUSS_LOBATTO, HOST, NARROW6, NARRO
 
 __all__ = [
     "SmcError", "SmcInvalidArgument", "SmcIntegrationError", "StencilChoice", "stencil_preset",
-    "build_narrow", "apply_narrow", "apply_wide", "first_derivative8", "HeatOperator",
+    "build_narrow", "apply_narrow", "apply_wide", "first_derivative8",
+    "apply_narrow_bounded", "first_derivative_bounded", "HeatOperator",
     "Narrow3DOperator", "Narrow3DSlab", "CallbackRhs", "DeviceCallbackRhs", "SdcStepper",
     "MrsdcStepper", "StepControls", "StiffOptions", "NewtonReport", "solve_backward_euler", "integrate_stiff", "nodes",
     "integration_matrices", "build_hierarchy", "SMC_M47", "SMC_M48", "OPTIMAL_M47", "NsOperator",
@@ -104,22 +105,59 @@ def _out_like(u):
 
 
 def apply_narrow(order: int, params, a, u, dx: float):
+    w = check_arrays(_capi.numel(u), a, u, names=("a", "u"))
     out = _out_like(u)
     pp, keep = _params(params)
     check(_capi.lib().smc_apply_narrow(order, pp, len(params), dptr(a), dptr(u), len(u), dx,
-                                       dptr(out), where_of(u)))
+                                       dptr(out), w))
     return out
 
 
 def first_derivative8(u, dx: float):
+    w = check_arrays(_capi.numel(u), u, names=("u",))
     out = _out_like(u)
-    check(_capi.lib().smc_first_derivative8(dptr(u), len(u), dx, dptr(out), where_of(u)))
+    check(_capi.lib().smc_first_derivative8(dptr(u), len(u), dx, dptr(out), w))
     return out
 
 
 def apply_wide(a, u, dx: float):
+    w = check_arrays(_capi.numel(u), a, u, names=("a", "u"))
     out = _out_like(u)
-    check(_capi.lib().smc_apply_wide(dptr(a), dptr(u), len(u), dx, dptr(out), where_of(u)))
+    check(_capi.lib().smc_apply_wide(dptr(a), dptr(u), len(u), dx, dptr(out), w))
+    return out
+
+
+def _lines(u):
+    """(n, nlines) of a 1-D line or a (nlines, n) batch of lines."""
+    shape = tuple(u.shape)
+    if len(shape) == 1:
+        return shape[0], 1
+    if len(shape) == 2:
+        return shape[1], shape[0]
+    raise SmcInvalidArgument("expected one line (n,) or a batch of lines (nlines, n)")
+
+
+def apply_narrow_bounded(a, u, dx: float, params=()):
+    """(a u_x)_x on non-periodic lines with the paper's boundary closure
+    (include/smc_b200.h smc_apply_narrow_bounded).  u, a:
+    (n,) or (nlines, n); params = () / (m47, m48) / (m47, m48, m36)."""
+    n, nl = _lines(u)
+    w = check_arrays(n * nl, a, u, names=("a", "u"))
+    if len(params) not in (0, 2, 3):
+        raise SmcInvalidArgument("params: (), (m47, m48) or (m47, m48, m36)")
+    keep = (C.c_double * 3)(*(list(params) + [0.0] * 3)[:3])
+    out = _out_like(u)
+    check(_capi.lib().smc_apply_narrow_bounded(C.cast(keep, C.POINTER(C.c_double)), len(params),
+                                               dptr(a), dptr(u), n, nl, dx, dptr(out), w))
+    return out
+
+
+def first_derivative_bounded(u, dx: float):
+    """du/dx on non-periodic lines with the paper's boundary closure."""
+    n, nl = _lines(u)
+    w = check_arrays(n * nl, u, names=("u",))
+    out = _out_like(u)
+    check(_capi.lib().smc_first_derivative_bounded(dptr(u), n, nl, dx, dptr(out), w))
     return out
 
 

@@ -76,6 +76,10 @@ _SIG = {
     "smc_apply_narrow": (C.c_int, [C.c_int, _D, C.c_int, _VP, _VP, C.c_int, C.c_double, _VP,
                                    C.c_int]),
     "smc_first_derivative8": (C.c_int, [_VP, C.c_int, C.c_double, _VP, C.c_int]),
+    "smc_apply_narrow_bounded": (C.c_int, [_D, C.c_int, _VP, _VP, C.c_int, C.c_int, C.c_double,
+                                           _VP, C.c_int]),
+    "smc_first_derivative_bounded": (C.c_int, [_VP, C.c_int, C.c_int, C.c_double, _VP,
+                                               C.c_int]),
     "smc_apply_wide": (C.c_int, [_VP, _VP, C.c_int, C.c_double, _VP, C.c_int]),
     "smc_heat_create": (C.c_int, [C.c_int, C.c_int, C.c_int, _D, _D, _D, _D, C.POINTER(_VP)]),
     "smc_heat_set_time_source": (C.c_int, [_VP, TIME_FN, _VP]),

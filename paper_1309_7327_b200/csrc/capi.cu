@@ -168,6 +168,43 @@ int smc_first_derivative8(const double* u, int n, double dx, double* out, int wh
   });
 }
 
+int smc_apply_narrow_bounded(const double* params, int nparams, const double* a, const double* u,
+                             int n, int nlines, double dx, double* out, int where) {
+  return guarded([&] {
+    need(a, "a"), need(u, "u"), need(out, "out");
+    smc::require(nparams == 0 || nparams == 2 || nparams == 3,
+                 "apply_narrow_bounded: params are {} or {m47, m48} or {m47, m48, m36}");
+    if (nparams) need(params, "params");
+    const double p8[2] = {nparams ? params[0] : 3557.0 / 44100.0,
+                          nparams ? params[1] : -2083.0 / 117600.0};
+    const double p6[1] = {nparams == 3 ? params[2] : 281.0 / 3600.0};
+    const smc::StencilM m8 = smc::make_stencil(8, p8, 2, nullptr);
+    const smc::StencilM m6 = smc::make_stencil(6, p6, 1, nullptr);
+    smc::require(n >= 8 && nlines >= 1, "apply_narrow_bounded: need n >= 8 and nlines >= 1");
+    const long long total = static_cast<long long>(n) * nlines;
+    Staged da(a, total, where, nullptr), du(u, total, where, nullptr);
+    StagedOut o(out, total, where);
+    smc::launch_narrow_bounded(m8, m6, da.dev, du.dev, o.dev, n, nlines, dx, nullptr);
+    o.finish(nullptr);
+    SMC_CUDA(cudaStreamSynchronize(nullptr));
+  });
+}
+
+int smc_first_derivative_bounded(const double* u, int n, int nlines, double dx, double* out,
+                                 int where) {
+  return guarded([&] {
+    need(u, "u"), need(out, "out");
+    smc::require(n >= 8 && nlines >= 1,
+                 "first_derivative_bounded: need n >= 8 and nlines >= 1");
+    const long long total = static_cast<long long>(n) * nlines;
+    Staged du(u, total, where, nullptr);
+    StagedOut o(out, total, where);
+    smc::launch_deriv_bounded(du.dev, o.dev, n, nlines, dx, nullptr);
+    o.finish(nullptr);
+    SMC_CUDA(cudaStreamSynchronize(nullptr));
+  });
+}
+
 int smc_apply_wide(const double* a, const double* u, int n, double dx, double* out, int where) {
   return guarded([&] {
     need(a, "a"), need(u, "u"), need(out, "out");

@@ -54,4 +54,12 @@ void launch_wide2d(const double* u, const double* a, const double* b, const doub
 void launch_deriv8(const double* u, double* out, int nx, int ny, int nz, int dir, double dx,
                    cudaStream_t st);
 
+// Non-periodic lines with the paper's boundary closure (bounded.cu): nlines
+// contiguous lines of n cells; m8 / m6 from make_stencil(8 / 6, ...).
+void launch_narrow_bounded(const StencilM& m8, const StencilM& m6, const double* a,
+                           const double* u, double* out, int n, int nlines, double dx,
+                           cudaStream_t st);
+void launch_deriv_bounded(const double* u, double* out, int n, int nlines, double dx,
+                          cudaStream_t st);
+
 }  // namespace smc
