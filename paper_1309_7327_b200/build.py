@@ -16,6 +16,13 @@ NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-std=c++20", "-lineinfo", "-Xcompiler", "-fPIC", "-Xcompiler", "-O3",
          "--expt-relaxed-constexpr", "-I", os.path.join(HERE, "..", "include")]
+# experiment variants: SMC_BUILD_DEFS="-DNAME=V ..." builds into build-<tag>/ and
+# libsmc_b200-<tag>.so (SMC_BUILD_TAG), which _capi loads when SMC_LIB_PATH names it
+if os.environ.get("SMC_BUILD_DEFS"):
+    FLAGS += os.environ["SMC_BUILD_DEFS"].split()
+    _tag = os.environ.get("SMC_BUILD_TAG", "variant")
+    OBJ = os.path.join(HERE, "build-" + _tag)
+    LIB = os.path.join(HERE, f"libsmc_b200-{_tag}.so")
 
 
 def _sources():

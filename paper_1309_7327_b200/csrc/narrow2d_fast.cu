@@ -14,6 +14,7 @@
 //     per SM.
 // Same interface sums and differencing order as the general kernel
 // (narrow.cu); requires nx % 32 == 0, ny % 8 == 0 and 16-byte aligned fields.
+// Large grids (nx % 256 == 0) take the y-march below instead (same bits).
 #include <algorithm>
 #include <cstdint>
 #include <cstdlib>
@@ -181,8 +182,8 @@ void launch2(const NarrowArgs& p, const StencilM& M, cudaStream_t st) {
 // x interfaces; the y window (2S rows of u and b for the thread's two
 // columns) lives in registers, its leading row prefetched two rows ahead.
 // Each interface is formed once: x neighbours' by shuffle, across warps
-// through shared memory, the segment's x0 - 1/2 by warp 0 lane 0; the y
-// interface below the chunk once per chunk.  Same interface sums and
+// through shared memory, the segment's x0 - 1/2 of every row of the chunk
+// up front by all four warps; the y interface below the chunk once per chunk.  Same interface sums and
 // differencing order as the tiled kernel (pde.cpp:118-124).
 constexpr int MW = 256;
 constexpr int MT = MW / 2;               // 128 threads
@@ -190,14 +191,15 @@ constexpr int MSW = MW + 2 * HALO2;      // staged row width
 constexpr int MCH = MSW / 2;             // 16-byte chunks per field per row
 constexpr int MCPT = (MCH + MT - 1) / MT;
 
+constexpr int MKC = 128;                 // rows per chunk at most
 struct MarchSmem {
   double row[3][2][MSW];  // u, a
   double xs[2][MT / 32];  // last x interface of each warp
-  double hxe[2];          // x0 - 1/2
+  double hxe[MKC];        // x0 - 1/2 of every row of the chunk
 };
 
-template <int S, bool SRC>
-__global__ void __launch_bounds__(MT, 3) narrow2d_march(const NarrowArgs p, const StencilM M) {
+template <int S, bool SRC, int OCCM>
+__global__ void __launch_bounds__(MT, OCCM) narrow2d_march(const NarrowArgs p, const StencilM M) {
   constexpr int WIN = 2 * S;
   __shared__ __align__(16) MarchSmem sm;
   const int segs = p.nx / MW;
@@ -252,6 +254,19 @@ __global__ void __launch_bounds__(MT, 3) narrow2d_march(const NarrowArgs p, cons
     hyp0 = narrow_iface<S>(b0, u0, M);
     hyp1 = narrow_iface<S>(b1, u1, M);
   }
+  // x0 - 1/2 of every row of the chunk, up front: row r goes to warp r % 4
+  // (lane r / 4), so the four warps -- one per scheduler -- share the edge
+  // work evenly instead of warp 0 forming one extra interface per row
+  for (int r = 4 * lane + wid; r < k1 - k0; r += MT) {
+    const long long ro = roff(k0 + r);
+    double uu[WIN], aa[WIN];
+#pragma unroll
+    for (int j = 0; j < WIN; ++j) {
+      const int c = wrap(x0 - S + j, nx);
+      uu[j] = __ldg(p.u + ro + c), aa[j] = __ldg(p.cx + ro + c);
+    }
+    sm.hxe[r] = narrow_iface<S>(aa, uu, M);
+  }
   asm volatile("cp.async.wait_group 1;\n" ::: "memory");
   __syncthreads();
   const double idx2 = p.idx2, idy2 = p.idy2;
@@ -294,12 +309,6 @@ __global__ void __launch_bounds__(MT, 3) narrow2d_march(const NarrowArgs p, cons
       narrow_iface2<S>(aa + OFF, ua + OFF, aa + OFF + 1, ua + OFF + 1, M, hx0, hx1);
     }
     if (lane == 31) sm.xs[hb][wid] = hx1;
-    if (cp == 0) {  // x0 - 1/2
-      double uu[WIN], aa[WIN];
-#pragma unroll
-      for (int j = 0; j < WIN; ++j) uu[j] = tu[HALO2 - S + j], aa[j] = ta[HALO2 - S + j];
-      sm.hxe[hb] = narrow_iface<S>(aa, uu, M);
-    }
     if (k + 2 < k1)
       stage((t + 2) % 3, k + 2);
     else
@@ -308,7 +317,7 @@ __global__ void __launch_bounds__(MT, 3) narrow2d_march(const NarrowArgs p, cons
     __syncthreads();
     // ---- (dHx)/dx^2 + (dHy)/dy^2 (+ g0 g(t)), pde.cpp:118-124
     double hxl = __shfl_up_sync(0xffffffffu, hx1, 1);
-    if (lane == 0) hxl = wid == 0 ? sm.hxe[hb] : sm.xs[hb][wid - 1];
+    if (lane == 0) hxl = wid == 0 ? sm.hxe[t] : sm.xs[hb][wid - 1];
     double o0 = __dmul_rn(__dsub_rn(hx0, hxl), idx2);
     double o1 = __dmul_rn(__dsub_rn(hx1, hx0), idx2);
     o0 = __dadd_rn(o0, __dmul_rn(__dsub_rn(hy0, hyp0), idy2));
@@ -338,22 +347,42 @@ void launch_march(NarrowArgs p, const StencilM& M, cudaStream_t st) {
   while (segs * chunks < 2LL * 3 * sms && (p.ny + chunks) / (chunks + 1) >= 8) ++chunks;
   p.kc = static_cast<int>((p.ny + chunks - 1) / chunks);
   if (const char* e = std::getenv("SMC_HEAT2D_KC")) p.kc = std::max(1, std::atoi(e));
+  p.kc = std::min(p.kc, MKC);
   const long long grid = segs * ((p.ny + p.kc - 1) / p.kc);
-  narrow2d_march<S, SRC><<<static_cast<unsigned>(grid), MT, 0, st>>>(p, M);
+  static const int occ = [] {
+    const char* e = std::getenv("SMC_HEAT2D_OCC");
+    return e ? std::atoi(e) : 3;
+  }();
+  if (occ == 4)
+    narrow2d_march<S, SRC, 4><<<static_cast<unsigned>(grid), MT, 0, st>>>(p, M);
+  else
+    narrow2d_march<S, SRC, 3><<<static_cast<unsigned>(grid), MT, 0, st>>>(p, M);
   SMC_CHECK_LAUNCH();
 }
 
-// SMC_HEAT2D=march selects the y-march where it applies (nx % 256 == 0).  It
-// gives the same bits as the tiled kernel but measured 0.199 against 0.197 ms
-// at 4096^2 (FP64 pipe 58 % at 2.8 warps per scheduler, against 64 % at 7.5
-// for the tiles; row chunks of 16 / 32 / 64 / 128: 0.201 / 0.199 / 0.207 /
-// 0.253 ms; four CTAs per SM spill), so the tiled kernel is the default.
-bool march_enabled() {
-  static bool m = [] {
+// The y-march is the default where it fills the GPU (nx % 256 == 0 and at
+// least two waves of 32-row chunks): 4096^2 0.187 ms against 0.192 ms for the
+// tiles (FP64 pipe 60 % at 2.8 warps per scheduler, 156 registers; row chunks
+// of 16 / 24 / 32 / 37 / 48: 0.191 / 0.190 / 0.187 / 0.186 / 0.199 ms; four
+// CTAs per SM at 128 registers spill and gain < 1 %).  Smaller grids take the
+// one-shot tiles.  SMC_HEAT2D=march / tiled forces either (same bits).
+int heat2d_mode() {
+  static int m = [] {
     const char* e = std::getenv("SMC_HEAT2D");
-    return e && std::string(e) == "march";
+    if (e && std::string(e) == "march") return 1;
+    if (e && std::string(e) == "tiled") return 2;
+    return 0;
   }();
   return m;
+}
+bool use_march(const NarrowArgs& p, int s) {
+  if (p.nx % MW != 0 || p.ny < 2 * s) return false;
+  const int mode = heat2d_mode();
+  if (mode) return mode == 1;
+  int dev = 0, sms = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  return static_cast<long long>(p.nx / MW) * (p.ny / 32) >= 2LL * 3 * sms;
 }
 
 }  // namespace
@@ -365,7 +394,7 @@ bool narrow2d_fast_applicable(const NarrowArgs& p) {
 }
 
 void launch_narrow2d_fast(const NarrowArgs& p, int s, const StencilM& M, cudaStream_t st) {
-  if (p.nx % MW == 0 && p.ny >= 2 * s && march_enabled()) {
+  if (use_march(p, s)) {
     if (p.g0)
       s == 4 ? launch_march<4, true>(p, M, st) : launch_march<3, true>(p, M, st);
     else

@@ -197,6 +197,37 @@ int main() {
     const B::Field ub = B::integrate_stiff(f, {1.0}, 0.0, 1.0, bso);
     check(ub[0] == ur[0], "integrate_stiff bitwise", std::fabs(ub[0] - ur[0]));
   }
+  // non-periodic lines (the paper's boundary closure; no reference
+  // counterpart): away from the ends they are the reference's periodic
+  // operators, and a too-short line throws like apply_narrow does
+  {
+    const int n = 96;
+    std::vector<double> a(n), u(n);
+    for (int i = 0; i < n; ++i) {
+      a[i] = 1.0 + 0.3 * std::sin(0.37 * i);
+      u[i] = std::cos(0.21 * i) + 0.1 * std::sin(1.3 * i);
+    }
+    const double dx = 1.0 / n;
+    const auto m = nsdc::build_narrow(8, {nsdc::kSmcM47, nsdc::kSmcM48});
+    const auto rp = nsdc::apply_narrow(m, a, u, dx);
+    const auto gb = B::apply_narrow_bounded(a, u, dx);
+    const auto rd = nsdc::first_derivative8(u, dx);
+    const auto gd = B::first_derivative_bounded(u, dx);
+    double e = 0.0, sc = 0.0, ed = 0.0, sd = 0.0;
+    for (int i = 8; i < n - 8; ++i) {
+      e = std::max(e, std::fabs(gb[i] - rp[i])), sc = std::max(sc, std::fabs(rp[i]));
+      ed = std::max(ed, std::fabs(gd[i] - rd[i])), sd = std::max(sd, std::fabs(rd[i]));
+    }
+    check(e <= 1e-12 * sc && ed <= 1e-12 * sd, "bounded lines = periodic operators inside",
+          std::max(e / sc, ed / sd));
+    bool threw = false;
+    try {
+      B::apply_narrow_bounded(std::vector<double>(7, 1.0), std::vector<double>(7, 1.0), 0.1);
+    } catch (const std::invalid_argument&) {
+      threw = true;
+    }
+    check(threw, "bounded line too short -> std::invalid_argument");
+  }
   // error behaviour mirrors the reference (pde_test.cpp:243-263)
   {
     bool threw = false;

@@ -412,8 +412,8 @@ np.save({out!r}, op(0.0, d['u']))
 
 
 def test_heat2d_march_equals_tiled_bitwise(cuda, tmp_path):
-    """The y-march (SMC_HEAT2D=march, a child process) and the one-shot tiled
-    kernel (the default) form every interface with the same operation
+    """The y-march and the one-shot tiled kernel (SMC_HEAT2D=march / tiled,
+    each in a child process) form every interface with the same operation
     sequence, so the heat RHS is bitwise identical."""
     import os
     import subprocess
@@ -422,16 +422,19 @@ def test_heat2d_march_equals_tiled_bitwise(cuda, tmp_path):
     rng = np.random.default_rng(5)
     a, b = rng.uniform(0.5, 2.0, (ny, nx)), rng.uniform(0.5, 2.0, (ny, nx))
     u = rng.standard_normal((ny, nx))
-    op = P.HeatOperator(nx, ny, P.StencilChoice.narrow8(*SMC), a, b)
-    got = op(0.0, u)
-    inp, out = str(tmp_path / "in.npz"), str(tmp_path / "out.npy")
+    inp = str(tmp_path / "in.npz")
     np.savez(inp, u=u, a=a, b=b)
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-    env = dict(os.environ, SMC_HEAT2D="march")
-    subprocess.run([sys.executable, "-c", _TILE_SCRIPT.format(root=root, inp=inp, out=out,
-                                                             smc=tuple(SMC))],
-                   env=env, check=True, timeout=300)
-    assert np.array_equal(got, np.load(out))
+    outs = []
+    for mode in ("march", "tiled"):
+        out = str(tmp_path / f"out_{mode}.npy")
+        subprocess.run([sys.executable, "-c", _TILE_SCRIPT.format(root=root, inp=inp, out=out,
+                                                                 smc=tuple(SMC))],
+                       env=dict(os.environ, SMC_HEAT2D=mode), check=True, timeout=300)
+        outs.append(np.load(out))
+    assert np.array_equal(outs[0], outs[1])
+    op = P.HeatOperator(nx, ny, P.StencilChoice.narrow8(*SMC), a, b)
+    assert np.array_equal(op(0.0, u), outs[0])
 
 
 @pytest.mark.parametrize("shape", [(9, 256), (75, 512), (300, 256)])
