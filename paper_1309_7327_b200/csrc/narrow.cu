@@ -20,6 +20,7 @@
 // The work is FP64-bound (341 flop / 24 B per cell); there
 // is nothing GEMM-shaped here, so no tensor cores.
 #include "common.cuh"
+#include <algorithm>
 #include <cstdlib>
 #include <string>
 
@@ -456,13 +457,245 @@ __global__ void __launch_bounds__(WT) wide_tiled(const double* __restrict__ u,
   }
 }
 
-bool wide_tiled_on() {
-  static const bool on = [] {
-    const char* e = std::getenv("SMC_WIDE");
-    return !(e && std::string(e) == "2pass");
-  }();
-  return on;
+// Wide route as a y-march (the heat RHS's narrow2d_march layout): a CTA owns
+// a segment of YW = 256 columns (128 threads, two adjacent columns each) and
+// a chunk of rows.  Per row k:
+//   x: w1 = a D_x u of row k goes to a shared row (own columns plus a
+//      4-column halo each side, formed by two lanes of every warp) and, after
+//      the row's barrier, D_x w1 at the own columns;
+//   y: the thread's two columns of u rows k .. k+8 and of w2 = b D_y u rows
+//      k-4 .. k+4 live in registers; each step shifts in u row k+8 and w2
+//      row k+4.
+// Staging (16-byte cp.async, YD rows ahead): u rows in a ring of 9 + YD rows
+// with an 8-column halo -- a row arrives once, feeds the y windows as their
+// leading row and eight steps later the x stencil as the centre row --, a
+// rows (4-column halo), b rows (four rows ahead of a) and g0 rows in rings of
+// YD + 1.  One read of u, a, b (and g0) and one write per point; the same
+// arithmetic and order as wide_pass1 / wide_pass2 (the same bits as the two
+// passes and as wide_tiled).
+constexpr int YW = 256, YT = YW / 2, YH = 2 * WH;   // segment, threads, u halo (8)
+constexpr int YUW = YW + 2 * YH;                    // staged u row: 272
+constexpr int YW1 = YW + 2 * WH;                    // a / w1 row: 264
+template <int D, bool SRC>
+struct YMarchSmem {
+  static constexpr int NU = 9 + D, NA = D + 1;  // ring depths
+  double u[NU][YUW];          // u row r, columns x0-8 ..      (slot r % NU)
+  double a[NA][YW1];          // a row r, columns x0-4 ..      (slot r % NA)
+  double b[NA][YW];           // b row r + 4, own columns      (slot r % NA)
+  double g[SRC ? NA : 1][YW]; // g0 row r, own columns
+  double w1[2][YW1];          // w1 of rows of even / odd parity
+};
+
+__device__ __forceinline__ void cp16w(double* dst, const double* src) {
+  const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(dst));
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(src));
 }
+
+template <int V>
+struct YRot {
+  static constexpr int value = V;
+};
+
+// D = staging distance in rows (one cp.async group per row).  Step k forms
+// out row k from w1 row k (formed in step k - 1) and the y windows, then w1
+// row k + 1, then stages row k + D; one barrier per row.  The y windows are
+// register rings: a step of rotation R writes the new row into slot R and
+// reads logical entry j from slot (j + R + 1) % 9, so the march is unrolled
+// by nine and nothing is shifted.
+template <int D, bool SRC>
+__global__ void __launch_bounds__(YT, 4)
+    wide_march(const double* __restrict__ u, const double* __restrict__ a,
+               const double* __restrict__ b, const double* __restrict__ g0, double gt,
+               double* __restrict__ out, int nx, int ny, int kc, double inv_dx, double inv_dy) {
+  using Sm = YMarchSmem<D, SRC>;
+  constexpr int NU = Sm::NU, NA = Sm::NA;
+  extern __shared__ __align__(16) unsigned char ym_raw[];
+  Sm& sm = *reinterpret_cast<Sm*>(ym_raw);
+  const int segs = nx / YW;
+  const int x0 = (blockIdx.x % segs) * YW;
+  const int k0 = static_cast<int>(blockIdx.x / segs) * kc;
+  const int k1 = min(k0 + kc, ny);
+  const int cp = threadIdx.x, lane = cp & 31, wid = cp >> 5;
+  const int col = x0 + 2 * cp;
+  const long long plane = static_cast<long long>(nx) * ny;
+  auto roff = [&](int k) { return static_cast<long long>(wrap(k, ny)) * nx; };
+  auto ld2 = [&](const double* f, int k) {
+    return __ldg(reinterpret_cast<const double2*>(f + roff(k) + col));
+  };
+  auto adv = [&](long long& ro) {  // next row, periodic
+    ro += nx;
+    if (ro >= plane) ro -= plane;
+  };
+
+  // this thread's 16-byte chunks: u (136 per row: threads 0..7 take two), a
+  // (132: threads 0..3 take two), b and g0 (one each)
+  const int uo0 = wrap(x0 - YH + 2 * cp, nx), uo1 = wrap(x0 - YH + 2 * (cp + YT), nx);
+  const int ao0 = wrap(x0 - WH + 2 * cp, nx), ao1 = wrap(x0 - WH + 2 * (cp + YT), nx);
+  const bool u2 = cp + YT < YUW / 2, a2 = cp + YT < YW1 / 2;
+  auto stage_u = [&](int s, long long ro) {
+    double* d = sm.u[s];
+    cp16w(d + 2 * cp, u + ro + uo0);
+    if (u2) cp16w(d + 2 * (cp + YT), u + ro + uo1);
+  };
+  // one group per row r: u row r + 8, a / g0 row r, b row r + 4 (slots and
+  // row offsets advanced incrementally)
+  int st_r = k0, st_su = (k0 + 8) % NU, st_sa = k0 % NA;
+  long long st_ru = roff(k0 + 8), st_ra = roff(k0), st_rb = roff(k0 + 4);
+  auto stage_next = [&]() {
+    if (st_r < k1) {
+      stage_u(st_su, st_ru);
+      cp16w(sm.a[st_sa] + 2 * cp, a + st_ra + ao0);
+      if (a2) cp16w(sm.a[st_sa] + 2 * (cp + YT), a + st_ra + ao1);
+      cp16w(sm.b[st_sa] + 2 * cp, b + st_rb + col);
+      if constexpr (SRC) cp16w(sm.g[st_sa] + 2 * cp, g0 + st_ra + col);
+    }
+    asm volatile("cp.async.commit_group;\n" ::);
+    ++st_r;
+    st_su = st_su + 1 == NU ? 0 : st_su + 1;
+    st_sa = st_sa + 1 == NA ? 0 : st_sa + 1;
+    adv(st_ru), adv(st_ra), adv(st_rb);
+  };
+  // the w1 halo column of this lane (lanes 0, 1 of every warp: 8 columns)
+  const int h = 2 * wid + lane;                            // 0 .. 7 for lane < 2
+  const int hc = h < WH ? h : YW + h;                      // w1 row index (0..3, 260..263)
+  // w1 = a D_x u of a staged row into w1[par]
+  auto form_w1 = [&](int su, int sa, int par) {
+    const double* ur = sm.u[su];
+    const double* ar = sm.a[sa];
+    double* w1 = sm.w1[par];
+    const double2 ak = *reinterpret_cast<const double2*>(ar + WH + 2 * cp);
+    double w[10];
+#pragma unroll
+    for (int j = 0; j < 5; ++j) {
+      const double2 v = *reinterpret_cast<const double2*>(ur + 2 * cp + WH + 2 * j);
+      w[2 * j] = v.x, w[2 * j + 1] = v.y;
+    }
+    *reinterpret_cast<double2*>(w1 + WH + 2 * cp) =
+        make_double2(ak.x * deriv8_w(w, inv_dx), ak.y * deriv8_w(w + 1, inv_dx));
+    if (lane < 2) {
+      double wh[9];
+#pragma unroll
+      for (int j = 0; j < 9; ++j) wh[j] = ur[hc + j];
+      w1[hc] = ar[hc] * deriv8_w(wh, inv_dx);
+    }
+  };
+
+  // prologue: the centre rows k0 .. k0+7 (one group), then rows k0 .. k0+D-1
+  {
+    long long ro = roff(k0);
+    for (int r = k0; r < k0 + 8; ++r) {
+      stage_u(r % NU, ro);
+      adv(ro);
+    }
+  }
+  asm volatile("cp.async.commit_group;\n" ::);
+#pragma unroll
+  for (int i = 0; i < D; ++i) stage_next();
+
+  // y rings: after the warm-up (rotation 8 -- eight pushes from rotation 0),
+  // logical uw[j] = u row k + j, ww[j] = w2 row k - 4 + j at the next push
+  double2 pu[9], pw[9];
+  auto w2_of = [&](const double2* w, int rot, double2 bv) {  // b * D_y u, logical window
+    double tx[9], ty[9];
+#pragma unroll
+    for (int j = 0; j < 9; ++j) tx[j] = w[(j + rot) % 9].x, ty[j] = w[(j + rot) % 9].y;
+    return make_double2(bv.x * deriv8_w(tx, inv_dy), bv.y * deriv8_w(ty, inv_dy));
+  };
+  // warm-up from global memory: u rows k0-8 .. k0+7 -> w2 rows k0-4 .. k0+3;
+  // the loads are issued together
+#pragma unroll
+  for (int j = 1; j < 9; ++j) pu[j] = ld2(u, k0 - 9 + j);
+  pu[0] = pw[0] = make_double2(0.0, 0.0);
+  {
+    double2 wu8[8], wb8[8];
+#pragma unroll
+    for (int r = 0; r < 8; ++r) wu8[r] = ld2(u, k0 + r), wb8[r] = ld2(b, k0 - 4 + r);
+#pragma unroll
+    for (int r = 0; r < 8; ++r) {  // push of rotation r
+      pu[r] = wu8[r];
+      pw[r] = w2_of(pu, r + 1, wb8[r]);
+    }
+  }
+  // row k0's group landed everywhere -> w1 row k0; then rows through k0 + 1
+  asm volatile("cp.async.wait_group %0;\n" ::"n"(D - 1) : "memory");
+  __syncthreads();
+  form_w1(k0 % NU, k0 % NA, 0);
+  asm volatile("cp.async.wait_group %0;\n" ::"n"(D - 2) : "memory");
+  __syncthreads();
+
+  int su8 = (k0 + 8) % NU, sa = k0 % NA, su1 = (k0 + 1) % NU, sa1 = (k0 + 1) % NA;
+  long long oo = static_cast<long long>(k0) * nx + col;
+  auto step = [&](auto rc, int k) {
+    constexpr int R = decltype(rc)::value;
+    const int par = (k - k0) & 1;
+    // ---- y: push u row k+8 and w2 row k+4 (b row k+4), both staged
+    pu[R] = *reinterpret_cast<const double2*>(&sm.u[su8][YH + 2 * cp]);
+    pw[R] = w2_of(pu, R + 1, *reinterpret_cast<const double2*>(&sm.b[sa][2 * cp]));
+    // ---- out row k = D_x w1 + D_y w2 (+ g0 g(t)), wide_pass2's order
+    {
+      const double* w1 = sm.w1[par];
+      double w[10];
+#pragma unroll
+      for (int j = 0; j < 5; ++j) {
+        const double2 v = *reinterpret_cast<const double2*>(w1 + 2 * cp + 2 * j);
+        w[2 * j] = v.x, w[2 * j + 1] = v.y;
+      }
+      double tx[9], ty[9];
+#pragma unroll
+      for (int j = 0; j < 9; ++j) tx[j] = pw[(j + R + 1) % 9].x, ty[j] = pw[(j + R + 1) % 9].y;
+      double o0 = __dadd_rn(deriv8_w(w, inv_dx), deriv8_w(tx, inv_dy));
+      double o1 = __dadd_rn(deriv8_w(w + 1, inv_dx), deriv8_w(ty, inv_dy));
+      if constexpr (SRC) {
+        const double2 g = *reinterpret_cast<const double2*>(&sm.g[sa][2 * cp]);
+        o0 = __dadd_rn(o0, __dmul_rn(g.x, gt));
+        o1 = __dadd_rn(o1, __dmul_rn(g.y, gt));
+      }
+      *reinterpret_cast<double2*>(out + oo) = make_double2(o0, o1);
+    }
+    // ---- w1 row k + 1 (its rows landed at the last barrier); stage row k +
+    //      D into the slots of row k - 1, all read before the last barrier
+    if (k + 1 < k1) form_w1(su1, sa1, par ^ 1);
+    stage_next();
+    asm volatile("cp.async.wait_group %0;\n" ::"n"(D - 2) : "memory");
+    __syncthreads();
+    su8 = su8 + 1 == NU ? 0 : su8 + 1;
+    su1 = su1 + 1 == NU ? 0 : su1 + 1;
+    sa = sa + 1 == NA ? 0 : sa + 1;
+    sa1 = sa1 + 1 == NA ? 0 : sa1 + 1;
+    oo += nx;
+  };
+  int k = k0;
+#pragma unroll 1
+  for (; k + 9 <= k1; k += 9) {
+    step(YRot<8>{}, k), step(YRot<0>{}, k + 1), step(YRot<1>{}, k + 2);
+    step(YRot<2>{}, k + 3), step(YRot<3>{}, k + 4), step(YRot<4>{}, k + 5);
+    step(YRot<5>{}, k + 6), step(YRot<6>{}, k + 7), step(YRot<7>{}, k + 8);
+  }
+  // the last < 9 rows
+  if (k < k1) step(YRot<8>{}, k++);
+  if (k < k1) step(YRot<0>{}, k++);
+  if (k < k1) step(YRot<1>{}, k++);
+  if (k < k1) step(YRot<2>{}, k++);
+  if (k < k1) step(YRot<3>{}, k++);
+  if (k < k1) step(YRot<4>{}, k++);
+  if (k < k1) step(YRot<5>{}, k++);
+  if (k < k1) step(YRot<6>{}, k++);
+  asm volatile("cp.async.wait_group 0;\n" ::: "memory");
+}
+
+// SMC_WIDE = 2pass / tiled / march forces a route; by default the y-march
+// where nx % 256 == 0 and the grid fills two waves, else the tiles.
+int wide_mode() {
+  static const int m = [] {
+    const char* e = std::getenv("SMC_WIDE");
+    if (!e) return 0;
+    const std::string v(e);
+    return v == "2pass" ? 1 : v == "tiled" ? 2 : v == "march" ? 3 : 0;
+  }();
+  return m;
+}
+bool wide_tiled_on() { return wide_mode() != 1; }
+
 
 }  // namespace
 
@@ -470,6 +703,36 @@ void launch_wide2d(const double* u, const double* a, const double* b, const doub
                    double* w1, double* w2, double* out, int nx, int ny, double dx, double dy,
                    cudaStream_t st) {
   const long long n = static_cast<long long>(nx) * ny;
+  if (b && nx % YW == 0 && ny >= 9 && wide_mode() != 1 && wide_mode() != 2) {
+    int dev = 0, sms = 0;
+    SMC_CUDA(cudaGetDevice(&dev));
+    SMC_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    const long long segs = nx / YW;
+    if (wide_mode() == 3 || segs * (ny / 16) >= sms) {
+      // one wave of four CTAs per SM (4096^2: 37 chunks of 111 rows; chunks of
+      // 32 / 37 / 56 / 64 / 111 rows: 0.126 / 0.116 / 0.113 / 0.122 / 0.105 ms),
+      // chunks of at least 16 rows
+      long long chunks = std::max(1LL, 4LL * sms / segs);
+      chunks = std::max(1LL, std::min(chunks, static_cast<long long>(ny) / 16));
+      int kc = static_cast<int>((ny + chunks - 1) / chunks);
+      if (const char* e = std::getenv("SMC_WIDE_KC")) kc = std::max(1, std::atoi(e));
+      const unsigned grid = static_cast<unsigned>(segs * ((ny + kc - 1) / kc));
+      auto go = [&](auto kern, std::size_t sh) {
+        static bool configured = false;  // one per instantiation
+        if (!configured) {
+          SMC_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        static_cast<int>(sh)));
+          configured = true;
+        }
+        kern<<<grid, YT, sh, st>>>(u, a, b, g0, gt, out, nx, ny, kc, 1.0 / dx, 1.0 / dy);
+      };
+      // staging distance 3 rows (4 measured the same, and takes more shared memory)
+      g0 ? go(wide_march<3, true>, sizeof(YMarchSmem<3, true>))
+         : go(wide_march<3, false>, sizeof(YMarchSmem<3, false>));
+      SMC_CHECK_LAUNCH();
+      return;
+    }
+  }
   if (b && nx % WX == 0 && ny % WY == 0 && nx >= UW && wide_tiled_on()) {
     static bool configured = false;
     if (!configured) {

@@ -504,3 +504,30 @@ def test_wide_tiled_equals_two_pass_bitwise(cuda, tmp_path, shape):
     subprocess.run([sys.executable, "-c", _WIDE_SCRIPT.format(root=root, inp=inp, out=out)],
                    env=env, check=True, timeout=300)
     assert np.array_equal(got, np.load(out))
+
+
+@pytest.mark.parametrize("shape", [(9, 256), (48, 256), (75, 512), (256, 512)])
+@pytest.mark.parametrize("src", [False, True])
+def test_wide_march_equals_two_pass_bitwise(cuda, tmp_path, shape, src):
+    """The y-march wide route (SMC_WIDE=march, the default on large grids)
+    keeps wide_pass1 / wide_pass2's arithmetic: the same bits as the two-pass
+    kernels, for one and several row chunks and ny not a multiple of them."""
+    import os
+    import subprocess
+    import sys
+    ny, nx = shape
+    rng = np.random.default_rng(ny + nx)
+    a, b = rng.uniform(0.5, 2.0, (ny, nx)), rng.uniform(0.5, 2.0, (ny, nx))
+    g = rng.standard_normal((ny, nx)) if src else np.zeros((ny, nx))
+    u = rng.standard_normal((ny, nx))
+    inp = str(tmp_path / "in.npz")
+    np.savez(inp, u=u, a=a, b=b, g=g)
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    outs = []
+    for mode in ("march", "2pass"):
+        out = str(tmp_path / f"out_{mode}.npy")
+        subprocess.run([sys.executable, "-c", _WIDE_SCRIPT.format(root=root, inp=inp, out=out)],
+                       env=dict(os.environ, SMC_WIDE=mode, SMC_WIDE_KC="16"), check=True,
+                       timeout=300)
+        outs.append(np.load(out))
+    assert np.array_equal(outs[0], outs[1])

@@ -6,7 +6,9 @@ the wide8 stencils at n x n on cuda:0 with CUDA events, and the 3-D narrow
 operator for reference, then evaluates the model with this box's measured
 FP64 peak and HBM bandwidth: narrow pays 112N+111 - (23N+8) extra flops per
 point, wide streams 64 extra bytes per point (N = 1 for the heat equation).
-Prints one JSON object; profiles/cost_model_r01.json keeps a run."""
+"model_fused_wide" is the same comparison for a single-pass wide kernel (no
+temporaries: both routes move 32 B per point).  Prints one JSON object;
+profiles/cost_model_r0*.json keep runs."""
 import json
 import math
 import os
@@ -68,6 +70,12 @@ def main():
                     "crossover_bandwidth_GBs": 64.0 * flops / (narrow_f - wide_f) / 1e9}
     res["measured_delta_ns_per_point"] = (res["narrow8"]["ns_per_point"] -
                                           res["wide8"]["ns_per_point"])
+    # the same machine with a single-pass (fused) wide route: no temporaries,
+    # both routes move 32 B per point, each bound by its own roofline
+    t_n = max(32.0 / bw, narrow_f / flops)
+    t_w = max(32.0 / bw, wide_f / flops)
+    res["model_fused_wide"] = {"narrow_ns_per_point": t_n * 1e9, "wide_ns_per_point": t_w * 1e9,
+                               "time_delta_ns_per_point": (t_n - t_w) * 1e9}
     # the single-pass wide kernel's HBM floor: u, a, b in, out written
     res["wide8"]["hbm_floor_s"] = 32.0 * n * n / bw
     res["wide8"]["hbm_frac"] = res["wide8"]["hbm_floor_s"] / res["wide8"]["s_per_rhs"]
