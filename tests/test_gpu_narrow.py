@@ -506,7 +506,7 @@ def test_wide_tiled_equals_two_pass_bitwise(cuda, tmp_path, shape):
     assert np.array_equal(got, np.load(out))
 
 
-@pytest.mark.parametrize("shape", [(9, 256), (48, 256), (75, 512), (256, 512)])
+@pytest.mark.parametrize("shape", [(9, 256), (48, 256), (75, 512), (256, 512), (2048, 2048)])
 @pytest.mark.parametrize("src", [False, True])
 def test_wide_march_equals_two_pass_bitwise(cuda, tmp_path, shape, src):
     """The y-march wide route (SMC_WIDE=march, the default on large grids)
@@ -524,10 +524,15 @@ def test_wide_march_equals_two_pass_bitwise(cuda, tmp_path, shape, src):
     np.savez(inp, u=u, a=a, b=b, g=g)
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
     outs = []
+    big = ny * nx >= 1 << 22  # the default route and chunking at this size
     for mode in ("march", "2pass"):
         out = str(tmp_path / f"out_{mode}.npy")
+        env = dict(os.environ, SMC_WIDE=mode)
+        if not big:
+            env["SMC_WIDE_KC"] = "16"
+        elif mode == "march":
+            env.pop("SMC_WIDE")
         subprocess.run([sys.executable, "-c", _WIDE_SCRIPT.format(root=root, inp=inp, out=out)],
-                       env=dict(os.environ, SMC_WIDE=mode, SMC_WIDE_KC="16"), check=True,
-                       timeout=300)
+                       env=env, check=True, timeout=300)
         outs.append(np.load(out))
     assert np.array_equal(outs[0], outs[1])
