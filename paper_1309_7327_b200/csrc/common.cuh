@@ -77,6 +77,12 @@ __host__ __device__ inline int wrap(int i, int n) {
   i %= n;
   return i < 0 ? i + n : i;
 }
+// wrap for indices a stencil reach away from [0, n): selects instead of the
+// integer division (which costs a dependent multiply-high chain per call)
+__host__ __device__ inline int wrap_near(int i, int n) {
+  if (i < -n || i >= 2 * n) return wrap(i, n);
+  return i < 0 ? i + n : i >= n ? i - n : i;
+}
 
 #ifdef __CUDACC__
 // H_{i+1/2} = sum_mm a_{i+mm} (sum_nn M[mm][nn] u_{i+nn}) for one interface

@@ -77,13 +77,13 @@ struct UV {
 };
 
 __device__ __forceinline__ long long zo(const Geo& g, int k) {
-  if (g.G == 0) k = wrap(k, g.nz);
+  if (g.G == 0) k = wrap_near(k, g.nz);
   return static_cast<long long>(k) * g.plane;
 }
 // offset of cell (i, j, k) + o along dir d (periodic in x, y; z periodic or ghosted)
 __device__ __forceinline__ long long nb(const Geo& g, int i, int j, int k, int d, int o) {
-  if (d == 0) i = wrap(i + o, g.nx);
-  else if (d == 1) j = wrap(j + o, g.ny);
+  if (d == 0) i = wrap_near(i + o, g.nx);
+  else if (d == 1) j = wrap_near(j + o, g.ny);
   else k += o;
   return zo(g, k) + static_cast<long long>(j) * g.nx + i;
 }
