@@ -58,7 +58,18 @@ struct Geo {
   int nx, ny, nz, G;
   long long plane, flen;
   double d1[3], d2[3];
+  double dc[3][4];  // the 8th-order first-derivative weights over the spacing, per direction
 };
+
+// 8th-order centred first derivative (stencil_kernel.hpp:48-54) from a
+// 9-point window w[0..8] centred at w[4], with the weights already divided
+// by the spacing (Geo::dc: kernel-parameter constants, no scaling multiply)
+__device__ __forceinline__ double deriv8_c(const double* w, const double* c) {
+  double r = c[0] * (w[5] - w[3]);
+  r = __fma_rn(c[1], w[6] - w[2], r);
+  r = __fma_rn(c[2], w[7] - w[1], r);
+  return __fma_rn(c[3], w[8] - w[0], r);
+}
 
 // Device view of the conserved state (NsStateView): the three blocks as
 // base pointers rebased so that block b's element of in-interior offset o
@@ -542,7 +553,11 @@ static Geo make_geo(const NsBox& b, const double* d) {
   g.nx = b.nx, g.ny = b.ny, g.nz = b.nz, g.G = b.G;
   g.plane = b.plane();
   g.flen = b.field_len();
-  for (int q = 0; q < 3; ++q) g.d1[q] = 1.0 / d[q], g.d2[q] = 1.0 / (d[q] * d[q]);
+  for (int q = 0; q < 3; ++q) {
+    g.d1[q] = 1.0 / d[q], g.d2[q] = 1.0 / (d[q] * d[q]);
+    const double c[4] = {4.0 / 5.0, -1.0 / 5.0, 4.0 / 105.0, -1.0 / 280.0};
+    for (int j = 0; j < 4; ++j) g.dc[q][j] = c[j] / d[q];
+  }
   return g;
 }
 

@@ -31,3 +31,9 @@ for name, r in (('full', op.full), ('advdiff', op.advdiff), ('chem', op.chem)):
     res[name] = ms
     print(name, round(ms, 3), 'ms', round(n ** 3 / ms / 1e6, 3), 'G cell-RHS/s', flush=True)
 print(json.dumps(res))
+# per-kernel CUDA-event times of one full evaluation (minimum over 3)
+prof = {}
+for _ in range(3):
+    for k, ms in op.profile(U, out):
+        prof[k] = min(prof.get(k, 1e9), ms)
+print('kernels', json.dumps({k: round(v, 3) for k, v in prof.items()}))
