@@ -459,9 +459,9 @@ void rhs_v2(const Geo& g, const UV& U, const double* F, double* A, double* GR, d
     if (marks) marks->mark(name, st);
   };
   static bool configured = false;
-  const std::size_t sm = sizeof(DirSmem);
+  const std::size_t sm0 = sizeof(DirSmem<0>), sm1 = sizeof(DirSmem<1>), sm2 = sizeof(DirSmem<2>);
   if (!configured) {
-    set_smem(ns_phase_a<0, S>, sm), set_smem(ns_phase_a<1, S>, sm), set_smem(ns_phase_a<2, S>, sm);
+    set_smem(ns_phase_a<0, S>, sm0), set_smem(ns_phase_a<1, S>, sm1), set_smem(ns_phase_a<2, S>, sm2);
     const std::size_t smb = sizeof(PBSmem);
     set_smem(ns_phase_b<0>, smb), set_smem(ns_phase_b<1>, smb), set_smem(ns_phase_b<2>, smb);
     configured = true;
@@ -474,18 +474,18 @@ void rhs_v2(const Geo& g, const UV& U, const double* F, double* A, double* GR, d
   double* hy1 = SC + SC_HY1 * n;
   double* na2 = SC + SC_NA2 * n;
   double* hy2 = SC + SC_HY2 * n;
-  constexpr int NT = Tile<0, NR_A>::THREADS;
+  constexpr int NT0 = Tile<0, nr_a<0>()>::THREADS, NT1 = Tile<1, nr_a<1>()>::THREADS;
   // ctoprim + the x / y passes over planes [k0, k0 + np)
   auto planes = [&](int k0, int np) {
     if (np <= 0) return;
     prim_kernel<<<blocks(np * g.plane), 256, 0, st>>>(U, const_cast<double*>(F), g, k0, k0 + np);
     SMC_CHECK_LAUNCH();
     mark("prim");
-    dim3 g0 = dir_grid<0, NR_A>(g, np), g1 = dir_grid<1, NR_A>(g, np);
-    ns_phase_a<0, S><<<g0, NT, sm, st>>>(F, A, A, GR, out, ofs, g, M, k0);
+    dim3 g0 = dir_grid<0, nr_a<0>()>(g, np), g1 = dir_grid<1, nr_a<1>()>(g, np);
+    ns_phase_a<0, S><<<g0, NT0, sm0, st>>>(F, A, A, GR, out, ofs, g, M, k0);
     SMC_CHECK_LAUNCH();
     mark("phase_a_x");
-    ns_phase_a<1, S><<<g1, NT, sm, st>>>(F, na1, A, GR, hy1, n, g, M, k0);
+    ns_phase_a<1, S><<<g1, NT1, sm1, st>>>(F, na1, A, GR, hy1, n, g, M, k0);
     SMC_CHECK_LAUNCH();
     mark("phase_a_y");
   };
@@ -496,7 +496,7 @@ void rhs_v2(const Geo& g, const UV& U, const double* F, double* A, double* GR, d
     planes(-g.G, g.G);
     planes(g.nz, g.G);
   }
-  ns_phase_a<2, S><<<dir_grid<2, NR_A>(g, allp), NT, sm, st>>>(F, na2, A, GR, hy2, n, g, M, 0);
+  ns_phase_a<2, S><<<dir_grid<2, nr_a<2>()>(g, allp), NT1, sm2, st>>>(F, na2, A, GR, hy2, n, g, M, 0);
   SMC_CHECK_LAUNCH();
   mark("phase_a_z");
   ns_mixed_fields<<<blocks(g.plane * allp), 256, 0, st>>>(F, GR, A, MX, g);
