@@ -35,10 +35,11 @@ enum : int {
 // and tau : grad u.  Phase A of y and z and phase B write the same layout
 // (first 4 / first 3 entries) into the scratch blocks below.
 enum : int { A_DM = 0, A_DY = 3, A_HEAT = 4, A_COUNT };
-// scratch_ blocks (interior arrays): NA_1 | HY_1 | NA_2 | HY_2 | PB_0 | PB_1 | PB_2
+// scratch_ blocks (interior arrays): NA_1 | HY_1 (phase A's x + y sums) |
+// PB_0 | PB_1 | PB_2
 enum : int {
-  SC_NA1 = 0, SC_HY1 = SC_NA1 + 4, SC_NA2 = SC_HY1 + SMC_NVAR, SC_HY2 = SC_NA2 + 4,
-  SC_PB0 = SC_HY2 + SMC_NVAR, SC_PB1 = SC_PB0 + 3, SC_PB2 = SC_PB1 + 3, SC_COUNT = SC_PB2 + 3
+  SC_NA1 = 0, SC_HY1 = SC_NA1 + 4, SC_PB0 = SC_HY1 + SMC_NVAR, SC_PB1 = SC_PB0 + 3,
+  SC_PB2 = SC_PB1 + 3, SC_COUNT = SC_PB2 + 3
 };
 // mixed_ fields (all planes): M_ij = eta d_i u_j for (i, j), i != j; L_i
 constexpr int MX_COUNT = 9;
@@ -472,8 +473,6 @@ void rhs_v2(const Geo& g, const UV& U, const double* F, double* A, double* GR, d
   // HY] x 2, phase B of the three directions; ns_assemble2 adds them in
   double* na1 = SC + SC_NA1 * n;
   double* hy1 = SC + SC_HY1 * n;
-  double* na2 = SC + SC_NA2 * n;
-  double* hy2 = SC + SC_HY2 * n;
   constexpr int NT0 = Tile<0, nr_a<0>()>::THREADS, NT1 = Tile<1, nr_a<1>()>::THREADS;
   // ctoprim + the x / y passes over planes [k0, k0 + np)
   auto planes = [&](int k0, int np) {
@@ -482,10 +481,10 @@ void rhs_v2(const Geo& g, const UV& U, const double* F, double* A, double* GR, d
     SMC_CHECK_LAUNCH();
     mark("prim");
     dim3 g0 = dir_grid<0, nr_a<0>()>(g, np), g1 = dir_grid<1, nr_a<1>()>(g, np);
-    ns_phase_a<0, S><<<g0, NT0, sm0, st>>>(F, A, A, GR, out, ofs, g, M, k0);
+    ns_phase_a<0, S><<<g0, NT0, sm0, st>>>(F, A, nullptr, GR, out, ofs, nullptr, 0, g, M, k0);
     SMC_CHECK_LAUNCH();
     mark("phase_a_x");
-    ns_phase_a<1, S><<<g1, NT1, sm1, st>>>(F, na1, A, GR, hy1, n, g, M, k0);
+    ns_phase_a<1, S><<<g1, NT1, sm1, st>>>(F, na1, A, GR, hy1, n, out, ofs, g, M, k0);
     SMC_CHECK_LAUNCH();
     mark("phase_a_y");
   };
@@ -496,7 +495,7 @@ void rhs_v2(const Geo& g, const UV& U, const double* F, double* A, double* GR, d
     planes(-g.G, g.G);
     planes(g.nz, g.G);
   }
-  ns_phase_a<2, S><<<dir_grid<2, nr_a<2>()>(g, allp), NT1, sm2, st>>>(F, na2, A, GR, hy2, n, g, M, 0);
+  ns_phase_a<2, S><<<dir_grid<2, nr_a<2>()>(g, allp), NT1, sm2, st>>>(F, A, na1, GR, out, ofs, hy1, n, g, M, 0);
   SMC_CHECK_LAUNCH();
   mark("phase_a_z");
   ns_mixed_fields<<<blocks(g.plane * allp), 256, 0, st>>>(F, GR, A, MX, g);
