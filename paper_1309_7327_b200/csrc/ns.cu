@@ -3,9 +3,9 @@
 //   prim      : ctoprim (Newton for T) + transport + coefficient fields
 //   phase A   : per direction, the narrow diffusion terms, hyperbolic flux
 //               derivatives, velocity gradients, V_c (ns_dir.inc)
-//   mixed     : eta d_i u_j, lam2 div, tau:grad u
-//   phase B   : mixed viscous derivatives (ns_dir.inc)
-//   assemble2 : direction sums in order + pointwise terms + wdot
+//   phase B   : per direction, the mixed viscous derivatives of
+//               eta d_i u_j and lam2 div u (formed while staging)
+//   assemble2 : pointwise terms (tau:grad u, u . div tau, V_c) + wdot
 #include <algorithm>
 #include <cmath>
 #include <cstdint>
@@ -29,21 +29,12 @@ enum : int {
   F_U = 0, F_T = 3, F_P, F_ETA, F_LAM, F_DHP, F_HYS, F_S, F_RHO, F_Y,
   F_X = F_Y + NSP, F_DH = F_X + NSP, F_DP = F_DH + NSP, F_COUNT = F_DP + NSP
 };
-// acc_ field indices (interior)
-// acc_ fields (interior): the narrow momentum results of direction x, the
-// direction's sum over species of the narrow species results (for div V_c)
-// and tau : grad u.  Phase A of y and z and phase B write the same layout
-// (first 4 / first 3 entries) into the scratch blocks below.
-enum : int { A_DM = 0, A_DY = 3, A_HEAT = 4, A_COUNT };
-// scratch_ blocks (interior arrays): NA_1 | HY_1 (phase A's x + y sums) |
-// PB_0 | PB_1 | PB_2
-enum : int {
-  SC_NA1 = 0, SC_HY1 = SC_NA1 + 4, SC_PB0 = SC_HY1 + SMC_NVAR, SC_PB1 = SC_PB0 + 3,
-  SC_PB2 = SC_PB1 + 3, SC_COUNT = SC_PB2 + 3
-};
-// mixed_ fields (all planes): M_ij = eta d_i u_j for (i, j), i != j; L_i
-constexpr int MX_COUNT = 9;
-__host__ __device__ constexpr int mx_index(int i, int j) { return 3 * i + j - (j > i) - i; }
+// acc_ fields (interior): the narrow momentum results (+ div tau, phase B)
+// and sum over species of the narrow species results (for div V_c), each
+// summed over the three directions in order
+enum : int { A_DM = 0, A_DY = 3, A_COUNT };
+// scratch_ blocks (interior arrays): NA_1 | HY_1 (phase A's x + y sums)
+enum : int { SC_NA1 = 0, SC_HY1 = SC_NA1 + 4, SC_COUNT = SC_HY1 + SMC_NVAR };
 
 struct Tables {
   double W[NSP], th[NSP][4], mu0[NSP], lam0[NSP], rhoD0[NSP];
@@ -453,8 +444,8 @@ void set_smem(K kern, std::size_t bytes) {
 // ghost plane (kNsInterior: ctoprim and the x / y passes on the interior
 // planes), the rest (kNsBoundary) or both (kNsAll).
 template <int S>
-void rhs_v2(const Geo& g, const UV& U, const double* F, double* A, double* GR, double* MX,
-            double* SC, double* out, long long ofs, const StencilM& M, int chem, int phase,
+void rhs_v2(const Geo& g, const UV& U, const double* F, double* A, double* GR, double* SC,
+            double* out, long long ofs, const StencilM& M, int chem, int phase,
             cudaStream_t st, KernelMarks* marks) {
   auto mark = [&](const char* name) {
     if (marks) marks->mark(name, st);
@@ -498,19 +489,16 @@ void rhs_v2(const Geo& g, const UV& U, const double* F, double* A, double* GR, d
   ns_phase_a<2, S><<<dir_grid<2, nr_a<2>()>(g, allp), NT1, sm2, st>>>(F, A, na1, GR, out, ofs, hy1, n, g, M, 0);
   SMC_CHECK_LAUNCH();
   mark("phase_a_z");
-  ns_mixed_fields<<<blocks(g.plane * allp), 256, 0, st>>>(F, GR, A, MX, g);
-  SMC_CHECK_LAUNCH();
-  mark("mixed_fields");
-  ns_phase_b<0><<<dir_grid<0>(g, g.nz), DT_THREADS, sizeof(PBSmem), st>>>(MX, SC + SC_PB0 * n, g);
+  ns_phase_b<0><<<dir_grid<0>(g, g.nz), DT_THREADS, sizeof(PBSmem), st>>>(F, GR, A, g);
   SMC_CHECK_LAUNCH();
   mark("phase_b_x");
-  ns_phase_b<1><<<dir_grid<1>(g, g.nz), DT_THREADS, sizeof(PBSmem), st>>>(MX, SC + SC_PB1 * n, g);
+  ns_phase_b<1><<<dir_grid<1>(g, g.nz), DT_THREADS, sizeof(PBSmem), st>>>(F, GR, A, g);
   SMC_CHECK_LAUNCH();
   mark("phase_b_y");
-  ns_phase_b<2><<<dir_grid<2>(g, g.nz), DT_THREADS, sizeof(PBSmem), st>>>(MX, SC + SC_PB2 * n, g);
+  ns_phase_b<2><<<dir_grid<2>(g, g.nz), DT_THREADS, sizeof(PBSmem), st>>>(F, GR, A, g);
   SMC_CHECK_LAUNCH();
   mark("phase_b_z");
-  ns_assemble2<<<blocks(n), 256, 0, st>>>(F, A, SC, out, ofs, g, chem);
+  ns_assemble2<<<blocks(n), 256, 0, st>>>(F, GR, A, out, ofs, g, chem);
   SMC_CHECK_LAUNCH();
   mark(chem ? "assemble_wdot" : "assemble");
 }
@@ -542,7 +530,6 @@ NsWorkspace::NsWorkspace(const NsBox& box, double dx, double dy, double dz, cons
   upload_tables();
   prim_.resize(static_cast<std::size_t>(F_COUNT) * box.field_len());
   acc_.resize(static_cast<std::size_t>(A_COUNT) * box.cells());
-  mixed_.resize(static_cast<std::size_t>(MX_COUNT) * box.field_len());
   grad_.resize(static_cast<std::size_t>(9) * box.field_len());
   scratch_.resize(static_cast<std::size_t>(SC_COUNT) * box.cells());
 }
@@ -604,10 +591,10 @@ void NsWorkspace::rhs(const NsStateView& U, double* out, long long out_fs, int p
   double* F = prim_.get();
   double* A = acc_.get();
   if (s_ == 4)
-    rhs_v2<4>(g, uv, F, A, grad_.get(), mixed_.get(), scratch_.get(), out, out_fs, M_,
+    rhs_v2<4>(g, uv, F, A, grad_.get(), scratch_.get(), out, out_fs, M_,
               part == kNsFull, phase, st, marks_);
   else
-    rhs_v2<3>(g, uv, F, A, grad_.get(), mixed_.get(), scratch_.get(), out, out_fs, M_,
+    rhs_v2<3>(g, uv, F, A, grad_.get(), scratch_.get(), out, out_fs, M_,
               part == kNsFull, phase, st, marks_);
 }
 

@@ -95,10 +95,9 @@ class NsWorkspace {
   StencilM M_;
   int s_;
   DevBuf prim_;   // primitive + coefficient fields (all planes)
-  DevBuf acc_;    // narrow-stencil accumulators + gradients (interior)
-  DevBuf mixed_;  // eta d_i u_j, lam2 sum d_j u_j (all planes)
-  DevBuf grad_;   // d_j u_i (all planes; v2 pipeline)
-  DevBuf scratch_;  // v2: per-direction results (93 interior arrays), summed in order
+  DevBuf acc_;    // direction sums: narrow momentum + div tau, sum_k narrow species (interior)
+  DevBuf grad_;   // d_j u_i (all planes)
+  DevBuf scratch_;  // phase A's x + y sums (18 interior arrays)
 };
 
 // Chunk boundaries of the host-buffer pipelines (0 = b[0] < ... < b.back() =
