@@ -525,7 +525,7 @@ def run_mrsdc(args):
     residual over the ranks in the library.  Device memory per cell: the
     MRSDC mode-1 stepper holds 43 states of 14 fields (9 fine-node values,
     F1 and F2 double-buffered, 8 node integrals, carries) plus the state and
-    the result, the NS workspace ~116 fields: ~6.0 KB per cell, ~800 GB for
+    the result, the NS workspace 78 fields: ~5.7 KB per cell, ~760 GB for
     512^3, so the 512^3 series starts at 8 GPUs."""
     import torch
     import torch.distributed as dist
@@ -542,7 +542,7 @@ def run_mrsdc(args):
     ng = args.n_global
     nz = ng // world
     cells_local = ng * ng * nz
-    need = 8.0 * (14 * (43 + 2) + 116) * cells_local
+    need = 8.0 * (14 * (43 + 2) + 78) * cells_local
     free, _ = torch.cuda.mem_get_info(dev)
     base = {"metric": f"configs[4] MRSDC mode-1 cell-steps/sec ({ng}^3, strong scaling)",
             "unit": "cell-steps/s", "n_gpus": world, "higher_is_better": True,
