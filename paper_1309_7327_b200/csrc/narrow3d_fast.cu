@@ -212,12 +212,13 @@ __device__ __forceinline__ void march_segment(FastSmem<FXT>& sm, const NarrowArg
     if (cp == 0) hxl = sm.hxe[hb][row];
     const double2 yu = lds2(&sm.hy[hb][row][2 * cp]);
     const double2 yd = lds2(&sm.hy[hb][row + 1][2 * cp]);
+    // x, y, z differences scaled and summed with two fused multiply-adds
     double o0 = __dmul_rn(__dsub_rn(hx0, hxl), idx2);
     double o1 = __dmul_rn(__dsub_rn(hx1, hx0), idx2);
-    o0 = __dadd_rn(o0, __dmul_rn(__dsub_rn(yd.x, yu.x), idy2));
-    o1 = __dadd_rn(o1, __dmul_rn(__dsub_rn(yd.y, yu.y), idy2));
-    o0 = __dadd_rn(o0, __dmul_rn(__dsub_rn(hz0, hzl0), idz2));
-    o1 = __dadd_rn(o1, __dmul_rn(__dsub_rn(hz1, hzl1), idz2));
+    o0 = __fma_rn(__dsub_rn(yd.x, yu.x), idy2, o0);
+    o1 = __fma_rn(__dsub_rn(yd.y, yu.y), idy2, o1);
+    o0 = __fma_rn(__dsub_rn(hz0, hzl0), idz2, o0);
+    o1 = __fma_rn(__dsub_rn(hz1, hzl1), idz2, o1);
     *reinterpret_cast<double2*>(p.out + oo + col_off) = make_double2(o0, o1);
   };
 
