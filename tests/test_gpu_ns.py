@@ -173,3 +173,20 @@ def test_ns_host_pipeline_uneven_chunks(cuda):
     dev = op.full(0.0, U).cpu().numpy()
     host = op.full(0.0, U.cpu().pin_memory()).numpy()
     assert max(_percomp(host, dev)) <= 1e-13
+
+
+@pytest.mark.parametrize("n,kw", [(16, {}), (48, {"hot_spot": True})])
+def test_ns_rhs_sixth_order_vs_oracle(cuda, n, kw):
+    """The sixth-order narrow family (half width 3: odd window offsets in the
+    direction passes, two-term coefficient-side velocity transform) against
+    the oracle with the same stencil."""
+    U, _ = _state(n, **kw)
+    m36 = P.DEFAULT_M36
+    m64, s = O.build_narrow(6, (m36,))
+    ref = O.ns_rhs(U, DX, P.NS_FULL, m64=m64, s=s)
+    op = P.NsOperator(n, n, n, DX, choice=P.StencilChoice.narrow6(m36))
+    got = op.full(0.0, U)
+    errs = _percomp(got, ref)
+    assert max(errs) <= TOL, errs
+    # and the sixth-order operator is not the eighth-order one
+    assert max(_percomp(P.NsOperator(n, n, n, DX).full(0.0, U), ref)) > 1e-9
