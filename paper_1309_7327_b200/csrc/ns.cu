@@ -83,13 +83,6 @@ __device__ __forceinline__ long long zo(const Geo& g, int k) {
   if (g.G == 0) k = wrap_near(k, g.nz);
   return static_cast<long long>(k) * g.plane;
 }
-// offset of cell (i, j, k) + o along dir d (periodic in x, y; z periodic or ghosted)
-__device__ __forceinline__ long long nb(const Geo& g, int i, int j, int k, int d, int o) {
-  if (d == 0) i = wrap_near(i + o, g.nx);
-  else if (d == 1) j = wrap_near(j + o, g.ny);
-  else k += o;
-  return zo(g, k) + static_cast<long long>(j) * g.nx + i;
-}
 
 // e_k, h_k, cv_k of the thermodynamic polynomial (smc_mechanism.h), Horner
 // form with host-derived coefficients
@@ -180,7 +173,6 @@ __global__ void __launch_bounds__(256, 3) prim_kernel(const UV U, double* __rest
   }
   eta *= s;
   lam *= s;
-  const double xi = SMC_XI_OVER_ETA * eta;
   for (int i = 0; i < 3; ++i) F[(F_U + i) * n + c] = u[i];
   F[F_T * n + c] = T;
   F[F_RHO * n + c] = rho;
@@ -456,6 +448,7 @@ void rhs_v2(const Geo& g, const UV& U, const double* F, double* A, double* GR, d
     set_smem(ns_phase_a<0, S>, sm0), set_smem(ns_phase_a<1, S>, sm1), set_smem(ns_phase_a<2, S>, sm2);
     const std::size_t smb = sizeof(PBSmem);
     set_smem(ns_phase_b<0>, smb), set_smem(ns_phase_b<1>, smb), set_smem(ns_phase_b<2>, smb);
+    set_smem(ns_phase_b3, sizeof(B3Smem));
     configured = true;
   }
   const int allp = g.nz + 2 * g.G;
@@ -489,16 +482,28 @@ void rhs_v2(const Geo& g, const UV& U, const double* F, double* A, double* GR, d
   ns_phase_a<2, S><<<dir_grid<2, nr_a<2>()>(g, allp), NT1, sm2, st>>>(F, A, na1, GR, out, ofs, hy1, n, g, M, 0);
   SMC_CHECK_LAUNCH();
   mark("phase_a_z");
-  ns_phase_b<0><<<dir_grid<0>(g, g.nz), DT_THREADS, sizeof(PBSmem), st>>>(F, GR, A, g);
-  SMC_CHECK_LAUNCH();
-  mark("phase_b_x");
-  ns_phase_b<1><<<dir_grid<1>(g, g.nz), DT_THREADS, sizeof(PBSmem), st>>>(F, GR, A, g);
-  SMC_CHECK_LAUNCH();
-  mark("phase_b_y");
-  ns_phase_b<2><<<dir_grid<2>(g, g.nz), DT_THREADS, sizeof(PBSmem), st>>>(F, GR, A, g);
-  SMC_CHECK_LAUNCH();
-  mark("phase_b_z");
-  ns_assemble2<<<blocks(n), 256, 0, st>>>(F, GR, A, out, ofs, g, chem);
+  if (g.nx % B3X == 0 && g.ny % B3Y == 0) {
+    // all three directions in one z-march
+    const int tiles = (g.nx / B3X) * (g.ny / B3Y);
+    const int resident = 2 * num_sms();
+    const int chunks = std::max(1, std::min(g.nz / 16, (4 * resident + tiles - 1) / tiles));
+    const int kc = (g.nz + chunks - 1) / chunks;
+    ns_phase_b3<<<dim3(tiles, (g.nz + kc - 1) / kc), B3T, sizeof(B3Smem), st>>>(F, GR, A, g, kc);
+    SMC_CHECK_LAUNCH();
+    mark("phase_b");
+    ns_assemble2<<<blocks(n), 256, 0, st>>>(F, GR, A, out, ofs, g, chem);
+  } else {
+    ns_phase_b<0><<<dir_grid<0>(g, g.nz), DT_THREADS, sizeof(PBSmem), st>>>(F, GR, A, g);
+    SMC_CHECK_LAUNCH();
+    mark("phase_b_x");
+    ns_phase_b<1><<<dir_grid<1>(g, g.nz), DT_THREADS, sizeof(PBSmem), st>>>(F, GR, A, g);
+    SMC_CHECK_LAUNCH();
+    mark("phase_b_y");
+    ns_phase_b<2><<<dir_grid<2>(g, g.nz), DT_THREADS, sizeof(PBSmem), st>>>(F, GR, A, g);
+    SMC_CHECK_LAUNCH();
+    mark("phase_b_z");
+    ns_assemble2<<<blocks(n), 256, 0, st>>>(F, GR, A, out, ofs, g, chem);
+  }
   SMC_CHECK_LAUNCH();
   mark(chem ? "assemble_wdot" : "assemble");
 }
