@@ -426,6 +426,10 @@ int blocks(long long n) { return static_cast<int>((n + 255) / 256); }
 
 #include "ns_dir.inc"
 
+#ifndef SMC_B3_WAVES
+#define SMC_B3_WAVES 4  // fused phase B: about this many waves of z-chunk CTAs
+#endif
+
 template <class K>
 void set_smem(K kern, std::size_t bytes) {
   SMC_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -486,7 +490,7 @@ void rhs_v2(const Geo& g, const UV& U, const double* F, double* A, double* GR, d
     // all three directions in one z-march
     const int tiles = (g.nx / B3X) * (g.ny / B3Y);
     const int resident = 2 * num_sms();
-    const int chunks = std::max(1, std::min(g.nz / 16, (4 * resident + tiles - 1) / tiles));
+    const int chunks = std::max(1, std::min(g.nz / 16, (SMC_B3_WAVES * resident + tiles - 1) / tiles));
     const int kc = (g.nz + chunks - 1) / chunks;
     ns_phase_b3<<<dim3(tiles, (g.nz + kc - 1) / kc), B3T, sizeof(B3Smem), st>>>(F, GR, A, g, kc);
     SMC_CHECK_LAUNCH();
