@@ -246,12 +246,37 @@ __device__ __forceinline__ double arrhenius_exp(double x) {
                               (static_cast<long long>(n) << 52));
 }
 
+// Temperature exponent and activation energy of every rate as compile-time
+// constants: a rate with no activation energy and a temperature exponent of
+// 0, -1 or -2 is A, A / T or A / T^2 (no exponential; 3 of the 26 rates of
+// the built-in mechanism)
+struct RxArr {
+  double bf, ef, br, er;
+};
+#define SMC_RX_ARR(r0, r1, r2, p0, p1, p2, tb, af, bf, ef, ar, br, er) RxArr{bf, ef, br, er},
+constexpr RxArr kArr[SMC_NREAC] = {SMC_REACTION_LIST(SMC_RX_ARR)};
+#undef SMC_RX_ARR
+
+template <int R, bool FWD>
+__device__ __forceinline__ double rate(double lnT, double invRT) {
+  constexpr double b = FWD ? kArr[R].bf : kArr[R].br, e = FWD ? kArr[R].ef : kArr[R].er;
+  const double* k = FWD ? cT.kf[R] : cT.kr[R];
+  if constexpr (e == 0.0 && b == 0.0) {
+    return k[0];
+  } else if constexpr (e == 0.0 && (b == -1.0 || b == -2.0)) {
+    const double invT = invRT * SMC_RU;
+    return b == -1.0 ? k[0] * invT : k[0] * (invT * invT);
+  } else {
+    return k[0] * arrhenius_exp(k[1] * lnT - k[2] * invRT);
+  }
+}
+
 template <int R>
 __device__ __forceinline__ void rx_step(const double* C, double M, double lnT, double invRT,
                                         double* om) {
   constexpr RxIdx x = kRx[R];
-  const double kf = cT.kf[R][0] * arrhenius_exp(cT.kf[R][1] * lnT - cT.kf[R][2] * invRT);
-  const double kr = cT.kr[R][0] * arrhenius_exp(cT.kr[R][1] * lnT - cT.kr[R][2] * invRT);
+  const double kf = rate<R, true>(lnT, invRT);
+  const double kr = rate<R, false>(lnT, invRT);
   double qf = kf, qr = kr;
   if constexpr (x.r[0] >= 0) qf *= C[x.r[0]];
   if constexpr (x.p[0] >= 0) qr *= C[x.p[0]];
