@@ -347,6 +347,37 @@ __global__ void __launch_bounds__(256) chem_kernel(const UV U, double* __restric
   for (int v = 0; v < NV; ++v) out[v * out_fs + c] = o[v];
 }
 
+// The MRSDC fine-node update fused with the chemistry part: per cell, the 14
+// updated state values next = cur + sum_d dc_d (da_d - db_d) + pre (the
+// arithmetic of sweep_update_kernel<ND, 0>) stay in registers for chem_cell,
+// so the chemistry does not re-read the state the update just wrote.
+struct ChemUpdP {
+  double* next;
+  const double *cur, *pre, *da[2], *db[2];
+  double dc[2];
+  double* out;
+  long long n;
+};
+template <int ND>
+__global__ void __launch_bounds__(256) chem_update_kernel(const ChemUpdP p) {
+  const long long c = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
+  if (c >= p.n) return;
+  double Uc[NV], o[NV];
+#pragma unroll
+  for (int v = 0; v < NV; ++v) {
+    const long long i = v * p.n + c;
+    double x = p.cur[i];
+#pragma unroll
+    for (int d = 0; d < ND; ++d) x = __fma_rn(p.dc[d], __dsub_rn(p.da[d][i], p.db[d][i]), x);
+    x = __dadd_rn(x, p.pre[i]);
+    p.next[i] = x;
+    Uc[v] = x;
+  }
+  chem_cell(Uc, o);
+#pragma unroll
+  for (int v = 0; v < NV; ++v) p.out[v * p.n + c] = o[v];
+}
+
 // The chemistry part's FD Jacobian, one cell per thread: column j from the
 // cell's state with component j perturbed, as DeviceNewton's column loop
 // (fd_perturb_kernel, the chemistry evaluation, fd_column_kernel) forms it,
@@ -738,6 +769,26 @@ void NsRhsOp::eval_host(double t, const double* u, double* out) {
   }
   SMC_CUDA(cudaStreamSynchronize(d2h_));
   ++evals_;
+}
+
+bool NsWorkspace::chem_after_update(double* next, const double* cur, int nd,
+                                    const double* const* da, const double* const* db,
+                                    const double* dc, const double* pre, double* out,
+                                    cudaStream_t st) {
+  if (box_.G != 0 || nd < 0 || nd > 2 || !pre) return false;
+  ChemUpdP p{};
+  p.next = next, p.cur = cur, p.pre = pre, p.out = out, p.n = box_.cells();
+  for (int d = 0; d < nd; ++d) p.da[d] = da[d], p.db[d] = db[d], p.dc[d] = dc[d];
+  const unsigned nb = static_cast<unsigned>((p.n + 255) / 256);
+  if (nd == 0)
+    chem_update_kernel<0><<<nb, 256, 0, st>>>(p);
+  else if (nd == 1)
+    chem_update_kernel<1><<<nb, 256, 0, st>>>(p);
+  else
+    chem_update_kernel<2><<<nb, 256, 0, st>>>(p);
+  SMC_CHECK_LAUNCH();
+  if (marks_) marks_->mark("chem_update", st);
+  return true;
 }
 
 bool NsWorkspace::chem_fd_jacobian(const double* U, const double* FU, double* jac, double atol,

@@ -78,6 +78,11 @@ class NsWorkspace {
   // Fused FD Jacobian of the chemistry part (RhsOp::fd_block_jacobian) for
   // the cell-block layout (block SMC_NVAR, field-major); false when the box
   // has ghost planes (the state is then not cell-block shaped).
+  // MRSDC fine node: the sweep update of the state (RhsOp::eval_after_update)
+  // fused with the chemistry part at the updated state (periodic box only)
+  bool chem_after_update(double* next, const double* cur, int nd, const double* const* da,
+                         const double* const* db, const double* dc, const double* pre,
+                         double* out, cudaStream_t st);
   bool chem_fd_jacobian(const double* U, const double* FU, double* jac, double atol,
                         double root_eps, cudaStream_t st);
   // T and p of every interior cell (ctoprim), for tests / diagnostics.
@@ -124,6 +129,14 @@ class NsRhsOp final : public RhsOp {
     ++evals_;
   }
   const char* name() const override { return "ns"; }
+  bool eval_after_update(double, double* next, const double* cur, int nd,
+                         const double* const* da, const double* const* db, const double* dc,
+                         const double* pre, double* out) override {
+    if (part_ != kNsChem || !ws_->chem_after_update(next, cur, nd, da, db, dc, pre, out, stream_))
+      return false;
+    ++evals_;
+    return true;
+  }
   bool fd_block_jacobian(const double* w, const double* fw, double* jac, long long block,
                          int interleaved, double atol, double root_eps) override {
     if (part_ != kNsChem || block != SMC_NVAR || !interleaved) return false;

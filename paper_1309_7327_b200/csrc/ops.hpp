@@ -87,6 +87,18 @@ class RhsOp {
     return false;
   }
 
+  // Optional fused sweep update + evaluation (MRSDC's fine nodes):
+  // next = cur + sum_{d < nd} dc_d (da_d - db_d) + pre elementwise, with the
+  // arithmetic of sweep_update_kernel<nd, 0>, then out = f(t, next), in one
+  // pass for a pointwise f.  Returns false when the operator has no fused
+  // form (the caller then launches the update and evaluates).
+  virtual bool eval_after_update(double /*t*/, double* /*next*/, const double* /*cur*/,
+                                 int /*nd*/, const double* const* /*da*/,
+                                 const double* const* /*db*/, const double* /*dc*/,
+                                 const double* /*pre*/, double* /*out*/) {
+    return false;
+  }
+
  protected:
   cudaStream_t stream_ = nullptr;
   long long evals_ = 0;

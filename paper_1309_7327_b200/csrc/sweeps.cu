@@ -773,9 +773,14 @@ void DeviceMrsdc::run(RhsOp& f1, RhsOp& f2, double t_n, double dt, bool have1, b
       int nd = 0;
       if (n1[p] != o1[p]) da[nd] = n1[p], db[nd] = o1[p], dc[nd] = dtq, ++nd;
       if (n2[q] != o2[q]) da[nd] = n2[q], db[nd] = o2[q], dc[nd] = dtq, ++nd;
-      launch_sweep_update(u_[q + 1], u_[q], nd, da, db, dc, 0, nullptr, nullptr, dt, so_[q], n,
-                          st);
-      f2.eval_device(t_n + t2[q + 1] * dt, u_[q + 1], s2[q]);
+      // the update of node q + 1 and f2 there, fused when f2 is pointwise
+      // (the NS chemistry part), else two passes
+      if (!f2.eval_after_update(t_n + t2[q + 1] * dt, u_[q + 1], u_[q], nd, da, db, dc, so_[q],
+                                s2[q])) {
+        launch_sweep_update(u_[q + 1], u_[q], nd, da, db, dc, 0, nullptr, nullptr, dt, so_[q], n,
+                            st);
+        f2.eval_device(t_n + t2[q + 1] * dt, u_[q + 1], s2[q]);
+      }
       n2[q + 1] = s2[q];
       ++d.f2_evals;
       if (const int pc = coarse_at[q + 1]; pc > 0) {
