@@ -65,6 +65,16 @@ class NsSlabOp final : public RhsOp {
   ~NsSlabOp() override;
   long long dim() const override { return SMC_NVAR * ws_->box().cells(); }
   void eval_device(double t, const double* u, double* out) override;
+  // the chemistry part is pointwise: the MRSDC fine-node update fused with it
+  // (the slab state is the rank's interior planes, 14 fields)
+  bool eval_after_update(double, double* next, const double* cur, int nd,
+                         const double* const* da, const double* const* db, const double* dc,
+                         const double* pre, double* out) override {
+    if (part_ != kNsChem || !ws_->chem_after_update(next, cur, nd, da, db, dc, pre, out, stream_))
+      return false;
+    ++evals_;
+    return true;
+  }
   const char* name() const override { return "ns_slab"; }
   HaloTransport& transport() { return *tr_; }
   void publish(const double* u) { tr_->publish(u, ws_->box().cells()); }

@@ -775,7 +775,7 @@ bool NsWorkspace::chem_after_update(double* next, const double* cur, int nd,
                                     const double* const* da, const double* const* db,
                                     const double* dc, const double* pre, double* out,
                                     cudaStream_t st) {
-  if (box_.G != 0 || nd < 0 || nd > 2 || !pre) return false;
+  if (nd < 0 || nd > 2 || !pre) return false;
   ChemUpdP p{};
   p.next = next, p.cur = cur, p.pre = pre, p.out = out, p.n = box_.cells();
   for (int d = 0; d < nd; ++d) p.da[d] = da[d], p.db[d] = db[d], p.dc[d] = dc[d];

@@ -79,7 +79,8 @@ class NsWorkspace {
   // the cell-block layout (block SMC_NVAR, field-major); false when the box
   // has ghost planes (the state is then not cell-block shaped).
   // MRSDC fine node: the sweep update of the state (RhsOp::eval_after_update)
-  // fused with the chemistry part at the updated state (periodic box only)
+  // fused with the chemistry part at the updated state; the state is the
+  // box's interior cells, 14 fields (a slab's own planes)
   bool chem_after_update(double* next, const double* cur, int nd, const double* const* da,
                          const double* const* db, const double* dc, const double* pre,
                          double* out, cudaStream_t st);
@@ -132,7 +133,8 @@ class NsRhsOp final : public RhsOp {
   bool eval_after_update(double, double* next, const double* cur, int nd,
                          const double* const* da, const double* const* db, const double* dc,
                          const double* pre, double* out) override {
-    if (part_ != kNsChem || !ws_->chem_after_update(next, cur, nd, da, db, dc, pre, out, stream_))
+    if (part_ != kNsChem || ws_->box().G != 0 ||
+        !ws_->chem_after_update(next, cur, nd, da, db, dc, pre, out, stream_))
       return false;
     ++evals_;
     return true;
