@@ -102,6 +102,35 @@ def test_nccl_single_rank_sdc_with_library_reducer(cuda):
     assert d.fresh_evals == dr.fresh_evals == 2 * 8 + 1
 
 
+def test_nccl_single_rank_mrsdc_equals_periodic(cuda):
+    """MRSDC mode 1 advancing the NCCL slab operators (advection-diffusion
+    with the halo exchange, the chemistry part with each fine node's update
+    fused into it) equals the periodic operators' advance bit for bit."""
+    import torch
+    from paper_1309_7327_b200 import _capi
+    from test_gpu_ns_steppers import acoustic_dt
+    n = 16
+    prims = W.ns_primitives(n, ignition=True)
+    U = O.ns_conserved(*prims)
+    dt = acoustic_dt(prims, DX)
+    try:
+        comm = Comm.nccl()
+    except _capi.SmcError as exc:
+        pytest.skip(f"NCCL unavailable: {exc}")
+    slab = NsSlab(comm, n, n, n, DX)
+    slab.set_stream(torch.cuda.current_stream())
+    st = P.MrsdcStepper(3, 5, P.StepControls(3, 0.0))
+    st.set_comm(comm)
+    got, d = st.integrate_mode1(slab.advdiff, slab.chem, torch.from_numpy(U).to(cuda), 0.0,
+                                2 * dt, 2)
+    torch.cuda.synchronize()
+    op = P.NsOperator(n, n, n, DX)
+    ref, dr = P.MrsdcStepper(3, 5, P.StepControls(3, 0.0)).integrate_mode1(
+        op.advdiff, op.chem, U, 0.0, 2 * dt, 2)
+    assert np.array_equal(got.cpu().numpy(), ref)
+    assert d.f2_evals == dr.f2_evals and d.f1_evals == dr.f1_evals
+
+
 def test_slab_rejects_thin_slabs(cuda):
     comms = Comm.local_group(2)
     with pytest.raises(ValueError):
