@@ -94,7 +94,10 @@ def test_ns_slab_matches_periodic(cuda):
 
 # anisotropic boxes: whole tiles along x (64) with short y / z extents
 @pytest.mark.parametrize("part", [P.NS_FULL, P.NS_ADVDIFF])
-@pytest.mark.parametrize("shape,kw", [((16, 16, 64), {}), ((16, 32, 64), {"hot_spot": True})])
+@pytest.mark.parametrize("shape,kw", [((16, 16, 64), {}), ((16, 32, 64), {"hot_spot": True}),
+                                      # partial y / z tiles of the direction passes, z chunks
+                                      # of the fused phase B that do not divide nz
+                                      ((52, 40, 32), {"hot_spot": True}), ((40, 24, 96), {})])
 def test_ns_rhs_anisotropic_vs_oracle(cuda, part, shape, kw):
     nz, ny, nx = shape
     T, p, uvw, Y = W.ns_primitives(nx, ny=ny, nz=nz, **kw)
