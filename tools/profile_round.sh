@@ -7,9 +7,13 @@ python bench.py --impl reference --steps 3 --warmup 1 > gpurun_out/bench_ref.jso
 python tools/ns_bench.py 256 1 > gpurun_out/nsb.log 2>&1 && \
 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none \
     --csv --log-file gpurun_out/ns256_launches.csv python tools/ns_bench.py 256 1 > gpurun_out/ncu_l.log 2>&1
-# full sections of one NS RHS (its 9 kernels) and of the configs[1] kernel
-ncu --set full --import-source on --clock-control none -k 'regex:ns_phase|prim_kernel|ns_assemble2|ns_mixed' \
-    -c 9 -o gpurun_out/prof_ns python tools/ns_bench.py 256 1 > gpurun_out/ncu_ns.log 2>&1
+# full sections of one NS RHS (its 6 kernels) and of the configs[1] kernel
+ncu --set full --import-source on --clock-control none -k 'regex:ns_phase|prim_kernel|ns_assemble2' \
+    -c 6 -o gpurun_out/prof_ns python tools/ns_bench.py 256 1 > gpurun_out/ncu_ns.log 2>&1
+# executed FP64 operations per kernel (profiles/ncu_ns_fp64_ops_r02.json)
+ncu --metrics smsp__sass_thread_inst_executed_op_dfma_pred_on.sum,smsp__sass_thread_inst_executed_op_dadd_pred_on.sum,smsp__sass_thread_inst_executed_op_dmul_pred_on.sum \
+    --clock-control none -k 'regex:ns_phase|prim_kernel|ns_assemble2' -c 6 --csv --log-file gpurun_out/ns_ops.csv \
+    python tools/ns_bench.py 256 1 > gpurun_out/ncu_ops.log 2>&1
 python tools/narrow_time.py 256 50 > gpurun_out/nt.log 2>&1 && \
 ncu --set full --import-source on --clock-control none -k regex:narrow3d_fast -s 3 -c 1 \
     -o gpurun_out/prof_narrow python tools/narrow_time.py 256 50 > gpurun_out/ncu_n.log 2>&1
